@@ -1,0 +1,219 @@
+#ifndef DISTWAR_H
+#define DISTWAR_H
+
+/* distwar -- B200-native (sm_100a) DISTWAR hot path: warp-level reduction of
+ * per-primitive gradient contributions, both trace-driven (the reference's
+ * WarpRecord model) and inside a tile-based Gaussian-splatting backward pass.
+ *
+ * Conventions are those of the reference C ABI (warpred.h:4-11, 20-33,
+ * capi.cpp:16-44), unchanged:
+ *   - every fallible call returns dw_status; DW_OK = 0;
+ *   - on failure the message is read with dw_last_error() (thread-local,
+ *     never NULL);
+ *   - a NULL required argument returns DW_ERR_INVALID_ARGUMENT with
+ *     "null argument";
+ *   - std::invalid_argument -> 1, std::ios_base::failure -> 2, any other
+ *     exception (including CUDA errors) -> 3;
+ *   - opaque handles are released with the matching _free;
+ *   - out-structs are caller-owned PODs; returned strings are library-owned.
+ * Device pointers are plain CUDA device addresses; `stream` is a
+ * cudaStream_t (NULL = legacy default stream). No torch types cross this
+ * boundary. Gradient buffers are [primitive][param] fp32, i.e. the reference's
+ * Address order (reducers.hpp:19-23): index = primitive * N + param.
+ */
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* warpred.h:20-25 */
+typedef enum dw_status {
+  DW_OK = 0,
+  DW_ERR_INVALID_ARGUMENT = 1,
+  DW_ERR_IO = 2,
+  DW_ERR_RUNTIME = 3
+} dw_status;
+
+/* warpred.h:27-33 (same values). DW_POLICY_HW_ATOMRED is the reference's
+ * simulated hardware unit; B200 has no such instruction, so it is rejected
+ * with DW_ERR_INVALID_ARGUMENT, as reducers::apply_policy rejects it
+ * (reducers.cpp:232-236). */
+typedef enum dw_policy_kind {
+  DW_POLICY_NATIVE = 0,
+  DW_POLICY_SW_S = 1,
+  DW_POLICY_SW_B = 2,
+  DW_POLICY_CCCL = 3,
+  DW_POLICY_HW_ATOMRED = 4
+} dw_policy_kind;
+
+/* warpred.h:35-38 */
+typedef enum dw_policy_family { DW_FAMILY_SW_S = 0, DW_FAMILY_SW_B = 1 } dw_policy_family;
+
+/* warpred.h:42-53 (same layout; replaces workload::SceneSpec). */
+typedef struct dw_scene_spec {
+  int32_t num_primitives;
+  int32_t params_per_primitive;
+  int32_t image_width;
+  int32_t image_height;
+  double mean_fragment_span;
+  double fragments_per_pixel_mean;
+  double activity_prob;
+  double locality;
+  uint64_t seed;
+  int32_t quantized_values;
+} dw_scene_spec;
+
+typedef struct dw_trace dw_trace;               /* host WarpRecord trace    */
+typedef struct dw_device_trace dw_device_trace; /* SoA fp32 copy in HBM     */
+typedef struct dw_rasterizer dw_rasterizer;     /* per-view device state    */
+
+/* Measured replacement of wr_run_metrics (warpred.h:68-77): cycles become
+ * device milliseconds; request counts are counted on the device. */
+typedef struct dw_gpu_metrics {
+  double kernel_ms;                 /* CUDA-event time of the reduce kernel */
+  uint64_t atomic_requests_to_l2;   /* global REDs issued (== reference
+                                       PolicyOutput.requests summed)        */
+  uint64_t contributions;           /* sum over records popc(active) * N    */
+  uint64_t records;
+} dw_gpu_metrics;
+
+/* warpred.h:79-84, cycles -> measured microseconds per threshold. */
+typedef struct dw_tune_report {
+  double us_by_threshold[33];
+  int32_t chosen;              /* argmin; ties -> lowest threshold (tuner.cpp:46-49) */
+  int32_t profile_iteration;
+  int32_t reprofile_period;    /* 2000, tuner.hpp:15 */
+} dw_tune_report;
+
+/* Camera for the Gaussian rasterizer: column-major 4x4 matrices
+ * (p' = M p, M[col*4+row]); projmatrix is the full proj*view transform. */
+typedef struct dw_camera {
+  int32_t width, height;
+  float viewmatrix[16];
+  float projmatrix[16];
+  float tan_fovx, tan_fovy;
+  float bg[3];
+  float scale_modifier;
+} dw_camera;
+
+/* ------------------------------------------------------------- library */
+const char* dw_version(void);          /* wr_version, warpred.h:86        */
+const char* dw_last_error(void);       /* wr_last_error, warpred.h:88-89  */
+int dw_device_count(void);             /* -1 when the CUDA runtime fails  */
+
+/* --------------------------------------------------- host traces (input) */
+void dw_scene_spec_init(dw_scene_spec* scene);                 /* warpred.h:91  */
+dw_status dw_trace_generate(const dw_scene_spec* scene, dw_trace** out); /* :98 */
+void dw_trace_free(dw_trace* trace);                            /* :99  */
+int64_t dw_trace_record_count(const dw_trace* trace);           /* :100, -1 on NULL */
+/* WRTRACEB binary container (trace_io.cpp:209-276); binary must be nonzero. */
+dw_status dw_trace_save(const dw_trace* trace, const char* path, int binary); /* :101 */
+dw_status dw_trace_load(const char* path, int binary, dw_trace** out);       /* :102 */
+dw_status dw_trace_histogram_distinct(const dw_trace* trace, uint64_t out_counts[33]); /* :106 */
+dw_status dw_trace_histogram_active(const dw_trace* trace, uint64_t out_counts[33]);   /* :108 */
+/* Builds a trace from flat caller arrays (prim[R*32], grads[R*32*N] lane-major). */
+dw_status dw_trace_from_arrays(int64_t num_records, int32_t params, int32_t num_primitives,
+                               const int32_t* warp_id, const int32_t* iteration,
+                               const uint32_t* active, const int32_t* prim,
+                               const double* grads, dw_trace** out);
+/* Borrowed views into a trace (valid until dw_trace_free). */
+dw_status dw_trace_arrays(const dw_trace* trace, const uint32_t** active,
+                          const int32_t** prim, const double** grads,
+                          dw_scene_spec* scene);
+
+/* ------------------------------------- trace-driven DISTWAR reduction (GPU) */
+/* Uploads a trace to HBM as SoA fp32: active u32[R], prim i32[R][32],
+ * vals f32[R][N][32] (param-major per record, so each param is one 128 B
+ * coalesced warp load). */
+dw_status dw_trace_upload(const dw_trace* trace, void* stream, dw_device_trace** out);
+void dw_device_trace_free(dw_device_trace* dtrace);
+dw_status dw_device_trace_view(const dw_device_trace* dtrace, const uint32_t** d_active,
+                               const int32_t** d_prim, const float** d_vals,
+                               int64_t* num_records, int32_t* params, int32_t* num_primitives);
+
+/* The hot path over raw device arrays: each warp applies `policy` (threshold
+ * in 0..33, used by SW_S / SW_B; warpred.h:113) to each record and issues the
+ * resulting RED.ADD.F32 into d_grad[prim * params + param] (accumulates; the
+ * caller zeroes). d_red_count (nullable) receives the number of global REDs
+ * issued -- the counting variant is a separate instantiation. */
+dw_status dw_reduce_records(const uint32_t* d_active, const int32_t* d_prim,
+                            const float* d_vals, int64_t num_records, int32_t params,
+                            int32_t num_primitives, dw_policy_kind policy,
+                            int32_t threshold, float* d_grad,
+                            unsigned long long* d_red_count, void* stream);
+
+/* Replaces wr_simulate (warpred.h:114-116): runs the policy on the real
+ * machine; host_grad_out (nullable, P*N floats) receives the sums. */
+dw_status dw_gpu_run(const dw_device_trace* dtrace, dw_policy_kind policy, int32_t threshold,
+                     float* host_grad_out, dw_gpu_metrics* out);
+
+/* Replaces wr_tune (warpred.h:120-122): measured sweep t = 0..32 on the
+ * records of `iteration` (< 0: the whole trace), argmin with ties to the
+ * lowest threshold (tuner.cpp:29-52). reps = timed repetitions per t. */
+dw_status dw_tune(const dw_trace* trace, dw_policy_family family, int32_t iteration,
+                  int32_t reps, dw_tune_report* out);
+dw_status dw_tune_report_save_csv(const dw_tune_report* report, const char* path); /* :123 */
+
+/* ------------------------------------------- Gaussian-splatting rasterizer */
+dw_status dw_rasterizer_create(dw_rasterizer** out);
+void dw_rasterizer_free(dw_rasterizer* r);
+
+/* render_forward: preprocess -> tile keys -> radix sort -> tile ranges ->
+ * front-to-back blend. All pointers are device pointers: means3D/scales P*3,
+ * rotations P*4 (r,x,y,z), opacities P, colors P*3 (RGB), out_color 3*H*W
+ * (channel-major), radii P (nullable). num_rendered (host, nullable) receives
+ * the number of (tile, Gaussian) instances. Synchronises `stream` once to
+ * size the sort. */
+dw_status dw_render_forward(dw_rasterizer* r, int32_t P, const float* means3D,
+                            const float* scales, const float* rotations,
+                            const float* opacities, const float* colors,
+                            const dw_camera* cam, float* out_color, int32_t* radii,
+                            int64_t* num_rendered, void* stream);
+
+/* render_backward: the DISTWAR hot path. dL_dpixels 3*H*W (device). Adds the
+ * 9 screen-space gradients per Gaussian into grad[P*9] in Address order
+ * (mean2D.x, mean2D.y, conic.x, conic.y, conic.z, opacity, r, g, b).
+ * pairs_out (host, nullable): number of (pixel, Gaussian) pairs that
+ * contributed, counted by a separate counting instantiation (so the timed
+ * path carries no counter). */
+dw_status dw_render_backward(dw_rasterizer* r, const float* dL_dpixels,
+                             dw_policy_kind policy, int32_t threshold, float* grad,
+                             uint64_t* pairs_out, void* stream);
+
+/* Number of global REDs issued by the last render_backward called with a
+ * non-NULL pairs_out (the counting instantiation). */
+dw_status dw_rasterizer_last_reds(const dw_rasterizer* r, uint64_t* out);
+
+/* Device views of the rasterizer's intermediate buffers (parity tests):
+ * 0 means2D f32[P*2], 1 depths f32[P], 2 radii i32[P], 3 conic_opacity
+ * f32[P*4], 4 tiles_touched u32[P], 5 keys u64[I] (sorted), 6 values u32[I]
+ * (sorted), 7 ranges u32[tiles*2], 8 final_T f32[H*W], 9 n_contrib u32[H*W].
+ * count = number of elements. */
+dw_status dw_rasterizer_buffer(const dw_rasterizer* r, int32_t which, const void** dptr,
+                               int64_t* count);
+
+/* Host-buffer end-to-end call (copies inside): forward + backward for one
+ * view, H2D of the scene and dL/dpixels, D2H of image and grad. */
+dw_status dw_render_host(dw_rasterizer* r, int32_t P, const float* means3D,
+                         const float* scales, const float* rotations, const float* opacities,
+                         const float* colors, const dw_camera* cam, const float* dL_dpixels,
+                         dw_policy_kind policy, int32_t threshold, float* out_color,
+                         float* grad, void* stream);
+
+/* Synchronous device->host copy of `bytes` (reads back dw_rasterizer_buffer
+ * views without the caller linking the CUDA runtime). */
+dw_status dw_copy_to_host(void* host_dst, const void* device_src, size_t bytes);
+
+/* --------------------------------------------------- roofline microbenchmarks */
+/* Measured f32 RED throughput (REDs/s) for `pattern`: 0 distinct addresses,
+ * 1 all 32 lanes of a warp on one address (the naive pattern), 2 distinct
+ * addresses with red.global.add.v4.f32 (counted as 4 REDs). */
+dw_status dw_microbench_red(int32_t pattern, int64_t ops, double* reds_per_s, void* stream);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+#endif /* DISTWAR_H */

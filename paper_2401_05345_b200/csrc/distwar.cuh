@@ -1,0 +1,228 @@
+// DISTWAR device-side reduction primitives for sm_100a.
+//
+// Each function is called by ALL 32 lanes of a warp in place of the N
+// per-lane atomicAdds of the gradient step (the SW-B
+// calling convention of PAPER.md:1858-1888: inactive lanes participate with
+// zero values and an `active` flag). Policy semantics follow the reference
+// restatement exactly -- which lanes issue, how many RED.ADD requests reach
+// L2, the balancing-threshold comparison `count >= t` -- while the arithmetic
+// is laid out for the B200 SM:
+//
+//   native   reducers.cpp:84-93   one RED per (active lane, param)
+//   sw_s     reducers.cpp:95-136  __match_any_sync groups; a group of size
+//                                 >= t is folded by its lowest lane in
+//                                 ascending lane order, then N REDs
+//   sw_b     reducers.cpp:138-175 all 32 lanes on one primitive and
+//                                 popc(active) >= t: a full-warp butterfly,
+//                                 then N REDs; else per-lane REDs
+//   cccl     reducers.cpp:177-206 per-param eligibility + per-param
+//                                 cub::WarpReduce, lane 0 issues
+//
+// SW-B's butterfly is a *reduce-scatter* xor butterfly: at each of the 5
+// levels a lane keeps half of its live params and ships the other half to
+// its partner, so N=9 needs 5+3+2+1+1 = 12 SHFL+FADD instead of 5*9 = 45, and
+// the N sums end in N distinct lanes which issue ONE RED instruction (N
+// active lanes, contiguous addresses) instead of N single-lane REDs. The
+// per-param sum is the same balanced 32-leaf tree as the reference's
+// shfl_down tree up to a relabelling of the leaves, so it is exact wherever
+// the reference's is (the k/256 grid) and otherwise within fp32 rounding.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cub/warp/warp_reduce.cuh>
+#include <cstdint>
+
+namespace dw {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+enum PolicyKind : int { kNative = 0, kSwS = 1, kSwB = 2, kCccl = 3 };
+
+// One fire-and-forget fp32 reduction at L2 (SASS RED.E.ADD.F32.FTZ.RN).
+__device__ __forceinline__ void red_add(float* addr, float v) {
+  asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(addr), "f"(v) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Reduce-scatter butterfly over compile-time N (<= 32 params).
+//
+// Register layout: at a level with CNT virtual slots, lanes with the level's
+// bit clear keep slots [0, H) and lanes with it set keep [H, 2H) moved down
+// to [0, H), H = ceil(CNT/2); slots past the parent's real range are
+// garbage that only ever meets garbage. Once CNT == 1 both partners keep the
+// slot (a plain butterfly step), so on exit v[0] of every lane is the full
+// 32-lane sum of the param bfly_slot() names.
+template <int CNT, int OFF>
+struct ReduceScatter {
+  template <int CAP>
+  __device__ __forceinline__ static void run(float (&v)[CAP], int lane) {
+    if constexpr (OFF >= 1) {
+      if constexpr (CNT <= 1) {
+        v[0] += __shfl_xor_sync(kFull, v[0], OFF);
+        ReduceScatter<1, OFF / 2>::run(v, lane);
+      } else {
+        constexpr int H = (CNT + 1) / 2;
+        const bool up = (lane & OFF) != 0;
+#pragma unroll
+        for (int k = 0; k < H; ++k) {
+          if (k + H < CNT) {
+            const float send = up ? v[k] : v[k + H];
+            const float recv = __shfl_xor_sync(kFull, send, OFF);
+            v[k] = (up ? v[k + H] : v[k]) + recv;
+          } else {  // odd CNT: the upper lane has no slot k+H
+            const float send = up ? v[k] : 0.0f;
+            const float recv = __shfl_xor_sync(kFull, send, OFF);
+            v[k] = v[k] + recv;  // garbage in upper lanes, never emitted
+          }
+        }
+        ReduceScatter<H, OFF / 2>::run(v, lane);
+      }
+    }
+  }
+};
+
+// Which param lane `lane` holds after ReduceScatter<N,16>, and whether it is
+// the one designated lane that issues that param's RED.
+template <int N>
+__device__ __forceinline__ int bfly_slot(int lane, bool* issuer) {
+  int lo = 0, real = N, cnt = N;
+  bool designated = true;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    if (cnt <= 1) {
+      if (lane & off) designated = false;  // both partners hold it; keep bit-0 side
+    } else {
+      const int h = (cnt + 1) / 2;
+      if (lane & off) {
+        lo += h;
+        real = real - h > 0 ? real - h : 0;
+      } else {
+        real = real < h ? real : h;
+      }
+      cnt = h;
+    }
+  }
+  *issuer = designated && real >= 1;
+  return lo;
+}
+
+// ---------------------------------------------------------------------------
+// Policies. `base` is this lane's &grad[idx * N]; `v` its N values (zeros
+// when inactive, as the SW-B convention requires); `active` its was_active
+// flag; `nred` counts the REDs this lane issues when COUNT.
+
+template <int N, bool COUNT>
+__device__ __forceinline__ void native_atomics(float* base, const float (&v)[N], bool active,
+                                               uint32_t& nred) {
+  if (active) {
+#pragma unroll
+    for (int p = 0; p < N; ++p) red_add(base + p, v[p]);
+    if (COUNT) nred += N;
+  }
+}
+
+// SW-B (reduce_bfly, PAPER.md:1779-1813 with the listing's bugs fixed: the
+// threshold is compared with popc(ballot), not the ballot mask). UNIFORM=true
+// skips the all-lanes-same-primitive vote when the caller guarantees it (the
+// rasterizer: every lane of a warp walks the same Gaussian list).
+template <int N, bool COUNT, bool UNIFORM>
+__device__ __forceinline__ void reduce_bfly(int idx, float* grad, float (&v)[N], int thr,
+                                            bool active, int lane, uint32_t& nred,
+                                            unsigned ballot) {
+  bool same = true;
+  int idx0 = idx;
+  if (!UNIFORM) {
+    idx0 = __shfl_sync(kFull, idx, 0);
+    same = __all_sync(kFull, idx == idx0) && idx0 >= 0;
+  }
+  const int cnt = __popc(ballot);
+  if (same && cnt > 0 && cnt >= thr) {
+    ReduceScatter<N, 16>::run(v, lane);
+    bool issuer;
+    const int p = bfly_slot<N>(lane, &issuer);
+    if (issuer) {
+      red_add(grad + static_cast<int64_t>(idx0) * N + p, v[0]);
+      if (COUNT) nred += 1;
+    }
+  } else {
+    native_atomics<N, COUNT>(grad + static_cast<int64_t>(idx) * N, v, active, nred);
+  }
+}
+
+// SW-S (reduce_serial, PAPER.md:1719-1759 with masked _sync shuffles): the
+// lowest lane of each __match_any_sync group of size >= thr folds the other
+// members' values in ascending lane order (reducers.cpp:101-121), then issues
+// N REDs; smaller groups issue per-lane REDs. Must be reached by all lanes.
+template <int N, bool COUNT>
+__device__ __forceinline__ void reduce_serial(int idx, float* grad, const float (&v)[N], int thr,
+                                              bool active, int lane, uint32_t& nred,
+                                              unsigned ballot) {
+  if (!active) return;  // inactive lanes take no part in SW-S (only `ballot` lanes)
+  const unsigned group = __match_any_sync(ballot, idx);
+  const int cnt = __popc(group);
+  const bool reduce = cnt >= thr;
+  const int leader = __ffs(group) - 1;
+  unsigned fetch = reduce ? (group & ~(1u << leader)) : 0u;
+  float sums[N];
+#pragma unroll
+  for (int p = 0; p < N; ++p) sums[p] = v[p];
+  // warp-uniform trip count: the largest reducing group's member count - 1
+  while (__any_sync(ballot, fetch != 0u)) {
+    const int src = fetch ? __ffs(fetch) - 1 : lane;
+#pragma unroll
+    for (int p = 0; p < N; ++p) {
+      const float x = __shfl_sync(ballot, v[p], src);
+      if (fetch && lane == leader) sums[p] += x;
+    }
+    fetch &= fetch - 1u;
+  }
+  float* base = grad + static_cast<int64_t>(idx) * N;
+  if (reduce) {
+    if (lane == leader) {
+#pragma unroll
+      for (int p = 0; p < N; ++p) red_add(base + p, sums[p]);
+      if (COUNT) nred += N;
+    }
+  } else {
+#pragma unroll
+    for (int p = 0; p < N; ++p) red_add(base + p, v[p]);
+    if (COUNT) nred += N;
+  }
+}
+
+// CCCL-style baseline (reducers.cpp:177-206): the eligibility check and a
+// library warp reduction repeated for every param, lane 0 issuing each RED.
+template <int N, bool COUNT>
+__device__ __forceinline__ void reduce_cccl(int idx, float* grad, const float (&v)[N],
+                                            bool active, int lane, uint32_t& nred,
+                                            unsigned ballot) {
+  using WR = cub::WarpReduce<float>;
+  typename WR::TempStorage tmp;  // shuffle-based for a full warp: no smem traffic
+#pragma unroll
+  for (int p = 0; p < N; ++p) {
+    const int idx0 = __shfl_sync(kFull, idx, 0);
+    const bool same = __all_sync(kFull, idx == idx0) && idx0 >= 0;
+    const int cnt = __popc(__ballot_sync(kFull, active));
+    if (same && cnt > 0) {
+      const float s = WR(tmp).Sum(v[p]);
+      if (lane == 0) {
+        red_add(grad + static_cast<int64_t>(idx0) * N + p, s);
+        if (COUNT) nred += 1;
+      }
+    } else if (active) {
+      red_add(grad + static_cast<int64_t>(idx) * N + p, v[p]);
+      if (COUNT) nred += 1;
+    }
+  }
+  (void)ballot;
+}
+
+// Warp-sum a per-lane counter and add it to a global u64 once per warp.
+__device__ __forceinline__ void flush_count(unsigned long long* ctr, uint32_t n, int lane) {
+  unsigned long long s = n;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
+  if (lane == 0 && s) atomicAdd(ctr, s);
+}
+
+}  // namespace dw

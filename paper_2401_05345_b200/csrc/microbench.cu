@@ -1,0 +1,87 @@
+// Roofline microbenchmarks: measured f32 RED throughput of the L2 atomic
+// units for the access patterns the policies generate (SURVEY.md §8(d):
+// "R_red_distinct, R_red_same, R_red_v4"). There is no published B200
+// figure, so bench.py measures these on the box in the same run.
+//   0 distinct: each warp instruction = 32 lanes -> 32 consecutive floats
+//   1 same:     each warp instruction = 32 lanes -> ONE float (naive pattern)
+//   2 v4:       red.global.add.v4.f32, 32 lanes -> 128 consecutive floats
+//   3 distwar:  9 lanes -> 9 consecutive floats of a pseudo-random primitive
+//               (the SW-B issue pattern of the rasterizer backward)
+#include <cuda_runtime.h>
+
+#include "distwar.cuh"
+#include "dw_internal.h"
+
+namespace dw {
+
+namespace {
+
+constexpr int64_t kRegionFloats = int64_t(1) << 24;  // 64 MB: L2-resident
+
+template <int PATTERN>
+__global__ void __launch_bounds__(256) k_red(float* __restrict__ buf, int iters) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const float v = 1.0f / 1024.0f;
+  for (int k = 0; k < iters; ++k) {
+    const int64_t w = warp + static_cast<int64_t>(k) * nwarps;
+    if (PATTERN == 0) {
+      red_add(buf + ((w * 32) & (kRegionFloats - 1)) + lane, v);
+    } else if (PATTERN == 1) {
+      red_add(buf + ((w * 32) & (kRegionFloats - 1)), v);
+    } else if (PATTERN == 2) {
+      float* p = buf + ((w * 128) & (kRegionFloats - 1)) + 4 * lane;
+      asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v),
+                   "f"(v), "f"(v), "f"(v)
+                   : "memory");
+    } else {
+      // multiplicative hash of the warp-iteration -> primitive id
+      const uint64_t prim = (static_cast<uint64_t>(w) * 2654435761ull) % 1000000ull;
+      if (lane < 9) red_add(buf + ((prim * 9) & (kRegionFloats - 1)) + lane, v);
+    }
+  }
+}
+
+template <int PATTERN>
+float run(float* buf, int grid, int iters, cudaStream_t s) {
+  cudaEvent_t a, b;
+  DW_CUDA(cudaEventCreate(&a));
+  DW_CUDA(cudaEventCreate(&b));
+  k_red<PATTERN><<<grid, 256, 0, s>>>(buf, 1);  // warm-up
+  DW_CUDA(cudaEventRecord(a, s));
+  k_red<PATTERN><<<grid, 256, 0, s>>>(buf, iters);
+  DW_CUDA(cudaEventRecord(b, s));
+  DW_CUDA(cudaEventSynchronize(b));
+  float ms = 0;
+  DW_CUDA(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return ms;
+}
+
+}  // namespace
+
+double microbench_red(int pattern, int64_t ops, cudaStream_t s) {
+  float* buf = nullptr;
+  DW_CUDA(cudaMalloc(&buf, (kRegionFloats + 1024) * sizeof(float)));
+  DW_CUDA(cudaMemsetAsync(buf, 0, (kRegionFloats + 1024) * sizeof(float), s));
+  const int grid = sm_count() * 8;
+  const int64_t warps = static_cast<int64_t>(grid) * 8;
+  const int reds_per_warp_inst = pattern == 2 ? 128 : (pattern == 3 ? 9 : 32);
+  int64_t iters64 = ops / (warps * reds_per_warp_inst);
+  if (iters64 < 1) iters64 = 1;
+  const int iters = static_cast<int>(iters64 > (1 << 30) ? (1 << 30) : iters64);
+  float ms = 0;
+  switch (pattern) {
+    case 0: ms = run<0>(buf, grid, iters, s); break;
+    case 1: ms = run<1>(buf, grid, iters, s); break;
+    case 2: ms = run<2>(buf, grid, iters, s); break;
+    default: ms = run<3>(buf, grid, iters, s); break;
+  }
+  DW_CUDA(cudaFree(buf));
+  const double reds = static_cast<double>(warps) * iters * reds_per_warp_inst;
+  return reds / (ms * 1e-3);
+}
+
+}  // namespace dw

@@ -1,0 +1,59 @@
+// Shared declarations of the tile-based Gaussian-splatting rasterizer.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/distwar.h"
+
+namespace dw {
+
+constexpr int kTile = 16;         // 16x16-pixel tiles, one 256-thread CTA each
+constexpr int kBlock = kTile * kTile;
+constexpr int kNParam = 9;        // mean2D.xy, conic.xyz, opacity, rgb
+
+// Kernel-parameter copy of dw_camera (lives in the constant bank).
+struct CamParams {
+  float vm[16];
+  float pm[16];
+  float tan_fovx, tan_fovy;
+  float bg[3];
+  float scale_modifier;
+  int W, H, tiles_x, tiles_y;
+};
+
+// In-tile thread t = warp*32 + lane covers pixel (8*(warp&1) + (lane&7),
+// 4*(warp>>1) + (lane>>3)): each warp owns an 8x4 block, the warp tiling of
+// the reference's workload model (workload.cpp:107-110), which maximises the
+// chance that all 32 lanes of a warp see the same Gaussian.
+__device__ __forceinline__ void tile_pixel(int tile, int t, int tiles_x, int* px, int* py) {
+  const int w = t >> 5, l = t & 31;
+  *px = (tile % tiles_x) * kTile + (w & 1) * 8 + (l & 7);
+  *py = (tile / tiles_x) * kTile + (w >> 1) * 4 + (l >> 3);
+}
+
+void launch_preprocess(int P, const float* means3D, const float* scales, const float* rotations,
+                       const float* opacities, const float* colors, const CamParams& cam,
+                       float2* means2D, float* depths, int* radii, float4* conic_opacity,
+                       float4* rgb, uint32_t* tiles_touched, cudaStream_t s);
+
+void launch_duplicate(int P, const float2* means2D, const float* depths, const int* radii,
+                      const uint64_t* offsets, const CamParams& cam, uint64_t* keys,
+                      uint32_t* values, cudaStream_t s);
+
+void launch_ranges(int64_t L, const uint64_t* keys, uint2* ranges, cudaStream_t s);
+
+void launch_forward_impl(const CamParams& cam, const uint2* ranges, const uint32_t* values,
+                         const float2* means2D, const float4* conic_opacity, const float4* rgb,
+                         const int* radii, float* final_T, uint32_t* n_contrib, float* out_color,
+                         cudaStream_t s);
+
+// counters (nullable): [0] += contributing (pixel, Gaussian) pairs, [1] += REDs.
+void launch_backward_impl(const CamParams& cam, const uint2* ranges, const uint32_t* values,
+                          const float2* means2D, const float4* co, const float4* rgb,
+                          const int* radii, const float* final_T, const uint32_t* n_contrib,
+                          const float* dL, int policy, int thr, float* grad,
+                          unsigned long long* counters, cudaStream_t s);
+
+}  // namespace dw

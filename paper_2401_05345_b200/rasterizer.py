@@ -1,0 +1,146 @@
+"""render_forward / render_backward over the C ABI (torch tensors as HBM).
+
+Mirrors the operator shape of a tile-based 3DGS rasterizer: one forward that
+projects, bins, sorts and blends a view, and one backward that scatters the
+per-pixel gradients into per-Gaussian gradients -- with the scatter done by a
+DISTWAR policy (``warpred.Policy``). torch is only the device-memory and
+stream plumbing: every tensor crosses the boundary as a raw pointer.
+
+Gradient buffer layout: float32 [P, 9] in Address order (reducers.hpp:19-23),
+params (mean2D.x, mean2D.y, conic.x, conic.y, conic.z, opacity, r, g, b).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+from .warpred import Policy, PolicyKind
+
+NPARAM = 9
+GRAD_NAMES = ("mean2D.x", "mean2D.y", "conic.x", "conic.y", "conic.z", "opacity", "r", "g", "b")
+
+# dw_rasterizer_buffer ids
+BUFFERS = {"means2D": (0, np.float32, 2), "depths": (1, np.float32, 1),
+           "radii": (2, np.int32, 1), "conic_opacity": (3, np.float32, 4),
+           "tiles_touched": (4, np.uint32, 1), "keys": (5, np.uint64, 1),
+           "values": (6, np.uint32, 1), "ranges": (7, np.uint32, 2),
+           "final_T": (8, np.float32, 1), "n_contrib": (9, np.uint32, 1)}
+
+
+def _ptr(t, name, dtype=None):
+    import torch
+
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}")
+    return t.data_ptr()
+
+
+def _stream(stream):
+    import torch
+
+    if stream is None:
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)
+
+
+class GaussianRasterizer:
+    """Owns one view's device state (``dw_rasterizer``)."""
+
+    def __init__(self):
+        h = C.c_void_p()
+        check(lib().dw_rasterizer_create(C.byref(h)))
+        self._h = h
+        self.P = 0
+        self.num_rendered = 0
+        self.camera = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and h.value and _lib._lib is not None:
+            _lib._lib.dw_rasterizer_free(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def render_forward(self, means3D, scales, rotations, opacities, colors, camera,
+                       out_color=None, radii=None, stream=None):
+        """Returns (out_color [3,H,W], radii [P], num_rendered)."""
+        import torch
+
+        f32 = torch.float32
+        P = int(means3D.shape[0])
+        if out_color is None:
+            out_color = torch.empty((3, camera.height, camera.width), dtype=f32,
+                                    device=means3D.device)
+        if radii is None:
+            radii = torch.empty((P,), dtype=torch.int32, device=means3D.device)
+        nr = C.c_int64()
+        cam = camera.to_c()
+        check(lib().dw_render_forward(
+            self._h, P, _ptr(means3D, "means3D", f32), _ptr(scales, "scales", f32),
+            _ptr(rotations, "rotations", f32), _ptr(opacities, "opacities", f32),
+            _ptr(colors, "colors", f32), C.byref(cam), _ptr(out_color, "out_color", f32),
+            _ptr(radii, "radii", torch.int32), C.byref(nr), _stream(stream)))
+        self.P, self.num_rendered, self.camera = P, nr.value, camera
+        return out_color, radii, nr.value
+
+    def render_backward(self, dL_dpixels, policy: Policy = Policy(PolicyKind.sw_b, 0),
+                        grad=None, count_pairs: bool = False, stream=None):
+        """Adds into grad [P, 9] (allocated zeroed if None). Returns grad, or
+        (grad, pairs) when count_pairs (a separate counting instantiation)."""
+        import torch
+
+        if grad is None:
+            grad = torch.zeros((self.P, NPARAM), dtype=torch.float32, device=dL_dpixels.device)
+        pairs = C.c_uint64()
+        check(lib().dw_render_backward(
+            self._h, _ptr(dL_dpixels, "dL_dpixels", torch.float32), int(policy.kind),
+            policy.threshold, _ptr(grad, "grad", torch.float32),
+            C.byref(pairs) if count_pairs else None, _stream(stream)))
+        return (grad, pairs.value) if count_pairs else grad
+
+    def buffer(self, name: str) -> np.ndarray:
+        """Host copy of an intermediate buffer (parity tests)."""
+        which, dtype, width = BUFFERS[name]
+        p, n = C.c_void_p(), C.c_int64()
+        check(lib().dw_rasterizer_buffer(self._h, which, C.byref(p), C.byref(n)))
+        out = np.zeros(n.value, dtype)
+        check(lib().dw_copy_to_host(out.ctypes.data, p, out.nbytes))
+        return out.reshape(-1, width) if width > 1 else out
+
+    def render_host(self, scene: dict, camera, dL_dpixels: np.ndarray,
+                    policy: Policy = Policy(PolicyKind.sw_b, 0)):
+        """End-to-end from host buffers (``dw_render_host``): returns
+        (image [3,H,W], grad [P,9]) as numpy."""
+        P = int(scene["means3D"].shape[0])
+        arrs = [np.ascontiguousarray(scene[k], np.float32)
+                for k in ("means3D", "scales", "rotations", "opacities", "colors")]
+        dL = np.ascontiguousarray(dL_dpixels, np.float32)
+        img = np.zeros((3, camera.height, camera.width), np.float32)
+        grad = np.zeros((P, NPARAM), np.float32)
+        cam = camera.to_c()
+        check(lib().dw_render_host(self._h, P, *[a.ctypes.data for a in arrs], C.byref(cam),
+                                   dL.ctypes.data, int(policy.kind), policy.threshold,
+                                   img.ctypes.data, grad.ctypes.data, None))
+        return img, grad
+
+
+def microbench_red(pattern: int, ops: int = 1 << 28, stream=None) -> float:
+    """Measured REDs/s: 0 distinct, 1 same-address warp, 2 v4, 3 DISTWAR 9-lane."""
+    out = C.c_double()
+    check(lib().dw_microbench_red(pattern, ops, C.byref(out),
+                                  None if stream is None else _stream(stream)))
+    return out.value

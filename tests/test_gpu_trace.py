@@ -1,0 +1,188 @@
+"""GPU parity of the trace-driven DISTWAR kernels against the oracle.
+
+Bar: on quantized traces (values k/256, < 65,793
+contributions per address) every policy's fp32 per-address sums equal the
+reference's f64 oracle_sum BIT-EXACTLY, and the number of REDs issued equals
+the reference's request count for the same (policy, threshold). Full-range
+values: relative 1e-6 of the per-address absolute sum (fp32 accumulation vs
+the reference's f64; reducers tests use 1e-6 relative, test_reducers.cpp:336).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+POLICIES = [(0, [0]), (1, [0, 1, 8, 16, 24, 32, 33]), (2, [0, 1, 8, 16, 24, 32, 33]), (3, [0])]
+
+
+def _spec(**kw):
+    from paper_2401_05345_b200 import warpred as wr
+
+    return wr.SceneSpec(**kw)
+
+
+def _check_trace(orc, tr_prod, tr_oracle, P, policies=POLICIES, exact=True):
+    from paper_2401_05345_b200 import warpred as wr
+
+    d = wr.DeviceTrace(tr_prod)
+    want, touched = orc.oracle_sum(tr_oracle, P)
+    absum = orc.oracle_sum(_abs_trace(tr_oracle), P)[0]
+    for kind, ts in policies:
+        for t in ts:
+            sums, m = wr.gpu_run(d, wr.Policy(wr.PolicyKind(kind), t))
+            _, counts = orc.apply_policy(tr_oracle, kind, t, P)
+            assert m.atomic_requests_to_l2 == counts["requests"], (kind, t)
+            assert m.contributions == tr_oracle.contributions()
+            got = sums.astype(np.float64)
+            if exact:
+                bad = np.flatnonzero(got != want)
+                assert bad.size == 0, (kind, t, bad[:5], got[bad[:5]], want[bad[:5]])
+            else:
+                tol = 1e-6 * np.maximum(1.0, absum) + 4 * np.finfo(np.float32).eps * absum
+                assert np.all(np.abs(got - want) <= tol), (kind, t)
+
+
+def _abs_trace(tr):
+    from oracle.bindings import Trace
+
+    return Trace(tr.spec, tr.warp_id, tr.iteration, tr.active, tr.prim, np.abs(tr.grads))
+
+
+@pytest.mark.parametrize("kw", [
+    dict(num_primitives=200, params_per_primitive=3, image_width=64, image_height=32,
+         locality=0.9, activity_prob=0.7, seed=911),
+    dict(num_primitives=300, params_per_primitive=9, image_width=128, image_height=64,
+         mean_fragment_span=24, fragments_per_pixel_mean=3, locality=0.6, activity_prob=0.5, seed=7),
+    dict(num_primitives=64, params_per_primitive=1, image_width=64, image_height=64,
+         locality=0.95, activity_prob=0.2, seed=2),
+    dict(num_primitives=80, params_per_primitive=2, image_width=64, image_height=64,
+         locality=0.5, activity_prob=1.0, seed=3),
+    dict(num_primitives=90, params_per_primitive=4, image_width=64, image_height=64,
+         locality=1.0, activity_prob=0.9, seed=4),
+    dict(num_primitives=120, params_per_primitive=5, image_width=48, image_height=32,
+         fragments_per_pixel_mean=2.0, locality=0.7, activity_prob=0.6, seed=55),   # generic N
+    dict(num_primitives=40, params_per_primitive=17, image_width=32, image_height=32,
+         locality=0.8, activity_prob=0.6, seed=56),                                 # N > 16
+])
+def test_quantized_sums_bit_exact_and_red_counts(orc, cuda, kw):
+    from oracle.bindings import scene
+    from paper_2401_05345_b200 import warpred as wr
+
+    tr = wr.generate(_spec(**kw))
+    otr = orc.generate(scene(**kw))
+    _check_trace(orc, tr, otr, kw["num_primitives"])
+
+
+def test_full_range_values_tolerance(orc, cuda):
+    from oracle.bindings import scene
+    from paper_2401_05345_b200 import warpred as wr
+
+    kw = dict(num_primitives=100, params_per_primitive=2, image_width=32, image_height=32,
+              locality=0.9, activity_prob=0.8, quantized_values=False, seed=414)
+    okw = dict(kw, quantized_values=0)
+    _check_trace(orc, wr.generate(_spec(**kw)), orc.generate(scene(**okw)), 100,
+                 policies=[(1, [8]), (2, [8]), (0, [0]), (3, [0])], exact=False)
+
+
+@pytest.mark.parametrize("name", ["small_default", "small_conservation_911", "small_n9_divergent",
+                                  "small_n1_lowact", "small_n5_generic"])
+def test_golden_traces(orc, cuda, name):
+    """Reference-written WRTRACEB files through the product loader and GPU."""
+    from paper_2401_05345_b200 import warpred as wr
+
+    g = json.load(open(os.path.join(GOLDEN, "golden.json")))["small"][name]
+    path = os.path.join(GOLDEN, g["file"])
+    tr = wr.Trace.load_binary(path)
+    otr = orc.load_binary(path)
+    P = tr.scene().num_primitives
+    d = wr.DeviceTrace(tr)
+    want, _ = orc.oracle_sum(otr, P)
+    for key, c in g["policies"].items():
+        name_, t = key.split(":")
+        sums, m = wr.gpu_run(d, wr.Policy(wr.parse_policy_kind(name_), int(t)))
+        assert m.atomic_requests_to_l2 == c["requests"], key
+        assert np.array_equal(sums.astype(np.float64), want), key
+
+
+@pytest.mark.parametrize("name", ["C1", "C4"])
+def test_baseline_family_full_size(orc, cuda, name):
+    """BASELINE-size traces: bit-exact sums and exact RED counts vs the golden
+    request counts the reference produced (tests/golden/golden.json)."""
+    from oracle.bindings import scene
+    from paper_2401_05345_b200 import warpred as wr
+
+    g = json.load(open(os.path.join(GOLDEN, "golden.json")))["family_t"][name]
+    tr = wr.generate(_spec(**g["spec"]))
+    assert tr.record_count() == g["records"]
+    otr = orc.generate(scene(**g["spec"]))
+    P = g["spec"]["num_primitives"]
+    want, _ = orc.oracle_sum(otr, P)
+    d = wr.DeviceTrace(tr)
+    for key, c in g["policies"].items():
+        k, t = key.split(":")
+        sums, m = wr.gpu_run(d, wr.Policy(wr.parse_policy_kind(k), int(t)))
+        assert m.atomic_requests_to_l2 == c["requests"], key
+        assert np.array_equal(sums.astype(np.float64), want), key
+
+
+def test_reduce_records_raw_pointers_and_stream(orc, cuda):
+    """dw_reduce_records on torch-owned buffers and a side stream; accumulates."""
+    import torch
+    from oracle.bindings import scene
+    from paper_2401_05345_b200 import warpred as wr
+
+    kw = dict(num_primitives=256, params_per_primitive=9, image_width=64, image_height=64,
+              locality=0.9, activity_prob=0.7, seed=5)
+    tr = wr.generate(_spec(**kw))
+    otr = orc.generate(scene(**kw))
+    a, p, g = tr.arrays()
+    R, n = a.shape[0], 9
+    da = torch.from_numpy(a.view(np.int32)).to(cuda)
+    dp = torch.from_numpy(p).to(cuda)
+    dv = torch.from_numpy(np.ascontiguousarray(g.transpose(0, 2, 1)).astype(np.float32)).to(cuda)
+    grad = torch.zeros(256 * n, dtype=torch.float32, device=cuda)
+    ctr = torch.zeros(1, dtype=torch.int64, device=cuda)
+    s = torch.cuda.Stream()
+    for _ in range(2):  # accumulates into grad
+        wr.reduce_records(da.data_ptr(), dp.data_ptr(), dv.data_ptr(), R, n, 256,
+                          wr.Policy(wr.PolicyKind.sw_b, 4), grad.data_ptr(), ctr.data_ptr(),
+                          s.cuda_stream)
+    s.synchronize()
+    want, _ = orc.oracle_sum(otr, 256)
+    assert np.array_equal(grad.cpu().numpy().astype(np.float64), 2 * want)
+    _, c = orc.apply_policy(otr, 2, 4, 256)
+    assert int(ctr.item()) == 2 * c["requests"]
+
+
+def test_tune_sweep(orc, cuda):
+    from paper_2401_05345_b200 import warpred as wr
+
+    kw = dict(num_primitives=10_000, params_per_primitive=9, image_width=256, image_height=256,
+              mean_fragment_span=48, fragments_per_pixel_mean=8, locality=0.99,
+              activity_prob=0.7, seed=1)
+    tr = wr.generate(_spec(**kw))
+    rep = wr.tune(tr, wr.PolicyFamily.sw_b, iteration=-1, reps=3)
+    assert set(rep.us_by_threshold) == set(range(33))
+    best = min(rep.us_by_threshold.values())
+    assert rep.us_by_threshold[rep.chosen] == best
+    assert all(rep.us_by_threshold[t] > best for t in range(rep.chosen))  # ties -> lowest
+    assert rep.reprofile_period == 2000
+    rep1 = wr.tune(tr, wr.PolicyFamily.sw_s, iteration=0, reps=1)
+    assert rep1.profile_iteration == 0
+
+
+def test_errors_follow_reference_conventions(cuda):
+    from paper_2401_05345_b200 import _lib
+    from paper_2401_05345_b200 import warpred as wr
+
+    tr = wr.generate(_spec(num_primitives=10, params_per_primitive=1))
+    d = wr.DeviceTrace(tr)
+    with pytest.raises(_lib.InvalidArgument, match="threshold"):
+        wr.gpu_run(d, wr.Policy(wr.PolicyKind.sw_b, 34))
+    with pytest.raises(_lib.InvalidArgument, match="hw_atomred"):
+        wr.gpu_run(d, wr.Policy(wr.PolicyKind.hw_atomred, 0))
