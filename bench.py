@@ -1,0 +1,452 @@
+"""DISTWAR hot-path benchmark (BASELINE.json metric: backward grad-contributions/s
+and ms/iter vs naive-atomic; L2-atomic roofline %).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Workload (config.workload): BASELINE configs[2] -- 1M synthetic Gaussians,
+1920x1080 -- the scene the north_star target is stated on, with a batch of
+`--views-per-gpu` orbit views resident per GPU. A STEP is the backward pass
+of the rasterizer over those views (DISTWAR SW-B, balancing threshold tuned
+on the box with the reference's sweep rule) plus, for N > 1, the NCCL
+all-reduce of the per-Gaussian gradient buffer. One unit = one gradient
+contribution = (contributing pixel, Gaussian, param), 9 per pair
+(SURVEY.md §8(d)). Weak scaling: every rank renders its own views.
+
+Printed on rank 0 as ONE JSON line; `value` = all ranks' contributions / the
+max over ranks of the device-timed steps; `e2e` = the same metric through the
+host-buffer C-ABI call dw_render_host (pinned H2D of the scene and dL/dpixel,
+forward + backward, D2H of image and gradients), the figure to compare with
+the reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = "c3_1m_1080p"  # paper_2401_05345_b200.scene.CONFIGS key (BASELINE configs[2])
+METRIC = "backward grad-contributions/sec & ms/iter vs naive-atomic; L2 atomic roofline %"
+UNIT = "contributions/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=WORKLOAD)
+    ap.add_argument("--views-per-gpu", type=int, default=4)
+    ap.add_argument("--threshold", default="auto", help="SW-B balancing threshold or 'auto'")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-tile-stride", type=int, default=1)
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------- utils
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.p = None
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100", "-i", str(gpu)], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        loaded = [s for s, p in zip(sm, power) if p > 200.0] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(power) if power else None}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def to_ocam(cam):
+    from oracle.bindings import Camera as OCam
+
+    oc = OCam()
+    cc = cam.to_c()
+    C.memmove(C.byref(oc), C.byref(cc), C.sizeof(oc))
+    return oc
+
+
+# ----------------------------------------------------------- CPU baselines
+def cpu_port_baseline(sc, cam, dL, stride: int) -> dict:
+    """The oracle port's CPU backward (gradient math + per-address
+    accumulation) on this box's host cores: the cpu_baseline of our arm."""
+    from oracle.bindings import Oracle
+
+    orc = Oracle()
+    threads = host_threads()
+    oc = to_ocam(cam)
+    st = orc.gs_prepare(sc, oc, threads)
+    try:
+        secs, pairs, _ = orc.gs_backward_timed(st, oc, dL, threads, stride)
+    finally:
+        orc.gs_free(st)
+    return {"value": 9 * pairs / secs, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"view 0 of {WORKLOAD}, every {stride} tile(s): {pairs} pairs "
+                      f"({9 * pairs} contributions) in {secs:.2f} s, oracle/gs_oracle.c "
+                      f"backward on {threads} threads"}
+
+
+def reference_arm(args) -> None:
+    """--impl reference: the reference's own CPU implementation of the path.
+    The reference (warpred) implements the reduction stage only
+    (reducers::apply_policy + per-address summation, oracle/_ref built from
+    /root/reference); the per-pair 3DGS gradient math it lacks is the oracle
+    port producing the per-warp WarpRecords it consumes. Each step: port
+    gradient math over a tile-strided sample of view 0 (all host threads) +
+    reference SW-B reduction of those records (all host threads)."""
+    from oracle.bindings import REF_SO, Oracle, Ref
+    from paper_2401_05345_b200.scene import CONFIGS, make_camera, make_dL_dpixels, make_scene
+
+    P, W, H, hc, _ = CONFIGS[args.workload]
+    sc = make_scene(P, W, H, seed=0, high_contention=hc)
+    cam = make_camera(W, H)
+    dL = make_dL_dpixels(W, H, seed=1)
+    orc = Oracle()
+    threads = host_threads()
+    oc = to_ocam(cam)
+    stride = max(args.cpu_tile_stride, 16)
+    have_ref = os.path.exists(REF_SO)
+    ref = Ref() if have_ref else None
+    st = orc.gs_prepare(sc, oc, threads)
+    times, contribs = [], 0
+    try:
+        for i in range(args.warmup + args.steps):
+            t_math, pairs, tap = orc.gs_backward_timed(st, oc, dL, threads, stride, tap=2)
+            if ref is not None:
+                h = ref.from_trace(tap)
+                t_red, c, _ = ref.time_policy(h, 2, 0, P, threads)
+                ref.free(h)
+            else:  # reference not built here: the oracle restatement of it
+                t0 = time.perf_counter()
+                orc.apply_policy(tap, 2, 0, P)
+                t_red, c = time.perf_counter() - t0, tap.contributions()
+            if i >= args.warmup:
+                times.append(t_math + t_red)
+                contribs += c
+    finally:
+        orc.gs_free(st)
+    total = sum(times)
+    v = contribs / total
+    kind = "reference" if have_ref else "port"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": args.workload, "gaussians": P, "width": W,
+                                        "height": H, "tile_stride": stride},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"every {stride}th tile of view 0 per step; "
+                                   "port gradient math + reference reducers::apply_policy(sw_b,0)"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- our arm
+def main() -> None:
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            reference_arm(args)
+        return
+
+    import numpy as np
+    import torch
+
+    from paper_2401_05345_b200 import warpred as wr
+    from paper_2401_05345_b200.rasterizer import GaussianRasterizer, microbench_red
+    from paper_2401_05345_b200.scene import CONFIGS, make_camera, make_dL_dpixels, make_scene, \
+        orbit_cameras
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    P, W, H, hc, _ = CONFIGS[args.workload]
+    V = args.views_per_gpu
+    sc = make_scene(P, W, H, seed=0, high_contention=hc)
+    cams = orbit_cameras(W, H, world * V)[rank * V:(rank + 1) * V] if world * V > 1 else \
+        [make_camera(W, H)]
+    t = {k: torch.from_numpy(v).to(dev) for k, v in sc.items()}
+    dLs = [torch.from_numpy(make_dL_dpixels(W, H, seed=1 + rank * V + i)).to(dev)
+           for i in range(V)]
+    stream = torch.cuda.current_stream()
+
+    # ---- forward: resident per-view states (timed for forward fps) -------
+    rasts = [GaussianRasterizer() for _ in range(V)]
+    fwd_ms = []
+    for i, r in enumerate(rasts):
+        for rep in range(2):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            r.render_forward(t["means3D"], t["scales"], t["rotations"], t["opacities"],
+                             t["colors"], cams[i])
+            e1.record()
+            torch.cuda.synchronize()
+            if rep == 1:
+                fwd_ms.append(e0.elapsed_time(e1))
+    grad = torch.zeros((P, 9), dtype=torch.float32, device=dev)
+
+    # ---- contributions per step (counting instantiation, untimed) --------
+    pairs_per_view = []
+    reds = {}
+    for r, dL in zip(rasts, dLs):
+        _, pairs = r.render_backward(dL, wr.Policy(wr.PolicyKind.native, 0), grad=grad,
+                                     count_pairs=True)
+        pairs_per_view.append(pairs)
+    contrib_rank = 9 * sum(pairs_per_view)
+
+    # ---- roofline microbenchmarks: measured L2 RED throughput ------------
+    red_peaks = {name: microbench_red(p, 1 << 28) for p, name in
+                 ((0, "distinct"), (1, "same_address_warp"), (2, "v4"), (3, "distwar_9lane"))}
+
+    # ---- balancing threshold: measured sweep 0..32 (tuner.cpp:29-52) -----
+    def time_backward(policy, reps=3, views=None):
+        views = range(V) if views is None else views
+        ms = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            grad.zero_()
+            e0.record()
+            for i in views:
+                rasts[i].render_backward(dLs[i], policy, grad=grad)
+            e1.record()
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        return statistics.median(ms)
+
+    sweep = {}
+    if args.threshold == "auto":
+        time_backward(wr.Policy(wr.PolicyKind.sw_b, 0), reps=2, views=[0])
+        best = None
+        for thr in range(33):
+            sweep[thr] = time_backward(wr.Policy(wr.PolicyKind.sw_b, thr), reps=3, views=[0])
+            if best is None or sweep[thr] < sweep[best]:
+                best = thr
+        thr = best
+        if dist is not None:  # one threshold for the job: rank 0's choice
+            b = torch.tensor([thr], device=dev)
+            dist.broadcast(b, 0)
+            thr = int(b.item())
+    else:
+        thr = int(args.threshold)
+    policy = wr.Policy(wr.PolicyKind.sw_b, thr)
+    from paper_2401_05345_b200 import _lib
+
+    def last_reds(r):
+        v = C.c_uint64()
+        _lib.check(_lib.lib().dw_rasterizer_last_reds(r.handle, C.byref(v)))
+        return v.value
+
+    reds_distwar = 0
+    for r, dL in zip(rasts, dLs):
+        r.render_backward(dL, policy, grad=grad, count_pairs=True)
+        reds_distwar += last_reds(r)
+
+    # ---- the timed loop ---------------------------------------------------
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def run_steps(pol, steps, warmup, sampler=None):
+        per_step, per_launch = [], []
+        for s in range(warmup + steps):
+            flush.fill_(float(s))  # L2 flush (256 MiB > 126 MB L2), outside the events
+            torch.cuda.synchronize()
+            if dist is not None:
+                dist.barrier()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * V + 2)]
+            ev[0].record()
+            grad.zero_()
+            for i in range(V):
+                ev[1 + 2 * i].record()
+                rasts[i].render_backward(dLs[i], pol, grad=grad)
+                ev[2 + 2 * i].record()
+            if dist is not None:
+                dist.all_reduce(grad)
+            ev[-1].record()
+            torch.cuda.synchronize()
+            if s >= warmup:
+                per_step.append(ev[0].elapsed_time(ev[-1]))
+                per_launch += [ev[1 + 2 * i].elapsed_time(ev[2 + 2 * i]) for i in range(V)]
+        total = sum(per_step)
+        if dist is not None:
+            tt = torch.tensor([total], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            total = float(tt.item())
+        return total, per_launch
+
+    sampler = ClockSampler(local)
+    time.sleep(0.3)
+    total_ms, launches = run_steps(policy, args.steps, args.warmup)
+    total_nv_ms, launches_nv = run_steps(wr.Policy(wr.PolicyKind.native, 0), args.steps, args.warmup)
+    clocks = sampler.stop()
+
+    ms_per_step = total_ms / args.steps
+    contrib_job = contrib_rank * world
+    if dist is not None:
+        c = torch.tensor([contrib_rank], device=dev, dtype=torch.float64)
+        dist.all_reduce(c)
+        contrib_job = float(c.item())
+    value = contrib_job * args.steps / (total_ms * 1e-3)
+    naive_value = contrib_job * args.steps / (total_nv_ms * 1e-3)
+
+    # ---- e2e through the host-buffer C-ABI call (dw_render_host) ---------
+    pin = {k: torch.from_numpy(v).pin_memory() for k, v in sc.items()}
+    dL_h = [d.cpu().pin_memory() for d in dLs]
+    img_h = torch.empty((3, H, W), dtype=torch.float32).pin_memory()
+    grad_h = torch.empty((P, 9), dtype=torch.float32).pin_memory()
+    e2e_r = GaussianRasterizer()
+    cam_c = [c.to_c() for c in cams]
+    lib = _lib.lib()
+
+    def e2e_view(i):
+        _lib.check(lib.dw_render_host(
+            e2e_r.handle, P, *[pin[k].data_ptr() for k in ("means3D", "scales", "rotations",
+                                                           "opacities", "colors")],
+            C.byref(cam_c[i]), dL_h[i].data_ptr(), int(policy.kind), policy.threshold,
+            img_h.data_ptr(), grad_h.data_ptr(), C.c_void_p(stream.cuda_stream)))
+
+    for i in range(V):
+        e2e_view(i)  # warm-up (allocations)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        for i in range(V):
+            e2e_view(i)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if dist is not None:
+        tt = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e_value = contrib_job * args.e2e_steps / e2e_s
+    h2d = sum(v.nbytes for v in sc.values()) * V + 3 * H * W * 4 * V
+    d2h = (3 * H * W * 4 + P * 9 * 4) * V
+
+    # ---- roofline of the dominant kernel (render_backward, one launch/view)
+    hbm_peak, peak_src = measured_peaks()
+    mean_launch_ms = statistics.mean(launches)
+    inst = statistics.mean(r.num_rendered for r in rasts)
+    vis = int(sum(int((r.buffer("radii") > 0).sum()) for r in rasts) / V)
+    alg_bytes = 4 * inst + 44 * vis + 20 * H * W + 36 * P
+    achieved_gbs = alg_bytes / (mean_launch_ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "backward_dram_bytes.json")
+    if os.path.exists(prof):
+        traffic = json.load(open(prof)).get(args.workload)
+    reds_per_launch = reds_distwar / V
+    red_rate = reds_per_launch / (mean_launch_ms * 1e-3)
+    naive_launch_ms = statistics.mean(launches_nv)
+    naive_red_rate = (contrib_rank / V) / (naive_launch_ms * 1e-3)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_port_baseline(sc, cams[0], make_dL_dpixels(W, H, seed=1), args.cpu_tile_stride)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.workload, "gaussians": P, "width": W, "height": H,
+                       "views_per_gpu": V, "policy": "sw_b", "threshold": thr,
+                       "parallelism": f"dp{world} (views) + NCCL all-reduce of grad[P,9]"
+                       if world > 1 else "dp1",
+                       "l2": "flushed between steps (256 MiB write, outside the events)"},
+            "gpu_launches": args.steps * V,
+            "clocks": clocks,
+            "naive": {"value": naive_value, "ms_per_step": total_nv_ms / args.steps,
+                      "speedup_distwar_vs_naive": naive_value and value / naive_value},
+            "forward": {"ms_per_view": statistics.mean(fwd_ms),
+                        "fps": 1e3 / statistics.mean(fwd_ms)},
+            "contributions_per_step": contrib_job, "pairs_per_view": pairs_per_view,
+            "instances_per_view": [r.num_rendered for r in rasts],
+            "threshold_sweep_ms": sweep,
+            "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": achieved_gbs / hbm_peak, "traffic": traffic,
+                         "kernel": "k_backward<sw_b>", "alg_bytes_per_launch": alg_bytes,
+                         "mean_launch_ms": mean_launch_ms, "peak_source": peak_src},
+            "roofline_l2_atomic": {
+                "distwar": {"reds_per_launch": reds_per_launch, "achieved": red_rate,
+                            "peak": red_peaks["distwar_9lane"],
+                            "frac": red_rate / red_peaks["distwar_9lane"]},
+                "naive": {"reds_per_launch": contrib_rank / V, "achieved": naive_red_rate,
+                          "peak": red_peaks["same_address_warp"],
+                          "frac": naive_red_rate / red_peaks["same_address_warp"]},
+                "measured_red_peaks_per_s": red_peaks, "unit": "REDs/s"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+                    "path": "dw_render_host (pinned H2D scene+dL, forward, backward, D2H image+grad)"},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

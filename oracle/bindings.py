@@ -319,7 +319,7 @@ class Oracle:
                 gabs = np.zeros(P * NPARAM, np.float64)
                 pairs = C.c_int64()
                 rc = L.gs_backward(st, C.byref(cam), dL.ctypes.data, grad.ctypes.data,
-                                   gabs.ctypes.data, threads, tile_stride, int(tap),
+                                   gabs.ctypes.data, threads, tile_stride, 1 if tap else 0,
                                    C.byref(pairs))
                 if rc:
                     raise RuntimeError(L.gs_last_error().decode())
@@ -337,27 +337,46 @@ class Oracle:
         finally:
             L.gs_state_free(st)
 
-    def gs_backward_timed(self, scene, cam, dL_dpixels, threads, tile_stride):
-        """(seconds, pairs) of the CPU backward on a strided tile sample."""
-        import time
+    def gs_prepare(self, scene, cam, threads):
+        """CPU forward; returns an opaque state for gs_backward_timed."""
         L = self.L
         st = L.gs_state_new()
         P = int(scene["means3D"].shape[0])
         ins = [np.ascontiguousarray(scene[k], np.float32)
                for k in ("means3D", "scales", "rotations", "opacities", "colors")]
-        try:
-            if L.gs_forward(st, P, *[a.ctypes.data for a in ins], C.byref(cam), threads):
-                raise RuntimeError(L.gs_last_error().decode())
-            dL = np.ascontiguousarray(dL_dpixels, np.float32)
-            grad = np.zeros(P * NPARAM, np.float64)
-            pairs = C.c_int64()
-            t0 = time.perf_counter()
-            if L.gs_backward(st, C.byref(cam), dL.ctypes.data, grad.ctypes.data, None,
-                             threads, tile_stride, 0, C.byref(pairs)):
-                raise RuntimeError(L.gs_last_error().decode())
-            return time.perf_counter() - t0, int(pairs.value)
-        finally:
+        if L.gs_forward(st, P, *[a.ctypes.data for a in ins], C.byref(cam), threads):
             L.gs_state_free(st)
+            raise RuntimeError(L.gs_last_error().decode())
+        return st
+
+    def gs_free(self, st):
+        self.L.gs_state_free(st)
+
+    def gs_backward_timed(self, st, cam, dL_dpixels, threads, tile_stride, tap=0):
+        """(seconds, pairs, tapped Trace or None) of the CPU backward over a
+        strided tile sample. tap=0 accumulates gradients (the port's whole
+        backward); tap=2 only emits the per-warp WarpRecords (gradient math
+        without accumulation, for the reference's reducers to consume)."""
+        import time
+        L = self.L
+        P = st.contents.P
+        dL = np.ascontiguousarray(dL_dpixels, np.float32)
+        grad = np.zeros(P * NPARAM, np.float64)
+        pairs = C.c_int64()
+        t0 = time.perf_counter()
+        if L.gs_backward(st, C.byref(cam), dL.ctypes.data, grad.ctypes.data, None,
+                         threads, tile_stride, tap, C.byref(pairs)):
+            raise RuntimeError(L.gs_last_error().decode())
+        dt = time.perf_counter() - t0
+        tr = None
+        if tap:
+            s = st.contents
+            r = s.tap_count
+            tr = Trace(scene_spec_for(P, NPARAM), _arr(s.tap_warp, r, np.int32),
+                       _arr(s.tap_iter, r, np.int32), _arr(s.tap_active, r, np.uint32),
+                       _arr(s.tap_prim, 32 * r, np.int32),
+                       _arr(s.tap_grads, 32 * NPARAM * r, np.float64))
+        return dt, int(pairs.value), tr
 
 
 def scene_spec_for(num_prims: int, n: int) -> SceneSpec:

@@ -222,6 +222,7 @@ typedef struct {
   double* gabs;
   int tid, nthreads, stride, tap;
   int64_t pairs;
+  gs_state tapbuf; /* per-thread tap records, merged after join */
 } job;
 
 static void forward_tile(gs_state* s, const gs_camera* cam, int tile) {
@@ -438,13 +439,14 @@ static void backward_warp(job* jb, int tile, int w) {
     for (int l = 0; l < 32; ++l) {
       if (!(active >> l & 1u)) continue;
       jb->pairs++;
+      if (jb->tap == 2) continue; /* records only */
       for (int p = 0; p < GS_NPARAM; ++p) {
         const double v = g[l * GS_NPARAM + p];
         jb->grad[(size_t)id * GS_NPARAM + p] += v;
         if (jb->gabs) jb->gabs[(size_t)id * GS_NPARAM + p] += fabs(v);
       }
     }
-    if (jb->tap) tap_push(s, tile * 8 + w, iter, active, (int32_t)id, g);
+    if (jb->tap) tap_push(&jb->tapbuf, tile * 8 + w, iter, active, (int32_t)id, g);
   }
 }
 
@@ -463,7 +465,6 @@ int gs_backward(gs_state* s, const gs_camera* cam, const float* dL_dpixels,
   if (!s->ranges) return fail("gs_backward before gs_forward");
   if (threads < 1) threads = 1;
   if (threads > 64) threads = 64;
-  if (tap && threads != 1) return fail("tap requires threads == 1");
   if (tile_stride < 1) tile_stride = 1;
   free_tap(s);
   const size_t words = (size_t)s->P * GS_NPARAM;
@@ -490,6 +491,13 @@ int gs_backward(gs_state* s, const gs_camera* cam, const float* dL_dpixels,
   for (int t = 0; t < threads; ++t) {
     if (threads > 1) pthread_join(th[t], NULL);
     pairs += jobs[t].pairs;
+    if (tap) {
+      gs_state* b = &jobs[t].tapbuf;
+      for (int64_t r = 0; r < b->tap_count; ++r)
+        tap_push(s, b->tap_warp[r], b->tap_iter[r], b->tap_active[r], b->tap_prim[r * 32],
+                 b->tap_grads + r * 32 * GS_NPARAM);
+      free_tap(b);
+    }
     if (t == 0) continue;
     for (size_t i = 0; i < words; ++i) grad[i] += jobs[t].grad[i];
     if (grad_abs)

@@ -59,8 +59,9 @@ int gs_forward(gs_state* s, int32_t P, const float* means3D, const float* scales
 
 /* backward blend; grad/grad_abs are P*9 f64 (grad_abs = sum of |terms|, for
  * the tolerance bound). tile_stride>1 processes every k-th tile only (bounded
- * CPU-baseline sample). tap!=0 records per-warp WarpRecords (threads must be
- * 1). pairs_out = number of (pixel, Gaussian) pairs that contributed. */
+ * CPU-baseline sample). tap: 0 accumulate only; 1 accumulate and record the
+ * per-warp WarpRecords (per-thread buffers, appended in thread order); 2
+ * record only (grad untouched). pairs_out = number of (pixel, Gaussian) pairs that contributed. */
 int gs_backward(gs_state* s, const gs_camera* cam, const float* dL_dpixels,
                 double* grad, double* grad_abs, int threads, int tile_stride,
                 int tap, int64_t* pairs_out);

@@ -1,0 +1,35 @@
+"""Data parallelism over camera views.
+
+Every rank owns a contiguous block of the view batch, renders and
+back-propagates its views into ONE local gradient buffer [P, 9] (the backward
+accumulates), and the ranks then combine the buffers with a single all-reduce
+(NCCL over NVLink on the GPU path; gloo in the CPU tests). Scene parameters are
+replicated; there is no other exchange -- views are independent.
+"""
+from __future__ import annotations
+
+from typing import Callable, Sequence
+
+
+def shard_views(num_views: int, world: int, rank: int) -> range:
+    """Contiguous block of view ids for `rank`; sizes differ by at most one."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("invalid world/rank")
+    base, extra = divmod(num_views, world)
+    start = rank * base + min(rank, extra)
+    return range(start, start + base + (1 if rank < extra else 0))
+
+
+def view_parallel_backward(backward_view: Callable, views: Sequence, grad, group=None,
+                           all_reduce: bool = True):
+    """Run `backward_view(view, grad)` (which ADDS into grad) for this rank's
+    shard of `views`, then sum `grad` over the group. Returns grad."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    for i in shard_views(len(views), world, rank):
+        backward_view(views[i], grad)
+    if all_reduce and world > 1:
+        dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=group)
+    return grad
