@@ -51,7 +51,45 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-tile-stride", type=int, default=1)
+    ap.add_argument("--no-trace-family", action="store_true")
     return ap.parse_args()
+
+
+# SURVEY.md §8(d) trace family T, config C3 (reference-pinned workload)
+TRACE_C3 = dict(num_primitives=1_000_000, params_per_primitive=9, image_width=1920,
+                image_height=1080, mean_fragment_span=48.0, fragments_per_pixel_mean=8.0,
+                locality=0.99, activity_prob=0.7, seed=1)
+
+
+def trace_family() -> dict:
+    """The reference's own workload (WarpRecord trace C3, byte-identical to
+    workload::generate) through the trace-driven kernels: measured threshold
+    sweep (dw_tune) and one device-timed launch per policy."""
+    from paper_2401_05345_b200 import warpred as wr
+
+    tr = wr.generate(wr.SceneSpec(**TRACE_C3))
+    rep = wr.tune(tr, wr.PolicyFamily.sw_b, iteration=-1, reps=3)
+    rep_s = wr.tune(tr, wr.PolicyFamily.sw_s, iteration=-1, reps=1)
+    d = wr.DeviceTrace(tr)
+    hbm, _ = measured_peaks()
+    alg = d.records * (132 + 128 * d.params) + 4 * d.num_primitives * d.params
+    out = {"config": "C3 trace: " + json.dumps(TRACE_C3), "records": d.records,
+           "sw_b_threshold": rep.chosen, "sw_s_threshold": rep_s.chosen,
+           "sw_b_sweep_us": {t: round(v, 2) for t, v in rep.us_by_threshold.items()}}
+    for name, pol in (("native", wr.Policy(wr.PolicyKind.native, 0)),
+                      ("sw_b", wr.Policy(wr.PolicyKind.sw_b, rep.chosen)),
+                      ("sw_s", wr.Policy(wr.PolicyKind.sw_s, rep_s.chosen)),
+                      ("cccl", wr.Policy(wr.PolicyKind.cccl, 0))):
+        best = None
+        for _ in range(3):
+            _, m = wr.gpu_run(d, pol, want_sums=False)
+            best = m if best is None or m.kernel_ms < best.kernel_ms else best
+        out[name] = {"ms": best.kernel_ms, "contributions": best.contributions,
+                     "value": best.contributions / (best.kernel_ms * 1e-3),
+                     "reds": best.atomic_requests_to_l2,
+                     "hbm_frac": alg / (best.kernel_ms * 1e-3) / (hbm * 1e9)}
+    out["speedup_sw_b_vs_native"] = out["native"]["ms"] / out["sw_b"]["ms"]
+    return out
 
 
 # --------------------------------------------------------------------- utils
@@ -220,7 +258,8 @@ def main() -> None:
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
-    if world > 1:
+    # DW_BENCH_FORCE_DIST=1 (under torchrun) exercises the NCCL path at N = 1
+    if world > 1 or os.environ.get("DW_BENCH_FORCE_DIST") == "1":
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
@@ -351,31 +390,36 @@ def main() -> None:
     value = contrib_job * args.steps / (total_ms * 1e-3)
     naive_value = contrib_job * args.steps / (total_nv_ms * 1e-3)
 
-    # ---- e2e through the host-buffer C-ABI call (dw_render_host) ---------
+    # ---- e2e through the host-buffer C-ABI call (dw_render_views_host) ---
+    # per step: pinned H2D of the scene + the V views' dL/dpixel, forward +
+    # backward of every view, D2H of the V images and of the gradients; at
+    # N > 1 the host gradients are summed across ranks (H2D, NCCL, D2H).
+    from paper_2401_05345_b200.rasterizer import render_views_host
+
     pin = {k: torch.from_numpy(v).pin_memory() for k, v in sc.items()}
-    dL_h = [d.cpu().pin_memory() for d in dLs]
-    img_h = torch.empty((3, H, W), dtype=torch.float32).pin_memory()
+    dL_h = torch.stack([d.cpu() for d in dLs]).pin_memory()
+    img_h = torch.empty((V, 3, H, W), dtype=torch.float32).pin_memory()
     grad_h = torch.empty((P, 9), dtype=torch.float32).pin_memory()
     e2e_r = GaussianRasterizer()
-    cam_c = [c.to_c() for c in cams]
-    lib = _lib.lib()
+    scene_ptrs = [pin[k].data_ptr() for k in ("means3D", "scales", "rotations", "opacities",
+                                               "colors")]
 
-    def e2e_view(i):
-        _lib.check(lib.dw_render_host(
-            e2e_r.handle, P, *[pin[k].data_ptr() for k in ("means3D", "scales", "rotations",
-                                                           "opacities", "colors")],
-            C.byref(cam_c[i]), dL_h[i].data_ptr(), int(policy.kind), policy.threshold,
-            img_h.data_ptr(), grad_h.data_ptr(), C.c_void_p(stream.cuda_stream)))
+    def e2e_step():
+        render_views_host(e2e_r, scene_ptrs, P, cams, dL_h.data_ptr(), policy, img_h.data_ptr(),
+                          grad_h.data_ptr(), stream)
+        if dist is not None:
+            g = grad_h.to(dev, non_blocking=True)
+            dist.all_reduce(g)
+            grad_h.copy_(g)
+            torch.cuda.synchronize()
 
-    for i in range(V):
-        e2e_view(i)  # warm-up (allocations)
+    e2e_step()  # warm-up (allocations)
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
-        for i in range(V):
-            e2e_view(i)
+        e2e_step()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if dist is not None:
@@ -383,8 +427,8 @@ def main() -> None:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
     e2e_value = contrib_job * args.e2e_steps / e2e_s
-    h2d = sum(v.nbytes for v in sc.values()) * V + 3 * H * W * 4 * V
-    d2h = (3 * H * W * 4 + P * 9 * 4) * V
+    h2d = sum(v.nbytes for v in sc.values()) + 3 * H * W * 4 * V + (P * 9 * 4 if world > 1 else 0)
+    d2h = 3 * H * W * 4 * V + P * 9 * 4 * (2 if world > 1 else 1)
 
     # ---- roofline of the dominant kernel (render_backward, one launch/view)
     hbm_peak, peak_src = measured_peaks()
@@ -401,6 +445,10 @@ def main() -> None:
     red_rate = reds_per_launch / (mean_launch_ms * 1e-3)
     naive_launch_ms = statistics.mean(launches_nv)
     naive_red_rate = (contrib_rank / V) / (naive_launch_ms * 1e-3)
+
+    tfam = None
+    if rank == 0 and not args.no_trace_family:
+        tfam = trace_family()
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -439,8 +487,11 @@ def main() -> None:
                 "measured_red_peaks_per_s": red_peaks, "unit": "REDs/s"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-                    "path": "dw_render_host (pinned H2D scene+dL, forward, backward, D2H image+grad)"},
+                    "path": "dw_render_views_host: pinned H2D scene + V dL/dpixel, forward + "
+                            "backward of V views, D2H V images + grad (copy streams "
+                            "double-buffered against compute)"},
             "cpu_baseline": cpu,
+            "trace_family": tfam,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

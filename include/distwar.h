@@ -207,6 +207,19 @@ dw_status dw_render_host(dw_rasterizer* r, int32_t P, const float* means3D,
  * views without the caller linking the CUDA runtime). */
 dw_status dw_copy_to_host(void* host_dst, const void* device_src, size_t bytes);
 
+/* One training step's rasterization from host buffers: the scene is uploaded
+ * once, then `num_views` cameras (same image size) are rendered and
+ * back-propagated into ONE gradient buffer (grad[P*9], host, overwritten).
+ * dL_dpixels is num_views*3*H*W (host); out_images (host, nullable) receives
+ * num_views*3*H*W. Per-view uploads/downloads run on two internal copy
+ * streams double-buffered against `stream` (overlap needs pinned memory). */
+dw_status dw_render_views_host(dw_rasterizer* r, int32_t P, const float* means3D,
+                               const float* scales, const float* rotations,
+                               const float* opacities, const float* colors,
+                               const dw_camera* cams, int32_t num_views,
+                               const float* dL_dpixels, dw_policy_kind policy, int32_t threshold,
+                               float* out_images, float* grad, void* stream);
+
 /* --------------------------------------------------- roofline microbenchmarks */
 /* Measured f32 RED throughput (REDs/s) for `pattern`: 0 distinct addresses,
  * 1 all 32 lanes of a warp on one address (the naive pattern), 2 distinct

@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "csrc", "libdistwar.so")
+# DISTWAR_LIB selects an alternative in-tree build (A/B experiments); default
+# is the one __graft_entry__.build() produces.
+LIB_PATH = os.environ.get("DISTWAR_LIB") or os.path.join(HERE, "csrc", "libdistwar.so")
 
 DW_OK, DW_ERR_INVALID_ARGUMENT, DW_ERR_IO, DW_ERR_RUNTIME = 0, 1, 2, 3
 
@@ -115,6 +117,8 @@ SIGNATURES = {
     "dw_rasterizer_buffer": (C.c_int, [vp, i32, C.POINTER(vp), C.POINTER(i64)]),
     "dw_render_host": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, C.POINTER(CameraC), vp, C.c_int,
                                  i32, vp, vp, vp]),
+    "dw_render_views_host": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, vp, i32, vp, C.c_int, i32,
+                                       vp, vp, vp]),
     "dw_copy_to_host": (C.c_int, [vp, vp, C.c_size_t]),
     "dw_microbench_red": (C.c_int, [i32, i64, C.POINTER(C.c_double), vp]),
 }

@@ -25,6 +25,10 @@ void raster_buffer(const dw_rasterizer* r, int which, const void** p, int64_t* c
 void raster_host(dw_rasterizer* r, int32_t P, const float* m, const float* sc, const float* rot,
                  const float* op, const float* col, const dw_camera* cam, const float* dL,
                  int policy, int thr, float* out_color, float* grad, cudaStream_t s);
+void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float* sc,
+                       const float* rot, const float* op, const float* col, const dw_camera* cams,
+                       int32_t V, const float* dL, int policy, int thr, float* out_images,
+                       float* grad, cudaStream_t s);
 dw_rasterizer* raster_new();
 void raster_delete(dw_rasterizer* r);
 }  // namespace dw
@@ -434,6 +438,24 @@ dw_status dw_render_host(dw_rasterizer* r, int32_t P, const float* means3D, cons
     check_policy(policy, threshold);
     dw::raster_host(r, P, means3D, scales, rotations, opacities, colors, cam, dL_dpixels, policy,
                     threshold, out_color, grad, dw::as_stream(stream));
+    return DW_OK;
+  });
+}
+
+dw_status dw_render_views_host(dw_rasterizer* r, int32_t P, const float* means3D,
+                               const float* scales, const float* rotations,
+                               const float* opacities, const float* colors,
+                               const dw_camera* cams, int32_t num_views,
+                               const float* dL_dpixels, dw_policy_kind policy, int32_t threshold,
+                               float* out_images, float* grad, void* stream) {
+  if (!r || !cams || !dL_dpixels || !grad ||
+      (P > 0 && (!means3D || !scales || !rotations || !opacities || !colors)))
+    return fail_invalid("null argument");
+  return guarded([&] {
+    check_policy(policy, threshold);
+    dw::raster_views_host(r, P, means3D, scales, rotations, opacities, colors, cams, num_views,
+                          dL_dpixels, policy, threshold, out_images, grad,
+                          dw::as_stream(stream));
     return DW_OK;
   });
 }

@@ -109,7 +109,9 @@ __device__ __forceinline__ int bfly_slot(int lane, bool* issuer) {
 // ---------------------------------------------------------------------------
 // Policies. `base` is this lane's &grad[idx * N]; `v` its N values (zeros
 // when inactive, as the SW-B convention requires); `active` its was_active
-// flag; `nred` counts the REDs this lane issues when COUNT.
+// flag; `nred` counts the REDs this lane issues when COUNT. reduce_bfly
+// takes the lane's (slot, issuer) from bfly_slot<N>(), computed once per
+// kernel.
 
 template <int N, bool COUNT>
 __device__ __forceinline__ void native_atomics(float* base, const float (&v)[N], bool active,
@@ -128,7 +130,7 @@ __device__ __forceinline__ void native_atomics(float* base, const float (&v)[N],
 template <int N, bool COUNT, bool UNIFORM>
 __device__ __forceinline__ void reduce_bfly(int idx, float* grad, float (&v)[N], int thr,
                                             bool active, int lane, uint32_t& nred,
-                                            unsigned ballot) {
+                                            unsigned ballot, int slot, bool issuer) {
   bool same = true;
   int idx0 = idx;
   if (!UNIFORM) {
@@ -138,10 +140,8 @@ __device__ __forceinline__ void reduce_bfly(int idx, float* grad, float (&v)[N],
   const int cnt = __popc(ballot);
   if (same && cnt > 0 && cnt >= thr) {
     ReduceScatter<N, 16>::run(v, lane);
-    bool issuer;
-    const int p = bfly_slot<N>(lane, &issuer);
     if (issuer) {
-      red_add(grad + static_cast<int64_t>(idx0) * N + p, v[0]);
+      red_add(grad + static_cast<int64_t>(idx0) * N + slot, v[0]);
       if (COUNT) nred += 1;
     }
   } else {

@@ -3,11 +3,11 @@
 // Per-view device state lives in grow-only HBM buffers owned by the
 // dw_rasterizer handle, so a training loop re-renders without reallocating:
 //   per Gaussian: means2D f32x2, depth, radius, conic+opacity f32x4,
-//                 rgb f32x4, tiles_touched u32, inclusive offsets u64
-//   per instance: keys u64 x2, values u32 x2 (double-buffered radix sort)
+//                 rgb f32x4, tiles_touched u32, depth keys u32 x2 + ids u32
+//                 x2 (double-buffered depth sort), inclusive offsets u64
+//   per instance: tile ids u32 x2, values u32 x2 (double-buffered tile sort)
 //   per tile:     ranges u32x2;  per pixel: final_T f32, n_contrib u32
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
+// Binning uses the hand-written sort of raster_sort.cu (no library calls).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -47,34 +47,56 @@ struct dw_rasterizer {
   uint32_t* tiles_touched = nullptr;
   uint64_t* offsets = nullptr;
 
-  size_t cap_i = 0, cap_i2 = 0, cap_i3 = 0, cap_i4 = 0;
-  uint64_t* keys_in = nullptr;
-  uint64_t* keys = nullptr;
-  uint32_t* vals_in = nullptr;
-  uint32_t* vals = nullptr;
+  size_t cap_d[4] = {0};
+  uint32_t* dkey[2] = {nullptr, nullptr};  // depth keys (double buffer)
+  uint32_t* dids[2] = {nullptr, nullptr};  // Gaussian ids (double buffer)
+  const uint32_t* order = nullptr;         // Gaussians in (depth, id) order
+
+  size_t cap_i[4] = {0};
+  uint32_t* itile[2] = {nullptr, nullptr};  // instance tile ids (double buffer)
+  uint32_t* ivals[2] = {nullptr, nullptr};  // instance Gaussian ids
+  uint32_t* tiles_sorted = nullptr;
+  uint32_t* vals = nullptr;                 // sorted Gaussian ids (the lists)
 
   size_t cap_t = 0, cap_px = 0, cap_px2 = 0;
   uint2* ranges = nullptr;
   float* final_T = nullptr;
   uint32_t* n_contrib = nullptr;
 
-  size_t cap_tmp = 0;
+  size_t cap_tmp = 0, cap_scan = 0, cap_keys = 0;
   unsigned char* tmp = nullptr;
+  unsigned char* scan_tmp = nullptr;
+  uint64_t* keys_dbg = nullptr;            // u64 keys, materialised on request
   unsigned long long* counters = nullptr;  // [pairs, reds]
   uint64_t* h_total = nullptr;             // pinned
 
-  // host-entry scratch (dw_render_host)
-  size_t cap_h[8] = {0};
-  float* h_bufs[8] = {nullptr};
+  // host-entry scratch (dw_render_host / dw_render_views_host)
+  size_t cap_h[12] = {0};
+  float* h_bufs[12] = {nullptr};
+  cudaStream_t s_in = nullptr, s_out = nullptr;  // copy streams of the batched host path
+  cudaEvent_t ev[7] = {};
+
+  void ensure_streams() {
+    if (s_in) return;
+    DW_CUDA(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
+    DW_CUDA(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+    for (auto& e : ev) DW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
 
   ~dw_rasterizer() {
-    void* ps[] = {means2D, depths, radii, conic_opacity, rgb, tiles_touched, offsets, keys_in,
-                  keys, vals_in, vals, ranges, final_T, n_contrib, tmp, counters};
+    void* ps[] = {means2D, depths, radii, conic_opacity, rgb, tiles_touched, offsets, dkey[0],
+                  dkey[1], dids[0], dids[1], itile[0], itile[1], ivals[0], ivals[1], ranges,
+                  final_T, n_contrib, tmp, scan_tmp, keys_dbg, counters};
     for (void* p : ps)
       if (p) cudaFree(p);
     for (float* p : h_bufs)
       if (p) cudaFree(p);
     if (h_total) cudaFreeHost(h_total);
+    if (s_in) {
+      cudaStreamDestroy(s_in);
+      cudaStreamDestroy(s_out);
+      for (auto e : ev) cudaEventDestroy(e);
+    }
   }
 
   void forward(int32_t P_, const float* means3D, const float* scales, const float* rotations,
@@ -115,14 +137,22 @@ struct dw_rasterizer {
     if (!counters) DW_CUDA(cudaMalloc(&counters, 2 * sizeof(unsigned long long)));
     if (!h_total) DW_CUDA(cudaMallocHost(&h_total, sizeof(uint64_t)));
 
+    for (int b = 0; b < 2; ++b) {
+      grow(dkey[b], cap_d[b], np);
+      grow(dids[b], cap_d[2 + b], np);
+    }
+    grow(scan_tmp, cap_scan, dw::scan_temp_bytes(P));
+
     dw::launch_preprocess(P, means3D, scales, rotations, opacities, colors, cam, means2D, depths,
                           radii, conic_opacity, rgb, tiles_touched, s);
     num_rendered = 0;
     if (P > 0) {
-      size_t scan_bytes = 0;
-      DW_CUDA(cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, tiles_touched, offsets, P, s));
-      ensure_tmp(scan_bytes);
-      DW_CUDA(cub::DeviceScan::InclusiveSum(tmp, scan_bytes, tiles_touched, offsets, P, s));
+      // 1. Gaussians in (depth, id) order: stable 32-bit LSD sort
+      dw::launch_depth_keys(P, depths, radii, dkey[0], dids[0], s);
+      ensure_tmp(dw::radix_sort_temp_bytes(P));
+      order = dids[dw::radix_sort_pairs(dkey, dids, P, 32, tmp, s)];
+      // instance offsets in that order
+      dw::inclusive_scan_gather(tiles_touched, order, P, offsets, scan_tmp, s);
       DW_CUDA(cudaMemcpyAsync(h_total, offsets + P - 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
       DW_CUDA(cudaStreamSynchronize(s));
       num_rendered = static_cast<int64_t>(*h_total);
@@ -130,21 +160,22 @@ struct dw_rasterizer {
     if (num_rendered >= (int64_t(1) << 32))
       throw std::runtime_error("more than 2^32 tile instances");
     const size_t ni = static_cast<size_t>(std::max<int64_t>(num_rendered, 1));
-    grow(keys_in, cap_i, ni);
-    grow(keys, cap_i2, ni);
-    grow(vals_in, cap_i3, ni);
-    grow(vals, cap_i4, ni);
-    dw::launch_duplicate(P, means2D, depths, radii, offsets, cam, keys_in, vals_in, s);
+    for (int b = 0; b < 2; ++b) {
+      grow(itile[b], cap_i[b], ni);
+      grow(ivals[b], cap_i[2 + b], ni);
+    }
+    tiles_sorted = itile[0];
+    vals = ivals[0];
     if (num_rendered > 0) {
-      size_t sort_bytes = 0;
-      DW_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, keys_in, keys, vals_in, vals,
-                                              num_rendered, 0, 32 + tile_bits, s));
-      ensure_tmp(sort_bytes);
-      DW_CUDA(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, keys_in, keys, vals_in, vals,
-                                              num_rendered, 0, 32 + tile_bits, s));
+      // 2. duplicate in depth order, 3. stable sort by tile id
+      dw::launch_duplicate_sorted(P, order, means2D, radii, offsets, cam, itile[0], ivals[0], s);
+      ensure_tmp(dw::radix_sort_temp_bytes(num_rendered));
+      const int cur = dw::radix_sort_pairs(itile, ivals, num_rendered, tile_bits, tmp, s);
+      tiles_sorted = itile[cur];
+      vals = ivals[cur];
     }
     DW_CUDA(cudaMemsetAsync(ranges, 0, sizeof(uint2) * ntiles, s));
-    dw::launch_ranges(num_rendered, keys, ranges, s);
+    dw::launch_ranges_u32(num_rendered, tiles_sorted, ranges, s);
     dw::launch_forward_impl(cam, ranges, vals, means2D, conic_opacity, rgb, radii, final_T,
                             n_contrib, out_color, s);
     if (radii_out && P > 0)
@@ -228,7 +259,15 @@ void raster_buffer(const dw_rasterizer* r, int which, const void** p, int64_t* c
     case 2: *p = r->radii; *count = P; break;
     case 3: *p = r->conic_opacity; *count = 4 * P; break;
     case 4: *p = r->tiles_touched; *count = P; break;
-    case 5: *p = r->keys; *count = I; break;
+    case 5: {  // (tile << 32 | depth bits) of the sorted instances, built on request
+      auto* m = const_cast<dw_rasterizer*>(r);
+      grow(m->keys_dbg, m->cap_keys, static_cast<size_t>(std::max<int64_t>(I, 1)));
+      launch_make_keys(I, r->tiles_sorted, r->vals, r->depths, m->keys_dbg, nullptr);
+      DW_CUDA(cudaDeviceSynchronize());
+      *p = r->keys_dbg;
+      *count = I;
+      break;
+    }
     case 6: *p = r->vals; *count = I; break;
     case 7: *p = r->ranges; *count = 2 * nt; break;
     case 8: *p = r->final_T; *count = npx; break;
@@ -267,6 +306,78 @@ void raster_host(dw_rasterizer* r, int32_t P, const float* m, const float* sc, c
     DW_CUDA(cudaMemcpyAsync(grad, d_g, kNParam * size_t(P) * sizeof(float),
                             cudaMemcpyDeviceToHost, s));
   DW_CUDA(cudaStreamSynchronize(s));
+}
+
+// One training step's rasterization from host buffers: the scene is uploaded
+// once, then V views are rendered and back-propagated into one gradient
+// buffer. dL/dpixel uploads (copy stream s_in) and image downloads (copy
+// stream s_out) are double-buffered against the compute stream, so with
+// pinned host memory the PCIe traffic of view k+1 / k-1 overlaps view k.
+void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float* sc,
+                       const float* rot, const float* op, const float* col, const dw_camera* cams,
+                       int32_t V, const float* dL, int policy, int thr, float* out_images,
+                       float* grad, cudaStream_t s) {
+  if (V < 1) throw std::invalid_argument("need at least one view");
+  for (int k = 1; k < V; ++k)
+    if (cams[k].width != cams[0].width || cams[k].height != cams[0].height)
+      throw std::invalid_argument("all views must share one image size");
+  r->ensure_streams();
+  const size_t np = static_cast<size_t>(std::max(P, 1));
+  const size_t npx = static_cast<size_t>(cams[0].width) * cams[0].height;
+  float* d_m = r->host_scratch(0, 3 * np);
+  float* d_sc = r->host_scratch(1, 3 * np);
+  float* d_rot = r->host_scratch(2, 4 * np);
+  float* d_op = r->host_scratch(3, np);
+  float* d_col = r->host_scratch(4, 3 * np);
+  float* d_g = r->host_scratch(7, kNParam * np);
+  float* d_dl[2] = {r->host_scratch(5, 3 * npx), r->host_scratch(8, 3 * npx)};
+  float* d_img[2] = {r->host_scratch(6, 3 * npx), r->host_scratch(9, 3 * npx)};
+  cudaEvent_t e_scene = r->ev[0], e_in[2] = {r->ev[1], r->ev[2]},
+              e_used[2] = {r->ev[3], r->ev[4]}, e_img[2] = {r->ev[5], r->ev[6]};
+  auto h2d = [&](float* d, const float* h, size_t n, cudaStream_t st) {
+    if (n) DW_CUDA(cudaMemcpyAsync(d, h, n * sizeof(float), cudaMemcpyHostToDevice, st));
+  };
+  // the copy streams must not run ahead of work already queued on `s`
+  DW_CUDA(cudaEventRecord(e_used[0], s));
+  DW_CUDA(cudaEventRecord(e_used[1], s));
+  DW_CUDA(cudaStreamWaitEvent(r->s_in, e_used[0], 0));
+  h2d(d_m, m, 3 * size_t(P), r->s_in);
+  h2d(d_sc, sc, 3 * size_t(P), r->s_in);
+  h2d(d_rot, rot, 4 * size_t(P), r->s_in);
+  h2d(d_op, op, size_t(P), r->s_in);
+  h2d(d_col, col, 3 * size_t(P), r->s_in);
+  DW_CUDA(cudaEventRecord(e_scene, r->s_in));
+  h2d(d_dl[0], dL, 3 * npx, r->s_in);
+  DW_CUDA(cudaEventRecord(e_in[0], r->s_in));
+  DW_CUDA(cudaMemsetAsync(d_g, 0, kNParam * np * sizeof(float), s));
+  DW_CUDA(cudaStreamWaitEvent(s, e_scene, 0));
+  for (int k = 0; k < V; ++k) {
+    const int b = k & 1;
+    if (k + 1 < V) {  // prefetch view k+1 once view k-1 released its buffer
+      DW_CUDA(cudaStreamWaitEvent(r->s_in, e_used[b ^ 1], 0));
+      h2d(d_dl[b ^ 1], dL + static_cast<size_t>(k + 1) * 3 * npx, 3 * npx, r->s_in);
+      DW_CUDA(cudaEventRecord(e_in[b ^ 1], r->s_in));
+    }
+    DW_CUDA(cudaStreamWaitEvent(s, e_in[b], 0));
+    if (k >= 2) DW_CUDA(cudaStreamWaitEvent(s, e_img[b], 0));  // image k-2 downloaded
+    r->forward(P, d_m, d_sc, d_rot, d_op, d_col, cams[k], d_img[b], nullptr, s);
+    r->backward(d_dl[b], policy, thr, d_g, nullptr, s);
+    DW_CUDA(cudaEventRecord(e_used[b], s));
+    if (out_images) {
+      DW_CUDA(cudaStreamWaitEvent(r->s_out, e_used[b], 0));
+      DW_CUDA(cudaMemcpyAsync(out_images + static_cast<size_t>(k) * 3 * npx, d_img[b],
+                              3 * npx * sizeof(float), cudaMemcpyDeviceToHost, r->s_out));
+      DW_CUDA(cudaEventRecord(e_img[b], r->s_out));
+    } else {
+      DW_CUDA(cudaEventRecord(e_img[b], s));
+    }
+  }
+  if (P > 0)
+    DW_CUDA(cudaMemcpyAsync(grad, d_g, kNParam * size_t(P) * sizeof(float),
+                            cudaMemcpyDeviceToHost, s));
+  DW_CUDA(cudaStreamSynchronize(s));
+  DW_CUDA(cudaStreamSynchronize(r->s_out));
+  DW_CUDA(cudaStreamSynchronize(r->s_in));
 }
 
 }  // namespace dw

@@ -44,6 +44,22 @@ void launch_duplicate(int P, const float2* means2D, const float* depths, const i
 
 void launch_ranges(int64_t L, const uint64_t* keys, uint2* ranges, cudaStream_t s);
 
+// raster_sort.cu: hand-written stable LSD radix sort + scan (no CUB).
+size_t radix_sort_temp_bytes(int64_t n);
+size_t scan_temp_bytes(int64_t n);
+int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* temp,
+                     cudaStream_t s);
+void inclusive_scan_gather(const uint32_t* in, const uint32_t* order, int64_t n, uint64_t* out,
+                           void* temp, cudaStream_t s);
+void launch_depth_keys(int P, const float* depths, const int* radii, uint32_t* dkey, uint32_t* ids,
+                       cudaStream_t s);
+void launch_duplicate_sorted(int P, const uint32_t* order, const float2* means2D, const int* radii,
+                             const uint64_t* offsets, const CamParams& cam, uint32_t* tile_ids,
+                             uint32_t* values, cudaStream_t s);
+void launch_ranges_u32(int64_t L, const uint32_t* tiles, uint2* ranges, cudaStream_t s);
+void launch_make_keys(int64_t L, const uint32_t* tiles, const uint32_t* values, const float* depths,
+                      uint64_t* keys, cudaStream_t s);
+
 void launch_forward_impl(const CamParams& cam, const uint2* ranges, const uint32_t* values,
                          const float2* means2D, const float4* conic_opacity, const float4* rgb,
                          const int* radii, float* final_T, uint32_t* n_contrib, float* out_color,

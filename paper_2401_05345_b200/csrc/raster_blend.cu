@@ -3,14 +3,20 @@
 //
 // One 256-thread CTA per 16x16 tile. The tile's sorted Gaussian list is
 // walked in batches of 256 staged in shared memory (48 B per Gaussian:
-// xy + radius + id, conic + opacity, rgb). Each warp owns an 8x4 pixel block
-// and, per Gaussian, first tests that block against the Gaussian's
-// conservative alpha footprint (warp-uniform branch): a Gaussian whose
-// alpha is below 1/255 over the whole block is skipped without any per-lane
-// exp. The footprint bound: alpha >= 1/255 needs d^T Sigma^-1 d <=
-// 2 ln(255 o) <= 2 ln 255, i.e. |d| <= sqrt(2 ln 255) sigma_max < 1.11 *
-// radius (radius = ceil(3 sigma_max)), so culling at 1.11 * radius + 1 px
-// never drops a pair the oracle keeps.
+// xy + id, conic + opacity, rgb). While staging, the thread that loads a
+// Gaussian also computes which of the tile's eight 8x4 warp blocks its
+// alpha >= 1/255 footprint can reach and stores that as an 8-bit mask; each
+// warp then ballots its bits of the 256 masks and walks ONLY the Gaussians
+// that can touch its pixels (warp-uniform: ffs over the ballot words), so the
+// (warp, Gaussian) pairs that cannot contribute cost no per-lane work.
+//
+// Footprint bound. alpha = min(0.99, o G) >= 1/255 with G = exp(-q/2),
+// q = d^T Q d (Q = conic), needs q <= tau = 2 ln(255 o). The ellipse
+// q <= tau lies in |dx| <= sqrt(tau Q^-1_xx), |dy| <= sqrt(tau Q^-1_yy), with
+// Q^-1_xx = c / (ac - b^2), Q^-1_yy = a / (ac - b^2). The kernel inflates tau
+// by 5 % + 0.05 to cover __expf and FMA rounding, so culling never drops a
+// pair the per-lane test would keep (o <= 1/255 -> never active; a
+// degenerate conic falls back to no culling).
 //
 // Backward: the GradComputation loop of PAPER.md:1481-1504 -- each pixel
 // thread walks its Gaussians back to front, cond1/cond2 are the
@@ -31,42 +37,58 @@ namespace dw {
 namespace {
 
 struct __align__(16) Staged {
-  float4 xyri;  // x, y, radius (int bits), id (uint bits)
-  float4 co;    // conic a, b, c, opacity
-  float4 col;   // r, g, b, -
+  float4 xyi;  // x, y, id (uint bits), -
+  float4 co;   // conic a, b, c, opacity
+  float4 col;  // r, g, b, -
 };
 
-__device__ __forceinline__ bool warp_culled(float gx, float gy, int radius, float opacity,
-                                            int wx0, int wy0) {
-  if (opacity > 1.0f) return false;  // the footprint bound assumes o <= 1
-  const float rc = 1.11f * (float)radius + 1.0f;
-  const float dx = fmaxf(0.0f, fmaxf((float)wx0 - gx, gx - (float)(wx0 + 7)));
-  const float dy = fmaxf(0.0f, fmaxf((float)wy0 - gy, gy - (float)(wy0 + 3)));
-  return dx > rc || dy > rc;
-}
-
-__device__ __forceinline__ void stage(Staged* s, int slot, uint32_t id,
-                                      const float2* __restrict__ means2D,
-                                      const float4* __restrict__ conic_opacity,
-                                      const float4* __restrict__ rgb, const int* __restrict__ radii) {
+// Stage Gaussian `id` into slot `slot` and return its 8-bit warp-block mask
+// for the tile whose top-left pixel is (tx0, ty0).
+__device__ __forceinline__ uint32_t stage(Staged* s, int slot, uint32_t id, int tx0, int ty0,
+                                          const float2* __restrict__ means2D,
+                                          const float4* __restrict__ conic_opacity,
+                                          const float4* __restrict__ rgb) {
   const float2 m = __ldg(means2D + id);
-  s[slot].xyri = make_float4(m.x, m.y, __int_as_float(__ldg(radii + id)), __uint_as_float(id));
-  s[slot].co = __ldg(conic_opacity + id);
+  const float4 co = __ldg(conic_opacity + id);
+  s[slot].xyi = make_float4(m.x, m.y, __uint_as_float(id), 0.0f);
+  s[slot].co = co;
   s[slot].col = __ldg(rgb + id);
+  if (!(co.w * 255.0f > 1.0f)) return 0u;  // alpha < 1/255 everywhere
+  const float det = co.x * co.z - co.y * co.y;
+  if (!(det > 0.0f) || !(co.x > 0.0f)) return 0xffu;  // degenerate: no culling
+  const float tau = 1.05f * 2.0f * __logf(255.0f * co.w) + 0.05f;
+  const float ex = sqrtf(tau * co.z / det), ey = sqrtf(tau * co.x / det);
+  uint32_t cx = 0, ry = 0;
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const float lo = (float)(tx0 + 8 * c), hi = lo + 7.0f;
+    if (m.x + ex >= lo && m.x - ex <= hi) cx |= 1u << c;
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const float lo = (float)(ty0 + 4 * r), hi = lo + 3.0f;
+    if (m.y + ey >= lo && m.y - ey <= hi) ry |= 1u << r;
+  }
+  // warp w covers column (w & 1), row (w >> 1)
+  uint32_t mask = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w)
+    if ((cx >> (w & 1) & 1u) && (ry >> (w >> 1) & 1u)) mask |= 1u << w;
+  return mask;
 }
 
 __global__ void __launch_bounds__(kBlock)
     k_forward(const CamParams cam, const uint2* __restrict__ ranges,
               const uint32_t* __restrict__ values, const float2* __restrict__ means2D,
               const float4* __restrict__ conic_opacity, const float4* __restrict__ rgb,
-              const int* __restrict__ radii, float* __restrict__ final_T,
-              uint32_t* __restrict__ n_contrib, float* __restrict__ out_color) {
+              float* __restrict__ final_T, uint32_t* __restrict__ n_contrib,
+              float* __restrict__ out_color) {
   __shared__ Staged sm[kBlock];
-  const int tile = blockIdx.x, t = threadIdx.x, w = t >> 5;
+  __shared__ uint8_t s_mask[kBlock];
+  const int tile = blockIdx.x, t = threadIdx.x, w = t >> 5, lane = t & 31;
+  const int tx0 = (tile % cam.tiles_x) * kTile, ty0 = (tile / cam.tiles_x) * kTile;
   int px, py;
   tile_pixel(tile, t, cam.tiles_x, &px, &py);
-  const int wx0 = (tile % cam.tiles_x) * kTile + (w & 1) * 8;
-  const int wy0 = (tile / cam.tiles_x) * kTile + (w >> 1) * 4;
   const bool inside = px < cam.W && py < cam.H;
   const float pfx = (float)px, pfy = (float)py;
   const uint2 range = ranges[tile];
@@ -74,35 +96,44 @@ __global__ void __launch_bounds__(kBlock)
   int todo = (int)(range.y - range.x);
   bool done = !inside;
   float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
-  uint32_t contributor = 0, last = 0;
+  uint32_t last = 0;
   for (int i = 0; i < rounds; ++i, todo -= kBlock) {
     if (__syncthreads_count(done) == kBlock) break;
     const uint32_t progress = range.x + i * kBlock + t;
-    if (progress < range.y) stage(sm, t, values[progress], means2D, conic_opacity, rgb, radii);
+    uint32_t mask = 0;
+    if (progress < range.y)
+      mask = stage(sm, t, values[progress], tx0, ty0, means2D, conic_opacity, rgb);
+    s_mask[t] = (uint8_t)mask;
     __syncthreads();
     const int n = min(kBlock, todo);
-    for (int j = 0; j < n && !done; ++j) {
-      contributor++;
-      const float4 g = sm[j].xyri;
-      const float4 co = sm[j].co;
-      if (warp_culled(g.x, g.y, __float_as_int(g.z), co.w, wx0, wy0)) continue;
-      const float dx = g.x - pfx, dy = g.y - pfy;
-      const float power = -0.5f * (co.x * dx * dx + co.z * dy * dy) - co.y * dx * dy;
-      if (power > 0.0f) continue;
-      const float alpha = fminf(0.99f, co.w * __expf(power));
-      if (alpha < 1.0f / 255.0f) continue;
-      const float test_T = T * (1.0f - alpha);
-      if (test_T < 0.0001f) {
-        done = true;
-        continue;
+    for (int k = 0; k * 32 < n; ++k) {
+      if (__all_sync(kFull, done)) break;
+      const int jl = k * 32 + lane;
+      unsigned bits = __ballot_sync(kFull, jl < n && ((s_mask[jl] >> w) & 1u));
+      while (bits) {
+        const int j = k * 32 + __ffs(bits) - 1;
+        bits &= bits - 1u;
+        if (done) continue;
+        const float4 g = sm[j].xyi;
+        const float4 co = sm[j].co;
+        const float dx = g.x - pfx, dy = g.y - pfy;
+        const float power = -0.5f * (co.x * dx * dx + co.z * dy * dy) - co.y * dx * dy;
+        if (power > 0.0f) continue;
+        const float alpha = fminf(0.99f, co.w * __expf(power));
+        if (alpha < 1.0f / 255.0f) continue;
+        const float test_T = T * (1.0f - alpha);
+        if (test_T < 0.0001f) {
+          done = true;
+          continue;
+        }
+        const float4 c = sm[j].col;
+        const float aT = alpha * T;
+        C0 += c.x * aT;
+        C1 += c.y * aT;
+        C2 += c.z * aT;
+        T = test_T;
+        last = (uint32_t)(i * kBlock + j + 1);  // 1-based list position
       }
-      const float4 c = sm[j].col;
-      const float aT = alpha * T;
-      C0 += c.x * aT;
-      C1 += c.y * aT;
-      C2 += c.z * aT;
-      T = test_T;
-      last = contributor;
     }
   }
   if (inside) {
@@ -116,21 +147,25 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+#ifndef DW_BWD_MIN_BLOCKS
+#define DW_BWD_MIN_BLOCKS 5  // 5 x 256 threads/SM: <= 51 registers, no spills (ptxas -v)
+#endif
+
 template <int POL, bool COUNT>
-__global__ void __launch_bounds__(kBlock)
+__global__ void __launch_bounds__(kBlock, DW_BWD_MIN_BLOCKS)
     k_backward(const CamParams cam, const uint2* __restrict__ ranges,
                const uint32_t* __restrict__ values, const float2* __restrict__ means2D,
                const float4* __restrict__ conic_opacity, const float4* __restrict__ rgb,
-               const int* __restrict__ radii, const float* __restrict__ final_Ts,
-               const uint32_t* __restrict__ n_contrib, const float* __restrict__ dL_dpixels,
-               int thr, float* __restrict__ grad, unsigned long long* __restrict__ counters) {
+               const float* __restrict__ final_Ts, const uint32_t* __restrict__ n_contrib,
+               const float* __restrict__ dL_dpixels, int thr, float* __restrict__ grad,
+               unsigned long long* __restrict__ counters) {
   __shared__ Staged sm[kBlock];
+  __shared__ uint8_t s_mask[kBlock];
   __shared__ uint32_t s_wmax[kBlock / 32];
   const int tile = blockIdx.x, t = threadIdx.x, w = t >> 5, lane = t & 31;
+  const int tx0 = (tile % cam.tiles_x) * kTile, ty0 = (tile / cam.tiles_x) * kTile;
   int px, py;
   tile_pixel(tile, t, cam.tiles_x, &px, &py);
-  const int wx0 = (tile % cam.tiles_x) * kTile + (w & 1) * 8;
-  const int wy0 = (tile / cam.tiles_x) * kTile + (w >> 1) * 4;
   const bool inside = px < cam.W && py < cam.H;
   const int pix = py * cam.W + px;
   const int HW = cam.H * cam.W;
@@ -149,8 +184,8 @@ __global__ void __launch_bounds__(kBlock)
   const float bg_dot = cam.bg[0] * dLp0 + cam.bg[1] * dLp1 + cam.bg[2] * dLp2;
   const float ddelx_dx = 0.5f * (float)cam.W, ddely_dy = 0.5f * (float)cam.H;
 
-  // Gaussians at list index >= max(last_contributor) over the tile cannot
-  // contribute to any of its pixels: start the back-to-front walk there.
+  // List positions >= max(last_contributor) over the tile cannot contribute
+  // to any of its pixels: start the back-to-front walk there.
   const uint32_t wmax = __reduce_max_sync(kFull, last_contributor);
   if (lane == 0) s_wmax[w] = wmax;
   __syncthreads();
@@ -160,75 +195,88 @@ __global__ void __launch_bounds__(kBlock)
 
   float acc0 = 0.0f, acc1 = 0.0f, acc2 = 0.0f;
   float lc0 = 0.0f, lc1 = 0.0f, lc2 = 0.0f, last_alpha = 0.0f;
-  uint32_t contributor = bmax;
   uint32_t nred = 0, npairs = 0;
+  bool issuer;
+  const int slot = bfly_slot<kNParam>(lane, &issuer);
   const int rounds = (int)((bmax + kBlock - 1) / kBlock);
   int todo = (int)bmax;
   const uint32_t top = range.x + bmax;  // exclusive end of the live list
   for (int i = 0; i < rounds; ++i, todo -= kBlock) {
     __syncthreads();
-    if (t < todo) stage(sm, t, values[top - 1 - (i * kBlock + t)], means2D, conic_opacity, rgb, radii);
+    uint32_t mask = 0;
+    if (t < todo)
+      mask = stage(sm, t, values[top - 1 - (i * kBlock + t)], tx0, ty0, means2D, conic_opacity,
+                   rgb);
+    s_mask[t] = (uint8_t)mask;
     __syncthreads();
     const int n = min(kBlock, todo);
-    for (int j = 0; j < n; ++j) {
-      contributor--;
-      if (contributor >= wmax) continue;  // warp-uniform: no lane can be active
-      const float4 g = sm[j].xyri;
-      const float4 co = sm[j].co;
-      if (warp_culled(g.x, g.y, __float_as_int(g.z), co.w, wx0, wy0)) continue;
-      const float dx = g.x - pfx, dy = g.y - pfy;
-      const float power = -0.5f * (co.x * dx * dx + co.z * dy * dy) - co.y * dx * dy;
-      const float G = __expf(power);
-      const float alpha = fminf(0.99f, co.w * G);
-      const bool act = inside && contributor < last_contributor && power <= 0.0f &&
-                       alpha >= 1.0f / 255.0f;
-      const unsigned ballot = __ballot_sync(kFull, act);
-      if (ballot == 0u) continue;
-      float v[kNParam];
-      if (act) {
-        const float4 c = sm[j].col;
-        const float one_m = 1.0f - alpha;
-        T = T / one_m;
-        const float dchannel_dcolor = alpha * T;
-        acc0 = last_alpha * lc0 + (1.0f - last_alpha) * acc0;
-        acc1 = last_alpha * lc1 + (1.0f - last_alpha) * acc1;
-        acc2 = last_alpha * lc2 + (1.0f - last_alpha) * acc2;
-        lc0 = c.x;
-        lc1 = c.y;
-        lc2 = c.z;
-        float dL_dalpha = (c.x - acc0) * dLp0;
-        dL_dalpha += (c.y - acc1) * dLp1;
-        dL_dalpha += (c.z - acc2) * dLp2;
-        v[6] = dchannel_dcolor * dLp0;
-        v[7] = dchannel_dcolor * dLp1;
-        v[8] = dchannel_dcolor * dLp2;
-        dL_dalpha *= T;
-        last_alpha = alpha;
-        dL_dalpha += (-T_final / one_m) * bg_dot;
-        const float dL_dG = co.w * dL_dalpha;
-        const float gdx = G * dx, gdy = G * dy;
-        const float dG_ddelx = -gdx * co.x - gdy * co.y;
-        const float dG_ddely = -gdy * co.z - gdx * co.y;
-        v[0] = dL_dG * dG_ddelx * ddelx_dx;
-        v[1] = dL_dG * dG_ddely * ddely_dy;
-        v[2] = -0.5f * gdx * dx * dL_dG;
-        v[3] = -0.5f * gdx * dy * dL_dG;
-        v[4] = -0.5f * gdy * dy * dL_dG;
-        v[5] = G * dL_dalpha;
-      } else {
+    // slot j holds list position c_j = bmax - 1 - (i*256 + j)
+    const uint32_t base = bmax - 1 - (uint32_t)(i * kBlock);
+    for (int k = 0; k * 32 < n; ++k) {
+      const int jl = k * 32 + lane;
+      unsigned bits = __ballot_sync(
+          kFull, jl < n && ((s_mask[jl] >> w) & 1u) && (base - (uint32_t)jl) < wmax);
+      while (bits) {
+        const int j = k * 32 + __ffs(bits) - 1;
+        bits &= bits - 1u;
+        const uint32_t contributor = base - (uint32_t)j;
+        const float4 g = sm[j].xyi;
+        const float4 co = sm[j].co;
+        const float dx = g.x - pfx, dy = g.y - pfy;
+        const float dxx = dx * dx, dxy = dx * dy, dyy = dy * dy;
+        const float power = -0.5f * (co.x * dxx + co.z * dyy) - co.y * dxy;
+        const float G = __expf(power);
+        const float alpha = fminf(0.99f, co.w * G);
+        const bool act = inside && contributor < last_contributor && power <= 0.0f &&
+                         alpha >= 1.0f / 255.0f;
+        const unsigned ballot = __ballot_sync(kFull, act);
+        if (ballot == 0u) continue;
+        float v[kNParam];
+        if (act) {
+          const float4 c = sm[j].col;
+          const float inv = __fdividef(1.0f, 1.0f - alpha);
+          T = T * inv;
+          const float dchannel_dcolor = alpha * T;
+          acc0 += last_alpha * (lc0 - acc0);  // = la*lc + (1-la)*acc
+          acc1 += last_alpha * (lc1 - acc1);
+          acc2 += last_alpha * (lc2 - acc2);
+          lc0 = c.x;
+          lc1 = c.y;
+          lc2 = c.z;
+          float dL_dalpha = (c.x - acc0) * dLp0;
+          dL_dalpha += (c.y - acc1) * dLp1;
+          dL_dalpha += (c.z - acc2) * dLp2;
+          v[6] = dchannel_dcolor * dLp0;
+          v[7] = dchannel_dcolor * dLp1;
+          v[8] = dchannel_dcolor * dLp2;
+          dL_dalpha *= T;
+          last_alpha = alpha;
+          dL_dalpha += (-T_final * inv) * bg_dot;
+          // dL/dG = o dL/dalpha; with q = G dL/dG the 3DGS terms
+          // dL_dG * dG/d(delta) and -0.5 G d d^T dL_dG reuse power's products
+          const float q = G * (co.w * dL_dalpha);
+          const float qh = -0.5f * q;
+          v[0] = -q * (co.x * dx + co.y * dy) * ddelx_dx;
+          v[1] = -q * (co.z * dy + co.y * dx) * ddely_dy;
+          v[2] = qh * dxx;
+          v[3] = qh * dxy;
+          v[4] = qh * dyy;
+          v[5] = G * dL_dalpha;
+        } else {
 #pragma unroll
-        for (int p = 0; p < kNParam; ++p) v[p] = 0.0f;
-      }
-      const int id = (int)__float_as_uint(g.w);
-      if (COUNT && lane == 0) npairs += __popc(ballot);
-      if (POL == kNative) {
-        native_atomics<kNParam, COUNT>(grad + static_cast<int64_t>(id) * kNParam, v, act, nred);
-      } else if (POL == kSwB) {
-        reduce_bfly<kNParam, COUNT, true>(id, grad, v, thr, act, lane, nred, ballot);
-      } else if (POL == kSwS) {
-        reduce_serial<kNParam, COUNT>(id, grad, v, thr, act, lane, nred, ballot);
-      } else {
-        reduce_cccl<kNParam, COUNT>(id, grad, v, act, lane, nred, ballot);
+          for (int p = 0; p < kNParam; ++p) v[p] = 0.0f;
+        }
+        const int id = (int)__float_as_uint(g.z);
+        if (COUNT && lane == 0) npairs += __popc(ballot);
+        if (POL == kNative) {
+          native_atomics<kNParam, COUNT>(grad + static_cast<int64_t>(id) * kNParam, v, act, nred);
+        } else if (POL == kSwB) {
+          reduce_bfly<kNParam, COUNT, true>(id, grad, v, thr, act, lane, nred, ballot, slot, issuer);
+        } else if (POL == kSwS) {
+          reduce_serial<kNParam, COUNT>(id, grad, v, thr, act, lane, nred, ballot);
+        } else {
+          reduce_cccl<kNParam, COUNT>(id, grad, v, act, lane, nred, ballot);
+        }
       }
     }
   }
@@ -240,16 +288,16 @@ __global__ void __launch_bounds__(kBlock)
 
 template <int POL>
 void launch_bwd(bool count, const CamParams& cam, const uint2* ranges, const uint32_t* values,
-                const float2* means2D, const float4* co, const float4* rgb, const int* radii,
-                const float* fT, const uint32_t* nc, const float* dL, int thr, float* grad,
+                const float2* means2D, const float4* co, const float4* rgb, const float* fT,
+                const uint32_t* nc, const float* dL, int thr, float* grad,
                 unsigned long long* ctr, cudaStream_t s) {
   const int grid = cam.tiles_x * cam.tiles_y;
   if (count)
-    k_backward<POL, true><<<grid, kBlock, 0, s>>>(cam, ranges, values, means2D, co, rgb, radii,
-                                                  fT, nc, dL, thr, grad, ctr);
+    k_backward<POL, true><<<grid, kBlock, 0, s>>>(cam, ranges, values, means2D, co, rgb, fT, nc,
+                                                  dL, thr, grad, ctr);
   else
-    k_backward<POL, false><<<grid, kBlock, 0, s>>>(cam, ranges, values, means2D, co, rgb, radii,
-                                                   fT, nc, dL, thr, grad, nullptr);
+    k_backward<POL, false><<<grid, kBlock, 0, s>>>(cam, ranges, values, means2D, co, rgb, fT,
+                                                   nc, dL, thr, grad, nullptr);
 }
 
 }  // namespace
@@ -258,9 +306,10 @@ void launch_forward_impl(const CamParams& cam, const uint2* ranges, const uint32
                          const float2* means2D, const float4* conic_opacity, const float4* rgb,
                          const int* radii, float* final_T, uint32_t* n_contrib, float* out_color,
                          cudaStream_t s) {
+  (void)radii;
   const int grid = cam.tiles_x * cam.tiles_y;
-  k_forward<<<grid, kBlock, 0, s>>>(cam, ranges, values, means2D, conic_opacity, rgb, radii,
-                                    final_T, n_contrib, out_color);
+  k_forward<<<grid, kBlock, 0, s>>>(cam, ranges, values, means2D, conic_opacity, rgb, final_T,
+                                    n_contrib, out_color);
   DW_CUDA(cudaGetLastError());
 }
 
@@ -269,23 +318,24 @@ void launch_backward_impl(const CamParams& cam, const uint2* ranges, const uint3
                           const int* radii, const float* final_T, const uint32_t* n_contrib,
                           const float* dL, int policy, int thr, float* grad,
                           unsigned long long* counters, cudaStream_t s) {
+  (void)radii;
   const bool count = counters != nullptr;
   switch (policy) {
     case kNative:
-      launch_bwd<kNative>(count, cam, ranges, values, means2D, co, rgb, radii, final_T,
-                          n_contrib, dL, thr, grad, counters, s);
+      launch_bwd<kNative>(count, cam, ranges, values, means2D, co, rgb, final_T, n_contrib, dL,
+                          thr, grad, counters, s);
       break;
     case kSwS:
-      launch_bwd<kSwS>(count, cam, ranges, values, means2D, co, rgb, radii, final_T, n_contrib,
-                       dL, thr, grad, counters, s);
+      launch_bwd<kSwS>(count, cam, ranges, values, means2D, co, rgb, final_T, n_contrib, dL, thr,
+                       grad, counters, s);
       break;
     case kSwB:
-      launch_bwd<kSwB>(count, cam, ranges, values, means2D, co, rgb, radii, final_T, n_contrib,
-                       dL, thr, grad, counters, s);
+      launch_bwd<kSwB>(count, cam, ranges, values, means2D, co, rgb, final_T, n_contrib, dL, thr,
+                       grad, counters, s);
       break;
     default:
-      launch_bwd<kCccl>(count, cam, ranges, values, means2D, co, rgb, radii, final_T, n_contrib,
-                        dL, thr, grad, counters, s);
+      launch_bwd<kCccl>(count, cam, ranges, values, means2D, co, rgb, final_T, n_contrib, dL,
+                        thr, grad, counters, s);
   }
   DW_CUDA(cudaGetLastError());
 }

@@ -1,0 +1,419 @@
+// Hand-written binning sort for sm_100a (replaces a 64-bit-key library radix
+// sort of every (tile, Gaussian) instance).
+//
+// The reference order is a STABLE sort of the instances by the 64-bit key
+// (tile << 32) | float_bits(depth), instances generated in (Gaussian, row,
+// column) order: within a tile, ascending depth, ties by Gaussian index. The
+// same order is produced here with far fewer bytes moved:
+//   1. stable LSD sort of the P Gaussians by their 32-bit depth key
+//      (4 passes over P, not over the ~4.5 P instances);
+//   2. duplicate the instances in that depth order, writing only a u32 tile
+//      id and the Gaussian id;
+//   3. stable LSD sort of the instances by tile id (ceil(tile_bits / 8)
+//      passes: 2 for 1080p's 8,160 tiles).
+// Stability of step 3 keeps step 1's (depth, index) order inside each tile,
+// so the result equals the 64-bit-key sort bit for bit (tests compare it with
+// the oracle's std-style stable sort).
+//
+// Each LSD pass is three launches over tiles of 4,096 elements:
+//   upsweep    per-tile 8-bit digit histogram (smem atomics) -> counts[d][tile]
+//   scan       per-digit exclusive scan over tiles + exclusive scan of the
+//              256 digit totals (two small kernels)
+//   downsweep  stable in-tile ranking: 16 rounds of 256 elements in
+//              element order; __match_any_sync ranks lanes within a warp,
+//              an smem per-digit prefix over the 8 warps orders the warps,
+//              a running per-digit base orders the rounds; then scatter.
+#include <cuda_runtime.h>
+
+#include "distwar.cuh"
+#include "dw_internal.h"
+#include "raster.cuh"
+
+namespace dw {
+
+namespace {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 elements
+
+__global__ void __launch_bounds__(kSortThreads)
+    k_upsweep(const uint32_t* __restrict__ keys, int64_t n, int shift, uint32_t mask,
+              uint32_t* __restrict__ counts, int64_t tiles) {
+  __shared__ uint32_t hist[256];
+  const int t = threadIdx.x;
+  hist[t] = 0;
+  __syncthreads();
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kSortTile;
+#pragma unroll 4
+  for (int r = 0; r < kSortItems; ++r) {
+    const int64_t e = base + r * kSortThreads + t;
+    if (e < n) atomicAdd(&hist[(__ldg(keys + e) >> shift) & mask], 1u);
+  }
+  __syncthreads();
+  counts[static_cast<int64_t>(t) * tiles + blockIdx.x] = hist[t];
+}
+
+// One block per digit: exclusive scan of counts[d][0..tiles) in place, total
+// to digit_total[d].
+__global__ void __launch_bounds__(1024)
+    k_scan_rows(uint32_t* __restrict__ counts, int64_t tiles, uint32_t* __restrict__ digit_total) {
+  __shared__ uint32_t warp_sums[32];
+  __shared__ uint32_t carry;
+  uint32_t* row = counts + static_cast<int64_t>(blockIdx.x) * tiles;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  if (t == 0) carry = 0;
+  __syncthreads();
+  for (int64_t b = 0; b < tiles; b += 1024) {
+    const int64_t i = b + t;
+    const uint32_t v = i < tiles ? row[i] : 0u;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_sums[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      uint32_t s = warp_sums[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, s, o);
+        if (lane >= o) s += y;
+      }
+      warp_sums[lane] = s;  // inclusive over warps
+    }
+    __syncthreads();
+    const uint32_t before = carry + (w ? warp_sums[w - 1] : 0u) + incl - v;
+    if (i < tiles) row[i] = before;
+    __syncthreads();
+    if (t == 0) carry += warp_sums[31];
+    __syncthreads();
+  }
+  if (t == 0) digit_total[blockIdx.x] = carry;
+}
+
+__global__ void k_scan_digits(uint32_t* __restrict__ digit_total, int ndigits) {
+  // 256 threads, exclusive scan in place (<= 256 digits)
+  __shared__ uint32_t s[256];
+  const int t = threadIdx.x;
+  s[t] = t < ndigits ? digit_total[t] : 0u;
+  __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {
+    const uint32_t y = t >= o ? s[t - o] : 0u;
+    __syncthreads();
+    s[t] += y;
+    __syncthreads();
+  }
+  if (t < ndigits) digit_total[t] = s[t] - (t < ndigits ? digit_total[t] : 0u);
+}
+
+__global__ void __launch_bounds__(kSortThreads)
+    k_downsweep(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, int64_t n,
+                int shift, uint32_t mask, const uint32_t* __restrict__ counts, int64_t tiles,
+                const uint32_t* __restrict__ digit_base, uint32_t* __restrict__ keys_out,
+                uint32_t* __restrict__ vals_out) {
+  __shared__ uint32_t s_cnt[kSortThreads / 32][256];
+  __shared__ uint32_t s_base[256];
+  const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  s_base[t] = digit_base[t] + counts[static_cast<int64_t>(t) * tiles + blockIdx.x];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kSortTile;
+  for (int r = 0; r < kSortItems; ++r) {
+    const int64_t e = base + r * kSortThreads + t;
+    const bool valid = e < n;
+    uint32_t key = 0, val = 0;
+    if (valid) {
+      key = __ldg(keys + e);
+      val = __ldg(vals + e);
+    }
+    const uint32_t digit = valid ? (key >> shift) & mask : 0x100u + 0u;
+#pragma unroll
+    for (int k = 0; k < kSortThreads / 32; ++k) s_cnt[k][t] = 0;
+    __syncthreads();
+    const unsigned peers = __match_any_sync(kFull, digit);
+    const uint32_t wrank = __popc(peers & lt);
+    if (valid && wrank == 0) s_cnt[w][digit] = __popc(peers);
+    __syncthreads();
+    {  // thread t owns digit t: exclusive prefix over warps, advance the base
+      uint32_t run = s_base[t];
+#pragma unroll
+      for (int k = 0; k < kSortThreads / 32; ++k) {
+        const uint32_t c = s_cnt[k][t];
+        s_cnt[k][t] = run;
+        run += c;
+      }
+      s_base[t] = run;
+    }
+    __syncthreads();
+    if (valid) {
+      const uint32_t pos = s_cnt[w][digit] + wrank;
+      keys_out[pos] = key;
+      vals_out[pos] = val;
+    }
+    __syncthreads();
+  }
+}
+
+// Inclusive scan u32 -> u64 of in[order[i]] (order may be null).
+__global__ void __launch_bounds__(kSortThreads)
+    k_scan_tile_sums(const uint32_t* __restrict__ in, const uint32_t* __restrict__ order,
+                     int64_t n, unsigned long long* __restrict__ tile_sums) {
+  __shared__ unsigned long long ws[kSortThreads / 32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kSortTile;
+  unsigned long long s = 0;
+  for (int r = 0; r < kSortItems; ++r) {
+    const int64_t e = base + r * kSortThreads + t;
+    if (e < n) s += __ldg(in + (order ? __ldg(order + e) : e));
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  if (lane == 0) ws[w] = s;
+  __syncthreads();
+  if (t == 0) {
+    unsigned long long tot = 0;
+    for (int k = 0; k < kSortThreads / 32; ++k) tot += ws[k];
+    tile_sums[blockIdx.x] = tot;
+  }
+}
+
+__global__ void k_scan_tile_prefix(unsigned long long* __restrict__ tile_sums, int64_t tiles) {
+  // single block of 1024: exclusive scan of tile sums in place (loop)
+  __shared__ unsigned long long warp_sums[32];
+  __shared__ unsigned long long carry;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  if (t == 0) carry = 0;
+  __syncthreads();
+  for (int64_t b = 0; b < tiles; b += 1024) {
+    const int64_t i = b + t;
+    const unsigned long long v = i < tiles ? tile_sums[i] : 0ull;
+    unsigned long long incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_sums[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      unsigned long long s = warp_sums[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(kFull, s, o);
+        if (lane >= o) s += y;
+      }
+      warp_sums[lane] = s;
+    }
+    __syncthreads();
+    if (i < tiles) tile_sums[i] = carry + (w ? warp_sums[w - 1] : 0ull) + incl - v;
+    __syncthreads();
+    if (t == 0) carry += warp_sums[31];
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kSortThreads)
+    k_scan_tile_apply(const uint32_t* __restrict__ in, const uint32_t* __restrict__ order,
+                      int64_t n, const unsigned long long* __restrict__ tile_prefix,
+                      uint64_t* __restrict__ out) {
+  // thread-blocked: thread t owns elements [16t, 16t+16) of the tile
+  __shared__ unsigned long long ws[kSortThreads / 32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int64_t first = static_cast<int64_t>(blockIdx.x) * kSortTile + t * kSortItems;
+  uint32_t v[kSortItems];
+  unsigned long long tot = 0;
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    const int64_t e = first + k;
+    v[k] = e < n ? __ldg(in + (order ? __ldg(order + e) : e)) : 0u;
+    tot += v[k];
+  }
+  unsigned long long incl = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) ws[w] = incl;
+  __syncthreads();
+  unsigned long long wbase = 0;
+  for (int k = 0; k < w; ++k) wbase += ws[k];
+  unsigned long long run = tile_prefix[blockIdx.x] + wbase + incl - tot;
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    run += v[k];
+    if (first + k < n) out[first + k] = run;
+  }
+}
+
+__global__ void k_iota_depthkey(int P, const float* __restrict__ depths, const int* __restrict__ radii,
+                                uint32_t* __restrict__ dkey, uint32_t* __restrict__ ids) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  dkey[i] = radii[i] > 0 ? __float_as_uint(depths[i]) : 0xffffffffu;
+  ids[i] = static_cast<uint32_t>(i);
+}
+
+__device__ __forceinline__ void rect_of(float2 m, int radius, int tiles_x, int tiles_y, int* r) {
+  const float fr = (float)radius;
+  const int v0 = (int)((m.x - fr) / (float)kTile), v1 = (int)((m.y - fr) / (float)kTile);
+  const int v2 = (int)((m.x + fr + (float)(kTile - 1)) / (float)kTile);
+  const int v3 = (int)((m.y + fr + (float)(kTile - 1)) / (float)kTile);
+  r[0] = min(tiles_x, max(0, v0));
+  r[1] = min(tiles_y, max(0, v1));
+  r[2] = min(tiles_x, max(0, v2));
+  r[3] = min(tiles_y, max(0, v3));
+}
+
+// One lane per Gaussian in depth order; rects wider than a warp are written
+// by the whole warp (C4-style scenes touch thousands of tiles).
+__global__ void __launch_bounds__(256)
+    k_duplicate_sorted(int P, const uint32_t* __restrict__ order, const float2* __restrict__ means2D,
+                       const int* __restrict__ radii, const uint64_t* __restrict__ offsets,
+                       int tiles_x, int tiles_y, uint32_t* __restrict__ tile_ids,
+                       uint32_t* __restrict__ values) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int r[4] = {0, 0, 0, 0};
+  uint64_t off = 0;
+  uint32_t gid = 0;
+  int area = 0;
+  if (i < P) {
+    gid = order[i];
+    const int rad = radii[gid];
+    if (rad > 0) {
+      rect_of(means2D[gid], rad, tiles_x, tiles_y, r);
+      off = i == 0 ? 0 : offsets[i - 1];
+      area = (r[2] - r[0]) * (r[3] - r[1]);
+    }
+  }
+  const bool big = area > 32;
+  if (!big) {
+    for (int y = r[1]; y < r[3]; ++y)
+      for (int x = r[0]; x < r[2]; ++x) {
+        tile_ids[off] = static_cast<uint32_t>(y * tiles_x + x);
+        values[off] = gid;
+        ++off;
+      }
+  }
+  unsigned todo = __ballot_sync(kFull, big);
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1u;
+    const int x0 = __shfl_sync(kFull, r[0], src);
+    const int y0 = __shfl_sync(kFull, r[1], src);
+    const int x1 = __shfl_sync(kFull, r[2], src);
+    const int a = __shfl_sync(kFull, area, src);
+    const uint64_t o = __shfl_sync(kFull, off, src);
+    const uint32_t g = __shfl_sync(kFull, gid, src);
+    const int w = x1 - x0;
+    for (int k = lane; k < a; k += 32) {
+      tile_ids[o + k] = static_cast<uint32_t>((y0 + k / w) * tiles_x + x0 + k % w);
+      values[o + k] = g;
+    }
+  }
+}
+
+__global__ void k_ranges_u32(int64_t L, const uint32_t* __restrict__ tiles, uint2* __restrict__ ranges) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= L) return;
+  const uint32_t tile = tiles[idx];
+  if (idx == 0) {
+    ranges[tile].x = 0;
+  } else {
+    const uint32_t prev = tiles[idx - 1];
+    if (tile != prev) {
+      ranges[prev].y = static_cast<uint32_t>(idx);
+      ranges[tile].x = static_cast<uint32_t>(idx);
+    }
+  }
+  if (idx == L - 1) ranges[tile].y = static_cast<uint32_t>(L);
+}
+
+__global__ void k_make_keys(int64_t L, const uint32_t* __restrict__ tiles,
+                            const uint32_t* __restrict__ values, const float* __restrict__ depths,
+                            uint64_t* __restrict__ keys) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < L) keys[i] = (static_cast<uint64_t>(tiles[i]) << 32) | __float_as_uint(depths[values[i]]);
+}
+
+inline unsigned blocks_for(int64_t n, int per) { return static_cast<unsigned>((n + per - 1) / per); }
+
+}  // namespace
+
+size_t radix_sort_temp_bytes(int64_t n) {
+  const int64_t tiles = (n + kSortTile - 1) / kSortTile;
+  return (static_cast<size_t>(tiles) * 256 + 256) * sizeof(uint32_t) + 256;
+}
+
+size_t scan_temp_bytes(int64_t n) {
+  return static_cast<size_t>((n + kSortTile - 1) / kSortTile + 1) * sizeof(unsigned long long);
+}
+
+// Stable LSD sort of (k[cur], v[cur]) on bits [0, bits); returns the index
+// (0/1) of the double buffer holding the result.
+int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* temp,
+                     cudaStream_t s) {
+  int cur = 0;
+  if (n <= 0 || bits <= 0) return cur;
+  const int64_t tiles = (n + kSortTile - 1) / kSortTile;
+  uint32_t* counts = static_cast<uint32_t*>(temp);
+  uint32_t* digit = counts + static_cast<size_t>(tiles) * 256;
+  for (int shift = 0; shift < bits; shift += 8) {
+    const int b = bits - shift < 8 ? bits - shift : 8;
+    const uint32_t mask = (1u << b) - 1u;
+    k_upsweep<<<static_cast<unsigned>(tiles), kSortThreads, 0, s>>>(k[cur], n, shift, mask, counts,
+                                                                    tiles);
+    k_scan_rows<<<256, 1024, 0, s>>>(counts, tiles, digit);
+    k_scan_digits<<<1, 256, 0, s>>>(digit, 256);
+    k_downsweep<<<static_cast<unsigned>(tiles), kSortThreads, 0, s>>>(
+        k[cur], v[cur], n, shift, mask, counts, tiles, digit, k[cur ^ 1], v[cur ^ 1]);
+    cur ^= 1;
+  }
+  DW_CUDA(cudaGetLastError());
+  return cur;
+}
+
+void inclusive_scan_gather(const uint32_t* in, const uint32_t* order, int64_t n, uint64_t* out,
+                           void* temp, cudaStream_t s) {
+  if (n <= 0) return;
+  const int64_t tiles = (n + kSortTile - 1) / kSortTile;
+  auto* sums = static_cast<unsigned long long*>(temp);
+  k_scan_tile_sums<<<static_cast<unsigned>(tiles), kSortThreads, 0, s>>>(in, order, n, sums);
+  k_scan_tile_prefix<<<1, 1024, 0, s>>>(sums, tiles);
+  k_scan_tile_apply<<<static_cast<unsigned>(tiles), kSortThreads, 0, s>>>(in, order, n, sums, out);
+  DW_CUDA(cudaGetLastError());
+}
+
+void launch_depth_keys(int P, const float* depths, const int* radii, uint32_t* dkey, uint32_t* ids,
+                       cudaStream_t s) {
+  if (P <= 0) return;
+  k_iota_depthkey<<<blocks_for(P, 256), 256, 0, s>>>(P, depths, radii, dkey, ids);
+  DW_CUDA(cudaGetLastError());
+}
+
+void launch_duplicate_sorted(int P, const uint32_t* order, const float2* means2D, const int* radii,
+                             const uint64_t* offsets, const CamParams& cam, uint32_t* tile_ids,
+                             uint32_t* values, cudaStream_t s) {
+  if (P <= 0) return;
+  k_duplicate_sorted<<<blocks_for(P, 256), 256, 0, s>>>(P, order, means2D, radii, offsets,
+                                                        cam.tiles_x, cam.tiles_y, tile_ids, values);
+  DW_CUDA(cudaGetLastError());
+}
+
+void launch_ranges_u32(int64_t L, const uint32_t* tiles, uint2* ranges, cudaStream_t s) {
+  if (L <= 0) return;
+  k_ranges_u32<<<blocks_for(L, 256), 256, 0, s>>>(L, tiles, ranges);
+  DW_CUDA(cudaGetLastError());
+}
+
+void launch_make_keys(int64_t L, const uint32_t* tiles, const uint32_t* values, const float* depths,
+                      uint64_t* keys, cudaStream_t s) {
+  if (L <= 0) return;
+  k_make_keys<<<blocks_for(L, 256), 256, 0, s>>>(L, tiles, values, depths, keys);
+  DW_CUDA(cudaGetLastError());
+}
+
+}  // namespace dw

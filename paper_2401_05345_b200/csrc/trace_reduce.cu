@@ -25,6 +25,8 @@ __global__ void __launch_bounds__(256) k_reduce_trace(const uint32_t* __restrict
   const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   uint32_t nred = 0;
+  bool issuer = false;
+  const int slot = bfly_slot<N>(lane, &issuer);
   for (int64_t r = w0; r < R; r += nw) {
     const uint32_t a = __ldg(active + r);
     const int idx = __ldg(prim + r * 32 + lane);
@@ -36,7 +38,7 @@ __global__ void __launch_bounds__(256) k_reduce_trace(const uint32_t* __restrict
     if (POL == kNative) {
       native_atomics<N, COUNT>(grad + static_cast<int64_t>(idx) * N, v, act, nred);
     } else if (POL == kSwB) {
-      reduce_bfly<N, COUNT, false>(idx, grad, v, thr, act, lane, nred, a);
+      reduce_bfly<N, COUNT, false>(idx, grad, v, thr, act, lane, nred, a, slot, issuer);
     } else if (POL == kSwS) {
       reduce_serial<N, COUNT>(idx, grad, v, thr, act, lane, nred, a);
     } else {

@@ -138,6 +138,16 @@ class GaussianRasterizer:
         return img, grad
 
 
+def render_views_host(rast: "GaussianRasterizer", scene_ptrs, P: int, cams, dL_ptr: int,
+                      policy: Policy, images_ptr, grad_ptr: int, stream=None) -> None:
+    """dw_render_views_host over raw host pointers (pinned for overlap):
+    scene_ptrs = (means3D, scales, rotations, opacities, colors)."""
+    arr = (_lib.CameraC * len(cams))(*[c.to_c() for c in cams])
+    check(lib().dw_render_views_host(rast.handle, P, *scene_ptrs, arr, len(cams), dL_ptr,
+                                     int(policy.kind), policy.threshold, images_ptr, grad_ptr,
+                                     None if stream is None else _stream(stream)))
+
+
 def microbench_red(pattern: int, ops: int = 1 << 28, stream=None) -> float:
     """Measured REDs/s: 0 distinct, 1 same-address warp, 2 v4, 3 DISTWAR 9-lane."""
     out = C.c_double()
