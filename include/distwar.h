@@ -183,6 +183,27 @@ dw_status dw_render_backward(dw_rasterizer* r, const float* dL_dpixels,
                              dw_policy_kind policy, int32_t threshold, float* grad,
                              uint64_t* pairs_out, void* stream);
 
+/* Preprocess backward (the step before the all-reduce): turns
+ * this view's screen-space grad2d[P*9] (dw_render_backward output) into 3D
+ * gradients, ADDED into grad3d[P*14] = (means3D xyz, scales xyz, rotation
+ * r x y z, opacity, r g b). means3D/scales/rotations are the forward's inputs
+ * (device). Accumulating over views yields the training gradient. */
+dw_status dw_preprocess_backward(dw_rasterizer* r, const float* means3D, const float* scales,
+                                 const float* rotations, const float* grad2d, float* grad3d,
+                                 void* stream);
+
+/* Adam step over the scene's parameters (device, updated in place) from
+ * grad3d[P*14]; exp_avg / exp_avg_sq are caller-owned [P*14] moment buffers
+ * (zero-initialised); step >= 1 (bias correction); lr per group: means,
+ * scales, rotations, opacities, colors. */
+typedef struct dw_adam_config {
+  float lr[5];
+  float beta1, beta2, eps;
+} dw_adam_config;
+dw_status dw_adam_step(int32_t P, float* means3D, float* scales, float* rotations,
+                       float* opacities, float* colors, const float* grad3d, float* exp_avg,
+                       float* exp_avg_sq, const dw_adam_config* cfg, int32_t step, void* stream);
+
 /* Number of global REDs issued by the last render_backward called with a
  * non-NULL pairs_out (the counting instantiation). */
 dw_status dw_rasterizer_last_reds(const dw_rasterizer* r, uint64_t* out);

@@ -498,3 +498,42 @@ class Ref:
         self._check(self.L.ref_time_policy(h, kind, threshold, num_prims, threads, max_records,
                                            C.byref(s), C.byref(c), C.byref(q)))
         return s.value, c.value, q.value
+
+
+def _gs_pb_setup(L):
+    L.gs_preprocess_backward.argtypes = [C.POINTER(_GsState), C.c_int32, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.POINTER(Camera), C.c_void_p, C.c_void_p]
+    L.gs_adam.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
+                          C.c_double, C.c_double, C.c_double, C.c_int]
+
+
+def gs_train_grads(orc: "Oracle", scene, cam: Camera, dL_dpixels, threads=8):
+    """CPU oracle of one view's full backward: (grad2d [P,9], grad3d [P,14])."""
+    L = orc.L
+    _gs_pb_setup(L)
+    P = int(scene["means3D"].shape[0])
+    ins = [np.ascontiguousarray(scene[k], np.float32)
+           for k in ("means3D", "scales", "rotations", "opacities", "colors")]
+    st = orc.gs_prepare(scene, cam, threads)
+    try:
+        dL = np.ascontiguousarray(dL_dpixels, np.float32)
+        g2 = np.zeros(P * NPARAM, np.float64)
+        pairs = C.c_int64()
+        if L.gs_backward(st, C.byref(cam), dL.ctypes.data, g2.ctypes.data, None, threads, 1, 0,
+                         C.byref(pairs)):
+            raise RuntimeError(L.gs_last_error().decode())
+        g3 = np.zeros(P * 14, np.float64)
+        if L.gs_preprocess_backward(st, P, ins[0].ctypes.data, ins[1].ctypes.data,
+                                    ins[2].ctypes.data, C.byref(cam), g2.ctypes.data,
+                                    g3.ctypes.data):
+            raise RuntimeError(L.gs_last_error().decode())
+        return g2.reshape(P, NPARAM), g3.reshape(P, 14)
+    finally:
+        orc.gs_free(st)
+
+
+def gs_adam(orc: "Oracle", param, grad, m, v, lr, beta1, beta2, eps, step):
+    """In-place float64 Adam step on contiguous float64 arrays."""
+    _gs_pb_setup(orc.L)
+    orc.L.gs_adam(param.size, param.ctypes.data, grad.ctypes.data, m.ctypes.data, v.ctypes.data,
+                  lr, beta1, beta2, eps, step)

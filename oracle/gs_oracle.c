@@ -508,3 +508,156 @@ int gs_backward(gs_state* s, const gs_camera* cam, const float* dL_dpixels,
   if (pairs_out) *pairs_out = pairs;
   return 0;
 }
+
+/* ------------------------------------------------- preprocess backward (f1)
+ * Restates the public 3DGS preprocess backward (Kerbl et al. 2023, their
+ * computeCov2D / computeCov3D / preprocess backward) in float64, for
+ * Sigma = R diag(s^2) R^T from a normalised (r, x, y, z) quaternion (the
+ * normalisation is differentiated too), cov2D = T Sigma T^T + 0.3 I with
+ * T = J W, and ndc = (P m)_xy / (P m)_w. Conventions of the screen-space
+ * gradients (gs_backward): mean2D is d/d ndc (pixel gradient x 0.5 W), the
+ * conic off-diagonal is HALF of d/d b. The clamp of the view-space x/y in J
+ * zeroes the x/y gradient (as 3DGS); mean gradients flow through both the
+ * projection and the covariance. Invisible Gaussians (radius 0) get none. */
+int gs_preprocess_backward(const gs_state* s, int32_t P, const float* means3D,
+                           const float* scales, const float* rotations,
+                           const gs_camera* cam, const double* grad2d, double* grad3d) {
+  if (!s || !means3D || !scales || !rotations || !cam || !grad2d || !grad3d)
+    return fail("null argument");
+  if (s->P != P || !s->radii) return fail("gs_preprocess_backward: forward state mismatch");
+  const float* vm = cam->viewmatrix;
+  const float* pm = cam->projmatrix;
+  const double fx = (double)cam->width / (2.0 * cam->tan_fovx);
+  const double fy = (double)cam->height / (2.0 * cam->tan_fovy);
+  for (int i = 0; i < P; ++i) {
+    if (s->radii[i] <= 0) continue;
+    const double* g2 = grad2d + (size_t)i * GS_NPARAM;
+    double* g3 = grad3d + (size_t)i * GS_NPARAM3D;
+    const double mx = means3D[3 * i], my = means3D[3 * i + 1], mz = means3D[3 * i + 2];
+    /* covariance chain */
+    const double qr0 = rotations[4 * i], qx0 = rotations[4 * i + 1], qy0 = rotations[4 * i + 2],
+                 qz0 = rotations[4 * i + 3];
+    const double qn = sqrt(qr0 * qr0 + qx0 * qx0 + qy0 * qy0 + qz0 * qz0);
+    const double r = qr0 / qn, x = qx0 / qn, y = qy0 / qn, z = qz0 / qn;
+    double R[3][3] = {{1 - 2 * (y * y + z * z), 2 * (x * y - r * z), 2 * (x * z + r * y)},
+                      {2 * (x * y + r * z), 1 - 2 * (x * x + z * z), 2 * (y * z - r * x)},
+                      {2 * (x * z - r * y), 2 * (y * z + r * x), 1 - 2 * (x * x + y * y)}};
+    const double mod = cam->scale_modifier;
+    double sv[3], var[3];
+    for (int k = 0; k < 3; ++k) {
+      sv[k] = mod * scales[3 * i + k];
+      var[k] = sv[k] * sv[k];
+    }
+    double Sig[3][3];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b)
+        Sig[a][b] = R[a][0] * var[0] * R[b][0] + R[a][1] * var[1] * R[b][1] + R[a][2] * var[2] * R[b][2];
+    double t[3];
+    for (int a = 0; a < 3; ++a) t[a] = vm[a] * mx + vm[4 + a] * my + vm[8 + a] * mz + vm[12 + a];
+    const double limx = 1.3 * cam->tan_fovx, limy = 1.3 * cam->tan_fovy;
+    const double txtz = t[0] / t[2], tytz = t[1] / t[2];
+    const double xmul = (txtz < -limx || txtz > limx) ? 0.0 : 1.0;
+    const double ymul = (tytz < -limy || tytz > limy) ? 0.0 : 1.0;
+    const double tx = fmin(limx, fmax(-limx, txtz)) * t[2];
+    const double ty = fmin(limy, fmax(-limy, tytz)) * t[2];
+    const double tz = t[2];
+    double J[2][3] = {{fx / tz, 0, -fx * tx / (tz * tz)}, {0, fy / tz, -fy * ty / (tz * tz)}};
+    double Wm[3][3];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) Wm[a][b] = vm[b * 4 + a];
+    double T[2][3];
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 3; ++b) T[a][b] = J[a][0] * Wm[0][b] + J[a][1] * Wm[1][b] + J[a][2] * Wm[2][b];
+    double cov[2][2];
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) {
+        double acc = 0;
+        for (int k = 0; k < 3; ++k)
+          for (int l = 0; l < 3; ++l) acc += T[a][k] * Sig[k][l] * T[b][l];
+        cov[a][b] = acc;
+      }
+    const double A = cov[0][0] + 0.3, B = cov[0][1], Cc = cov[1][1] + 0.3;
+    const double D = A * Cc - B * B, D2 = D * D;
+    const double ga = g2[2], gb = 2.0 * g2[3], gc = g2[4];
+    const double dA = (-Cc * Cc * ga + B * Cc * gb - B * B * gc) / D2;
+    const double dC = (-B * B * ga + A * B * gb - A * A * gc) / D2;
+    const double dB = (2 * B * Cc * ga - (D + 2 * B * B) * gb + 2 * A * B * gc) / D2;
+    const double G[2][2] = {{dA, 0.5 * dB}, {0.5 * dB, dC}};
+    /* dL/dSigma = T^T G T ; dL/dT = 2 G T Sigma */
+    double dSig[3][3], dT[2][3], TS[2][3];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        double acc = 0;
+        for (int k = 0; k < 2; ++k)
+          for (int l = 0; l < 2; ++l) acc += T[k][a] * G[k][l] * T[l][b];
+        dSig[a][b] = acc;
+      }
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 3; ++b) TS[a][b] = T[a][0] * Sig[0][b] + T[a][1] * Sig[1][b] + T[a][2] * Sig[2][b];
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 3; ++b) dT[a][b] = 2 * (G[a][0] * TS[0][b] + G[a][1] * TS[1][b]);
+    /* dL/dJ = dT W^T */
+    double dJ[2][3];
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 3; ++b) dJ[a][b] = dT[a][0] * Wm[b][0] + dT[a][1] * Wm[b][1] + dT[a][2] * Wm[b][2];
+    const double tz2 = tz * tz, tz3 = tz2 * tz;
+    double dt[3];
+    dt[0] = xmul * (-fx / tz2) * dJ[0][2];
+    dt[1] = ymul * (-fy / tz2) * dJ[1][2];
+    dt[2] = -fx / tz2 * dJ[0][0] - fy / tz2 * dJ[1][1] + 2 * fx * tx / tz3 * dJ[0][2] +
+            2 * fy * ty / tz3 * dJ[1][2];
+    double dm[3];
+    for (int b = 0; b < 3; ++b) dm[b] = Wm[0][b] * dt[0] + Wm[1][b] * dt[1] + Wm[2][b] * dt[2];
+    /* projection path: ndc = (P m)_xy / ((P m)_w + 1e-7) */
+    const double hx = pm[0] * mx + pm[4] * my + pm[8] * mz + pm[12];
+    const double hy = pm[1] * mx + pm[5] * my + pm[9] * mz + pm[13];
+    const double hw = pm[3] * mx + pm[7] * my + pm[11] * mz + pm[15] + 1e-7;
+    for (int b = 0; b < 3; ++b) {
+      const double dnx = (pm[4 * b] * hw - hx * pm[4 * b + 3]) / (hw * hw);
+      const double dny = (pm[4 * b + 1] * hw - hy * pm[4 * b + 3]) / (hw * hw);
+      dm[b] += g2[0] * dnx + g2[1] * dny;
+    }
+    /* Sigma = R diag(var) R^T: dvar_k = (R^T dSig R)_kk; dR = 2 dSig R diag(var) */
+    double dR[3][3];
+    for (int k = 0; k < 3; ++k) {
+      double acc = 0;
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) acc += R[a][k] * dSig[a][b] * R[b][k];
+      g3[3 + k] += acc * 2.0 * mod * sv[k];
+    }
+    for (int a = 0; a < 3; ++a)
+      for (int k = 0; k < 3; ++k)
+        dR[a][k] = 2 * (dSig[a][0] * R[0][k] + dSig[a][1] * R[1][k] + dSig[a][2] * R[2][k]) * var[k];
+    const double dRr[3][3] = {{0, -2 * z, 2 * y}, {2 * z, 0, -2 * x}, {-2 * y, 2 * x, 0}};
+    const double dRx[3][3] = {{0, 2 * y, 2 * z}, {2 * y, -4 * x, -2 * r}, {2 * z, 2 * r, -4 * x}};
+    const double dRy[3][3] = {{-4 * y, 2 * x, 2 * r}, {2 * x, 0, 2 * z}, {-2 * r, 2 * z, -4 * y}};
+    const double dRz[3][3] = {{-4 * z, -2 * r, 2 * x}, {2 * r, -4 * z, 2 * y}, {2 * x, 2 * y, 0}};
+    double dqn[4] = {0, 0, 0, 0};
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        dqn[0] += dR[a][b] * dRr[a][b];
+        dqn[1] += dR[a][b] * dRx[a][b];
+        dqn[2] += dR[a][b] * dRy[a][b];
+        dqn[3] += dR[a][b] * dRz[a][b];
+      }
+    const double qv[4] = {r, x, y, z};
+    const double dot = qv[0] * dqn[0] + qv[1] * dqn[1] + qv[2] * dqn[2] + qv[3] * dqn[3];
+    for (int k = 0; k < 4; ++k) g3[6 + k] += (dqn[k] - qv[k] * dot) / qn;
+    for (int b = 0; b < 3; ++b) g3[b] += dm[b];
+    g3[10] += g2[5];
+    g3[11] += g2[6];
+    g3[12] += g2[7];
+    g3[13] += g2[8];
+  }
+  return 0;
+}
+
+void gs_adam(int64_t n, double* param, const double* grad, double* m, double* v, double lr,
+             double beta1, double beta2, double eps, int step) {
+  const double bc1 = 1.0 - pow(beta1, step), bc2 = 1.0 - pow(beta2, step);
+  for (int64_t i = 0; i < n; ++i) {
+    m[i] = beta1 * m[i] + (1.0 - beta1) * grad[i];
+    v[i] = beta2 * v[i] + (1.0 - beta2) * grad[i] * grad[i];
+    param[i] -= lr * (m[i] / bc1) / (sqrt(v[i] / bc2) + eps);
+  }
+}

@@ -66,6 +66,19 @@ int gs_backward(gs_state* s, const gs_camera* cam, const float* dL_dpixels,
                 double* grad, double* grad_abs, int threads, int tile_stride,
                 int tap, int64_t* pairs_out);
 
+#define GS_NPARAM3D 14 /* means3D xyz, scales xyz, rotation rxyz, opacity, rgb */
+
+/* Preprocess backward, float64: screen-space gradients
+ * grad2d[P*9] of one view (gs_backward's output for the SAME camera and
+ * scene as the last gs_forward) -> 3D gradients grad3d[P*14], ADDED. */
+int gs_preprocess_backward(const gs_state* s, int32_t P, const float* means3D,
+                           const float* scales, const float* rotations,
+                           const gs_camera* cam, const double* grad2d, double* grad3d);
+
+/* One Adam step (float64 reference) over n parameters. */
+void gs_adam(int64_t n, double* param, const double* grad, double* m, double* v, double lr,
+             double beta1, double beta2, double eps, int step);
+
 #ifdef __cplusplus
 }
 #endif

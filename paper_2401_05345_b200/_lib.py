@@ -81,6 +81,11 @@ class CameraC(C.Structure):
     ]
 
 
+class AdamConfigC(C.Structure):
+    _fields_ = [("lr", C.c_float * 5), ("beta1", C.c_float), ("beta2", C.c_float),
+                ("eps", C.c_float)]
+
+
 vp = C.c_void_p
 i32, i64, u64 = C.c_int32, C.c_int64, C.c_uint64
 
@@ -114,6 +119,8 @@ SIGNATURES = {
                                     C.POINTER(i64), vp]),
     "dw_render_backward": (C.c_int, [vp, vp, C.c_int, i32, vp, C.POINTER(u64), vp]),
     "dw_rasterizer_last_reds": (C.c_int, [vp, C.POINTER(u64)]),
+    "dw_preprocess_backward": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
+    "dw_adam_step": (C.c_int, [i32, vp, vp, vp, vp, vp, vp, vp, vp, C.c_void_p, i32, vp]),
     "dw_rasterizer_buffer": (C.c_int, [vp, i32, C.POINTER(vp), C.POINTER(i64)]),
     "dw_render_host": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, C.POINTER(CameraC), vp, C.c_int,
                                  i32, vp, vp, vp]),

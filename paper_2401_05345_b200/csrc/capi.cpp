@@ -29,6 +29,12 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
                        const float* rot, const float* op, const float* col, const dw_camera* cams,
                        int32_t V, const float* dL, int policy, int thr, float* out_images,
                        float* grad, cudaStream_t s);
+void raster_preprocess_backward(dw_rasterizer* r, const float* means3D, const float* scales,
+                                const float* rotations, const float* grad2d, float* grad3d,
+                                cudaStream_t s);
+void launch_adam(int P, float* means3D, float* scales, float* rotations, float* opacities,
+                 float* colors, const float* grad, float* m, float* v, const float lr[5], float b1,
+                 float b2, float eps, int step, cudaStream_t s);
 dw_rasterizer* raster_new();
 void raster_delete(dw_rasterizer* r);
 }  // namespace dw
@@ -408,6 +414,35 @@ dw_status dw_render_backward(dw_rasterizer* r, const float* dL_dpixels, dw_polic
   return guarded([&] {
     check_policy(policy, threshold);
     dw::raster_backward(r, dL_dpixels, policy, threshold, grad, pairs_out, dw::as_stream(stream));
+    return DW_OK;
+  });
+}
+
+dw_status dw_preprocess_backward(dw_rasterizer* r, const float* means3D, const float* scales,
+                                 const float* rotations, const float* grad2d, float* grad3d,
+                                 void* stream) {
+  if (!r || !means3D || !scales || !rotations || !grad2d || !grad3d)
+    return fail_invalid("null argument");
+  return guarded([&] {
+    dw::raster_preprocess_backward(r, means3D, scales, rotations, grad2d, grad3d,
+                                   dw::as_stream(stream));
+    return DW_OK;
+  });
+}
+
+dw_status dw_adam_step(int32_t P, float* means3D, float* scales, float* rotations,
+                       float* opacities, float* colors, const float* grad3d, float* exp_avg,
+                       float* exp_avg_sq, const dw_adam_config* cfg, int32_t step, void* stream) {
+  if (!cfg || (P > 0 && (!means3D || !scales || !rotations || !opacities || !colors || !grad3d ||
+                         !exp_avg || !exp_avg_sq)))
+    return fail_invalid("null argument");
+  return guarded([&] {
+    if (P < 0) throw std::invalid_argument("P must be >= 0");
+    if (step < 1) throw std::invalid_argument("adam step must be >= 1");
+    if (!(cfg->beta1 >= 0.f && cfg->beta1 < 1.f) || !(cfg->beta2 >= 0.f && cfg->beta2 < 1.f))
+      throw std::invalid_argument("adam betas must be in [0, 1)");
+    dw::launch_adam(P, means3D, scales, rotations, opacities, colors, grad3d, exp_avg, exp_avg_sq,
+                    cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, step, dw::as_stream(stream));
     return DW_OK;
   });
 }

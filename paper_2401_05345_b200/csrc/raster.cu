@@ -250,6 +250,13 @@ void raster_backward(dw_rasterizer* r, const float* dL, int policy, int thr, flo
 
 uint64_t raster_last_reds(const dw_rasterizer* r) { return r->last_reds; }
 
+void raster_preprocess_backward(dw_rasterizer* r, const float* means3D, const float* scales,
+                                const float* rotations, const float* grad2d, float* grad3d,
+                                cudaStream_t s) {
+  if (!r->forward_done) throw std::invalid_argument("preprocess_backward before render_forward");
+  launch_preprocess_backward(r->P, means3D, scales, rotations, r->radii, r->cam, grad2d, grad3d, s);
+}
+
 void raster_buffer(const dw_rasterizer* r, int which, const void** p, int64_t* count) {
   const int64_t P = r->P, I = r->num_rendered, npx = int64_t(r->W) * r->H;
   const int64_t nt = int64_t(r->cam.tiles_x) * r->cam.tiles_y;

@@ -12,6 +12,7 @@ namespace dw {
 constexpr int kTile = 16;         // 16x16-pixel tiles, one 256-thread CTA each
 constexpr int kBlock = kTile * kTile;
 constexpr int kNParam = 9;        // mean2D.xy, conic.xyz, opacity, rgb
+constexpr int kNParam3D = 14;     // means3D xyz, scales xyz, rotation rxyz, opacity, rgb
 
 // Kernel-parameter copy of dw_camera (lives in the constant bank).
 struct CamParams {
@@ -43,6 +44,14 @@ void launch_duplicate(int P, const float2* means2D, const float* depths, const i
                       uint32_t* values, cudaStream_t s);
 
 void launch_ranges(int64_t L, const uint64_t* keys, uint2* ranges, cudaStream_t s);
+
+// raster_train.cu: preprocess backward (adds into grad3d[P][14]) and Adam.
+void launch_preprocess_backward(int P, const float* means3D, const float* scales,
+                                const float* rotations, const int* radii, const CamParams& cam,
+                                const float* grad2d, float* grad3d, cudaStream_t s);
+void launch_adam(int P, float* means3D, float* scales, float* rotations, float* opacities,
+                 float* colors, const float* grad, float* m, float* v, const float lr[5], float b1,
+                 float b2, float eps, int step, cudaStream_t s);
 
 // raster_sort.cu: hand-written stable LSD radix sort + scan (no CUB).
 size_t radix_sort_temp_bytes(int64_t n);

@@ -20,7 +20,42 @@ from ._lib import check, lib
 from .warpred import Policy, PolicyKind
 
 NPARAM = 9
+NPARAM3D = 14
 GRAD_NAMES = ("mean2D.x", "mean2D.y", "conic.x", "conic.y", "conic.z", "opacity", "r", "g", "b")
+GRAD3D_NAMES = ("mean.x", "mean.y", "mean.z", "scale.x", "scale.y", "scale.z", "rot.r", "rot.x",
+                "rot.y", "rot.z", "opacity", "r", "g", "b")
+
+
+class Adam:
+    """Fused Adam over a scene dict of CUDA tensors (dw_adam_step); moments
+    are [P, 14] in the grad3d layout. lr per group: means, scales,
+    rotations, opacities, colors."""
+
+    def __init__(self, scene: dict, lr=(1.6e-4, 5e-3, 1e-3, 5e-2, 2.5e-3), betas=(0.9, 0.999),
+                 eps=1e-15):
+        import torch
+
+        self.scene = scene
+        P = int(scene["means3D"].shape[0])
+        dev = scene["means3D"].device
+        self.exp_avg = torch.zeros((P, NPARAM3D), dtype=torch.float32, device=dev)
+        self.exp_avg_sq = torch.zeros((P, NPARAM3D), dtype=torch.float32, device=dev)
+        self.cfg = _lib.AdamConfigC((C.c_float * 5)(*lr), betas[0], betas[1], eps)
+        self.t = 0
+
+    def step(self, grad3d, stream=None):
+        import torch
+
+        self.t += 1
+        s = self.scene
+        f32 = torch.float32
+        check(lib().dw_adam_step(
+            int(s["means3D"].shape[0]), _ptr(s["means3D"], "means3D", f32),
+            _ptr(s["scales"], "scales", f32), _ptr(s["rotations"], "rotations", f32),
+            _ptr(s["opacities"], "opacities", f32), _ptr(s["colors"], "colors", f32),
+            _ptr(grad3d, "grad3d", f32), _ptr(self.exp_avg, "exp_avg", f32),
+            _ptr(self.exp_avg_sq, "exp_avg_sq", f32), C.byref(self.cfg), self.t,
+            _stream(stream)))
 
 # dw_rasterizer_buffer ids
 BUFFERS = {"means2D": (0, np.float32, 2), "depths": (1, np.float32, 1),
@@ -111,6 +146,20 @@ class GaussianRasterizer:
             policy.threshold, _ptr(grad, "grad", torch.float32),
             C.byref(pairs) if count_pairs else None, _stream(stream)))
         return (grad, pairs.value) if count_pairs else grad
+
+    def preprocess_backward(self, means3D, scales, rotations, grad2d, grad3d=None, stream=None):
+        """Adds this view's 3D gradients (from grad2d [P, 9]) into grad3d
+        [P, 14] (means3D xyz, scales xyz, rotation rxyz, opacity, rgb)."""
+        import torch
+
+        if grad3d is None:
+            grad3d = torch.zeros((self.P, NPARAM3D), dtype=torch.float32, device=grad2d.device)
+        f32 = torch.float32
+        check(lib().dw_preprocess_backward(
+            self._h, _ptr(means3D, "means3D", f32), _ptr(scales, "scales", f32),
+            _ptr(rotations, "rotations", f32), _ptr(grad2d, "grad2d", f32),
+            _ptr(grad3d, "grad3d", f32), _stream(stream)))
+        return grad3d
 
     def buffer(self, name: str) -> np.ndarray:
         """Host copy of an intermediate buffer (parity tests)."""

@@ -227,3 +227,64 @@ def test_multithreaded_backward_equals_single(orc, small):
     np.testing.assert_allclose(ref8["grad"], ref1["grad"], rtol=1e-12, atol=1e-12)
     assert ref8["pairs"] == ref1["pairs"]
     np.testing.assert_array_equal(ref8["image"], ref1["image"])
+
+
+def test_preprocess_backward_matches_finite_differences(orc):
+    """3D gradients (means, scales, quaternion, opacity, colour) of the oracle
+    vs central differences of the float64 projection + blend chain."""
+    from oracle.bindings import gs_train_grads
+    from paper_2401_05345_b200.scene import make_camera, make_dL_dpixels, make_scene
+
+    W, H = 40, 32
+    sc = make_scene(16, W, H, seed=8)
+    cam = make_camera(W, H, yaw_deg=6.0)
+    dL = make_dL_dpixels(W, H, seed=9).astype(np.float64)
+    ref = orc.gs_render(sc, ocam(cam), dL.astype(np.float32))
+    tiles_of, order = _tiles_and_order(ref)
+    _, g3 = gs_train_grads(orc, sc, ocam(cam), dL.astype(np.float32), threads=1)
+
+    def loss(s):
+        pix, _, conic, _ = project64(s, cam)
+        return float((dL * blend64(order, tiles_of, pix, conic,
+                                   s["opacities"].astype(np.float64),
+                                   s["colors"].astype(np.float64), W, H, cam.bg)).sum())
+
+    base = {k: v.astype(np.float64) for k, v in sc.items()}
+    checked = 0
+    rng = np.random.default_rng(1)
+    for g in rng.permutation(order)[:8]:
+        want = g3[g]
+        fd = np.zeros(14)
+        slots = [("means3D", 0), ("means3D", 1), ("means3D", 2), ("scales", 0), ("scales", 1),
+                 ("scales", 2), ("rotations", 0), ("rotations", 1), ("rotations", 2),
+                 ("rotations", 3), ("opacities", None), ("colors", 0), ("colors", 1),
+                 ("colors", 2)]
+        for p, (key, col) in enumerate(slots):
+            h = 1e-6 * max(1.0, abs(base[key][g] if col is None else base[key][g, col]))
+            vals = []
+            for sgn in (+1, -1):
+                s = {k: v.copy() for k, v in base.items()}
+                if col is None:
+                    s[key][g] += sgn * h
+                else:
+                    s[key][g, col] += sgn * h
+                vals.append(loss(s))
+            fd[p] = (vals[0] - vals[1]) / (2 * h)
+        scale = np.abs(fd).max()
+        if scale == 0:
+            continue
+        np.testing.assert_allclose(want, fd, rtol=5e-3, atol=5e-3 * scale)
+        checked += 1
+    assert checked >= 6
+
+
+def test_adam_reference_step(orc):
+    from oracle.bindings import gs_adam
+
+    rng = np.random.default_rng(0)
+    p, g = rng.normal(size=50), rng.normal(size=50)
+    m, v = np.zeros(50), np.zeros(50)
+    p0 = p.copy()
+    gs_adam(orc, p, g, m, v, 1e-3, 0.9, 0.999, 1e-8, 1)
+    # first step of Adam: m_hat = g, v_hat = g^2 -> update lr * sign(g)
+    np.testing.assert_allclose(p0 - p, 1e-3 * g / (np.abs(g) + 1e-8), rtol=1e-9)
