@@ -183,6 +183,16 @@ dw_status dw_render_backward(dw_rasterizer* r, const float* dL_dpixels,
                              dw_policy_kind policy, int32_t threshold, float* grad,
                              uint64_t* pairs_out, void* stream);
 
+/* SW-B render_backward that also taps the rasterizer's per-warp WarpRecords
+ * (SURVEY §8(f2)): every (warp, Gaussian) with >= 1 active lane becomes one
+ * record (prim = the Gaussian in all 32 lanes, 9 grads per lane, zeros in
+ * inactive lanes), returned as a host trace that dw_trace_save writes as
+ * WRTRACEB -- the reference's simulator / tuner / reducers read it directly.
+ * At most max_records are kept; total_records (nullable) gets the count. */
+dw_status dw_render_backward_tap(dw_rasterizer* r, const float* dL_dpixels, int32_t threshold,
+                                 float* grad, int64_t max_records, dw_trace** out,
+                                 int64_t* total_records, void* stream);
+
 /* Preprocess backward (the step before the all-reduce): turns
  * this view's screen-space grad2d[P*9] (dw_render_backward output) into 3D
  * gradients, ADDED into grad3d[P*14] = (means3D xyz, scales xyz, rotation

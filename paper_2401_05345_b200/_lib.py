@@ -120,6 +120,8 @@ SIGNATURES = {
     "dw_render_backward": (C.c_int, [vp, vp, C.c_int, i32, vp, C.POINTER(u64), vp]),
     "dw_rasterizer_last_reds": (C.c_int, [vp, C.POINTER(u64)]),
     "dw_preprocess_backward": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
+    "dw_render_backward_tap": (C.c_int, [vp, vp, i32, vp, i64, C.POINTER(vp), C.POINTER(i64),
+                                         vp]),
     "dw_adam_step": (C.c_int, [i32, vp, vp, vp, vp, vp, vp, vp, vp, C.c_void_p, i32, vp]),
     "dw_rasterizer_buffer": (C.c_int, [vp, i32, C.POINTER(vp), C.POINTER(i64)]),
     "dw_render_host": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, C.POINTER(CameraC), vp, C.c_int,

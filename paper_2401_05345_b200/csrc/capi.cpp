@@ -32,6 +32,8 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
 void raster_preprocess_backward(dw_rasterizer* r, const float* means3D, const float* scales,
                                 const float* rotations, const float* grad2d, float* grad3d,
                                 cudaStream_t s);
+dw::HostTrace raster_backward_tap(dw_rasterizer* r, const float* dL, int thr, float* grad,
+                                  int64_t max_records, int64_t* total, cudaStream_t s);
 void launch_adam(int P, float* means3D, float* scales, float* rotations, float* opacities,
                  float* colors, const float* grad, float* m, float* v, const float lr[5], float b1,
                  float b2, float eps, int step, cudaStream_t s);
@@ -414,6 +416,22 @@ dw_status dw_render_backward(dw_rasterizer* r, const float* dL_dpixels, dw_polic
   return guarded([&] {
     check_policy(policy, threshold);
     dw::raster_backward(r, dL_dpixels, policy, threshold, grad, pairs_out, dw::as_stream(stream));
+    return DW_OK;
+  });
+}
+
+dw_status dw_render_backward_tap(dw_rasterizer* r, const float* dL_dpixels, int32_t threshold,
+                                 float* grad, int64_t max_records, dw_trace** out,
+                                 int64_t* total_records, void* stream) {
+  if (!r || !dL_dpixels || !grad || !out) return fail_invalid("null argument");
+  return guarded([&] {
+    check_policy(DW_POLICY_SW_B, threshold);
+    int64_t total = 0;
+    auto t = std::make_unique<dw_trace>();
+    t->t = dw::raster_backward_tap(r, dL_dpixels, threshold, grad, max_records, &total,
+                                   dw::as_stream(stream));
+    if (total_records) *total_records = total;
+    *out = t.release();
     return DW_OK;
   });
 }

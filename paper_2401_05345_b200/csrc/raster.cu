@@ -250,6 +250,80 @@ void raster_backward(dw_rasterizer* r, const float* dL, int policy, int thr, flo
 
 uint64_t raster_last_reds(const dw_rasterizer* r) { return r->last_reds; }
 
+// SW-B backward that also taps its WarpRecords into a host
+// trace: records sorted by (warp, descending list position) -- the order
+// each warp executed them; prim = the warp-uniform Gaussian id in all 32
+// lanes; grads lane-major f64 with zeros in inactive lanes (workload.hpp:41-65).
+dw::HostTrace raster_backward_tap(dw_rasterizer* r, const float* dL, int thr, float* grad,
+                                  int64_t max_records, int64_t* total, cudaStream_t s) {
+  if (!r->forward_done) throw std::invalid_argument("render_backward before render_forward");
+  if (max_records < 0) throw std::invalid_argument("max_records must be >= 0");
+  const size_t cap = static_cast<size_t>(std::max<int64_t>(max_records, 1));
+  TapBuf tb;
+  tb.cap = static_cast<unsigned long long>(max_records);
+  DW_CUDA(cudaMalloc(&tb.count, sizeof(unsigned long long)));
+  DW_CUDA(cudaMalloc(&tb.warp_id, cap * sizeof(int32_t)));
+  DW_CUDA(cudaMalloc(&tb.iteration, cap * sizeof(int32_t)));
+  DW_CUDA(cudaMalloc(&tb.active, cap * sizeof(uint32_t)));
+  DW_CUDA(cudaMalloc(&tb.prim, cap * 32 * sizeof(int32_t)));
+  DW_CUDA(cudaMalloc(&tb.vals, cap * 32 * kNParam * sizeof(float)));
+  struct Free {
+    TapBuf& t;
+    ~Free() {
+      cudaFree(t.count); cudaFree(t.warp_id); cudaFree(t.iteration); cudaFree(t.active);
+      cudaFree(t.prim); cudaFree(t.vals);
+    }
+  } guard{tb};
+  DW_CUDA(cudaMemsetAsync(tb.count, 0, sizeof(unsigned long long), s));
+  if (r->P > 0)
+    launch_backward_tap(r->cam, r->ranges, r->vals, r->means2D, r->conic_opacity, r->rgb,
+                        r->final_T, r->n_contrib, dL, thr, grad, tb, s);
+  unsigned long long count = 0;
+  DW_CUDA(cudaMemcpyAsync(&count, tb.count, sizeof(count), cudaMemcpyDeviceToHost, s));
+  DW_CUDA(cudaStreamSynchronize(s));
+  *total = static_cast<int64_t>(count);
+  const size_t R = std::min<size_t>(count, static_cast<size_t>(max_records));
+  std::vector<int32_t> wid(R), it(R), prim(R * 32);
+  std::vector<uint32_t> act(R);
+  std::vector<float> vals(R * 32 * kNParam);
+  if (R) {
+    DW_CUDA(cudaMemcpy(wid.data(), tb.warp_id, R * 4, cudaMemcpyDeviceToHost));
+    DW_CUDA(cudaMemcpy(it.data(), tb.iteration, R * 4, cudaMemcpyDeviceToHost));
+    DW_CUDA(cudaMemcpy(act.data(), tb.active, R * 4, cudaMemcpyDeviceToHost));
+    DW_CUDA(cudaMemcpy(prim.data(), tb.prim, R * 128, cudaMemcpyDeviceToHost));
+    DW_CUDA(cudaMemcpy(vals.data(), tb.vals, vals.size() * 4, cudaMemcpyDeviceToHost));
+  }
+  std::vector<size_t> order(R);
+  for (size_t i = 0; i < R; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+    return wid[a] != wid[b] ? wid[a] < wid[b] : it[a] > it[b];
+  });
+  dw::HostTrace t;
+  dw::scene_defaults(&t.scene);
+  t.scene.num_primitives = std::max(r->P, 1);
+  t.scene.params_per_primitive = kNParam;
+  t.scene.image_width = r->W;
+  t.scene.image_height = r->H;
+  t.scene.quantized_values = 0;
+  t.warp_id.resize(R);
+  t.iteration.resize(R);
+  t.active.resize(R);
+  t.prim.resize(R * 32);
+  t.grads.resize(R * 32 * kNParam);
+  for (size_t k = 0; k < R; ++k) {
+    const size_t i = order[k];
+    t.warp_id[k] = wid[i];
+    t.iteration[k] = it[i];
+    t.active[k] = act[i];
+    for (int l = 0; l < 32; ++l) {
+      t.prim[k * 32 + l] = prim[i * 32 + l];
+      for (int p = 0; p < kNParam; ++p)
+        t.grads[(k * 32 + l) * kNParam + p] = vals[(i * kNParam + p) * 32 + l];
+    }
+  }
+  return t;
+}
+
 void raster_preprocess_backward(dw_rasterizer* r, const float* means3D, const float* scales,
                                 const float* rotations, const float* grad2d, float* grad3d,
                                 cudaStream_t s) {

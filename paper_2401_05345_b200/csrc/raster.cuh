@@ -45,6 +45,23 @@ void launch_duplicate(int P, const float2* means2D, const float* depths, const i
 
 void launch_ranges(int64_t L, const uint64_t* keys, uint2* ranges, cudaStream_t s);
 
+// Device buffers of the backward's WarpRecord tap (SoA like dw_device_trace).
+struct TapBuf {
+  unsigned long long* count = nullptr;
+  unsigned long long cap = 0;
+  int32_t* warp_id = nullptr;
+  int32_t* iteration = nullptr;
+  uint32_t* active = nullptr;
+  int32_t* prim = nullptr;   // [cap][32]
+  float* vals = nullptr;     // [cap][9][32]
+};
+
+// SW-B backward that also records its per-warp records (raster_blend.cu).
+void launch_backward_tap(const CamParams& cam, const uint2* ranges, const uint32_t* values,
+                         const float2* means2D, const float4* co, const float4* rgb,
+                         const float* final_T, const uint32_t* n_contrib, const float* dL, int thr,
+                         float* grad, const TapBuf& tap, cudaStream_t s);
+
 // raster_train.cu: preprocess backward (adds into grad3d[P][14]) and Adam.
 void launch_preprocess_backward(int P, const float* means3D, const float* scales,
                                 const float* rotations, const int* radii, const CamParams& cam,

@@ -151,14 +151,17 @@ __global__ void __launch_bounds__(kBlock)
 #define DW_BWD_MIN_BLOCKS 5  // 5 x 256 threads/SM: <= 51 registers, no spills (ptxas -v)
 #endif
 
-template <int POL, bool COUNT>
+// TAP=true (a separate instantiation) also records every (warp, Gaussian)
+// WarpRecord with >= 1 active lane -- the reference's trace model
+// (workload.hpp:41-65) of the real rasterizer traffic, for WRTRACEB export.
+template <int POL, bool COUNT, bool TAP = false>
 __global__ void __launch_bounds__(kBlock, DW_BWD_MIN_BLOCKS)
     k_backward(const CamParams cam, const uint2* __restrict__ ranges,
                const uint32_t* __restrict__ values, const float2* __restrict__ means2D,
                const float4* __restrict__ conic_opacity, const float4* __restrict__ rgb,
                const float* __restrict__ final_Ts, const uint32_t* __restrict__ n_contrib,
                const float* __restrict__ dL_dpixels, int thr, float* __restrict__ grad,
-               unsigned long long* __restrict__ counters) {
+               unsigned long long* __restrict__ counters, const TapBuf tap) {
   __shared__ Staged sm[kBlock];
   __shared__ uint8_t s_mask[kBlock];
   __shared__ uint32_t s_wmax[kBlock / 32];
@@ -268,6 +271,21 @@ __global__ void __launch_bounds__(kBlock, DW_BWD_MIN_BLOCKS)
         }
         const int id = (int)__float_as_uint(g.z);
         if (COUNT && lane == 0) npairs += __popc(ballot);
+        if (TAP) {  // before the policy: reduce_bfly reduces v in place
+          unsigned long long slot = 0;
+          if (lane == 0) slot = atomicAdd(tap.count, 1ull);
+          slot = __shfl_sync(kFull, slot, 0);
+          if (slot < tap.cap) {
+            if (lane == 0) {
+              tap.warp_id[slot] = tile * (kBlock / 32) + w;
+              tap.iteration[slot] = (int32_t)contributor;
+              tap.active[slot] = ballot;
+            }
+            tap.prim[slot * 32 + lane] = id;
+#pragma unroll
+            for (int p = 0; p < kNParam; ++p) tap.vals[(slot * kNParam + p) * 32 + lane] = v[p];
+          }
+        }
         if (POL == kNative) {
           native_atomics<kNParam, COUNT>(grad + static_cast<int64_t>(id) * kNParam, v, act, nred);
         } else if (POL == kSwB) {
@@ -294,13 +312,24 @@ void launch_bwd(bool count, const CamParams& cam, const uint2* ranges, const uin
   const int grid = cam.tiles_x * cam.tiles_y;
   if (count)
     k_backward<POL, true><<<grid, kBlock, 0, s>>>(cam, ranges, values, means2D, co, rgb, fT, nc,
-                                                  dL, thr, grad, ctr);
+                                                  dL, thr, grad, ctr, TapBuf{});
   else
     k_backward<POL, false><<<grid, kBlock, 0, s>>>(cam, ranges, values, means2D, co, rgb, fT,
-                                                   nc, dL, thr, grad, nullptr);
+                                                   nc, dL, thr, grad, nullptr, TapBuf{});
 }
 
 }  // namespace
+
+void launch_backward_tap(const CamParams& cam, const uint2* ranges, const uint32_t* values,
+                         const float2* means2D, const float4* co, const float4* rgb,
+                         const float* final_T, const uint32_t* n_contrib, const float* dL, int thr,
+                         float* grad, const TapBuf& tap, cudaStream_t s) {
+  const int grid = cam.tiles_x * cam.tiles_y;
+  k_backward<kSwB, false, true><<<grid, kBlock, 0, s>>>(cam, ranges, values, means2D, co, rgb,
+                                                        final_T, n_contrib, dL, thr, grad, nullptr,
+                                                        tap);
+  DW_CUDA(cudaGetLastError());
+}
 
 void launch_forward_impl(const CamParams& cam, const uint2* ranges, const uint32_t* values,
                          const float2* means2D, const float4* conic_opacity, const float4* rgb,

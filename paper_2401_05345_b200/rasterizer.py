@@ -147,6 +147,24 @@ class GaussianRasterizer:
             C.byref(pairs) if count_pairs else None, _stream(stream)))
         return (grad, pairs.value) if count_pairs else grad
 
+    def render_backward_tap(self, dL_dpixels, threshold: int = 0, grad=None,
+                            max_records: int = 1 << 22, stream=None):
+        """SW-B backward that also returns the per-warp WarpRecords it
+        reduced, as a warpred.Trace (save with .save_binary -> WRTRACEB).
+        Returns (grad, trace, total_records)."""
+        import torch
+
+        from .warpred import Trace
+
+        if grad is None:
+            grad = torch.zeros((self.P, NPARAM), dtype=torch.float32, device=dL_dpixels.device)
+        h, total = C.c_void_p(), C.c_int64()
+        check(lib().dw_render_backward_tap(
+            self._h, _ptr(dL_dpixels, "dL_dpixels", torch.float32), threshold,
+            _ptr(grad, "grad", torch.float32), max_records, C.byref(h), C.byref(total),
+            _stream(stream)))
+        return grad, Trace(h.value), total.value
+
     def preprocess_backward(self, means3D, scales, rotations, grad2d, grad3d=None, stream=None):
         """Adds this view's 3D gradients (from grad2d [P, 9]) into grad3d
         [P, 14] (means3D xyz, scales xyz, rotation rxyz, opacity, rgb)."""
@@ -185,6 +203,60 @@ class GaussianRasterizer:
                                    dL.ctypes.data, int(policy.kind), policy.threshold,
                                    img.ctypes.data, grad.ctypes.data, None))
         return img, grad
+
+
+class ThresholdTuner:
+    """Online balancing-threshold selection for a training loop (SURVEY
+    §8(f4), tuner.hpp:15): on the first iteration and then
+    every `period` iterations, time one backward per threshold 0..32 on the
+    current view and keep the argmin, ties to the lowest t (tuner.cpp:46-49).
+    `timer(threshold) -> ms` may be injected; the default times
+    render_backward on a scratch gradient with CUDA events."""
+
+    def __init__(self, period: int = 2000, kind: PolicyKind = PolicyKind.sw_b, reps: int = 1,
+                 timer=None):
+        if period < 1:
+            raise ValueError("period must be >= 1")
+        if kind not in (PolicyKind.sw_s, PolicyKind.sw_b):
+            raise ValueError("only sw_s / sw_b take a threshold")
+        self.period, self.kind, self.reps, self.timer = period, kind, reps, timer
+        self.iteration = 0
+        self.chosen = None
+        self.history = []  # (iteration, chosen, {t: ms})
+
+    def _cuda_timer(self, rast, dL):
+        import torch
+
+        scratch = torch.zeros((rast.P, NPARAM), dtype=torch.float32, device=dL.device)
+
+        def time_t(t):
+            best = None
+            for _ in range(self.reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                rast.render_backward(dL, Policy(self.kind, t), grad=scratch)
+                e1.record()
+                e1.synchronize()
+                ms = e0.elapsed_time(e1)
+                best = ms if best is None else min(best, ms)
+            return best
+
+        return time_t
+
+    def policy(self, rast=None, dL=None) -> Policy:
+        """The policy for this iteration (re-tunes when due); call once per
+        iteration after render_forward of the view about to be back-propagated."""
+        if self.chosen is None or self.iteration % self.period == 0:
+            timer = self.timer or self._cuda_timer(rast, dL)
+            sweep = {t: timer(t) for t in range(33)}
+            best = 0
+            for t in range(1, 33):
+                if sweep[t] < sweep[best]:
+                    best = t
+            self.chosen = best
+            self.history.append((self.iteration, best, sweep))
+        self.iteration += 1
+        return Policy(self.kind, self.chosen)
 
 
 def render_views_host(rast: "GaussianRasterizer", scene_ptrs, P: int, cams, dL_ptr: int,
