@@ -37,21 +37,56 @@ constexpr int kSortThreads = 256;
 constexpr int kSortItems = 16;
 constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 elements
 
+constexpr int kWarps = kSortThreads / 32;
+
+// Lanes of this warp whose digit equals mine (warp multi-split by votes: one
+// ballot per digit bit instead of a __match_any_sync, which is a multi-cycle
+// instruction). Invalid lanes never match valid ones.
+__device__ __forceinline__ unsigned digit_peers(uint32_t d, int bits, bool valid) {
+  unsigned peers = __ballot_sync(kFull, valid);
+  if (!valid) peers = ~peers;
+  for (int b = 0; b < bits; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const unsigned m = __ballot_sync(kFull, bit);
+    peers &= bit ? m : ~m;
+  }
+  return peers;
+}
+
+// Per-tile digit histogram. A tile is ITEMS*256 consecutive elements; warp w
+// owns the contiguous chunk [w*ITEMS*32, (w+1)*ITEMS*32) and counts it into
+// a warp-private smem histogram, one update per distinct digit per warp
+// instruction (__match_any_sync aggregation: no atomics, no contention).
+template <int ITEMS>
 __global__ void __launch_bounds__(kSortThreads)
     k_upsweep(const uint32_t* __restrict__ keys, int64_t n, int shift, uint32_t mask,
-              uint32_t* __restrict__ counts, int64_t tiles) {
-  __shared__ uint32_t hist[256];
-  const int t = threadIdx.x;
-  hist[t] = 0;
+              int bits, uint32_t* __restrict__ counts, int64_t tiles) {
+  __shared__ uint32_t hist[kWarps][256];
+  const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+#pragma unroll
+  for (int k = 0; k < kWarps; ++k) hist[k][t] = 0;
   __syncthreads();
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kSortTile;
-#pragma unroll 4
-  for (int r = 0; r < kSortItems; ++r) {
-    const int64_t e = base + r * kSortThreads + t;
-    if (e < n) atomicAdd(&hist[(__ldg(keys + e) >> shift) & mask], 1u);
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * (ITEMS * kSortThreads) +
+                       static_cast<int64_t>(w) * ITEMS * 32;
+  uint32_t key[ITEMS];
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const int64_t e = base + k * 32 + lane;
+    key[k] = e < n ? __ldg(keys + e) : 0u;
+  }
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const bool valid = base + k * 32 + lane < n;
+    const uint32_t d = (key[k] >> shift) & mask;
+    const unsigned peers = digit_peers(d, bits, valid);
+    if (valid && (__ffs(peers) - 1) == lane) hist[w][d] += __popc(peers);
+    __syncwarp();
   }
   __syncthreads();
-  counts[static_cast<int64_t>(t) * tiles + blockIdx.x] = hist[t];
+  uint32_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kWarps; ++k) s += hist[k][t];
+  counts[static_cast<int64_t>(t) * tiles + blockIdx.x] = s;
 }
 
 // One block per digit: exclusive scan of counts[d][0..tiles) in place, total
@@ -109,50 +144,99 @@ __global__ void k_scan_digits(uint32_t* __restrict__ digit_total, int ndigits) {
   if (t < ndigits) digit_total[t] = s[t] - (t < ndigits ? digit_total[t] : 0u);
 }
 
+// Stable scatter of one tile. Same warp-contiguous chunks as the upsweep:
+// each warp ranks its ITEMS*32 elements against a warp-private running
+// digit counter (rank = counter + popc(peers below me); the lowest peer
+// lane advances the counter), keeping keys / values / ranks in registers;
+// then ONE block-wide exclusive prefix per digit over the warps (in warp
+// order) turns warp-local ranks into global positions. Element order inside
+// the tile is (warp, step, lane) = index order, so the pass is stable.
+// Three block barriers per tile.
+template <int ITEMS>
 __global__ void __launch_bounds__(kSortThreads)
     k_downsweep(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, int64_t n,
-                int shift, uint32_t mask, const uint32_t* __restrict__ counts, int64_t tiles,
-                const uint32_t* __restrict__ digit_base, uint32_t* __restrict__ keys_out,
-                uint32_t* __restrict__ vals_out) {
-  __shared__ uint32_t s_cnt[kSortThreads / 32][256];
-  __shared__ uint32_t s_base[256];
+                int shift, uint32_t mask, int bits, const uint32_t* __restrict__ counts,
+                int64_t tiles, const uint32_t* __restrict__ digit_base,
+                uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
+  constexpr int TILE = ITEMS * kSortThreads;
+  __shared__ uint32_t s_cnt[kWarps][256];  // warp digit counts -> tile-local offsets
+  __shared__ uint32_t s_dstart[256];       // tile-local start of each digit's run
+  __shared__ uint32_t s_gbase[256];        // global start of this tile's run of each digit
+  __shared__ uint32_t s_wsum[kWarps];
+  __shared__ uint32_t s_key[TILE], s_val[TILE];
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
   const uint32_t lt = (1u << lane) - 1u;
-  s_base[t] = digit_base[t] + counts[static_cast<int64_t>(t) * tiles + blockIdx.x];
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kSortTile;
-  for (int r = 0; r < kSortItems; ++r) {
-    const int64_t e = base + r * kSortThreads + t;
-    const bool valid = e < n;
-    uint32_t key = 0, val = 0;
-    if (valid) {
-      key = __ldg(keys + e);
-      val = __ldg(vals + e);
-    }
-    const uint32_t digit = valid ? (key >> shift) & mask : 0x100u + 0u;
 #pragma unroll
-    for (int k = 0; k < kSortThreads / 32; ++k) s_cnt[k][t] = 0;
-    __syncthreads();
-    const unsigned peers = __match_any_sync(kFull, digit);
-    const uint32_t wrank = __popc(peers & lt);
-    if (valid && wrank == 0) s_cnt[w][digit] = __popc(peers);
-    __syncthreads();
-    {  // thread t owns digit t: exclusive prefix over warps, advance the base
-      uint32_t run = s_base[t];
+  for (int k = 0; k < kWarps; ++k) s_cnt[k][t] = 0;
+  s_gbase[t] = digit_base[t] + counts[static_cast<int64_t>(t) * tiles + blockIdx.x];
+  const int64_t tile0 = static_cast<int64_t>(blockIdx.x) * TILE;
+  const int64_t base = tile0 + static_cast<int64_t>(w) * ITEMS * 32;
+  uint32_t key[ITEMS], val[ITEMS], rank[ITEMS];
 #pragma unroll
-      for (int k = 0; k < kSortThreads / 32; ++k) {
-        const uint32_t c = s_cnt[k][t];
-        s_cnt[k][t] = run;
-        run += c;
-      }
-      s_base[t] = run;
+  for (int k = 0; k < ITEMS; ++k) {
+    const int64_t e = base + k * 32 + lane;
+    key[k] = e < n ? __ldg(keys + e) : 0u;
+    val[k] = e < n ? __ldg(vals + e) : 0u;
+  }
+  __syncthreads();
+  // 1. rank inside the warp's contiguous chunk (warp-private counters)
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    const bool valid = base + k * 32 + lane < n;
+    const uint32_t d = (key[k] >> shift) & mask;
+    const unsigned peers = digit_peers(d, bits, valid);
+    const int leader = __ffs(peers) - 1;
+    uint32_t old = 0;
+    if (valid && leader == lane) {
+      old = s_cnt[w][d];
+      s_cnt[w][d] = old + __popc(peers);
     }
-    __syncthreads();
-    if (valid) {
-      const uint32_t pos = s_cnt[w][digit] + wrank;
-      keys_out[pos] = key;
-      vals_out[pos] = val;
+    rank[k] = __shfl_sync(kFull, old, leader) + __popc(peers & lt);
+    __syncwarp();
+  }
+  __syncthreads();
+  // 2. thread t owns digit t: tile total, exclusive scan over digits
+  uint32_t tot = 0;
+#pragma unroll
+  for (int k = 0; k < kWarps; ++k) tot += s_cnt[k][t];
+  uint32_t incl = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_wsum[w] = incl;
+  __syncthreads();
+  uint32_t start = incl - tot;
+  for (int k = 0; k < w; ++k) start += s_wsum[k];
+  s_dstart[t] = start;
+  uint32_t run = start;  // warp offsets inside the digit's run, in warp order
+#pragma unroll
+  for (int k = 0; k < kWarps; ++k) {
+    const uint32_t c = s_cnt[k][t];
+    s_cnt[k][t] = run;
+    run += c;
+  }
+  __syncthreads();
+  // 3. local sort through shared memory (stable: warp, step, lane order)
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    if (base + k * 32 + lane < n) {
+      const uint32_t local = s_cnt[w][(key[k] >> shift) & mask] + rank[k];
+      s_key[local] = key[k];
+      s_val[local] = val[k];
     }
-    __syncthreads();
+  }
+  __syncthreads();
+  // 4. coalesced write-out: consecutive threads write consecutive elements of
+  //    each digit's run
+  const int count = static_cast<int>(n - tile0 < TILE ? n - tile0 : TILE);
+  for (int i = t; i < count; i += kSortThreads) {
+    const uint32_t kk = s_key[i];
+    const uint32_t d = (kk >> shift) & mask;
+    const uint32_t g = s_gbase[d] + (static_cast<uint32_t>(i) - s_dstart[d]);
+    keys_out[g] = kk;
+    vals_out[g] = s_val[i];
   }
 }
 
@@ -343,8 +427,14 @@ inline unsigned blocks_for(int64_t n, int per) { return static_cast<unsigned>((n
 
 }  // namespace
 
+// Tile size per pass: 16 items/thread (4096-element tiles) once there are
+// enough tiles to fill every SM a few times over, else 4 (1024-element tiles)
+// so small inputs (the P-element depth sort) still spread over 148 SMs.
+constexpr int64_t kBigSortN = int64_t(148) * 4 * 4096;
+inline int sort_items(int64_t n) { return n >= kBigSortN ? 16 : 4; }
+
 size_t radix_sort_temp_bytes(int64_t n) {
-  const int64_t tiles = (n + kSortTile - 1) / kSortTile;
+  const int64_t tiles = (n + 1023) / 1024;  // worst case: 4-item tiles
   return (static_cast<size_t>(tiles) * 256 + 256) * sizeof(uint32_t) + 256;
 }
 
@@ -358,18 +448,27 @@ int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* 
                      cudaStream_t s) {
   int cur = 0;
   if (n <= 0 || bits <= 0) return cur;
-  const int64_t tiles = (n + kSortTile - 1) / kSortTile;
+  const int items = sort_items(n);
+  const int64_t tile_n = static_cast<int64_t>(items) * kSortThreads;
+  const int64_t tiles = (n + tile_n - 1) / tile_n;
   uint32_t* counts = static_cast<uint32_t*>(temp);
   uint32_t* digit = counts + static_cast<size_t>(tiles) * 256;
+  const unsigned grid = static_cast<unsigned>(tiles);
   for (int shift = 0; shift < bits; shift += 8) {
     const int b = bits - shift < 8 ? bits - shift : 8;
     const uint32_t mask = (1u << b) - 1u;
-    k_upsweep<<<static_cast<unsigned>(tiles), kSortThreads, 0, s>>>(k[cur], n, shift, mask, counts,
-                                                                    tiles);
+    if (items == 16)
+      k_upsweep<16><<<grid, kSortThreads, 0, s>>>(k[cur], n, shift, mask, b, counts, tiles);
+    else
+      k_upsweep<4><<<grid, kSortThreads, 0, s>>>(k[cur], n, shift, mask, b, counts, tiles);
     k_scan_rows<<<256, 1024, 0, s>>>(counts, tiles, digit);
     k_scan_digits<<<1, 256, 0, s>>>(digit, 256);
-    k_downsweep<<<static_cast<unsigned>(tiles), kSortThreads, 0, s>>>(
-        k[cur], v[cur], n, shift, mask, counts, tiles, digit, k[cur ^ 1], v[cur ^ 1]);
+    if (items == 16)
+      k_downsweep<16><<<grid, kSortThreads, 0, s>>>(k[cur], v[cur], n, shift, mask, b, counts,
+                                                    tiles, digit, k[cur ^ 1], v[cur ^ 1]);
+    else
+      k_downsweep<4><<<grid, kSortThreads, 0, s>>>(k[cur], v[cur], n, shift, mask, b, counts,
+                                                   tiles, digit, k[cur ^ 1], v[cur ^ 1]);
     cur ^= 1;
   }
   DW_CUDA(cudaGetLastError());
