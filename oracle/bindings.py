@@ -100,6 +100,7 @@ class _GsState(C.Structure):
         ("tap_active", C.POINTER(C.c_uint32)),
         ("tap_prim", C.POINTER(C.c_int32)),
         ("tap_grads", C.POINTER(C.c_double)),
+        ("tap_ppt", C.c_int32),
     ]
 
 
@@ -284,8 +285,10 @@ class Oracle:
 
     # -- Gaussian rasterizer ---------------------------------------------
     def gs_render(self, scene, cam: Camera, dL_dpixels=None, threads=1, tile_stride=1,
-                  tap=False, backward=True):
-        """Forward (+ backward) on the CPU oracle. Returns a dict of arrays."""
+                  tap=False, backward=True, tap_ppt=1):
+        """Forward (+ backward) on the CPU oracle. Returns a dict of arrays.
+        tap_ppt selects the record layout of the tap: 1 = one pixel per lane
+        (8x4 per warp), 2 = the GPU reduction kernel's two pixels per lane."""
         L = self.L
         st = L.gs_state_new()
         P = int(scene["means3D"].shape[0])
@@ -318,6 +321,7 @@ class Oracle:
                 grad = np.zeros(P * NPARAM, np.float64)
                 gabs = np.zeros(P * NPARAM, np.float64)
                 pairs = C.c_int64()
+                st.contents.tap_ppt = tap_ppt
                 rc = L.gs_backward(st, C.byref(cam), dL.ctypes.data, grad.ctypes.data,
                                    gabs.ctypes.data, threads, tile_stride, 1 if tap else 0,
                                    C.byref(pairs))
@@ -363,6 +367,7 @@ class Oracle:
         dL = np.ascontiguousarray(dL_dpixels, np.float32)
         grad = np.zeros(P * NPARAM, np.float64)
         pairs = C.c_int64()
+        st.contents.tap_ppt = 2  # records in the GPU reduction kernel's lane layout
         t0 = time.perf_counter()
         if L.gs_backward(st, C.byref(cam), dL.ctypes.data, grad.ctypes.data, None,
                          threads, tile_stride, tap, C.byref(pairs)):

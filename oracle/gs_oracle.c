@@ -361,17 +361,28 @@ static int tap_push(gs_state* s, int32_t warp, int32_t iter, uint32_t active,
 /* Backward of one warp (8x4 pixels) over its tile's list, back to front: the
  * GradComputation loop of PAPER.md:1481-1504 with the 3DGS analytic
  * gradients as the "..." and 9 atomicAdds per participating pixel. */
-static void backward_warp(job* jb, int tile, int w) {
+/* ppt = pixels per lane of the record layout: 1 = one 8x4 pixel block per
+ * warp (warp w of 8); 2 = the GPU's reduction-policy kernel layout
+ * (k_backward_ppt2): warp w of 4 owns an 8x8 block and lane l holds pixels
+ * (l & 7, l >> 3) and (l & 7, (l >> 3) + 4); the lane's record value is the
+ * sum of its pixels' gradients and it is active if either pixel is. */
+static void backward_warp(job* jb, int tile, int w, int ppt) {
   gs_state* s = jb->s;
   const gs_camera* cam = jb->cam;
   const uint32_t rs = s->ranges[2 * tile], re = s->ranges[2 * tile + 1];
   const int HW = s->H * s->W;
-  float T[32], Tfin[32], dLp[32][3], acc[32][3], lastc[32][3], lasta[32], bgdot[32];
-  uint32_t contrib[32], lastcontrib[32];
-  int inside[32], pxs[32], pys[32];
-  for (int l = 0; l < 32; ++l) {
+  const int npix = 32 * ppt;
+  float T[64], Tfin[64], dLp[64][3], acc[64][3], lastc[64][3], lasta[64], bgdot[64];
+  uint32_t contrib[64], lastcontrib[64];
+  int inside[64], pxs[64], pys[64];
+  for (int l = 0; l < npix; ++l) {
     int px, py;
-    pixel_of(tile, w * 32 + l, s->tiles_x, &px, &py);
+    if (ppt == 1) {
+      pixel_of(tile, w * 32 + l, s->tiles_x, &px, &py);
+    } else {
+      px = (tile % s->tiles_x) * GS_TILE + (w & 1) * 8 + (l & 7);
+      py = (tile / s->tiles_x) * GS_TILE + (w >> 1) * 8 + (l >> 3);
+    }
     pxs[l] = px;
     pys[l] = py;
     inside[l] = px < s->W && py < s->H;
@@ -390,15 +401,15 @@ static void backward_warp(job* jb, int tile, int w) {
     }
   }
   const float ddelx_dx = 0.5f * (float)s->W, ddely_dy = 0.5f * (float)s->H;
-  double g[32 * GS_NPARAM];
+  double g[64 * GS_NPARAM], rec[32 * GS_NPARAM];
   int32_t iter = 0;
   for (uint32_t jj = re; jj > rs; --jj, ++iter) {
     const uint32_t id = s->values[jj - 1];
     const float* co = s->conic_opacity + 4 * id;
     const float* col = s->rgb + 3 * id;
-    uint32_t active = 0;
+    uint64_t active = 0;
     memset(g, 0, sizeof g);
-    for (int l = 0; l < 32; ++l) {
+    for (int l = 0; l < npix; ++l) {
       if (!inside[l]) continue;
       contrib[l]--;
       if (contrib[l] >= lastcontrib[l]) continue;
@@ -433,11 +444,11 @@ static void backward_warp(job* jb, int tile, int w) {
       gl[3] = -0.5f * gdx * dy * dL_dG;
       gl[4] = -0.5f * gdy * dy * dL_dG;
       gl[5] = G * dL_dalpha;
-      active |= 1u << l;
+      active |= 1ull << l;
     }
     if (!active) continue;
-    for (int l = 0; l < 32; ++l) {
-      if (!(active >> l & 1u)) continue;
+    for (int l = 0; l < npix; ++l) {
+      if (!(active >> l & 1ull)) continue;
       jb->pairs++;
       if (jb->tap == 2) continue; /* records only */
       for (int p = 0; p < GS_NPARAM; ++p) {
@@ -446,15 +457,26 @@ static void backward_warp(job* jb, int tile, int w) {
         if (jb->gabs) jb->gabs[(size_t)id * GS_NPARAM + p] += fabs(v);
       }
     }
-    if (jb->tap) tap_push(&jb->tapbuf, tile * 8 + w, iter, active, (int32_t)id, g);
+    if (jb->tap) {
+      uint32_t lanes = 0;
+      for (int l = 0; l < 32; ++l) {
+        const int hit = (int)(active >> l & 1ull) | (ppt == 2 ? (int)(active >> (l + 32) & 1ull) : 0);
+        if (hit) lanes |= 1u << l;
+        for (int p = 0; p < GS_NPARAM; ++p)
+          rec[l * GS_NPARAM + p] = g[l * GS_NPARAM + p] +
+                                   (ppt == 2 ? g[(l + 32) * GS_NPARAM + p] : 0.0);
+      }
+      tap_push(&jb->tapbuf, tile * (8 / ppt) + w, iter, lanes, (int32_t)id, rec);
+    }
   }
 }
 
 static void* backward_worker(void* arg) {
   job* jb = arg;
   const int ntiles = jb->s->tiles_x * jb->s->tiles_y;
+  const int ppt = jb->s->tap_ppt == 2 ? 2 : 1;
   for (int tile = jb->tid * jb->stride; tile < ntiles; tile += jb->nthreads * jb->stride)
-    for (int w = 0; w < 8; ++w) backward_warp(jb, tile, w);
+    for (int w = 0; w < 8 / ppt; ++w) backward_warp(jb, tile, w, ppt);
   return NULL;
 }
 

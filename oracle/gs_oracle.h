@@ -46,6 +46,7 @@ typedef struct gs_state {
   uint32_t* tap_active;
   int32_t* tap_prim;     /* 32 per record (warp-uniform) */
   double* tap_grads;     /* 32*9 per record, lane-major */
+  int32_t tap_ppt;       /* record layout: 1 (8x4 px per warp) or 2 (8x8, 2 px per lane) */
 } gs_state;
 
 const char* gs_last_error(void);

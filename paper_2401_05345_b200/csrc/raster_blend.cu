@@ -151,17 +151,18 @@ __global__ void __launch_bounds__(kBlock)
 #define DW_BWD_MIN_BLOCKS 5  // 5 x 256 threads/SM: <= 51 registers, no spills (ptxas -v)
 #endif
 
-// TAP=true (a separate instantiation) also records every (warp, Gaussian)
-// WarpRecord with >= 1 active lane -- the reference's trace model
-// (workload.hpp:41-65) of the real rasterizer traffic, for WRTRACEB export.
-template <int POL, bool COUNT, bool TAP = false>
+// One pixel per thread -- the paper's GradComputation layout ("thread corr.
+// to pixel"). Production use: the native (naive-atomic)
+// baseline, whose fastest layout this is; the reduction policies run
+// k_backward_ppt2 below (any policy compiles here, for A/B runs).
+template <int POL, bool COUNT>
 __global__ void __launch_bounds__(kBlock, DW_BWD_MIN_BLOCKS)
     k_backward(const CamParams cam, const uint2* __restrict__ ranges,
                const uint32_t* __restrict__ values, const float2* __restrict__ means2D,
                const float4* __restrict__ conic_opacity, const float4* __restrict__ rgb,
                const float* __restrict__ final_Ts, const uint32_t* __restrict__ n_contrib,
                const float* __restrict__ dL_dpixels, int thr, float* __restrict__ grad,
-               unsigned long long* __restrict__ counters, const TapBuf tap) {
+               unsigned long long* __restrict__ counters) {
   __shared__ Staged sm[kBlock];
   __shared__ uint8_t s_mask[kBlock];
   __shared__ uint32_t s_wmax[kBlock / 32];
@@ -271,23 +272,197 @@ __global__ void __launch_bounds__(kBlock, DW_BWD_MIN_BLOCKS)
         }
         const int id = (int)__float_as_uint(g.z);
         if (COUNT && lane == 0) npairs += __popc(ballot);
-        if (TAP) {  // before the policy: reduce_bfly reduces v in place
-          unsigned long long slot = 0;
-          if (lane == 0) slot = atomicAdd(tap.count, 1ull);
-          slot = __shfl_sync(kFull, slot, 0);
-          if (slot < tap.cap) {
-            if (lane == 0) {
-              tap.warp_id[slot] = tile * (kBlock / 32) + w;
-              tap.iteration[slot] = (int32_t)contributor;
-              tap.active[slot] = ballot;
-            }
-            tap.prim[slot * 32 + lane] = id;
-#pragma unroll
-            for (int p = 0; p < kNParam; ++p) tap.vals[(slot * kNParam + p) * 32 + lane] = v[p];
-          }
-        }
         if (POL == kNative) {
           native_atomics<kNParam, COUNT>(grad + static_cast<int64_t>(id) * kNParam, v, act, nred);
+        } else if (POL == kSwB) {
+          reduce_bfly<kNParam, COUNT, true>(id, grad, v, thr, act, lane, nred, ballot, slot, issuer);
+        } else if (POL == kSwS) {
+          reduce_serial<kNParam, COUNT>(id, grad, v, thr, act, lane, nred, ballot);
+        } else {
+          reduce_cccl<kNParam, COUNT>(id, grad, v, act, lane, nred, ballot);
+        }
+      }
+    }
+  }
+  if (COUNT) {
+    flush_count(counters, npairs, lane);
+    flush_count(counters + 1, nred, lane);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Two pixels per thread (PPT = 2): 128 threads per 16x16 tile, warp w owns the
+// 8x8 block (column w & 1, row band w >> 1); lane l holds pixel (l & 7, l >> 3)
+// and the pixel 4 rows below. Per Gaussian, a lane first adds its two
+// pixels' 9 gradients in registers, then the warp runs the DISTWAR policy on
+// the lane sums (a lane is active if either pixel is). The mask / ballot /
+// staging overhead and the warp reduction are paid once per 64 pixels.
+// native keeps one RED per (active pixel, param): the paper's baseline.
+struct Pix {
+  float pfx, pfy, T, T_final, dLp0, dLp1, dLp2, bg_dot;
+  float acc0, acc1, acc2, lc0, lc1, lc2, last_alpha;
+  uint32_t last;
+  bool inside;
+};
+
+__device__ __forceinline__ void pix_init(Pix& s, int px, int py, const CamParams& cam,
+                                         const float* __restrict__ final_Ts,
+                                         const uint32_t* __restrict__ n_contrib,
+                                         const float* __restrict__ dL) {
+  s.inside = px < cam.W && py < cam.H;
+  const int pix = py * cam.W + px, HW = cam.H * cam.W;
+  s.pfx = (float)px;
+  s.pfy = (float)py;
+  s.T_final = s.inside ? final_Ts[pix] : 0.0f;
+  s.T = s.T_final;
+  s.last = s.inside ? n_contrib[pix] : 0u;
+  s.dLp0 = s.inside ? dL[pix] : 0.0f;
+  s.dLp1 = s.inside ? dL[HW + pix] : 0.0f;
+  s.dLp2 = s.inside ? dL[2 * HW + pix] : 0.0f;
+  s.bg_dot = cam.bg[0] * s.dLp0 + cam.bg[1] * s.dLp1 + cam.bg[2] * s.dLp2;
+  s.acc0 = s.acc1 = s.acc2 = s.lc0 = s.lc1 = s.lc2 = s.last_alpha = 0.0f;
+}
+
+// Activity test + (if active) gradient into v (added when ADD, else assigned).
+template <bool ADD>
+__device__ __forceinline__ bool pix_step(Pix& s, uint32_t contributor, const float4& g,
+                                         const float4& co, const float4& c, float hw, float hh,
+                                         float (&v)[kNParam]) {
+  const float dx = g.x - s.pfx, dy = g.y - s.pfy;
+  const float dxx = dx * dx, dxy = dx * dy, dyy = dy * dy;
+  const float power = -0.5f * (co.x * dxx + co.z * dyy) - co.y * dxy;
+  const float G = __expf(power);
+  const float alpha = fminf(0.99f, co.w * G);
+  const bool act = s.inside && contributor < s.last && power <= 0.0f && alpha >= 1.0f / 255.0f;
+  if (act) {
+    const float inv = __fdividef(1.0f, 1.0f - alpha);
+    s.T = s.T * inv;
+    const float dcd = alpha * s.T;
+    s.acc0 += s.last_alpha * (s.lc0 - s.acc0);
+    s.acc1 += s.last_alpha * (s.lc1 - s.acc1);
+    s.acc2 += s.last_alpha * (s.lc2 - s.acc2);
+    s.lc0 = c.x;
+    s.lc1 = c.y;
+    s.lc2 = c.z;
+    float dL_dalpha = (c.x - s.acc0) * s.dLp0;
+    dL_dalpha += (c.y - s.acc1) * s.dLp1;
+    dL_dalpha += (c.z - s.acc2) * s.dLp2;
+    dL_dalpha *= s.T;
+    s.last_alpha = alpha;
+    dL_dalpha += (-s.T_final * inv) * s.bg_dot;
+    const float q = G * (co.w * dL_dalpha);
+    const float qh = -0.5f * q;
+    const float r[kNParam] = {-q * (co.x * dx + co.y * dy) * hw, -q * (co.z * dy + co.y * dx) * hh,
+                              qh * dxx, qh * dxy, qh * dyy, G * dL_dalpha, dcd * s.dLp0,
+                              dcd * s.dLp1, dcd * s.dLp2};
+#pragma unroll
+    for (int p = 0; p < kNParam; ++p) v[p] = ADD ? v[p] + r[p] : r[p];
+  } else if (!ADD) {
+#pragma unroll
+    for (int p = 0; p < kNParam; ++p) v[p] = 0.0f;
+  }
+  return act;
+}
+
+#ifndef DW_PPT2_MIN_BLOCKS
+#define DW_PPT2_MIN_BLOCKS 6  // 6 x 128 threads/SM: <= 80 registers, no spills (ptxas -v)
+#endif
+
+template <int POL, bool COUNT, bool TAP = false>
+__global__ void __launch_bounds__(128, DW_PPT2_MIN_BLOCKS)
+    k_backward_ppt2(const CamParams cam, const uint2* __restrict__ ranges,
+                    const uint32_t* __restrict__ values, const float2* __restrict__ means2D,
+                    const float4* __restrict__ conic_opacity, const float4* __restrict__ rgb,
+                    const float* __restrict__ final_Ts, const uint32_t* __restrict__ n_contrib,
+                    const float* __restrict__ dL_dpixels, int thr, float* __restrict__ grad,
+                    unsigned long long* __restrict__ counters, const TapBuf tap) {
+  __shared__ Staged sm[kBlock];
+  __shared__ uint8_t s_mask[kBlock];
+  __shared__ uint32_t s_wmax[4];
+  const int tile = blockIdx.x, t = threadIdx.x, w = t >> 5, lane = t & 31;
+  const int tx0 = (tile % cam.tiles_x) * kTile, ty0 = (tile / cam.tiles_x) * kTile;
+  const int px = tx0 + (w & 1) * 8 + (lane & 7);
+  const int py = ty0 + (w >> 1) * 8 + (lane >> 3);
+  Pix a, b;
+  pix_init(a, px, py, cam, final_Ts, n_contrib, dL_dpixels);
+  pix_init(b, px, py + 4, cam, final_Ts, n_contrib, dL_dpixels);
+  const float hw = 0.5f * (float)cam.W, hh = 0.5f * (float)cam.H;
+  const uint2 range = ranges[tile];
+  const uint32_t wmax = __reduce_max_sync(kFull, max(a.last, b.last));
+  if (lane == 0) s_wmax[w] = wmax;
+  __syncthreads();
+  const uint32_t bmax = max(max(s_wmax[0], s_wmax[1]), max(s_wmax[2], s_wmax[3]));
+  // this warp's two 8x4 bands in the 8-bit staging mask (stage(): warp-of-8 layout)
+  const int wa = 4 * (w >> 1) + (w & 1), wb = wa + 2;
+  uint32_t nred = 0, npairs = 0;
+  bool issuer;
+  const int slot = bfly_slot<kNParam>(lane, &issuer);
+  const int rounds = (int)((bmax + kBlock - 1) / kBlock);
+  int todo = (int)bmax;
+  const uint32_t top = range.x + bmax;
+  for (int i = 0; i < rounds; ++i, todo -= kBlock) {
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int st = t + h * 128;
+      uint32_t mask = 0;
+      if (st < todo)
+        mask = stage(sm, st, values[top - 1 - (i * kBlock + st)], tx0, ty0, means2D,
+                     conic_opacity, rgb);
+      s_mask[st] = (uint8_t)mask;
+    }
+    __syncthreads();
+    const int n = min(kBlock, todo);
+    const uint32_t base = bmax - 1 - (uint32_t)(i * kBlock);
+    for (int k = 0; k * 32 < n; ++k) {
+      const int jl = k * 32 + lane;
+      unsigned bits = 0;
+      {
+        const uint32_t m = jl < n ? s_mask[jl] : 0u;
+        bits = __ballot_sync(kFull, (((m >> wa) | (m >> wb)) & 1u) && (base - (uint32_t)jl) < wmax);
+      }
+      while (bits) {
+        const int j = k * 32 + __ffs(bits) - 1;
+        bits &= bits - 1u;
+        const uint32_t contributor = base - (uint32_t)j;
+        const float4 g = sm[j].xyi;
+        const float4 co = sm[j].co;
+        const float4 c = sm[j].col;
+        float v[kNParam], vb[kNParam];
+        const bool act_a = pix_step<false>(a, contributor, g, co, c, hw, hh, v);
+        bool act_b;
+        if (POL == kNative) {
+          act_b = pix_step<false>(b, contributor, g, co, c, hw, hh, vb);
+        } else {
+          act_b = pix_step<true>(b, contributor, g, co, c, hw, hh, v);
+        }
+        const bool act = act_a || act_b;
+        const unsigned ballot = __ballot_sync(kFull, act);
+        if (ballot == 0u) continue;
+        const int id = (int)__float_as_uint(g.z);
+        if (COUNT) {
+          const uint32_t cnt = __popc(__ballot_sync(kFull, act_a)) + __popc(__ballot_sync(kFull, act_b));
+          if (lane == 0) npairs += cnt;
+        }
+        if (TAP) {  // the record the policy reduces: lane value = its two pixels' sum
+          unsigned long long rec = 0;
+          if (lane == 0) rec = atomicAdd(tap.count, 1ull);
+          rec = __shfl_sync(kFull, rec, 0);
+          if (rec < tap.cap) {
+            if (lane == 0) {
+              tap.warp_id[rec] = tile * 4 + w;
+              tap.iteration[rec] = (int32_t)contributor;
+              tap.active[rec] = ballot;
+            }
+            tap.prim[rec * 32 + lane] = id;
+#pragma unroll
+            for (int p = 0; p < kNParam; ++p) tap.vals[(rec * kNParam + p) * 32 + lane] = v[p];
+          }
+        }
+        float* base_g = grad + static_cast<int64_t>(id) * kNParam;
+        if (POL == kNative) {
+          native_atomics<kNParam, COUNT>(base_g, v, act_a, nred);
+          native_atomics<kNParam, COUNT>(base_g, vb, act_b, nred);
         } else if (POL == kSwB) {
           reduce_bfly<kNParam, COUNT, true>(id, grad, v, thr, act, lane, nred, ballot, slot, issuer);
         } else if (POL == kSwS) {
@@ -310,12 +485,24 @@ void launch_bwd(bool count, const CamParams& cam, const uint2* ranges, const uin
                 const uint32_t* nc, const float* dL, int thr, float* grad,
                 unsigned long long* ctr, cudaStream_t s) {
   const int grid = cam.tiles_x * cam.tiles_y;
+  // The reduction policies run two pixels per thread; native keeps the
+  // paper's thread-per-pixel kernel (its faster layout: 7.8 vs 8.2 ms on C3,
+  // profiles/r01/ab_ppt.jsonl), so the naive baseline is not handicapped.
+  if (POL != kNative) {
+    if (count)
+      k_backward_ppt2<POL, true><<<grid, 128, 0, s>>>(cam, ranges, values, means2D, co, rgb, fT,
+                                                       nc, dL, thr, grad, ctr, TapBuf{});
+    else
+      k_backward_ppt2<POL, false><<<grid, 128, 0, s>>>(cam, ranges, values, means2D, co, rgb, fT,
+                                                        nc, dL, thr, grad, nullptr, TapBuf{});
+    return;
+  }
   if (count)
     k_backward<POL, true><<<grid, kBlock, 0, s>>>(cam, ranges, values, means2D, co, rgb, fT, nc,
-                                                  dL, thr, grad, ctr, TapBuf{});
+                                                  dL, thr, grad, ctr);
   else
     k_backward<POL, false><<<grid, kBlock, 0, s>>>(cam, ranges, values, means2D, co, rgb, fT,
-                                                   nc, dL, thr, grad, nullptr, TapBuf{});
+                                                   nc, dL, thr, grad, nullptr);
 }
 
 }  // namespace
@@ -325,9 +512,9 @@ void launch_backward_tap(const CamParams& cam, const uint2* ranges, const uint32
                          const float* final_T, const uint32_t* n_contrib, const float* dL, int thr,
                          float* grad, const TapBuf& tap, cudaStream_t s) {
   const int grid = cam.tiles_x * cam.tiles_y;
-  k_backward<kSwB, false, true><<<grid, kBlock, 0, s>>>(cam, ranges, values, means2D, co, rgb,
-                                                        final_T, n_contrib, dL, thr, grad, nullptr,
-                                                        tap);
+  k_backward_ppt2<kSwB, false, true><<<grid, 128, 0, s>>>(cam, ranges, values, means2D, co, rgb,
+                                                          final_T, n_contrib, dL, thr, grad,
+                                                          nullptr, tap);
   DW_CUDA(cudaGetLastError());
 }
 

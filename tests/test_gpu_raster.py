@@ -120,8 +120,12 @@ def test_red_count_matches_reference_policy_on_tapped_trace(cuda, orc):
     sc = make_scene(P, W, H, seed=9)
     cam = make_camera(W, H)
     dL = make_dL_dpixels(W, H, seed=10)
-    ref = orc.gs_render(sc, _ocam(cam), dL, tap=True)
+    # native runs one pixel per lane (8x4 warp blocks); the reduction policies
+    # run two pixels per lane (8x8 blocks, lane value = its pixels' sum):
+    # tap the CPU backward in each layout
+    ref = orc.gs_render(sc, _ocam(cam), dL, tap=True, tap_ppt=1)
     tap = ref["tap"]
+    tap2 = orc.gs_render(sc, _ocam(cam), dL, tap=True, tap_ppt=2)["tap"]
     r = GaussianRasterizer()
     t = {k: torch.from_numpy(v).to(cuda) for k, v in sc.items()}
     r.render_forward(t["means3D"], t["scales"], t["rotations"], t["opacities"], t["colors"], cam)
@@ -130,7 +134,7 @@ def test_red_count_matches_reference_policy_on_tapped_trace(cuda, orc):
     from paper_2401_05345_b200 import _lib
     lib = _lib.lib()
     for kind, t_ in [(0, 0), (2, 0), (2, 12), (2, 33), (1, 0), (1, 20), (3, 0)]:
-        _, c = orc.apply_policy(tap, kind, t_, P)
+        _, c = orc.apply_policy(tap if kind == 0 else tap2, kind, t_, P)
         grad = torch.zeros((P, 9), dtype=torch.float32, device=cuda)
         pairs = C.c_uint64()
         _lib.check(lib.dw_render_backward(r.handle, torch.from_numpy(dL).to(cuda).data_ptr(),
@@ -158,7 +162,7 @@ def test_gpu_tap_matches_oracle_tap(cuda, orc, tmp_path):
     sc = make_scene(P, W, H, seed=9)
     cam = make_camera(W, H)
     dL = make_dL_dpixels(W, H, seed=10)
-    ref = orc.gs_render(sc, _ocam(cam), dL, tap=True)
+    ref = orc.gs_render(sc, _ocam(cam), dL, tap=True, tap_ppt=2)  # the GPU kernel's layout
     r = GaussianRasterizer()
     t = {k: torch.from_numpy(v).to(cuda) for k, v in sc.items()}
     r.render_forward(t["means3D"], t["scales"], t["rotations"], t["opacities"], t["colors"], cam)
@@ -177,6 +181,10 @@ def test_gpu_tap_matches_oracle_tap(cuda, orc, tmp_path):
     assert len(common) >= 0.999 * max(len(key_gpu), len(key_cpu))
     same_mask = sum(key_gpu[k][0] == key_cpu[k][0] for k in common)
     assert same_mask >= len(common) - 2
+    kk = sorted(k for k in common if key_gpu[k][0] == key_cpu[k][0])
+    gg = np.stack([key_gpu[k][1] for k in kk]).astype(np.float64)
+    gc = np.stack([key_cpu[k][1] for k in kk])
+    assert np.linalg.norm(gg - gc) / np.linalg.norm(gc) < GRAD_REL_L2
     path = str(tmp_path / "tap.wrtb")
     tr.save_binary(path)
     back = orc.load_binary(path)
