@@ -1,0 +1,64 @@
+"""Exercise every libdistwar kernel once on small inputs, for
+compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
+
+    compute-sanitizer --tool racecheck python tools/sanitize_driver.py
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    import torch
+
+    from paper_2401_05345_b200 import warpred as wr
+    from paper_2401_05345_b200.rasterizer import Adam, GaussianRasterizer, render_views_host
+    from paper_2401_05345_b200.scene import make_camera, make_dL_dpixels, make_scene, orbit_cameras
+
+    dev = torch.device("cuda:0")
+    # trace-driven kernels: every compiled N and policy, counted and not
+    for n in (1, 2, 3, 4, 5, 9, 17):
+        tr = wr.generate(wr.SceneSpec(num_primitives=300, params_per_primitive=n, image_width=64,
+                                      image_height=32, locality=0.7, activity_prob=0.6, seed=n))
+        d = wr.DeviceTrace(tr)
+        for kind, t in ((0, 0), (1, 8), (2, 8), (3, 0)):
+            wr.gpu_run(d, wr.Policy(wr.PolicyKind(kind), t))
+    # rasterizer: odd image size, all policies, tap, preprocess backward, Adam
+    P, W, H = 4000, 77, 53
+    sc = {k: torch.from_numpy(v).to(dev) for k, v in make_scene(P, W, H, seed=2).items()}
+    cam = make_camera(W, H)
+    dL = torch.from_numpy(make_dL_dpixels(W, H)).to(dev)
+    r = GaussianRasterizer()
+    r.render_forward(sc["means3D"], sc["scales"], sc["rotations"], sc["opacities"], sc["colors"], cam)
+    for kind, t in ((0, 0), (1, 8), (2, 8), (3, 0)):
+        r.render_backward(dL, wr.Policy(wr.PolicyKind(kind), t))
+        r.render_backward(dL, wr.Policy(wr.PolicyKind(kind), t), count_pairs=True)
+    g2, tr, _ = r.render_backward_tap(dL, threshold=4)
+    g3 = r.preprocess_backward(sc["means3D"], sc["scales"], sc["rotations"], g2)
+    Adam(sc).step(g3)
+    r.buffer("keys")
+    # a large-list scene (wide rects -> warp-cooperative duplication, 4096-tiles sort)
+    big = {k: torch.from_numpy(v).to(dev) for k, v in
+           make_scene(3000, 640, 480, seed=3, high_contention=True).items()}
+    cam2 = make_camera(640, 480)
+    r.render_forward(big["means3D"], big["scales"], big["rotations"], big["opacities"],
+                     big["colors"], cam2)
+    r.render_backward(torch.from_numpy(make_dL_dpixels(640, 480)).to(dev),
+                      wr.Policy(wr.PolicyKind.sw_b, 8))
+    # batched host path
+    cams = orbit_cameras(W, H, 3)
+    pin = {k: v.cpu().pin_memory() for k, v in sc.items()}
+    dLh = torch.stack([dL.cpu()] * 3).pin_memory()
+    img = torch.empty((3, 3, H, W)).pin_memory()
+    grad = torch.empty((P, 9)).pin_memory()
+    render_views_host(r, [pin[k].data_ptr() for k in ("means3D", "scales", "rotations",
+                                                      "opacities", "colors")],
+                      P, cams, dLh.data_ptr(), wr.Policy(wr.PolicyKind.sw_b, 8), img.data_ptr(),
+                      grad.data_ptr())
+    torch.cuda.synchronize()
+    print("sanitize driver OK")
+
+
+if __name__ == "__main__":
+    main()
