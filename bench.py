@@ -441,6 +441,21 @@ def main() -> None:
     prof = os.path.join(ROOT, "profiles", "backward_dram_bytes.json")
     if os.path.exists(prof):
         traffic = json.load(open(prof)).get(args.workload)
+    # issue roofline: warp instructions per launch (ncu, committed sweep at the
+    # nearest profiled threshold) over the measured launch time, against
+    # 148 SMs x 4 schedulers x 1 inst/cycle at the SM clock seen in the run
+    issue = None
+    inst_file = os.path.join(ROOT, "profiles", "backward_inst.json")
+    if os.path.exists(inst_file):
+        table = json.load(open(inst_file)).get(args.workload, {})
+        sw_b = {int(k.split(":")[1]): v for k, v in table.items() if k.startswith("sw_b:")}
+        if sw_b and clocks.get("sm_mhz"):
+            t_near = min(sw_b, key=lambda t: abs(t - thr))
+            ach = sw_b[t_near] / (mean_launch_ms * 1e-3)
+            peak = 148 * 4 * clocks["sm_mhz"] * 1e6
+            issue = {"bound": "issue", "achieved": ach, "peak": peak, "unit": "warp-inst/s",
+                     "frac": ach / peak, "inst_per_launch": sw_b[t_near],
+                     "inst_source": f"ncu sm__inst_executed.sum at sw_b:{t_near}"}
     reds_per_launch = reds_distwar / V
     red_rate = reds_per_launch / (mean_launch_ms * 1e-3)
     naive_launch_ms = statistics.mean(launches_nv)
@@ -477,6 +492,7 @@ def main() -> None:
                          "unit": "GB/s", "frac": achieved_gbs / hbm_peak, "traffic": traffic,
                          "kernel": "k_backward<sw_b>", "alg_bytes_per_launch": alg_bytes,
                          "mean_launch_ms": mean_launch_ms, "peak_source": peak_src},
+            "roofline_issue": issue,
             "roofline_l2_atomic": {
                 "distwar": {"reds_per_launch": reds_per_launch, "achieved": red_rate,
                             "peak": red_peaks["distwar_9lane"],

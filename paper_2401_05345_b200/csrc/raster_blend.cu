@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kBlock)
 // One pixel per thread -- the paper's GradComputation layout ("thread corr.
 // to pixel"). Production use: the native (naive-atomic)
 // baseline, whose fastest layout this is; the reduction policies run
-// k_backward_ppt2 below (any policy compiles here, for A/B runs).
+// k_backward_multi below (any policy compiles here, for A/B runs).
 template <int POL, bool COUNT>
 __global__ void __launch_bounds__(kBlock, DW_BWD_MIN_BLOCKS)
     k_backward(const CamParams cam, const uint2* __restrict__ ranges,
@@ -364,36 +364,58 @@ __device__ __forceinline__ bool pix_step(Pix& s, uint32_t contributor, const flo
   return act;
 }
 
-#ifndef DW_PPT2_MIN_BLOCKS
-#define DW_PPT2_MIN_BLOCKS 6  // 6 x 128 threads/SM: <= 80 registers, no spills (ptxas -v)
+// Pixels per lane of the reduction-policy kernel (A/B: -DDW_BWD_PPT=4).
+#ifndef DW_BWD_PPT
+#define DW_BWD_PPT 2
+#endif
+// CTAs per SM the register allocator must allow (ptxas -v: no spills):
+// PPT 2 -> 6 x 128 threads (<= 80 regs), PPT 4 -> 8 x 64 threads (<= 128 regs).
+#ifndef DW_MULTI_MIN_BLOCKS
+#define DW_MULTI_MIN_BLOCKS (DW_BWD_PPT == 4 ? 8 : 6)
 #endif
 
-template <int POL, bool COUNT, bool TAP = false>
-__global__ void __launch_bounds__(128, DW_PPT2_MIN_BLOCKS)
-    k_backward_ppt2(const CamParams cam, const uint2* __restrict__ ranges,
-                    const uint32_t* __restrict__ values, const float2* __restrict__ means2D,
-                    const float4* __restrict__ conic_opacity, const float4* __restrict__ rgb,
-                    const float* __restrict__ final_Ts, const uint32_t* __restrict__ n_contrib,
-                    const float* __restrict__ dL_dpixels, int thr, float* __restrict__ grad,
-                    unsigned long long* __restrict__ counters, const TapBuf tap) {
+// PPT pixels per lane: 256/PPT threads per 16x16 tile; warp w owns the
+// 8 x 4PPT block (column w & 1, row band w >> 1) and lane l holds pixels
+// (l & 7, (l >> 3) + 4k), k < PPT. Per Gaussian a lane sums its pixels' 9
+// gradients in registers, then the warp runs the DISTWAR policy on the lane
+// sums (a lane is active if any of its pixels is). Mask / ballot / staging
+// overhead and the warp reduction are paid once per 32 PPT pixels.
+template <int PPT, int POL, bool COUNT, bool TAP = false>
+__global__ void __launch_bounds__(256 / PPT, DW_MULTI_MIN_BLOCKS)
+    k_backward_multi(const CamParams cam, const uint2* __restrict__ ranges,
+                     const uint32_t* __restrict__ values, const float2* __restrict__ means2D,
+                     const float4* __restrict__ conic_opacity, const float4* __restrict__ rgb,
+                     const float* __restrict__ final_Ts, const uint32_t* __restrict__ n_contrib,
+                     const float* __restrict__ dL_dpixels, int thr, float* __restrict__ grad,
+                     unsigned long long* __restrict__ counters, const TapBuf tap) {
+  static_assert(POL != kNative, "native runs the thread-per-pixel kernel");
+  constexpr int NT = 256 / PPT, NW = 8 / PPT;
   __shared__ Staged sm[kBlock];
   __shared__ uint8_t s_mask[kBlock];
-  __shared__ uint32_t s_wmax[4];
+  __shared__ uint32_t s_wmax[NW];
   const int tile = blockIdx.x, t = threadIdx.x, w = t >> 5, lane = t & 31;
   const int tx0 = (tile % cam.tiles_x) * kTile, ty0 = (tile / cam.tiles_x) * kTile;
   const int px = tx0 + (w & 1) * 8 + (lane & 7);
-  const int py = ty0 + (w >> 1) * 8 + (lane >> 3);
-  Pix a, b;
-  pix_init(a, px, py, cam, final_Ts, n_contrib, dL_dpixels);
-  pix_init(b, px, py + 4, cam, final_Ts, n_contrib, dL_dpixels);
+  const int py = ty0 + (w >> 1) * (4 * PPT) + (lane >> 3);
+  Pix pxl[PPT];
+  uint32_t lmax = 0;
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    pix_init(pxl[k], px, py + 4 * k, cam, final_Ts, n_contrib, dL_dpixels);
+    lmax = max(lmax, pxl[k].last);
+  }
   const float hw = 0.5f * (float)cam.W, hh = 0.5f * (float)cam.H;
   const uint2 range = ranges[tile];
-  const uint32_t wmax = __reduce_max_sync(kFull, max(a.last, b.last));
+  const uint32_t wmax = __reduce_max_sync(kFull, lmax);
   if (lane == 0) s_wmax[w] = wmax;
   __syncthreads();
-  const uint32_t bmax = max(max(s_wmax[0], s_wmax[1]), max(s_wmax[2], s_wmax[3]));
-  // this warp's two 8x4 bands in the 8-bit staging mask (stage(): warp-of-8 layout)
-  const int wa = 4 * (w >> 1) + (w & 1), wb = wa + 2;
+  uint32_t bmax = 0;
+#pragma unroll
+  for (int k = 0; k < NW; ++k) bmax = max(bmax, s_wmax[k]);
+  // this warp's PPT 8x4 bands in the 8-bit staging mask (stage(): 8x4 layout)
+  uint32_t wbits = 0;
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) wbits |= 1u << (2 * ((w >> 1) * PPT + k) + (w & 1));
   uint32_t nred = 0, npairs = 0;
   bool issuer;
   const int slot = bfly_slot<kNParam>(lane, &issuer);
@@ -403,8 +425,8 @@ __global__ void __launch_bounds__(128, DW_PPT2_MIN_BLOCKS)
   for (int i = 0; i < rounds; ++i, todo -= kBlock) {
     __syncthreads();
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int st = t + h * 128;
+    for (int h = 0; h < PPT; ++h) {
+      const int st = t + h * NT;
       uint32_t mask = 0;
       if (st < todo)
         mask = stage(sm, st, values[top - 1 - (i * kBlock + st)], tx0, ty0, means2D,
@@ -416,11 +438,8 @@ __global__ void __launch_bounds__(128, DW_PPT2_MIN_BLOCKS)
     const uint32_t base = bmax - 1 - (uint32_t)(i * kBlock);
     for (int k = 0; k * 32 < n; ++k) {
       const int jl = k * 32 + lane;
-      unsigned bits = 0;
-      {
-        const uint32_t m = jl < n ? s_mask[jl] : 0u;
-        bits = __ballot_sync(kFull, (((m >> wa) | (m >> wb)) & 1u) && (base - (uint32_t)jl) < wmax);
-      }
+      const uint32_t m = jl < n ? s_mask[jl] : 0u;
+      unsigned bits = __ballot_sync(kFull, (m & wbits) != 0u && (base - (uint32_t)jl) < wmax);
       while (bits) {
         const int j = k * 32 + __ffs(bits) - 1;
         bits &= bits - 1u;
@@ -428,29 +447,26 @@ __global__ void __launch_bounds__(128, DW_PPT2_MIN_BLOCKS)
         const float4 g = sm[j].xyi;
         const float4 co = sm[j].co;
         const float4 c = sm[j].col;
-        float v[kNParam], vb[kNParam];
-        const bool act_a = pix_step<false>(a, contributor, g, co, c, hw, hh, v);
-        bool act_b;
-        if (POL == kNative) {
-          act_b = pix_step<false>(b, contributor, g, co, c, hw, hh, vb);
-        } else {
-          act_b = pix_step<true>(b, contributor, g, co, c, hw, hh, v);
+        float v[kNParam];
+        bool act = pix_step<false>(pxl[0], contributor, g, co, c, hw, hh, v);
+        uint32_t cnt = COUNT ? __popc(__ballot_sync(kFull, act)) : 0u;
+#pragma unroll
+        for (int q = 1; q < PPT; ++q) {
+          const bool a = pix_step<true>(pxl[q], contributor, g, co, c, hw, hh, v);
+          if (COUNT) cnt += __popc(__ballot_sync(kFull, a));
+          act = act || a;
         }
-        const bool act = act_a || act_b;
         const unsigned ballot = __ballot_sync(kFull, act);
         if (ballot == 0u) continue;
         const int id = (int)__float_as_uint(g.z);
-        if (COUNT) {
-          const uint32_t cnt = __popc(__ballot_sync(kFull, act_a)) + __popc(__ballot_sync(kFull, act_b));
-          if (lane == 0) npairs += cnt;
-        }
-        if (TAP) {  // the record the policy reduces: lane value = its two pixels' sum
+        if (COUNT && lane == 0) npairs += cnt;
+        if (TAP) {  // the record the policy reduces: lane value = its pixels' sum
           unsigned long long rec = 0;
           if (lane == 0) rec = atomicAdd(tap.count, 1ull);
           rec = __shfl_sync(kFull, rec, 0);
           if (rec < tap.cap) {
             if (lane == 0) {
-              tap.warp_id[rec] = tile * 4 + w;
+              tap.warp_id[rec] = tile * NW + w;
               tap.iteration[rec] = (int32_t)contributor;
               tap.active[rec] = ballot;
             }
@@ -459,11 +475,7 @@ __global__ void __launch_bounds__(128, DW_PPT2_MIN_BLOCKS)
             for (int p = 0; p < kNParam; ++p) tap.vals[(rec * kNParam + p) * 32 + lane] = v[p];
           }
         }
-        float* base_g = grad + static_cast<int64_t>(id) * kNParam;
-        if (POL == kNative) {
-          native_atomics<kNParam, COUNT>(base_g, v, act_a, nred);
-          native_atomics<kNParam, COUNT>(base_g, vb, act_b, nred);
-        } else if (POL == kSwB) {
+        if (POL == kSwB) {
           reduce_bfly<kNParam, COUNT, true>(id, grad, v, thr, act, lane, nred, ballot, slot, issuer);
         } else if (POL == kSwS) {
           reduce_serial<kNParam, COUNT>(id, grad, v, thr, act, lane, nred, ballot);
@@ -488,13 +500,14 @@ void launch_bwd(bool count, const CamParams& cam, const uint2* ranges, const uin
   // The reduction policies run two pixels per thread; native keeps the
   // paper's thread-per-pixel kernel (its faster layout: 7.8 vs 8.2 ms on C3,
   // profiles/r01/ab_ppt.jsonl), so the naive baseline is not handicapped.
-  if (POL != kNative) {
+  if constexpr (POL != kNative) {
+    constexpr int NT = 256 / DW_BWD_PPT;
     if (count)
-      k_backward_ppt2<POL, true><<<grid, 128, 0, s>>>(cam, ranges, values, means2D, co, rgb, fT,
-                                                       nc, dL, thr, grad, ctr, TapBuf{});
+      k_backward_multi<DW_BWD_PPT, POL, true><<<grid, NT, 0, s>>>(
+          cam, ranges, values, means2D, co, rgb, fT, nc, dL, thr, grad, ctr, TapBuf{});
     else
-      k_backward_ppt2<POL, false><<<grid, 128, 0, s>>>(cam, ranges, values, means2D, co, rgb, fT,
-                                                        nc, dL, thr, grad, nullptr, TapBuf{});
+      k_backward_multi<DW_BWD_PPT, POL, false><<<grid, NT, 0, s>>>(
+          cam, ranges, values, means2D, co, rgb, fT, nc, dL, thr, grad, nullptr, TapBuf{});
     return;
   }
   if (count)
@@ -512,9 +525,8 @@ void launch_backward_tap(const CamParams& cam, const uint2* ranges, const uint32
                          const float* final_T, const uint32_t* n_contrib, const float* dL, int thr,
                          float* grad, const TapBuf& tap, cudaStream_t s) {
   const int grid = cam.tiles_x * cam.tiles_y;
-  k_backward_ppt2<kSwB, false, true><<<grid, 128, 0, s>>>(cam, ranges, values, means2D, co, rgb,
-                                                          final_T, n_contrib, dL, thr, grad,
-                                                          nullptr, tap);
+  k_backward_multi<DW_BWD_PPT, kSwB, false, true><<<grid, 256 / DW_BWD_PPT, 0, s>>>(
+      cam, ranges, values, means2D, co, rgb, final_T, n_contrib, dL, thr, grad, nullptr, tap);
   DW_CUDA(cudaGetLastError());
 }
 
