@@ -27,13 +27,30 @@ __global__ void __launch_bounds__(256) k_reduce_trace(const uint32_t* __restrict
   uint32_t nred = 0;
   bool issuer = false;
   const int slot = bfly_slot<N>(lane, &issuer);
+  // software pipeline: the next record's N+2 loads are in flight while this
+  // record is reduced (streaming, L1-bypassing loads)
+  uint32_t a_n = 0;
+  int idx_n = 0;
+  float v_n[N];
+  if (w0 < R) {
+    a_n = __ldcs(active + w0);
+    idx_n = __ldcs(prim + w0 * 32 + lane);
+#pragma unroll
+    for (int p = 0; p < N; ++p) v_n[p] = __ldcs(vals + w0 * (32 * N) + p * 32 + lane);
+  }
   for (int64_t r = w0; r < R; r += nw) {
-    const uint32_t a = __ldg(active + r);
-    const int idx = __ldg(prim + r * 32 + lane);
-    const float* vr = vals + r * (32 * N) + lane;
+    const uint32_t a = a_n;
+    const int idx = idx_n;
     float v[N];
 #pragma unroll
-    for (int p = 0; p < N; ++p) v[p] = __ldg(vr + p * 32);
+    for (int p = 0; p < N; ++p) v[p] = v_n[p];
+    const int64_t rn = r + nw;
+    if (rn < R) {
+      a_n = __ldcs(active + rn);
+      idx_n = __ldcs(prim + rn * 32 + lane);
+#pragma unroll
+      for (int p = 0; p < N; ++p) v_n[p] = __ldcs(vals + rn * (32 * N) + p * 32 + lane);
+    }
     const bool act = (a >> lane) & 1u;
     if (POL == kNative) {
       native_atomics<N, COUNT>(grad + static_cast<int64_t>(idx) * N, v, act, nred);
