@@ -5,19 +5,21 @@ and ms/iter vs naive-atomic; L2-atomic roofline %).
     torchrun --nproc-per-node N bench.py --gpus N ...
 
 Workload (config.workload): BASELINE configs[2] -- 1M synthetic Gaussians,
-1920x1080 -- the scene the north_star target is stated on, with a batch of
-`--views-per-gpu` orbit views resident per GPU. A STEP is the backward pass
-of the rasterizer over those views (DISTWAR SW-B, balancing threshold tuned
-on the box with the reference's sweep rule) plus, for N > 1, the NCCL
-all-reduce of the per-Gaussian gradient buffer. One unit = one gradient
-contribution = (contributing pixel, Gaussian, param), 9 per pair
-(SURVEY.md §8(d)). Weak scaling: every rank renders its own views.
+1920x1080, the scene the north_star target is stated on -- rendered as
+BASELINE configs[4]'s structure: a fixed batch of `--views` (64) orbit views
+sharded across the N ranks (strong scaling), every rank's views resident in
+HBM. A STEP is the backward pass of the rasterizer over the rank's views
+(DISTWAR SW-B, balancing threshold tuned on the box with the reference's sweep
+rule) plus, for N > 1, the NCCL all-reduce of the per-Gaussian gradient
+buffer. `--views-per-gpu V` switches to weak scaling (V views per rank).
+One unit = one gradient contribution = (contributing pixel, Gaussian, param),
+9 per pair.
 
 Printed on rank 0 as ONE JSON line; `value` = all ranks' contributions / the
 max over ranks of the device-timed steps; `e2e` = the same metric through the
-host-buffer C-ABI call dw_render_host (pinned H2D of the scene and dL/dpixel,
-forward + backward, D2H of image and gradients), the figure to compare with
-the reference arm.
+host-buffer C-ABI call dw_render_views_host (pinned H2D of the scene and
+dL/dpixel, forward + backward, D2H of images and gradients), the figure to
+compare with the reference arm.
 """
 from __future__ import annotations
 
@@ -46,7 +48,12 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=WORKLOAD)
-    ap.add_argument("--views-per-gpu", type=int, default=4)
+    ap.add_argument("--views", type=int, default=64,
+                    help="view batch sharded across ranks (strong scaling)")
+    ap.add_argument("--views-per-gpu", type=int, default=0,
+                    help="if > 0: weak scaling, this many views per rank")
+    ap.add_argument("--naive-steps", type=int, default=0,
+                    help="timed steps of the naive comparison (0: max(3, steps // 4))")
     ap.add_argument("--threshold", default="auto", help="SW-B balancing threshold or 'auto'")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -263,14 +270,20 @@ def main() -> None:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
+    from paper_2401_05345_b200.dist import shard_views
+
     P, W, H, hc, _ = CONFIGS[args.workload]
-    V = args.views_per_gpu
+    weak = args.views_per_gpu > 0
+    total_views = args.views_per_gpu * world if weak else args.views
+    if total_views < world:
+        raise SystemExit("need at least one view per rank")
+    my_views = list(shard_views(total_views, world, rank))
+    V = len(my_views)
     sc = make_scene(P, W, H, seed=0, high_contention=hc)
-    cams = orbit_cameras(W, H, world * V)[rank * V:(rank + 1) * V] if world * V > 1 else \
-        [make_camera(W, H)]
+    all_cams = orbit_cameras(W, H, total_views) if total_views > 1 else [make_camera(W, H)]
+    cams = [all_cams[i] for i in my_views]
     t = {k: torch.from_numpy(v).to(dev) for k, v in sc.items()}
-    dLs = [torch.from_numpy(make_dL_dpixels(W, H, seed=1 + rank * V + i)).to(dev)
-           for i in range(V)]
+    dLs = [torch.from_numpy(make_dL_dpixels(W, H, seed=1 + i)).to(dev) for i in my_views]
     stream = torch.cuda.current_stream()
 
     # ---- forward: resident per-view states (timed for forward fps) -------
@@ -378,7 +391,9 @@ def main() -> None:
     sampler = ClockSampler(local)
     time.sleep(0.3)
     total_ms, launches = run_steps(policy, args.steps, args.warmup)
-    total_nv_ms, launches_nv = run_steps(wr.Policy(wr.PolicyKind.native, 0), args.steps, args.warmup)
+    nv_steps = args.naive_steps or max(3, args.steps // 4)
+    total_nv_ms, launches_nv = run_steps(wr.Policy(wr.PolicyKind.native, 0), nv_steps,
+                                         min(args.warmup, 3))
     clocks = sampler.stop()
 
     ms_per_step = total_ms / args.steps
@@ -388,7 +403,7 @@ def main() -> None:
         dist.all_reduce(c)
         contrib_job = float(c.item())
     value = contrib_job * args.steps / (total_ms * 1e-3)
-    naive_value = contrib_job * args.steps / (total_nv_ms * 1e-3)
+    naive_value = contrib_job * nv_steps / (total_nv_ms * 1e-3)
 
     # ---- e2e through the host-buffer C-ABI call (dw_render_views_host) ---
     # per step: pinned H2D of the scene + the V views' dL/dpixel, forward +
@@ -473,15 +488,18 @@ def main() -> None:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
             "config": {"workload": args.workload, "gaussians": P, "width": W, "height": H,
-                       "views_per_gpu": V, "policy": "sw_b", "threshold": thr,
+                       "views_total": total_views, "views_per_gpu": V,
+                       "policy": "sw_b", "threshold": thr,
                        "parallelism": f"dp{world} (views) + NCCL all-reduce of grad[P,9]"
                        if world > 1 else "dp1",
                        "l2": "flushed between steps (256 MiB write, outside the events)"},
             "gpu_launches": args.steps * V,
             "clocks": clocks,
-            "naive": {"value": naive_value, "ms_per_step": total_nv_ms / args.steps,
+            "naive": {"value": naive_value, "ms_per_step": total_nv_ms / nv_steps,
+                      "steps": nv_steps,
                       "speedup_distwar_vs_naive": naive_value and value / naive_value},
             "forward": {"ms_per_view": statistics.mean(fwd_ms),
                         "fps": 1e3 / statistics.mean(fwd_ms)},
