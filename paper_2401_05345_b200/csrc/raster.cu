@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 
 #include "distwar.cuh"
@@ -221,12 +222,16 @@ struct dw_rasterizer {
 
 namespace dw {
 
+// SM count of the current device, cached per device (thread-safe: a racing
+// first query just stores the same value twice).
 int sm_count() {
-  static int n = 0;
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  DW_CUDA(cudaGetDevice(&dev));
+  int n = (dev >= 0 && dev < 64) ? cache[dev].load(std::memory_order_relaxed) : 0;
   if (!n) {
-    int dev = 0;
-    DW_CUDA(cudaGetDevice(&dev));
     DW_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    if (dev >= 0 && dev < 64) cache[dev].store(n, std::memory_order_relaxed);
   }
   return n;
 }

@@ -9,6 +9,8 @@
 // line; HBM roofline: (132 + 128N) B/record.
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "distwar.cuh"
 #include "dw_internal.h"
 
@@ -131,10 +133,13 @@ namespace {
 template <int N, int POL, bool COUNT>
 void launch_n(const uint32_t* a, const int32_t* p, const float* v, int64_t R, int thr,
               float* g, unsigned long long* c, cudaStream_t s) {
-  static int blocks_per_sm = 0;
-  if (!blocks_per_sm)
+  static std::atomic<int> cached{0};  // occupancy of this instantiation (thread-safe)
+  int blocks_per_sm = cached.load(std::memory_order_relaxed);
+  if (!blocks_per_sm) {
     DW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm,
                                                           k_reduce_trace<N, POL, COUNT>, 256, 0));
+    cached.store(blocks_per_sm, std::memory_order_relaxed);
+  }
   const int64_t want = (R + 7) / 8;
   const int64_t cap = static_cast<int64_t>(sm_count()) * (blocks_per_sm ? blocks_per_sm : 1);
   const int grid = static_cast<int>(want < cap ? want : cap);
