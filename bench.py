@@ -187,57 +187,69 @@ def cpu_port_baseline(sc, cam, dL, stride: int) -> dict:
                       f"backward on {threads} threads"}
 
 
-def reference_arm(args) -> None:
-    """--impl reference: the reference's own CPU implementation of the path.
-    The reference (warpred) implements the reduction stage only
+def reference_measure(workload: str, steps: int, warmup: int, stride: int):
+    """The reference's own CPU implementation of the path on this box's host
+    cores. The reference (warpred) implements the reduction stage only
     (reducers::apply_policy + per-address summation, oracle/_ref built from
     /root/reference); the per-pair 3DGS gradient math it lacks is the oracle
-    port producing the per-warp WarpRecords it consumes. Each step: port
-    gradient math over a tile-strided sample of view 0 (all host threads) +
-    reference SW-B reduction of those records (all host threads)."""
+    port producing the per-warp WarpRecords it consumes (in the GPU reduction
+    kernel's two-pixels-per-lane layout). Each step: port gradient math over a
+    tile-strided sample of view 0 (all host threads) + the reference's SW-B
+    reduction of those records (all host threads). Returns a cpu_baseline dict
+    plus the total seconds of the timed steps."""
     from oracle.bindings import REF_SO, Oracle, Ref
     from paper_2401_05345_b200.scene import CONFIGS, make_camera, make_dL_dpixels, make_scene
 
-    P, W, H, hc, _ = CONFIGS[args.workload]
+    P, W, H, hc, _ = CONFIGS[workload]
     sc = make_scene(P, W, H, seed=0, high_contention=hc)
     cam = make_camera(W, H)
     dL = make_dL_dpixels(W, H, seed=1)
     orc = Oracle()
     threads = host_threads()
     oc = to_ocam(cam)
-    stride = max(args.cpu_tile_stride, 16)
     have_ref = os.path.exists(REF_SO)
     ref = Ref() if have_ref else None
     st = orc.gs_prepare(sc, oc, threads)
     times, contribs = [], 0
     try:
-        for i in range(args.warmup + args.steps):
+        for i in range(warmup + steps):
             t_math, pairs, tap = orc.gs_backward_timed(st, oc, dL, threads, stride, tap=2)
             if ref is not None:
                 h = ref.from_trace(tap)
-                t_red, c, _ = ref.time_policy(h, 2, 0, P, threads)
+                t_red, _, _ = ref.time_policy(h, 2, 0, P, threads)
                 ref.free(h)
             else:  # reference not built here: the oracle restatement of it
                 t0 = time.perf_counter()
                 orc.apply_policy(tap, 2, 0, P)
-                t_red, c = time.perf_counter() - t0, tap.contributions()
-            if i >= args.warmup:
+                t_red = time.perf_counter() - t0
+            if i >= warmup:
                 times.append(t_math + t_red)
-                contribs += c
+                contribs += 9 * pairs
     finally:
         orc.gs_free(st)
     total = sum(times)
-    v = contribs / total
-    kind = "reference" if have_ref else "port"
+    return {"value": contribs / total, "unit": UNIT, "cores": threads,
+            "kind": "reference" if have_ref else "port",
+            "sample": f"every {stride}th tile of view 0 of {workload}, {steps} step(s): port "
+                      "gradient math + reference reducers::apply_policy(sw_b, 0) + per-address "
+                      f"sums, {threads} host threads"}, total
+
+
+def reference_arm(args) -> None:
+    """--impl reference: reference_measure() over the arm's --steps/--warmup."""
+    from paper_2401_05345_b200.scene import CONFIGS
+
+    P, W, H, _, _ = CONFIGS[args.workload]
+    stride = max(args.cpu_tile_stride, 16)
+    cpu, total = reference_measure(args.workload, args.steps, args.warmup, stride)
+    v = cpu["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": args.workload, "gaussians": P, "width": W,
                                         "height": H, "tile_stride": stride},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"every {stride}th tile of view 0 per step; "
-                                   "port gradient math + reference reducers::apply_policy(sw_b,0)"},
+        "cpu_baseline": cpu,
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -480,9 +492,13 @@ def main() -> None:
     if rank == 0 and not args.no_trace_family:
         tfam = trace_family()
 
-    cpu = None
+    cpu = cpu_port = None
     if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_port_baseline(sc, cams[0], make_dL_dpixels(W, H, seed=1), args.cpu_tile_stride)
+        # the reference's CPU path (oracle/_ref) on a bounded sample, and the
+        # oracle port's whole backward on every tile, both on this box's cores
+        cpu, _ = reference_measure(args.workload, 3, 1, 16)
+        cpu_port = cpu_port_baseline(sc, make_camera(W, H), make_dL_dpixels(W, H, seed=1),
+                                     args.cpu_tile_stride)
 
     if rank == 0:
         line = {
@@ -525,6 +541,7 @@ def main() -> None:
                             "backward of V views, D2H V images + grad (copy streams "
                             "double-buffered against compute)"},
             "cpu_baseline": cpu,
+            "cpu_port": cpu_port,
             "trace_family": tfam,
         }
         print(json.dumps(line), flush=True)
