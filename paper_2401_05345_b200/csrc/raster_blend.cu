@@ -147,6 +147,107 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+// Forward with two pixels per thread (128 threads per tile, warp = 8x8
+// block, lane pixels (l & 7, l >> 3) and 4 rows below), same staging and
+// masks; each pixel keeps its own early-termination state.
+struct FwdPix {
+  float pfx, pfy, T, C0, C1, C2;
+  uint32_t last;
+  bool done;
+};
+
+__device__ __forceinline__ void fwd_step(FwdPix& s, const float4& g, const float4& co,
+                                         const float4& c, uint32_t pos) {
+  if (s.done) return;
+  const float dx = g.x - s.pfx, dy = g.y - s.pfy;
+  const float power = -0.5f * (co.x * dx * dx + co.z * dy * dy) - co.y * dx * dy;
+  if (power > 0.0f) return;
+  const float alpha = fminf(0.99f, co.w * __expf(power));
+  if (alpha < 1.0f / 255.0f) return;
+  const float test_T = s.T * (1.0f - alpha);
+  if (test_T < 0.0001f) {
+    s.done = true;
+    return;
+  }
+  const float aT = alpha * s.T;
+  s.C0 += c.x * aT;
+  s.C1 += c.y * aT;
+  s.C2 += c.z * aT;
+  s.T = test_T;
+  s.last = pos;
+}
+
+__global__ void __launch_bounds__(128)
+    k_forward_ppt2(const CamParams cam, const uint2* __restrict__ ranges,
+                   const uint32_t* __restrict__ values, const float2* __restrict__ means2D,
+                   const float4* __restrict__ conic_opacity, const float4* __restrict__ rgb,
+                   float* __restrict__ final_T, uint32_t* __restrict__ n_contrib,
+                   float* __restrict__ out_color) {
+  __shared__ Staged sm[kBlock];
+  __shared__ uint8_t s_mask[kBlock];
+  const int tile = blockIdx.x, t = threadIdx.x, w = t >> 5, lane = t & 31;
+  const int tx0 = (tile % cam.tiles_x) * kTile, ty0 = (tile / cam.tiles_x) * kTile;
+  const int px = tx0 + (w & 1) * 8 + (lane & 7);
+  const int py = ty0 + (w >> 1) * 8 + (lane >> 3);
+  FwdPix p[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    p[k].pfx = (float)px;
+    p[k].pfy = (float)(py + 4 * k);
+    p[k].T = 1.0f;
+    p[k].C0 = p[k].C1 = p[k].C2 = 0.0f;
+    p[k].last = 0;
+    p[k].done = !(px < cam.W && py + 4 * k < cam.H);
+  }
+  const uint32_t wbits = (1u << (4 * (w >> 1) + (w & 1))) | (1u << (4 * (w >> 1) + (w & 1) + 2));
+  const uint2 range = ranges[tile];
+  const int rounds = (int)((range.y - range.x + kBlock - 1) / kBlock);
+  int todo = (int)(range.y - range.x);
+  for (int i = 0; i < rounds; ++i, todo -= kBlock) {
+    if (__syncthreads_count(p[0].done && p[1].done) == 128) break;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int st = t + h * 128;
+      const uint32_t progress = range.x + i * kBlock + st;
+      uint32_t mask = 0;
+      if (progress < range.y)
+        mask = stage(sm, st, values[progress], tx0, ty0, means2D, conic_opacity, rgb);
+      s_mask[st] = (uint8_t)mask;
+    }
+    __syncthreads();
+    const int n = min(kBlock, todo);
+    for (int k = 0; k * 32 < n; ++k) {
+      if (__all_sync(kFull, p[0].done && p[1].done)) break;
+      const int jl = k * 32 + lane;
+      const uint32_t m = jl < n ? s_mask[jl] : 0u;
+      unsigned bits = __ballot_sync(kFull, (m & wbits) != 0u);
+      while (bits) {
+        const int j = k * 32 + __ffs(bits) - 1;
+        bits &= bits - 1u;
+        const float4 g = sm[j].xyi;
+        const float4 co = sm[j].co;
+        const float4 c = sm[j].col;
+        const uint32_t pos = (uint32_t)(i * kBlock + j + 1);  // 1-based list position
+        fwd_step(p[0], g, co, c, pos);
+        fwd_step(p[1], g, co, c, pos);
+      }
+    }
+  }
+  const int HW = cam.H * cam.W;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int y = py + 4 * k;
+    if (px < cam.W && y < cam.H) {
+      const int pix = y * cam.W + px;
+      final_T[pix] = p[k].T;
+      n_contrib[pix] = p[k].last;
+      out_color[pix] = p[k].C0 + p[k].T * cam.bg[0];
+      out_color[HW + pix] = p[k].C1 + p[k].T * cam.bg[1];
+      out_color[2 * HW + pix] = p[k].C2 + p[k].T * cam.bg[2];
+    }
+  }
+}
+
 #ifndef DW_BWD_MIN_BLOCKS
 #define DW_BWD_MIN_BLOCKS 5  // 5 x 256 threads/SM: <= 51 registers, no spills (ptxas -v)
 #endif
@@ -536,8 +637,15 @@ void launch_forward_impl(const CamParams& cam, const uint2* ranges, const uint32
                          cudaStream_t s) {
   (void)radii;
   const int grid = cam.tiles_x * cam.tiles_y;
-  k_forward<<<grid, kBlock, 0, s>>>(cam, ranges, values, means2D, conic_opacity, rgb, final_T,
-                                    n_contrib, out_color);
+#ifndef DW_FWD_PPT
+#define DW_FWD_PPT 2  // A/B on C3: 0.527 vs 0.558 ms (profiles/r01/ab_fwd2.jsonl)
+#endif
+  if (DW_FWD_PPT == 2)
+    k_forward_ppt2<<<grid, 128, 0, s>>>(cam, ranges, values, means2D, conic_opacity, rgb, final_T,
+                                        n_contrib, out_color);
+  else
+    k_forward<<<grid, kBlock, 0, s>>>(cam, ranges, values, means2D, conic_opacity, rgb, final_T,
+                                      n_contrib, out_color);
   DW_CUDA(cudaGetLastError());
 }
 
