@@ -173,6 +173,27 @@ dw_status dw_render_forward(dw_rasterizer* r, int32_t P, const float* means3D,
                             const dw_camera* cam, float* out_color, int32_t* radii,
                             int64_t* num_rendered, void* stream);
 
+/* render_forward without any host synchronisation (CUDA-graph capturable):
+ * the instance count stays on the device and the binning kernels run over the
+ * capacity set by dw_rasterizer_reserve (required first; no allocation
+ * happens). If the view needs more instances than reserved, nothing is binned
+ * (the image is the background) and the overflow flag is raised -- read it,
+ * with the count, through dw_rasterizer_num_rendered (which synchronises). */
+dw_status dw_render_forward_async(dw_rasterizer* r, int32_t P, const float* means3D,
+                                  const float* scales, const float* rotations,
+                                  const float* opacities, const float* colors,
+                                  const dw_camera* cam, float* out_color, int32_t* radii,
+                                  void* stream);
+
+/* Pre-size every per-view buffer for up to P Gaussians, a width x height
+ * image and max_instances (tile, Gaussian) instances. */
+dw_status dw_rasterizer_reserve(dw_rasterizer* r, int32_t P, int32_t width, int32_t height,
+                                int64_t max_instances);
+
+/* Instance count of the last forward (synchronises after a no-sync forward);
+ * overflowed (nullable) = 1 if that no-sync forward exceeded the reserve. */
+dw_status dw_rasterizer_num_rendered(dw_rasterizer* r, int64_t* num_rendered, int* overflowed);
+
 /* render_backward: the DISTWAR hot path. dL_dpixels 3*H*W (device). Adds the
  * 9 screen-space gradients per Gaussian into grad[P*9] in Address order
  * (mean2D.x, mean2D.y, conic.x, conic.y, conic.z, opacity, r, g, b).

@@ -17,7 +17,9 @@ struct dw_rasterizer;
 namespace dw {
 void raster_forward(dw_rasterizer* r, int32_t P, const float* m, const float* sc, const float* rot,
                     const float* op, const float* col, const dw_camera* cam, float* out,
-                    int32_t* radii, int64_t* nr, cudaStream_t s);
+                    int32_t* radii, int64_t* nr, cudaStream_t s, bool nosync);
+void raster_reserve(dw_rasterizer* r, int32_t P, int32_t W, int32_t H, int64_t max_instances);
+int64_t raster_resolve(dw_rasterizer* r, bool* overflowed);
 void raster_backward(dw_rasterizer* r, const float* dL, int policy, int thr, float* grad,
                      uint64_t* pairs, cudaStream_t s);
 uint64_t raster_last_reds(const dw_rasterizer* r);
@@ -405,7 +407,39 @@ dw_status dw_render_forward(dw_rasterizer* r, int32_t P, const float* means3D, c
     return fail_invalid("null argument");
   return guarded([&] {
     dw::raster_forward(r, P, means3D, scales, rotations, opacities, colors, cam, out_color, radii,
-                       num_rendered, dw::as_stream(stream));
+                       num_rendered, dw::as_stream(stream), false);
+    return DW_OK;
+  });
+}
+
+dw_status dw_render_forward_async(dw_rasterizer* r, int32_t P, const float* means3D,
+                                  const float* scales, const float* rotations,
+                                  const float* opacities, const float* colors, const dw_camera* cam,
+                                  float* out_color, int32_t* radii, void* stream) {
+  if (!r || !cam || !out_color || (P > 0 && (!means3D || !scales || !rotations || !opacities || !colors)))
+    return fail_invalid("null argument");
+  return guarded([&] {
+    dw::raster_forward(r, P, means3D, scales, rotations, opacities, colors, cam, out_color, radii,
+                       nullptr, dw::as_stream(stream), true);
+    return DW_OK;
+  });
+}
+
+dw_status dw_rasterizer_reserve(dw_rasterizer* r, int32_t P, int32_t width, int32_t height,
+                                int64_t max_instances) {
+  if (!r) return fail_invalid("null argument");
+  return guarded([&] {
+    dw::raster_reserve(r, P, width, height, max_instances);
+    return DW_OK;
+  });
+}
+
+dw_status dw_rasterizer_num_rendered(dw_rasterizer* r, int64_t* num_rendered, int* overflowed) {
+  if (!r || !num_rendered) return fail_invalid("null argument");
+  return guarded([&] {
+    bool ovf = false;
+    *num_rendered = dw::raster_resolve(r, &ovf);
+    if (overflowed) *overflowed = ovf ? 1 : 0;
     return DW_OK;
   });
 }

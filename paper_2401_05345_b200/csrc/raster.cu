@@ -87,7 +87,7 @@ struct dw_rasterizer {
   ~dw_rasterizer() {
     void* ps[] = {means2D, depths, radii, conic_opacity, rgb, tiles_touched, offsets, dkey[0],
                   dkey[1], dids[0], dids[1], itile[0], itile[1], ivals[0], ivals[1], ranges,
-                  final_T, n_contrib, tmp, scan_tmp, keys_dbg, counters};
+                  final_T, n_contrib, tmp, scan_tmp, keys_dbg, counters, live_dev, overflow_dev};
     for (void* p : ps)
       if (p) cudaFree(p);
     for (float* p : h_bufs)
@@ -100,9 +100,76 @@ struct dw_rasterizer {
     }
   }
 
+  // no-sync forward state: live instance count + overflow flag on the device
+  unsigned long long* live_dev = nullptr;
+  unsigned int* overflow_dev = nullptr;
+  bool count_pending = false;  // num_rendered not read back yet (no-sync forward)
+
+  void ensure_small() {
+    if (!counters) DW_CUDA(cudaMalloc(&counters, 2 * sizeof(unsigned long long)));
+    if (!h_total) DW_CUDA(cudaMallocHost(&h_total, sizeof(uint64_t)));
+    if (!live_dev) DW_CUDA(cudaMalloc(&live_dev, sizeof(unsigned long long)));
+    if (!overflow_dev) {
+      DW_CUDA(cudaMalloc(&overflow_dev, sizeof(unsigned int)));
+      DW_CUDA(cudaMemset(overflow_dev, 0, sizeof(unsigned int)));
+    }
+  }
+
+  // Pre-size every buffer (no allocation happens in a later forward/backward
+  // that stays within these sizes -- required before CUDA-graph capture).
+  void reserve(int32_t P_, int32_t W_, int32_t H_, int64_t max_instances) {
+    if (P_ < 0 || W_ < 1 || H_ < 1 || max_instances < 0)
+      throw std::invalid_argument("invalid reserve sizes");
+    const size_t np = static_cast<size_t>(std::max(P_, 1));
+    const size_t npx = static_cast<size_t>(W_) * H_;
+    const size_t ntiles = static_cast<size_t>((W_ + dw::kTile - 1) / dw::kTile) *
+                          ((H_ + dw::kTile - 1) / dw::kTile);
+    grow(means2D, cap_p, np);
+    grow(depths, cap_p2, np);
+    grow(radii, cap_p3, np);
+    grow(conic_opacity, cap_p4, np);
+    grow(rgb, cap_p5, np);
+    grow(tiles_touched, cap_p6, np);
+    grow(offsets, cap_p7, np);
+    for (int b = 0; b < 2; ++b) {
+      grow(dkey[b], cap_d[b], np);
+      grow(dids[b], cap_d[2 + b], np);
+    }
+    grow(scan_tmp, cap_scan, dw::scan_temp_bytes(P_));
+    grow(ranges, cap_t, ntiles);
+    grow(final_T, cap_px, npx);
+    grow(n_contrib, cap_px2, npx);
+    const size_t ni = static_cast<size_t>(std::max<int64_t>(max_instances, 1));
+    for (int b = 0; b < 2; ++b) {
+      grow(itile[b], cap_i[b], ni);
+      grow(ivals[b], cap_i[2 + b], ni);
+    }
+    ensure_tmp(std::max(dw::radix_sort_temp_bytes(P_),
+                        dw::radix_sort_temp_bytes(static_cast<int64_t>(std::min(cap_i[0], cap_i[2])))));
+    ensure_small();
+  }
+
+  // Host view of the instance count (reads the device value back after a
+  // no-sync forward); overflow = the no-sync forward exceeded the reserve.
+  int64_t resolve_count(bool* overflowed) {
+    unsigned int ovf = 0;
+    if (count_pending) {
+      unsigned long long n = 0;
+      DW_CUDA(cudaMemcpy(&n, live_dev, sizeof(n), cudaMemcpyDeviceToHost));
+      DW_CUDA(cudaMemcpy(&ovf, overflow_dev, sizeof(ovf), cudaMemcpyDeviceToHost));
+      num_rendered = static_cast<int64_t>(n);
+      count_pending = false;
+      last_overflow = ovf != 0;
+    }
+    if (overflowed) *overflowed = last_overflow;
+    return num_rendered;
+  }
+  bool last_overflow = false;
+
   void forward(int32_t P_, const float* means3D, const float* scales, const float* rotations,
                const float* opacities, const float* colors, const dw_camera& c, float* out_color,
-               int32_t* radii_out, cudaStream_t s) {
+               int32_t* radii_out, cudaStream_t s, bool nosync = false) {
+    last_overflow = false;
     if (P_ < 0) throw std::invalid_argument("P must be >= 0");
     if (c.width < 1 || c.height < 1) throw std::invalid_argument("camera size must be >= 1");
     if (!(c.tan_fovx > 0.0f) || !(c.tan_fovy > 0.0f))
@@ -135,8 +202,7 @@ struct dw_rasterizer {
     grow(ranges, cap_t, static_cast<size_t>(ntiles));
     grow(final_T, cap_px, static_cast<size_t>(W) * H);
     grow(n_contrib, cap_px2, static_cast<size_t>(W) * H);
-    if (!counters) DW_CUDA(cudaMalloc(&counters, 2 * sizeof(unsigned long long)));
-    if (!h_total) DW_CUDA(cudaMallocHost(&h_total, sizeof(uint64_t)));
+    ensure_small();
 
     for (int b = 0; b < 2; ++b) {
       grow(dkey[b], cap_d[b], np);
@@ -146,7 +212,13 @@ struct dw_rasterizer {
 
     dw::launch_preprocess(P, means3D, scales, rotations, opacities, colors, cam, means2D, depths,
                           radii, conic_opacity, rgb, tiles_touched, s);
+    // Instance count: read back (one host sync) to size the buffers, or --
+    // nosync -- kept on the device against the reserved capacity
+    // (dw_rasterizer_reserve), so the whole forward is graph-capturable.
+    int64_t n_grid = 0;                        // element count the grids are sized for
+    const unsigned long long* n_dev = nullptr;  // live count on the device (nosync)
     num_rendered = 0;
+    count_pending = false;
     if (P > 0) {
       // 1. Gaussians in (depth, id) order: stable 32-bit LSD sort
       dw::launch_depth_keys(P, depths, radii, dkey[0], dids[0], s);
@@ -154,29 +226,41 @@ struct dw_rasterizer {
       order = dids[dw::radix_sort_pairs(dkey, dids, P, 32, tmp, s)];
       // instance offsets in that order
       dw::inclusive_scan_gather(tiles_touched, order, P, offsets, scan_tmp, s);
-      DW_CUDA(cudaMemcpyAsync(h_total, offsets + P - 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-      DW_CUDA(cudaStreamSynchronize(s));
-      num_rendered = static_cast<int64_t>(*h_total);
+      if (nosync) {
+        if (cap_i[0] == 0 || cap_i[2] == 0)
+          throw std::invalid_argument("no-sync forward needs dw_rasterizer_reserve first");
+        n_grid = static_cast<int64_t>(std::min(cap_i[0], cap_i[2]));
+        dw::launch_clamp_total(offsets, P, static_cast<uint64_t>(n_grid), live_dev, overflow_dev,
+                               s);
+        n_dev = live_dev;
+        count_pending = true;
+      } else {
+        DW_CUDA(cudaMemcpyAsync(h_total, offsets + P - 1, sizeof(uint64_t),
+                                cudaMemcpyDeviceToHost, s));
+        DW_CUDA(cudaStreamSynchronize(s));
+        num_rendered = static_cast<int64_t>(*h_total);
+        n_grid = num_rendered;
+      }
     }
-    if (num_rendered >= (int64_t(1) << 32))
-      throw std::runtime_error("more than 2^32 tile instances");
-    const size_t ni = static_cast<size_t>(std::max<int64_t>(num_rendered, 1));
+    if (n_grid >= (int64_t(1) << 32)) throw std::runtime_error("more than 2^32 tile instances");
+    const size_t ni = static_cast<size_t>(std::max<int64_t>(n_grid, 1));
     for (int b = 0; b < 2; ++b) {
       grow(itile[b], cap_i[b], ni);
       grow(ivals[b], cap_i[2 + b], ni);
     }
     tiles_sorted = itile[0];
     vals = ivals[0];
-    if (num_rendered > 0) {
+    if (n_grid > 0) {
       // 2. duplicate in depth order, 3. stable sort by tile id
-      dw::launch_duplicate_sorted(P, order, means2D, radii, offsets, cam, itile[0], ivals[0], s);
-      ensure_tmp(dw::radix_sort_temp_bytes(num_rendered));
-      const int cur = dw::radix_sort_pairs(itile, ivals, num_rendered, tile_bits, tmp, s);
+      dw::launch_duplicate_sorted(P, order, means2D, radii, offsets, cam, itile[0], ivals[0],
+                                  static_cast<uint64_t>(n_grid), s);
+      ensure_tmp(dw::radix_sort_temp_bytes(n_grid));
+      const int cur = dw::radix_sort_pairs(itile, ivals, n_grid, tile_bits, tmp, s, n_dev);
       tiles_sorted = itile[cur];
       vals = ivals[cur];
     }
     DW_CUDA(cudaMemsetAsync(ranges, 0, sizeof(uint2) * ntiles, s));
-    dw::launch_ranges_u32(num_rendered, tiles_sorted, ranges, s);
+    dw::launch_ranges_u32(n_grid, tiles_sorted, ranges, s, n_dev);
     dw::launch_forward_impl(cam, ranges, vals, means2D, conic_opacity, rgb, radii, final_T,
                             n_contrib, out_color, s);
     if (radii_out && P > 0)
@@ -243,9 +327,9 @@ namespace dw {
 
 void raster_forward(dw_rasterizer* r, int32_t P, const float* m, const float* sc, const float* rot,
                     const float* op, const float* col, const dw_camera* cam, float* out,
-                    int32_t* radii, int64_t* nr, cudaStream_t s) {
-  r->forward(P, m, sc, rot, op, col, *cam, out, radii, s);
-  if (nr) *nr = r->num_rendered;
+                    int32_t* radii, int64_t* nr, cudaStream_t s, bool nosync) {
+  r->forward(P, m, sc, rot, op, col, *cam, out, radii, s, nosync);
+  if (nr) *nr = nosync ? -1 : r->num_rendered;
 }
 
 void raster_backward(dw_rasterizer* r, const float* dL, int policy, int thr, float* grad,
@@ -254,6 +338,12 @@ void raster_backward(dw_rasterizer* r, const float* dL, int policy, int thr, flo
 }
 
 uint64_t raster_last_reds(const dw_rasterizer* r) { return r->last_reds; }
+
+void raster_reserve(dw_rasterizer* r, int32_t P, int32_t W, int32_t H, int64_t max_instances) {
+  r->reserve(P, W, H, max_instances);
+}
+
+int64_t raster_resolve(dw_rasterizer* r, bool* overflowed) { return r->resolve_count(overflowed); }
 
 // SW-B backward that also taps its WarpRecords into a host
 // trace: records sorted by (warp, descending list position) -- the order
@@ -337,7 +427,8 @@ void raster_preprocess_backward(dw_rasterizer* r, const float* means3D, const fl
 }
 
 void raster_buffer(const dw_rasterizer* r, int which, const void** p, int64_t* count) {
-  const int64_t P = r->P, I = r->num_rendered, npx = int64_t(r->W) * r->H;
+  const int64_t P = r->P, npx = int64_t(r->W) * r->H;
+  const int64_t I = const_cast<dw_rasterizer*>(r)->resolve_count(nullptr);
   const int64_t nt = int64_t(r->cam.tiles_x) * r->cam.tiles_y;
   switch (which) {
     case 0: *p = r->means2D; *count = 2 * P; break;

@@ -39,12 +39,6 @@ void launch_preprocess(int P, const float* means3D, const float* scales, const f
                        float2* means2D, float* depths, int* radii, float4* conic_opacity,
                        float4* rgb, uint32_t* tiles_touched, cudaStream_t s);
 
-void launch_duplicate(int P, const float2* means2D, const float* depths, const int* radii,
-                      const uint64_t* offsets, const CamParams& cam, uint64_t* keys,
-                      uint32_t* values, cudaStream_t s);
-
-void launch_ranges(int64_t L, const uint64_t* keys, uint2* ranges, cudaStream_t s);
-
 // Device buffers of the backward's WarpRecord tap (SoA like dw_device_trace).
 struct TapBuf {
   unsigned long long* count = nullptr;
@@ -73,16 +67,21 @@ void launch_adam(int P, float* means3D, float* scales, float* rotations, float* 
 // raster_sort.cu: hand-written stable LSD radix sort + scan (no CUB).
 size_t radix_sort_temp_bytes(int64_t n);
 size_t scan_temp_bytes(int64_t n);
+// n_dev (nullable): live element count read on the device (<= n, the
+// capacity the grids are sized for) -- the no-host-sync forward.
 int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* temp,
-                     cudaStream_t s);
+                     cudaStream_t s, const unsigned long long* n_dev = nullptr);
 void inclusive_scan_gather(const uint32_t* in, const uint32_t* order, int64_t n, uint64_t* out,
                            void* temp, cudaStream_t s);
 void launch_depth_keys(int P, const float* depths, const int* radii, uint32_t* dkey, uint32_t* ids,
                        cudaStream_t s);
 void launch_duplicate_sorted(int P, const uint32_t* order, const float2* means2D, const int* radii,
                              const uint64_t* offsets, const CamParams& cam, uint32_t* tile_ids,
-                             uint32_t* values, cudaStream_t s);
-void launch_ranges_u32(int64_t L, const uint32_t* tiles, uint2* ranges, cudaStream_t s);
+                             uint32_t* values, uint64_t cap, cudaStream_t s);
+void launch_ranges_u32(int64_t L, const uint32_t* tiles, uint2* ranges, cudaStream_t s,
+                       const unsigned long long* n_dev = nullptr);
+void launch_clamp_total(const uint64_t* offsets, int P, uint64_t cap, unsigned long long* n_live,
+                        unsigned int* overflow, cudaStream_t s);
 void launch_make_keys(int64_t L, const uint32_t* tiles, const uint32_t* values, const float* depths,
                       uint64_t* keys, cudaStream_t s);
 

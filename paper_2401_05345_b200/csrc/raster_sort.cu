@@ -56,13 +56,23 @@ __device__ __forceinline__ unsigned digit_peers(uint32_t d, int bits, bool valid
 // Per-tile digit histogram. A tile is ITEMS*256 consecutive elements; warp w
 // owns the contiguous chunk [w*ITEMS*32, (w+1)*ITEMS*32) and counts it into
 // a warp-private smem histogram, one update per distinct digit per warp
-// instruction (__match_any_sync aggregation: no atomics, no contention).
+// instruction (ballot multi-split aggregation: no atomics, no contention).
+// n_dev (nullable): element count read on the device, capped by n -- the
+// no-host-sync forward sizes the grid for the capacity n.
+__device__ __forceinline__ int64_t live_n(int64_t n, const unsigned long long* n_dev) {
+  if (!n_dev) return n;
+  const int64_t d = static_cast<int64_t>(*n_dev);
+  return d < n ? d : n;
+}
+
 template <int ITEMS>
 __global__ void __launch_bounds__(kSortThreads)
     k_upsweep(const uint32_t* __restrict__ keys, int64_t n, int shift, uint32_t mask,
-              int bits, uint32_t* __restrict__ counts, int64_t tiles) {
+              int bits, uint32_t* __restrict__ counts, int64_t tiles,
+              const unsigned long long* __restrict__ n_dev) {
   __shared__ uint32_t hist[kWarps][256];
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+  n = live_n(n, n_dev);
 #pragma unroll
   for (int k = 0; k < kWarps; ++k) hist[k][t] = 0;
   __syncthreads();
@@ -157,7 +167,8 @@ __global__ void __launch_bounds__(kSortThreads)
     k_downsweep(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, int64_t n,
                 int shift, uint32_t mask, int bits, const uint32_t* __restrict__ counts,
                 int64_t tiles, const uint32_t* __restrict__ digit_base,
-                uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
+                uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
+                const unsigned long long* __restrict__ n_dev) {
   constexpr int TILE = ITEMS * kSortThreads;
   __shared__ uint32_t s_cnt[kWarps][256];  // warp digit counts -> tile-local offsets
   __shared__ uint32_t s_dstart[256];       // tile-local start of each digit's run
@@ -165,6 +176,7 @@ __global__ void __launch_bounds__(kSortThreads)
   __shared__ uint32_t s_wsum[kWarps];
   __shared__ uint32_t s_key[TILE], s_val[TILE];
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+  n = live_n(n, n_dev);
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
   for (int k = 0; k < kWarps; ++k) s_cnt[k][t] = 0;
@@ -357,7 +369,7 @@ __global__ void __launch_bounds__(256)
     k_duplicate_sorted(int P, const uint32_t* __restrict__ order, const float2* __restrict__ means2D,
                        const int* __restrict__ radii, const uint64_t* __restrict__ offsets,
                        int tiles_x, int tiles_y, uint32_t* __restrict__ tile_ids,
-                       uint32_t* __restrict__ values) {
+                       uint32_t* __restrict__ values, uint64_t cap) {
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   int r[4] = {0, 0, 0, 0};
@@ -371,8 +383,10 @@ __global__ void __launch_bounds__(256)
       rect_of(means2D[gid], rad, tiles_x, tiles_y, r);
       off = i == 0 ? 0 : offsets[i - 1];
       area = (r[2] - r[0]) * (r[3] - r[1]);
+      if (off + static_cast<uint64_t>(area) > cap) area = 0;  // over capacity: write nothing
     }
   }
+  if (area == 0) r[0] = r[1] = r[2] = r[3] = 0;
   const bool big = area > 32;
   if (!big) {
     for (int y = r[1]; y < r[3]; ++y)
@@ -400,8 +414,22 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-__global__ void k_ranges_u32(int64_t L, const uint32_t* __restrict__ tiles, uint2* __restrict__ ranges) {
+// No-host-sync sizing: the live instance count is the scan total when it fits
+// the reserved capacity, else 0 (the frame renders empty) and the overflow
+// flag is raised for the host to read later.
+__global__ void k_clamp_total(const uint64_t* __restrict__ offsets, int P, uint64_t cap,
+                              unsigned long long* __restrict__ n_live,
+                              unsigned int* __restrict__ overflow) {
+  const uint64_t total = P > 0 ? offsets[P - 1] : 0;
+  const bool fits = total <= cap;
+  *n_live = fits ? total : 0ull;
+  *overflow = fits ? 0u : 1u;
+}
+
+__global__ void k_ranges_u32(int64_t L, const uint32_t* __restrict__ tiles, uint2* __restrict__ ranges,
+                             const unsigned long long* __restrict__ n_dev) {
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  L = live_n(L, n_dev);
   if (idx >= L) return;
   const uint32_t tile = tiles[idx];
   if (idx == 0) {
@@ -445,7 +473,7 @@ size_t scan_temp_bytes(int64_t n) {
 // Stable LSD sort of (k[cur], v[cur]) on bits [0, bits); returns the index
 // (0/1) of the double buffer holding the result.
 int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* temp,
-                     cudaStream_t s) {
+                     cudaStream_t s, const unsigned long long* n_dev) {
   int cur = 0;
   if (n <= 0 || bits <= 0) return cur;
   const int items = sort_items(n);
@@ -458,17 +486,18 @@ int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* 
     const int b = bits - shift < 8 ? bits - shift : 8;
     const uint32_t mask = (1u << b) - 1u;
     if (items == 16)
-      k_upsweep<16><<<grid, kSortThreads, 0, s>>>(k[cur], n, shift, mask, b, counts, tiles);
+      k_upsweep<16><<<grid, kSortThreads, 0, s>>>(k[cur], n, shift, mask, b, counts, tiles,
+                                                  n_dev);
     else
-      k_upsweep<4><<<grid, kSortThreads, 0, s>>>(k[cur], n, shift, mask, b, counts, tiles);
+      k_upsweep<4><<<grid, kSortThreads, 0, s>>>(k[cur], n, shift, mask, b, counts, tiles, n_dev);
     k_scan_rows<<<256, 1024, 0, s>>>(counts, tiles, digit);
     k_scan_digits<<<1, 256, 0, s>>>(digit, 256);
     if (items == 16)
       k_downsweep<16><<<grid, kSortThreads, 0, s>>>(k[cur], v[cur], n, shift, mask, b, counts,
-                                                    tiles, digit, k[cur ^ 1], v[cur ^ 1]);
+                                                    tiles, digit, k[cur ^ 1], v[cur ^ 1], n_dev);
     else
       k_downsweep<4><<<grid, kSortThreads, 0, s>>>(k[cur], v[cur], n, shift, mask, b, counts,
-                                                   tiles, digit, k[cur ^ 1], v[cur ^ 1]);
+                                                   tiles, digit, k[cur ^ 1], v[cur ^ 1], n_dev);
     cur ^= 1;
   }
   DW_CUDA(cudaGetLastError());
@@ -495,16 +524,24 @@ void launch_depth_keys(int P, const float* depths, const int* radii, uint32_t* d
 
 void launch_duplicate_sorted(int P, const uint32_t* order, const float2* means2D, const int* radii,
                              const uint64_t* offsets, const CamParams& cam, uint32_t* tile_ids,
-                             uint32_t* values, cudaStream_t s) {
+                             uint32_t* values, uint64_t cap, cudaStream_t s) {
   if (P <= 0) return;
   k_duplicate_sorted<<<blocks_for(P, 256), 256, 0, s>>>(P, order, means2D, radii, offsets,
-                                                        cam.tiles_x, cam.tiles_y, tile_ids, values);
+                                                        cam.tiles_x, cam.tiles_y, tile_ids, values,
+                                                        cap);
   DW_CUDA(cudaGetLastError());
 }
 
-void launch_ranges_u32(int64_t L, const uint32_t* tiles, uint2* ranges, cudaStream_t s) {
+void launch_ranges_u32(int64_t L, const uint32_t* tiles, uint2* ranges, cudaStream_t s,
+                       const unsigned long long* n_dev) {
   if (L <= 0) return;
-  k_ranges_u32<<<blocks_for(L, 256), 256, 0, s>>>(L, tiles, ranges);
+  k_ranges_u32<<<blocks_for(L, 256), 256, 0, s>>>(L, tiles, ranges, n_dev);
+  DW_CUDA(cudaGetLastError());
+}
+
+void launch_clamp_total(const uint64_t* offsets, int P, uint64_t cap, unsigned long long* n_live,
+                        unsigned int* overflow, cudaStream_t s) {
+  k_clamp_total<<<1, 1, 0, s>>>(offsets, P, cap, n_live, overflow);
   DW_CUDA(cudaGetLastError());
 }
 

@@ -132,6 +132,37 @@ class GaussianRasterizer:
         self.P, self.num_rendered, self.camera = P, nr.value, camera
         return out_color, radii, nr.value
 
+    def reserve(self, P: int, width: int, height: int, max_instances: int):
+        """Pre-size every buffer (dw_rasterizer_reserve) so that a forward /
+        backward within these sizes allocates nothing -- required before
+        render_forward_async and before capturing a CUDA graph."""
+        check(lib().dw_rasterizer_reserve(self._h, int(P), int(width), int(height),
+                                          int(max_instances)))
+
+    def render_forward_async(self, means3D, scales, rotations, opacities, colors, camera,
+                             out_color, radii, stream=None):
+        """render_forward with no host synchronisation (graph-capturable): the
+        instance count stays on the device; read it with instances()."""
+        import torch
+
+        f32 = torch.float32
+        P = int(means3D.shape[0])
+        cam = camera.to_c()
+        check(lib().dw_render_forward_async(
+            self._h, P, _ptr(means3D, "means3D", f32), _ptr(scales, "scales", f32),
+            _ptr(rotations, "rotations", f32), _ptr(opacities, "opacities", f32),
+            _ptr(colors, "colors", f32), C.byref(cam), _ptr(out_color, "out_color", f32),
+            _ptr(radii, "radii", torch.int32), _stream(stream)))
+        self.P, self.num_rendered, self.camera = P, None, camera
+        return out_color, radii
+
+    def instances(self):
+        """(num_rendered, overflowed) of the last forward; synchronises."""
+        n, ovf = C.c_int64(), C.c_int()
+        check(lib().dw_rasterizer_num_rendered(self._h, C.byref(n), C.byref(ovf)))
+        self.num_rendered = n.value
+        return n.value, bool(ovf.value)
+
     def render_backward(self, dL_dpixels, policy: Policy = Policy(PolicyKind.sw_b, 0),
                         grad=None, count_pairs: bool = False, stream=None):
         """Adds into grad [P, 9] (allocated zeroed if None). Returns grad, or

@@ -187,3 +187,143 @@ def test_training_loop_reduces_loss(cuda):
         g3 = r.preprocess_backward(s["means3D"], s["scales"], s["rotations"], g2)
         opt.step(g3)
     assert losses[-1] < 0.5 * losses[0], losses
+
+
+def _scene_t(cuda, sc):
+    import torch
+
+    return {k: torch.from_numpy(v.copy()).to(cuda) for k, v in sc.items()}
+
+
+_KEYS = ("means3D", "scales", "rotations", "opacities", "colors")
+
+
+@pytest.mark.parametrize("yaw", [0.0, 23.0])
+def test_forward_async_matches_sync(cuda, yaw):
+    """The no-host-sync forward (device-side instance count over a reserved
+    capacity) bins and blends exactly like the synchronising forward."""
+    import torch
+
+    from paper_2401_05345_b200.rasterizer import GaussianRasterizer
+    from paper_2401_05345_b200.scene import make_camera, make_scene
+
+    P, W, H = 30_000, 320, 240
+    s = _scene_t(cuda, make_scene(P, W, H, seed=41))
+    cam = make_camera(W, H, yaw_deg=yaw)
+    a = GaussianRasterizer()
+    img_a, rad_a, nr = a.render_forward(*[s[k] for k in _KEYS], cam)
+    img_a, rad_a = img_a.clone(), rad_a.clone()
+    b = GaussianRasterizer()
+    b.reserve(P, W, H, 2 * nr + 1000)
+    img_b = torch.full((3, H, W), float("nan"), device=cuda)
+    rad_b = torch.full((P,), -7, dtype=torch.int32, device=cuda)
+    b.render_forward_async(*[s[k] for k in _KEYS], cam, img_b, rad_b)
+    assert b.instances() == (nr, False)
+    assert torch.equal(img_a, img_b)
+    assert torch.equal(rad_a, rad_b)
+    for name in ("ranges", "values", "n_contrib", "final_T"):
+        assert np.array_equal(a.buffer(name), b.buffer(name)), name
+    # over capacity: nothing binned, the frame is the background, flag raised
+    c = GaussianRasterizer()
+    c.reserve(P, W, H, nr // 2)
+    img_c = torch.empty((3, H, W), device=cuda)
+    rad_c = torch.empty((P,), dtype=torch.int32, device=cuda)
+    c.render_forward_async(*[s[k] for k in _KEYS], cam, img_c, rad_c)
+    n_c, ovf = c.instances()
+    assert ovf and n_c == 0
+    bg = torch.tensor(cam.bg, device=cuda).view(3, 1, 1).expand(3, H, W)
+    assert torch.equal(img_c, bg.contiguous())
+    # and the next in-capacity forward clears the flag
+    c.reserve(P, W, H, nr)
+    c.render_forward_async(*[s[k] for k in _KEYS], cam, img_c, rad_c)
+    assert c.instances() == (nr, False)
+    assert torch.equal(img_c, img_a)
+
+
+def test_forward_async_requires_reserve(cuda):
+    import torch
+
+    from paper_2401_05345_b200._lib import InvalidArgument
+    from paper_2401_05345_b200.rasterizer import GaussianRasterizer
+    from paper_2401_05345_b200.scene import make_camera, make_scene
+
+    s = _scene_t(cuda, make_scene(100, 64, 64, seed=1))
+    r = GaussianRasterizer()
+    with pytest.raises(InvalidArgument):
+        r.render_forward_async(*[s[k] for k in _KEYS], make_camera(64, 64),
+                               torch.empty((3, 64, 64), device=cuda),
+                               torch.empty((100,), dtype=torch.int32, device=cuda))
+    with pytest.raises(InvalidArgument):
+        r.reserve(-1, 64, 64, 10)
+
+
+def test_whole_training_step_is_cuda_graph_capturable(cuda):
+    """forward (no host sync) -> L2 image loss -> DISTWAR backward ->
+    preprocess backward -> Adam: one CUDA graph per training step. One replay
+    matches one eager step; repeated replays train the scene."""
+    import torch
+
+    from paper_2401_05345_b200 import warpred as wr
+    from paper_2401_05345_b200.rasterizer import Adam, GaussianRasterizer
+    from paper_2401_05345_b200.scene import make_camera, make_scene
+
+    P, W, H = 6000, 192, 128
+    cam = make_camera(W, H)
+    tgt = _scene_t(cuda, make_scene(P, W, H, seed=51))
+    r0 = GaussianRasterizer()
+    target, _, nr = r0.render_forward(*[tgt[k] for k in _KEYS], cam)
+    target = target.clone()
+    init = make_scene(P, W, H, seed=51)
+    rng = np.random.default_rng(52)
+    init["colors"] = np.clip(init["colors"] + rng.normal(0, 0.2, init["colors"].shape), 0, 1
+                             ).astype(np.float32)
+    pol = wr.Policy(wr.PolicyKind.sw_b, 8)
+    lr = (1e-4, 1e-4, 1e-3, 1e-3, 1e-2)
+
+    def setup():
+        s = _scene_t(cuda, init)
+        r = GaussianRasterizer()
+        r.reserve(P, W, H, 4 * nr)
+        bufs = dict(img=torch.empty((3, H, W), device=cuda),
+                    radii=torch.empty((P,), dtype=torch.int32, device=cuda),
+                    g2=torch.zeros((P, 9), device=cuda), g3=torch.zeros((P, 14), device=cuda),
+                    loss=torch.zeros((), device=cuda))
+        return s, r, Adam(s, lr=lr, eps=1e-15), bufs
+
+    def step(s, r, opt, b):
+        r.render_forward_async(*[s[k] for k in _KEYS], cam, b["img"], b["radii"])
+        diff = b["img"] - target
+        b["loss"].copy_((diff * diff).mean())
+        b["g2"].zero_()
+        r.render_backward((2.0 / diff.numel()) * diff, pol, grad=b["g2"])
+        b["g3"].zero_()
+        r.preprocess_backward(s["means3D"], s["scales"], s["rotations"], b["g2"], grad3d=b["g3"])
+        opt.step(b["g3"])
+
+    s_e, r_e, opt_e, b_e = setup()
+    step(s_e, r_e, opt_e, b_e)
+    torch.cuda.synchronize()
+
+    s_g, r_g, opt_g, b_g = setup()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    opt_g.t = 0
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(graph, stream=side):
+            step(s_g, r_g, opt_g, b_g)
+    torch.cuda.synchronize()
+    assert torch.equal(s_g["colors"], torch.from_numpy(init["colors"]).to(cuda))
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(b_g["img"], b_e["img"])
+    assert float(b_g["loss"]) == float(b_e["loss"])
+    rel = (b_g["g3"] - b_e["g3"]).norm() / b_e["g3"].norm()
+    assert rel < 1e-4, float(rel)
+    losses = [float(b_g["loss"])]
+    for _ in range(40):
+        graph.replay()
+        torch.cuda.synchronize()
+        losses.append(float(b_g["loss"]))
+        assert r_g.instances()[1] is False
+    assert losses[-1] < 0.6 * losses[0], losses
