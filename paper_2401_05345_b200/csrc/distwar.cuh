@@ -149,6 +149,31 @@ __device__ __forceinline__ void reduce_bfly(int idx, float* grad, float (&v)[N],
   }
 }
 
+// SW-B for callers that hand in gradients with a per-param constant factor
+// still to apply (grad[p] = scale[p] * v[p]): the factor is linear in the sum,
+// so the reducing path multiplies once after the butterfly (`lane_scale` =
+// scale[slot], precomputed per lane) and only the per-lane fallback scales all
+// N values. Same request semantics as reduce_bfly<N, COUNT, true>.
+template <int N, bool COUNT>
+__device__ __forceinline__ void reduce_bfly_scaled(int idx, float* grad, float (&v)[N], int thr,
+                                                   bool active, int lane, uint32_t& nred,
+                                                   unsigned ballot, int slot, bool issuer,
+                                                   float lane_scale, const float (&scale)[N]) {
+  const int cnt = __popc(ballot);
+  if (cnt >= thr) {  // cnt > 0: callers skip empty ballots
+    ReduceScatter<N, 16>::run(v, lane);
+    if (issuer) {
+      red_add(grad + static_cast<int64_t>(idx) * N + slot, v[0] * lane_scale);
+      if (COUNT) nred += 1;
+    }
+  } else if (active) {
+    float* base = grad + static_cast<int64_t>(idx) * N;
+#pragma unroll
+    for (int p = 0; p < N; ++p) red_add(base + p, v[p] * scale[p]);
+    if (COUNT) nred += N;
+  }
+}
+
 // SW-S (reduce_serial, PAPER.md:1719-1759 with masked _sync shuffles): the
 // lowest lane of each __match_any_sync group of size >= thr folds the other
 // members' values in ascending lane order (reducers.cpp:101-121), then issues

@@ -592,6 +592,322 @@ __global__ void __launch_bounds__(256 / PPT, DW_MULTI_MIN_BLOCKS)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Packed-FP32 two-pixel kernels (sm_100 FFMA2 / FMUL2 / FADD2).
+//
+// A lane's two pixels (px, py) and (px, py + 4) run the same blend / gradient
+// arithmetic on different data, which is exactly the shape of Blackwell's
+// packed f32x2 instructions: one issue slot computes both pixels. The backward
+// is issue-bound (ncu: issue slots ~80 % busy, FMA pipe ~42 %), so halving the
+// FP instruction count of the per-pixel math is the lever. To keep the packed
+// path branch-free, a pixel's per-Gaussian activity enters as a multiplier
+// m in {0, 1}: the effective alpha am = m * alpha leaves T and the colour
+// accumulator unchanged when m = 0, and zeroes its nine gradients. The
+// accumulator is folded eagerly (acc += am (c - acc) after the gradient, the
+// same value the paper's loop folds lazily at the next contributor), which
+// removes the last_alpha / last_color state. dx is shared by both pixels.
+// The mean2D / conic factors (-W/2, -H/2, -1/2) are linear in the sums and
+// are applied after the warp reduction (reduce_bfly_scaled).
+__device__ __forceinline__ float2 bc2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Offsets, quadratic form and Gaussian of one staged Gaussian at the lane's two
+// pixels -- shared by the forward and the backward so both take identical
+// alpha decisions.
+struct Eval2 {
+  float dx, dxx;
+  float2 dy, dxy, dyy, power, G;
+};
+__device__ __forceinline__ void eval2(const float4& g, const float4& co, float pfx, float2 npfy,
+                                      Eval2& e) {
+  constexpr float kLog2e = 1.4426950408889634f;
+  e.dx = g.x - pfx;
+  e.dy = add2(bc2(g.y), npfy);
+  e.dxx = e.dx * e.dx;
+  e.dxy = mul2(bc2(e.dx), e.dy);
+  e.dyy = mul2(e.dy, e.dy);
+  const float2 t = fma2(bc2(co.z), e.dyy, bc2(co.x * e.dxx));
+  e.power = fma2(bc2(-co.y), e.dxy, mul2(bc2(-0.5f), t));
+  const float2 pl = mul2(e.power, bc2(kLog2e));
+  e.G = make_float2(ex2_approx(pl.x), ex2_approx(pl.y));
+}
+
+__global__ void __launch_bounds__(128)
+    k_forward_x2(const CamParams cam, const uint2* __restrict__ ranges,
+                 const uint32_t* __restrict__ values, const float2* __restrict__ means2D,
+                 const float4* __restrict__ conic_opacity, const float4* __restrict__ rgb,
+                 float* __restrict__ final_T, uint32_t* __restrict__ n_contrib,
+                 float* __restrict__ out_color) {
+  __shared__ Staged sm[kBlock];
+  __shared__ uint8_t s_mask[kBlock];
+  const int tile = blockIdx.x, t = threadIdx.x, w = t >> 5, lane = t & 31;
+  const int tx0 = (tile % cam.tiles_x) * kTile, ty0 = (tile / cam.tiles_x) * kTile;
+  const int px = tx0 + (w & 1) * 8 + (lane & 7);
+  const int py = ty0 + (w >> 1) * 8 + (lane >> 3);
+  const float pfx = (float)px;
+  const float2 npfy = make_float2(-(float)py, -(float)(py + 4));
+  float2 T = bc2(1.0f), C0 = bc2(0.0f), C1 = bc2(0.0f), C2 = bc2(0.0f);
+  uint32_t last0 = 0, last1 = 0;
+  bool done0 = !(px < cam.W && py < cam.H), done1 = !(px < cam.W && py + 4 < cam.H);
+  const uint32_t wbits = (1u << (4 * (w >> 1) + (w & 1))) | (1u << (4 * (w >> 1) + (w & 1) + 2));
+  const uint2 range = ranges[tile];
+  const int rounds = (int)((range.y - range.x + kBlock - 1) / kBlock);
+  int todo = (int)(range.y - range.x);
+  for (int i = 0; i < rounds; ++i, todo -= kBlock) {
+    if (__syncthreads_count(done0 && done1) == 128) break;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int st = t + h * 128;
+      const uint32_t progress = range.x + i * kBlock + st;
+      uint32_t mask = 0;
+      if (progress < range.y)
+        mask = stage(sm, st, values[progress], tx0, ty0, means2D, conic_opacity, rgb);
+      s_mask[st] = (uint8_t)mask;
+    }
+    __syncthreads();
+    const int n = min(kBlock, todo);
+    for (int k = 0; k * 32 < n; ++k) {
+      if (__all_sync(kFull, done0 && done1)) break;
+      const int jl = k * 32 + lane;
+      const uint32_t m = jl < n ? s_mask[jl] : 0u;
+      unsigned bits = __ballot_sync(kFull, (m & wbits) != 0u);
+      while (bits) {
+        const int j = k * 32 + __ffs(bits) - 1;
+        bits &= bits - 1u;
+        const float4 g = sm[j].xyi;
+        const float4 co = sm[j].co;
+        Eval2 e;
+        eval2(g, co, pfx, npfy, e);
+        const float2 Go = mul2(e.G, bc2(co.w));
+        const float2 alpha = make_float2(fminf(0.99f, Go.x), fminf(0.99f, Go.y));
+        const float2 om = fma2(alpha, bc2(-1.0f), bc2(1.0f));
+        const float2 test_T = mul2(T, om);
+        bool a0 = !done0 && e.power.x <= 0.0f && alpha.x >= 1.0f / 255.0f;
+        bool a1 = !done1 && e.power.y <= 0.0f && alpha.y >= 1.0f / 255.0f;
+        done0 = done0 || (a0 && test_T.x < 0.0001f);
+        done1 = done1 || (a1 && test_T.y < 0.0001f);
+        a0 = a0 && !done0;
+        a1 = a1 && !done1;
+        const float2 am = mul2(alpha, make_float2(a0 ? 1.0f : 0.0f, a1 ? 1.0f : 0.0f));
+        const float4 c = sm[j].col;
+        const float2 aT = mul2(am, T);
+        C0 = fma2(bc2(c.x), aT, C0);
+        C1 = fma2(bc2(c.y), aT, C1);
+        C2 = fma2(bc2(c.z), aT, C2);
+        T = mul2(T, fma2(am, bc2(-1.0f), bc2(1.0f)));  // == test_T when active, T when not
+        const uint32_t pos = (uint32_t)(i * kBlock + j + 1);  // 1-based list position
+        last0 = a0 ? pos : last0;
+        last1 = a1 ? pos : last1;
+      }
+    }
+  }
+  const int HW = cam.H * cam.W;
+  const float Ts[2] = {T.x, T.y}, c0[2] = {C0.x, C0.y}, c1[2] = {C1.x, C1.y},
+              c2[2] = {C2.x, C2.y};
+  const uint32_t ls[2] = {last0, last1};
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int y = py + 4 * k;
+    if (px < cam.W && y < cam.H) {
+      const int pix = y * cam.W + px;
+      final_T[pix] = Ts[k];
+      n_contrib[pix] = ls[k];
+      out_color[pix] = c0[k] + Ts[k] * cam.bg[0];
+      out_color[HW + pix] = c1[k] + Ts[k] * cam.bg[1];
+      out_color[2 * HW + pix] = c2[k] + Ts[k] * cam.bg[2];
+    }
+  }
+}
+
+// Backward, packed two-pixel form of k_backward_multi<2, POL> (same tile /
+// warp / lane layout, staging, masks, list-position bound and policy calls).
+template <int POL, bool COUNT, bool TAP = false>
+__global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
+    k_backward_x2(const CamParams cam, const uint2* __restrict__ ranges,
+                  const uint32_t* __restrict__ values, const float2* __restrict__ means2D,
+                  const float4* __restrict__ conic_opacity, const float4* __restrict__ rgb,
+                  const float* __restrict__ final_Ts, const uint32_t* __restrict__ n_contrib,
+                  const float* __restrict__ dL_dpixels, int thr, float* __restrict__ grad,
+                  unsigned long long* __restrict__ counters, const TapBuf tap) {
+  static_assert(POL != kNative, "native runs the thread-per-pixel kernel");
+  constexpr int NW = 4;
+  __shared__ Staged sm[kBlock];
+  __shared__ uint8_t s_mask[kBlock];
+  __shared__ uint32_t s_wmax[NW];
+  const int tile = blockIdx.x, t = threadIdx.x, w = t >> 5, lane = t & 31;
+  const int tx0 = (tile % cam.tiles_x) * kTile, ty0 = (tile / cam.tiles_x) * kTile;
+  const int px = tx0 + (w & 1) * 8 + (lane & 7);
+  const int py = ty0 + (w >> 1) * 8 + (lane >> 3);
+  const float pfx = (float)px;
+  const float2 npfy = make_float2(-(float)py, -(float)(py + 4));
+  const int HW = cam.H * cam.W;
+  // per-pixel constants and state, packed (pixel 0 in .x, pixel 1 in .y)
+  float2 T, nTb, dL0, dL1, dL2;
+  uint32_t last0 = 0, last1 = 0;
+  {
+    float Tf[2] = {0.0f, 0.0f}, d0[2] = {0.0f, 0.0f}, d1[2] = {0.0f, 0.0f}, d2[2] = {0.0f, 0.0f};
+    uint32_t ls[2] = {0u, 0u};
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int y = py + 4 * k;
+      if (px < cam.W && y < cam.H) {
+        const int pix = y * cam.W + px;
+        Tf[k] = final_Ts[pix];
+        ls[k] = n_contrib[pix];
+        d0[k] = dL_dpixels[pix];
+        d1[k] = dL_dpixels[HW + pix];
+        d2[k] = dL_dpixels[2 * HW + pix];
+      }
+    }
+    T = make_float2(Tf[0], Tf[1]);
+    dL0 = make_float2(d0[0], d0[1]);
+    dL1 = make_float2(d1[0], d1[1]);
+    dL2 = make_float2(d2[0], d2[1]);
+    const float2 bg_dot = fma2(bc2(cam.bg[2]), dL2,
+                               fma2(bc2(cam.bg[1]), dL1, mul2(bc2(cam.bg[0]), dL0)));
+    nTb = mul2(mul2(T, bc2(-1.0f)), bg_dot);  // -T_final * (bg . dL/dpixel)
+    last0 = ls[0];
+    last1 = ls[1];
+  }
+  float2 acc0 = bc2(0.0f), acc1 = bc2(0.0f), acc2 = bc2(0.0f);
+  const float hw = 0.5f * (float)cam.W, hh = 0.5f * (float)cam.H;
+  const float scale[kNParam] = {-hw, -hh, -0.5f, -0.5f, -0.5f, 1.0f, 1.0f, 1.0f, 1.0f};
+  const uint2 range = ranges[tile];
+  const uint32_t wmax = __reduce_max_sync(kFull, max(last0, last1));
+  if (lane == 0) s_wmax[w] = wmax;
+  __syncthreads();
+  uint32_t bmax = 0;
+#pragma unroll
+  for (int k = 0; k < NW; ++k) bmax = max(bmax, s_wmax[k]);
+  const uint32_t wbits = (1u << (4 * (w >> 1) + (w & 1))) | (1u << (4 * (w >> 1) + (w & 1) + 2));
+  uint32_t nred = 0, npairs = 0;
+  bool issuer;
+  const int slot = bfly_slot<kNParam>(lane, &issuer);
+  float lane_scale = 1.0f;
+#pragma unroll
+  for (int p = 0; p < kNParam; ++p)
+    if (slot == p) lane_scale = scale[p];
+  const int rounds = (int)((bmax + kBlock - 1) / kBlock);
+  int todo = (int)bmax;
+  const uint32_t top = range.x + bmax;
+  for (int i = 0; i < rounds; ++i, todo -= kBlock) {
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int st = t + h * 128;
+      uint32_t mask = 0;
+      if (st < todo)
+        mask = stage(sm, st, values[top - 1 - (i * kBlock + st)], tx0, ty0, means2D,
+                     conic_opacity, rgb);
+      s_mask[st] = (uint8_t)mask;
+    }
+    __syncthreads();
+    const int n = min(kBlock, todo);
+    const uint32_t base = bmax - 1 - (uint32_t)(i * kBlock);
+    for (int k = 0; k * 32 < n; ++k) {
+      const int jl = k * 32 + lane;
+      const uint32_t m = jl < n ? s_mask[jl] : 0u;
+      unsigned bits = __ballot_sync(kFull, (m & wbits) != 0u && (base - (uint32_t)jl) < wmax);
+      while (bits) {
+        const int j = k * 32 + __ffs(bits) - 1;
+        bits &= bits - 1u;
+        const uint32_t contributor = base - (uint32_t)j;
+        const float4 g = sm[j].xyi;
+        const float4 co = sm[j].co;
+        Eval2 e;
+        eval2(g, co, pfx, npfy, e);
+        const float2 Go = mul2(e.G, bc2(co.w));
+        const float2 alpha = make_float2(fminf(0.99f, Go.x), fminf(0.99f, Go.y));
+        const bool a0 = contributor < last0 && e.power.x <= 0.0f && alpha.x >= 1.0f / 255.0f;
+        const bool a1 = contributor < last1 && e.power.y <= 0.0f && alpha.y >= 1.0f / 255.0f;
+        const bool act = a0 || a1;
+        const unsigned ballot = __ballot_sync(kFull, act);
+        if (ballot == 0u) continue;
+        const float2 msk = make_float2(a0 ? 1.0f : 0.0f, a1 ? 1.0f : 0.0f);
+        const float4 c = sm[j].col;
+        const float2 am = mul2(alpha, msk);
+        const float2 om = fma2(am, bc2(-1.0f), bc2(1.0f));
+        const float2 inv = make_float2(rcp_approx(om.x), rcp_approx(om.y));
+        T = mul2(T, inv);
+        const float2 dcd = mul2(am, T);
+        const float2 d0 = fma2(acc0, bc2(-1.0f), bc2(c.x));  // c - acc
+        const float2 d1 = fma2(acc1, bc2(-1.0f), bc2(c.y));
+        const float2 d2 = fma2(acc2, bc2(-1.0f), bc2(c.z));
+        float2 dLa = fma2(d2, dL2, fma2(d1, dL1, mul2(d0, dL0)));
+        dLa = fma2(dLa, T, mul2(nTb, inv));
+        acc0 = fma2(am, d0, acc0);
+        acc1 = fma2(am, d1, acc1);
+        acc2 = fma2(am, d2, acc2);
+        // unscaled gradients: r0,r1 x (-W/2, -H/2) and r2..r4 x (-1/2) after the sum
+        const float2 q = mul2(mul2(Go, msk), dLa);  // o G dL/dalpha
+        const float2 adb = fma2(bc2(co.y), e.dy, bc2(co.x * e.dx));
+        const float2 cdb = fma2(bc2(co.z), e.dy, bc2(co.y * e.dx));
+        const float2 r[kNParam] = {mul2(q, adb),        mul2(q, cdb),
+                                   mul2(q, bc2(e.dxx)), mul2(q, e.dxy),
+                                   mul2(q, e.dyy),      mul2(mul2(e.G, msk), dLa),
+                                   mul2(dcd, dL0),      mul2(dcd, dL1),
+                                   mul2(dcd, dL2)};
+        float v[kNParam];
+#pragma unroll
+        for (int p = 0; p < kNParam; ++p) v[p] = r[p].x + r[p].y;
+        const int id = (int)__float_as_uint(g.z);
+        if (COUNT) {
+          const uint32_t cnt = __popc(__ballot_sync(kFull, a0)) + __popc(__ballot_sync(kFull, a1));
+          if (lane == 0) npairs += cnt;
+        }
+        if (TAP || POL != kSwB) {
+#pragma unroll
+          for (int p = 0; p < kNParam; ++p) v[p] *= scale[p];
+        }
+        if (TAP) {  // the record the policy reduces: lane value = its pixels' sum
+          unsigned long long rec = 0;
+          if (lane == 0) rec = atomicAdd(tap.count, 1ull);
+          rec = __shfl_sync(kFull, rec, 0);
+          if (rec < tap.cap) {
+            if (lane == 0) {
+              tap.warp_id[rec] = tile * NW + w;
+              tap.iteration[rec] = (int32_t)contributor;
+              tap.active[rec] = ballot;
+            }
+            tap.prim[rec * 32 + lane] = id;
+#pragma unroll
+            for (int p = 0; p < kNParam; ++p) tap.vals[(rec * kNParam + p) * 32 + lane] = v[p];
+          }
+          reduce_bfly<kNParam, COUNT, true>(id, grad, v, thr, act, lane, nred, ballot, slot,
+                                            issuer);
+        } else if (POL == kSwB) {
+          reduce_bfly_scaled<kNParam, COUNT>(id, grad, v, thr, act, lane, nred, ballot, slot,
+                                             issuer, lane_scale, scale);
+        } else if (POL == kSwS) {
+          reduce_serial<kNParam, COUNT>(id, grad, v, thr, act, lane, nred, ballot);
+        } else {
+          reduce_cccl<kNParam, COUNT>(id, grad, v, act, lane, nred, ballot);
+        }
+      }
+    }
+  }
+  if (COUNT) {
+    flush_count(counters, npairs, lane);
+    flush_count(counters + 1, nred, lane);
+  }
+}
+
+#ifndef DW_BLEND_X2
+#define DW_BLEND_X2 1  // packed f32x2 two-pixel kernels (0: k_backward_multi / k_forward_ppt2)
+#endif
+
 template <int POL>
 void launch_bwd(bool count, const CamParams& cam, const uint2* ranges, const uint32_t* values,
                 const float2* means2D, const float4* co, const float4* rgb, const float* fT,
@@ -602,6 +918,15 @@ void launch_bwd(bool count, const CamParams& cam, const uint2* ranges, const uin
   // paper's thread-per-pixel kernel (its faster layout: 7.8 vs 8.2 ms on C3,
   // profiles/r01/ab_ppt.jsonl), so the naive baseline is not handicapped.
   if constexpr (POL != kNative) {
+    if (DW_BLEND_X2) {
+      if (count)
+        k_backward_x2<POL, true><<<grid, 128, 0, s>>>(cam, ranges, values, means2D, co, rgb, fT,
+                                                      nc, dL, thr, grad, ctr, TapBuf{});
+      else
+        k_backward_x2<POL, false><<<grid, 128, 0, s>>>(cam, ranges, values, means2D, co, rgb, fT,
+                                                       nc, dL, thr, grad, nullptr, TapBuf{});
+      return;
+    }
     constexpr int NT = 256 / DW_BWD_PPT;
     if (count)
       k_backward_multi<DW_BWD_PPT, POL, true><<<grid, NT, 0, s>>>(
@@ -626,8 +951,12 @@ void launch_backward_tap(const CamParams& cam, const uint2* ranges, const uint32
                          const float* final_T, const uint32_t* n_contrib, const float* dL, int thr,
                          float* grad, const TapBuf& tap, cudaStream_t s) {
   const int grid = cam.tiles_x * cam.tiles_y;
-  k_backward_multi<DW_BWD_PPT, kSwB, false, true><<<grid, 256 / DW_BWD_PPT, 0, s>>>(
-      cam, ranges, values, means2D, co, rgb, final_T, n_contrib, dL, thr, grad, nullptr, tap);
+  if (DW_BLEND_X2)
+    k_backward_x2<kSwB, false, true><<<grid, 128, 0, s>>>(
+        cam, ranges, values, means2D, co, rgb, final_T, n_contrib, dL, thr, grad, nullptr, tap);
+  else
+    k_backward_multi<DW_BWD_PPT, kSwB, false, true><<<grid, 256 / DW_BWD_PPT, 0, s>>>(
+        cam, ranges, values, means2D, co, rgb, final_T, n_contrib, dL, thr, grad, nullptr, tap);
   DW_CUDA(cudaGetLastError());
 }
 
@@ -640,7 +969,10 @@ void launch_forward_impl(const CamParams& cam, const uint2* ranges, const uint32
 #ifndef DW_FWD_PPT
 #define DW_FWD_PPT 2  // A/B on C3: 0.527 vs 0.558 ms (profiles/r01/ab_fwd2.jsonl)
 #endif
-  if (DW_FWD_PPT == 2)
+  if (DW_BLEND_X2)
+    k_forward_x2<<<grid, 128, 0, s>>>(cam, ranges, values, means2D, conic_opacity, rgb, final_T,
+                                      n_contrib, out_color);
+  else if (DW_FWD_PPT == 2)
     k_forward_ppt2<<<grid, 128, 0, s>>>(cam, ranges, values, means2D, conic_opacity, rgb, final_T,
                                         n_contrib, out_color);
   else

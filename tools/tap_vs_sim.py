@@ -71,7 +71,7 @@ def main():
     L.wr_trace_free.argtypes = [C.c_void_p]
     res = {"workload": a.workload, "records": tap.num_records,
            "contributions_in_records": tap.contributions(), "pairs": out["pairs"],
-           "layout": "two pixels per lane (k_backward_multi<2>)", "presets": {}}
+           "layout": "two pixels per lane (k_backward_x2)", "presets": {}}
     with tempfile.TemporaryDirectory() as td:
         path = os.path.join(td, "tap.wrtb")
         orc.save_binary(tap, path)
