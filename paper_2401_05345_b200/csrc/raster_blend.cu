@@ -37,7 +37,7 @@ namespace dw {
 namespace {
 
 struct __align__(16) Staged {
-  float4 xyi;  // x, y, id (uint bits), -
+  float4 xyi;  // x, y, id (uint bits), 1/opacity
   float4 co;   // conic a, b, c, opacity
   float4 col;  // r, g, b, -
 };
@@ -50,7 +50,8 @@ __device__ __forceinline__ uint32_t stage(Staged* s, int slot, uint32_t id, int 
                                           const float4* __restrict__ rgb) {
   const float2 m = __ldg(means2D + id);
   const float4 co = __ldg(conic_opacity + id);
-  s[slot].xyi = make_float4(m.x, m.y, __uint_as_float(id), 0.0f);
+  s[slot].xyi = make_float4(m.x, m.y, __uint_as_float(id),
+                            co.w > 0.0f ? __fdividef(1.0f, co.w) : 0.0f);  // w: 1/opacity
   s[slot].co = co;
   s[slot].col = __ldg(rgb + id);
   if (!(co.w * 255.0f > 1.0f)) return 0u;  // alpha < 1/255 everywhere
@@ -617,6 +618,15 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 16-byte shared load from a 32-bit shared-window address held in a register
+// (ptxas otherwise re-derives the window base in every loop iteration).
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a));
+  return v;
+}
 __device__ __forceinline__ float rcp_approx(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -799,6 +809,10 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
 #pragma unroll
   for (int p = 0; p < kNParam; ++p)
     if (slot == p) lane_scale = scale[p];
+  // keep it in a register: ptxas otherwise re-derives it in every reducing iteration
+  asm volatile("" : "+f"(lane_scale));
+  uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
+  asm volatile("" : "+r"(sbase));
   const int rounds = (int)((bmax + kBlock - 1) / kBlock);
   int todo = (int)bmax;
   const uint32_t top = range.x + bmax;
@@ -824,8 +838,8 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
         const int j = k * 32 + __ffs(bits) - 1;
         bits &= bits - 1u;
         const uint32_t contributor = base - (uint32_t)j;
-        const float4 g = sm[j].xyi;
-        const float4 co = sm[j].co;
+        const float4 g = lds128(sbase + 48u * (uint32_t)j);
+        const float4 co = lds128(sbase + 48u * (uint32_t)j + 16u);
         Eval2 e;
         eval2(g, co, pfx, npfy, e);
         const float2 Go = mul2(e.G, bc2(co.w));
@@ -836,9 +850,9 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
         const unsigned ballot = __ballot_sync(kFull, act);
         if (ballot == 0u) continue;
         const float2 msk = make_float2(a0 ? 1.0f : 0.0f, a1 ? 1.0f : 0.0f);
-        const float4 c = sm[j].col;
+        const float4 c = lds128(sbase + 48u * (uint32_t)j + 32u);
         const float2 am = mul2(alpha, msk);
-        const float2 om = fma2(am, bc2(-1.0f), bc2(1.0f));
+        const float2 om = add2(bc2(1.0f), make_float2(-am.x, -am.y));
         const float2 inv = make_float2(rcp_approx(om.x), rcp_approx(om.y));
         T = mul2(T, inv);
         const float2 dcd = mul2(am, T);
@@ -850,18 +864,27 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
         acc0 = fma2(am, d0, acc0);
         acc1 = fma2(am, d1, acc1);
         acc2 = fma2(am, d2, acc2);
-        // unscaled gradients: r0,r1 x (-W/2, -H/2) and r2..r4 x (-1/2) after the sum
-        const float2 q = mul2(mul2(Go, msk), dLa);  // o G dL/dalpha
-        const float2 adb = fma2(bc2(co.y), e.dy, bc2(co.x * e.dx));
-        const float2 cdb = fma2(bc2(co.z), e.dy, bc2(co.y * e.dx));
-        const float2 r[kNParam] = {mul2(q, adb),        mul2(q, cdb),
-                                   mul2(q, bc2(e.dxx)), mul2(q, e.dxy),
-                                   mul2(q, e.dyy),      mul2(mul2(e.G, msk), dLa),
-                                   mul2(dcd, dL0),      mul2(dcd, dL1),
-                                   mul2(dcd, dL2)};
-        float v[kNParam];
-#pragma unroll
-        for (int p = 0; p < kNParam; ++p) v[p] = r[p].x + r[p].y;
+        // Lane sums of the nine gradients with the factors -W/2, -H/2 (mean2D)
+        // and -1/2 (conic) left for after the warp sum. With q = o G dL/dalpha
+        // per pixel and dx shared by the lane's two pixels:
+        //   mean2D = (a dx Q + b Qy, c Qy + b dx Q),  conic = (dx^2 Q, dx Qy, Qyy),
+        //   opacity = Q / o,  colour = sum_pix alpha T dL/dpixel,
+        // Q = sum q, Qy = sum q dy, Qyy = sum q dy^2 -- the pixel sum folds into
+        // the products instead of nine separate adds.
+        const float2 q = mul2(mul2(Go, msk), dLa);
+        const float2 qdy = mul2(q, e.dy);
+        const float Q = q.x + q.y, Qy = qdy.x + qdy.y;
+        const float Qyy = fmaf(qdy.y, e.dy.y, qdy.x * e.dy.x);
+        const float tq = e.dx * Q;
+        float v[kNParam] = {fmaf(co.x, tq, co.y * Qy),
+                            fmaf(co.z, Qy, co.y * tq),
+                            e.dxx * Q,
+                            e.dx * Qy,
+                            Qyy,
+                            Q * g.w,
+                            fmaf(dcd.y, dL0.y, dcd.x * dL0.x),
+                            fmaf(dcd.y, dL1.y, dcd.x * dL1.x),
+                            fmaf(dcd.y, dL2.y, dcd.x * dL2.x)};
         const int id = (int)__float_as_uint(g.z);
         if (COUNT) {
           const uint32_t cnt = __popc(__ballot_sync(kFull, a0)) + __popc(__ballot_sync(kFull, a1));
