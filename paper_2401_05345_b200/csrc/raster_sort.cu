@@ -42,7 +42,11 @@ constexpr int kWarps = kSortThreads / 32;
 // Lanes of this warp whose digit equals mine (warp multi-split by votes: one
 // ballot per digit bit instead of a __match_any_sync, which is a multi-cycle
 // instruction). Invalid lanes never match valid ones.
+#ifndef DW_SORT_MATCH
+#define DW_SORT_MATCH 0  // 1: one __match_any_sync instead of `bits` ballots
+#endif
 __device__ __forceinline__ unsigned digit_peers(uint32_t d, int bits, bool valid) {
+  if (DW_SORT_MATCH) return __match_any_sync(kFull, valid ? d : 0xffffffffu);
   unsigned peers = __ballot_sync(kFull, valid);
   if (!valid) peers = ~peers;
   for (int b = 0; b < bits; ++b) {
@@ -459,7 +463,10 @@ inline unsigned blocks_for(int64_t n, int per) { return static_cast<unsigned>((n
 // enough tiles to fill every SM a few times over, else 4 (1024-element tiles)
 // so small inputs (the P-element depth sort) still spread over 148 SMs.
 constexpr int64_t kBigSortN = int64_t(148) * 4 * 4096;
-inline int sort_items(int64_t n) { return n >= kBigSortN ? 16 : 4; }
+#ifndef DW_SORT_BIG_ITEMS
+#define DW_SORT_BIG_ITEMS 8  // A/B on C3: 0.836 vs 0.843 ms forward (16)
+#endif
+inline int sort_items(int64_t n) { return n >= kBigSortN ? DW_SORT_BIG_ITEMS : 4; }
 
 size_t radix_sort_temp_bytes(int64_t n) {
   const int64_t tiles = (n + 1023) / 1024;  // worst case: 4-item tiles
@@ -485,19 +492,34 @@ int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* 
   for (int shift = 0; shift < bits; shift += 8) {
     const int b = bits - shift < 8 ? bits - shift : 8;
     const uint32_t mask = (1u << b) - 1u;
-    if (items == 16)
-      k_upsweep<16><<<grid, kSortThreads, 0, s>>>(k[cur], n, shift, mask, b, counts, tiles,
-                                                  n_dev);
-    else
-      k_upsweep<4><<<grid, kSortThreads, 0, s>>>(k[cur], n, shift, mask, b, counts, tiles, n_dev);
+    switch (items) {
+      case 16:
+        k_upsweep<16><<<grid, kSortThreads, 0, s>>>(k[cur], n, shift, mask, b, counts, tiles,
+                                                    n_dev);
+        break;
+      case 8:
+        k_upsweep<8><<<grid, kSortThreads, 0, s>>>(k[cur], n, shift, mask, b, counts, tiles,
+                                                   n_dev);
+        break;
+      default:
+        k_upsweep<4><<<grid, kSortThreads, 0, s>>>(k[cur], n, shift, mask, b, counts, tiles,
+                                                   n_dev);
+    }
     k_scan_rows<<<256, 1024, 0, s>>>(counts, tiles, digit);
     k_scan_digits<<<1, 256, 0, s>>>(digit, 256);
-    if (items == 16)
-      k_downsweep<16><<<grid, kSortThreads, 0, s>>>(k[cur], v[cur], n, shift, mask, b, counts,
-                                                    tiles, digit, k[cur ^ 1], v[cur ^ 1], n_dev);
-    else
-      k_downsweep<4><<<grid, kSortThreads, 0, s>>>(k[cur], v[cur], n, shift, mask, b, counts,
-                                                   tiles, digit, k[cur ^ 1], v[cur ^ 1], n_dev);
+    switch (items) {
+      case 16:
+        k_downsweep<16><<<grid, kSortThreads, 0, s>>>(k[cur], v[cur], n, shift, mask, b, counts,
+                                                      tiles, digit, k[cur ^ 1], v[cur ^ 1], n_dev);
+        break;
+      case 8:
+        k_downsweep<8><<<grid, kSortThreads, 0, s>>>(k[cur], v[cur], n, shift, mask, b, counts,
+                                                     tiles, digit, k[cur ^ 1], v[cur ^ 1], n_dev);
+        break;
+      default:
+        k_downsweep<4><<<grid, kSortThreads, 0, s>>>(k[cur], v[cur], n, shift, mask, b, counts,
+                                                     tiles, digit, k[cur ^ 1], v[cur ^ 1], n_dev);
+    }
     cur ^= 1;
   }
   DW_CUDA(cudaGetLastError());

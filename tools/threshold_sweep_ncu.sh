@@ -13,9 +13,10 @@ sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pi
 sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_active,\
 sm__inst_executed.sum,sm__cycles_elapsed.max,smsp__sass_thread_inst_executed_op_fadd_pred_on.sum,\
 smsp__pcsamp_warps_issue_stalled_lg_throttle,smsp__pcsamp_warps_issue_stalled_mio_throttle,\
-smsp__pcsamp_warps_issue_stalled_long_scoreboard,smsp__pcsamp_sample_count
+smsp__pcsamp_warps_issue_stalled_long_scoreboard,smsp__pcsamp_sample_count,\
+dram__bytes_read.sum,dram__bytes_write.sum
 mkdir -p gpurun_out
-for spec in native:0 sw_b:0 sw_b:4 sw_b:8 sw_b:12 sw_b:16 sw_b:20 sw_b:24 sw_b:28 sw_b:32 sw_s:0 sw_s:16 sw_s:32 cccl:0; do
+for spec in native:0 sw_b:0 sw_b:4 sw_b:8 sw_b:10 sw_b:12 sw_b:16 sw_b:20 sw_b:24 sw_b:28 sw_b:32 sw_s:0 sw_s:16 sw_s:32 cccl:0; do
   pol=${spec%%:*}; t=${spec##*:}
   timeout 300 ncu --metrics "$METRICS" --clock-control none -k regex:k_backward -s 1 -c 1 --csv \
     python tools/profile_backward.py --workload "$WL" --policy "$pol" --threshold "$t" --reps 2 \

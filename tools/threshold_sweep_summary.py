@@ -29,6 +29,8 @@ def load(path):
         if r[mi] == "gpu__time_duration.sum":
             v *= {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3,
                   "msecond": 1.0, "ms": 1.0}.get(r[ui].strip(), 1.0)
+        else:  # byte counters in bytes
+            v *= {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(r[ui].strip(), 1.0)
         out[r[mi]] = v
     return out
 
