@@ -168,7 +168,8 @@ struct dw_rasterizer {
 
   void forward(int32_t P_, const float* means3D, const float* scales, const float* rotations,
                const float* opacities, const float* colors, const dw_camera& c, float* out_color,
-               int32_t* radii_out, cudaStream_t s, bool nosync = false) {
+               int32_t* radii_out, cudaStream_t s, bool nosync = false,
+               bool sticky_overflow = false) {
     last_overflow = false;
     if (P_ < 0) throw std::invalid_argument("P must be >= 0");
     if (c.width < 1 || c.height < 1) throw std::invalid_argument("camera size must be >= 1");
@@ -230,6 +231,7 @@ struct dw_rasterizer {
         if (cap_i[0] == 0 || cap_i[2] == 0)
           throw std::invalid_argument("no-sync forward needs dw_rasterizer_reserve first");
         n_grid = static_cast<int64_t>(std::min(cap_i[0], cap_i[2]));
+        if (!sticky_overflow) DW_CUDA(cudaMemsetAsync(overflow_dev, 0, sizeof(unsigned int), s));
         dw::launch_clamp_total(offsets, P, static_cast<uint64_t>(n_grid), live_dev, overflow_dev,
                                s);
         n_dev = live_dev;
@@ -528,26 +530,54 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
   DW_CUDA(cudaEventRecord(e_in[0], r->s_in));
   DW_CUDA(cudaMemsetAsync(d_g, 0, kNParam * np * sizeof(float), s));
   DW_CUDA(cudaStreamWaitEvent(s, e_scene, 0));
-  for (int k = 0; k < V; ++k) {
-    const int b = k & 1;
-    if (k + 1 < V) {  // prefetch view k+1 once view k-1 released its buffer
-      DW_CUDA(cudaStreamWaitEvent(r->s_in, e_used[b ^ 1], 0));
-      h2d(d_dl[b ^ 1], dL + static_cast<size_t>(k + 1) * 3 * npx, 3 * npx, r->s_in);
-      DW_CUDA(cudaEventRecord(e_in[b ^ 1], r->s_in));
+  // View 0 reads its instance count back (one host sync) and reserves 1.5x
+  // that; views 1.. then keep the count on the device (no host sync per
+  // view, so the host runs ahead and the copy streams overlap freely). A view
+  // that outgrows the reserve raises the sticky overflow flag and the whole
+  // batch is redone with per-view host syncs.
+  bool nosync_ok = V > 1;
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) {  // redo from the start: zero the gradients, re-upload view 0's dL/dpixel
+      DW_CUDA(cudaMemsetAsync(d_g, 0, kNParam * np * sizeof(float), s));
+      h2d(d_dl[0], dL, 3 * npx, r->s_in);
+      DW_CUDA(cudaEventRecord(e_in[0], r->s_in));
     }
-    DW_CUDA(cudaStreamWaitEvent(s, e_in[b], 0));
-    if (k >= 2) DW_CUDA(cudaStreamWaitEvent(s, e_img[b], 0));  // image k-2 downloaded
-    r->forward(P, d_m, d_sc, d_rot, d_op, d_col, cams[k], d_img[b], nullptr, s);
-    r->backward(d_dl[b], policy, thr, d_g, nullptr, s);
-    DW_CUDA(cudaEventRecord(e_used[b], s));
-    if (out_images) {
-      DW_CUDA(cudaStreamWaitEvent(r->s_out, e_used[b], 0));
-      DW_CUDA(cudaMemcpyAsync(out_images + static_cast<size_t>(k) * 3 * npx, d_img[b],
-                              3 * npx * sizeof(float), cudaMemcpyDeviceToHost, r->s_out));
-      DW_CUDA(cudaEventRecord(e_img[b], r->s_out));
-    } else {
-      DW_CUDA(cudaEventRecord(e_img[b], s));
+    for (int k = 0; k < V; ++k) {
+      const int b = k & 1;
+      if (k + 1 < V) {  // prefetch view k+1 once view k-1 released its buffer
+        DW_CUDA(cudaStreamWaitEvent(r->s_in, e_used[b ^ 1], 0));
+        h2d(d_dl[b ^ 1], dL + static_cast<size_t>(k + 1) * 3 * npx, 3 * npx, r->s_in);
+        DW_CUDA(cudaEventRecord(e_in[b ^ 1], r->s_in));
+      }
+      DW_CUDA(cudaStreamWaitEvent(s, e_in[b], 0));
+      if (k >= 2) DW_CUDA(cudaStreamWaitEvent(s, e_img[b], 0));  // image k-2 downloaded
+      if (nosync_ok && k == 1) {  // view 0 is done with the buffers a reserve may move
+        const int64_t want = r->num_rendered + r->num_rendered / 2 + 4096;
+        if (static_cast<int64_t>(std::min(r->cap_i[0], r->cap_i[2])) < want) {
+          DW_CUDA(cudaStreamSynchronize(s));
+          r->reserve(P, cams[0].width, cams[0].height, want);
+        }
+        DW_CUDA(cudaMemsetAsync(r->overflow_dev, 0, sizeof(unsigned int), s));
+      }
+      const bool nosync = nosync_ok && k > 0;
+      r->forward(P, d_m, d_sc, d_rot, d_op, d_col, cams[k], d_img[b], nullptr, s, nosync,
+                 /*sticky_overflow=*/true);
+      r->backward(d_dl[b], policy, thr, d_g, nullptr, s);
+      DW_CUDA(cudaEventRecord(e_used[b], s));
+      if (out_images) {
+        DW_CUDA(cudaStreamWaitEvent(r->s_out, e_used[b], 0));
+        DW_CUDA(cudaMemcpyAsync(out_images + static_cast<size_t>(k) * 3 * npx, d_img[b],
+                                3 * npx * sizeof(float), cudaMemcpyDeviceToHost, r->s_out));
+        DW_CUDA(cudaEventRecord(e_img[b], r->s_out));
+      } else {
+        DW_CUDA(cudaEventRecord(e_img[b], s));
+      }
     }
+    if (!nosync_ok) break;
+    bool ovf = false;
+    r->resolve_count(&ovf);  // synchronous: the batch's sticky flag
+    if (!ovf) break;
+    nosync_ok = false;  // redo every view with host-read instance counts
   }
   if (P > 0)
     DW_CUDA(cudaMemcpyAsync(grad, d_g, kNParam * size_t(P) * sizeof(float),

@@ -427,7 +427,7 @@ __global__ void k_clamp_total(const uint64_t* __restrict__ offsets, int P, uint6
   const uint64_t total = P > 0 ? offsets[P - 1] : 0;
   const bool fits = total <= cap;
   *n_live = fits ? total : 0ull;
-  *overflow = fits ? 0u : 1u;
+  if (!fits) *overflow = 1u;  // sticky: cleared by the caller (per forward, or per view batch)
 }
 
 __global__ void k_ranges_u32(int64_t L, const uint32_t* __restrict__ tiles, uint2* __restrict__ ranges,

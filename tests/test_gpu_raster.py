@@ -262,6 +262,41 @@ def test_render_views_host_matches_per_view(cuda, orc):
         assert np.linalg.norm(g - want_g) / np.linalg.norm(want_g) < GRAD_REL_L2
 
 
+def test_render_views_host_reserve_overflow_redo(cuda, orc):
+    """Views after the first keep their instance count on the device against
+    a reserve of 1.5x view 0's count; a later view that outgrows it (view 0
+    is zoomed far out) raises the overflow flag and the batch is redone
+    with host-read counts -- the result still equals the per-view oracle."""
+    import torch
+
+    from paper_2401_05345_b200 import warpred as wr
+    from paper_2401_05345_b200.rasterizer import GaussianRasterizer, render_views_host
+    from paper_2401_05345_b200.scene import make_camera, make_dL_dpixels, make_scene
+
+    P, W, H = 4000, 160, 128
+    sc = make_scene(P, W, H, seed=33)
+    cams = [make_camera(W, H, fov_x_deg=150.0), make_camera(W, H), make_camera(W, H, yaw_deg=5.0)]
+    V = len(cams)
+    dL = np.stack([make_dL_dpixels(W, H, seed=60 + k) for k in range(V)])
+    want_g = np.zeros((P, 9))
+    refs = [orc.gs_render(sc, _ocam(cams[k]), dL[k], threads=8) for k in range(V)]
+    for ref in refs:
+        want_g += ref["grad"]
+    assert refs[1]["num_rendered"] > refs[0]["num_rendered"] * 3 // 2 + 4096
+    pin = {k: torch.from_numpy(v).pin_memory() for k, v in sc.items()}
+    dL_h = torch.from_numpy(dL.astype(np.float32)).pin_memory()
+    img = torch.empty((V, 3, H, W), dtype=torch.float32).pin_memory()
+    grad = torch.empty((P, 9), dtype=torch.float32).pin_memory()
+    r = GaussianRasterizer()
+    ptrs = [pin[k].data_ptr() for k in ("means3D", "scales", "rotations", "opacities", "colors")]
+    render_views_host(r, ptrs, P, cams, dL_h.data_ptr(), wr.Policy(wr.PolicyKind.sw_b, 8),
+                      img.data_ptr(), grad.data_ptr())
+    for k in range(V):
+        assert np.abs(img[k].numpy() - refs[k]["image"]).max() < IMG_ATOL
+    g = grad.numpy().astype(np.float64)
+    assert np.linalg.norm(g - want_g) / np.linalg.norm(want_g) < GRAD_REL_L2
+
+
 def test_empty_and_culled_scenes(cuda):
     import torch
 
