@@ -152,8 +152,10 @@ __global__ void __launch_bounds__(kBlock)
   depths[i] = tv2;
   radii[i] = radius;
   means2D[i] = make_float2(ix, iy);
-  conic_opacity[i] = make_float4(cv2 * det_inv, -cv1 * det_inv, cv0 * det_inv, __ldg(opacities + i));
-  rgb[i] = make_float4(s_col[3 * t], s_col[3 * t + 1], s_col[3 * t + 2], 0.0f);
+  const float op = __ldg(opacities + i);
+  conic_opacity[i] = make_float4(cv2 * det_inv, -cv1 * det_inv, cv0 * det_inv, op);
+  // w: 1/opacity for the backward's opacity gradient (sum q / o, raster_blend.cu)
+  rgb[i] = make_float4(s_col[3 * t], s_col[3 * t + 1], s_col[3 * t + 2], op > 0.0f ? 1.0f / op : 0.0f);
   tiles_touched[i] = static_cast<uint32_t>(area);
 }
 
