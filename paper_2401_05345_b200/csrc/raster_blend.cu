@@ -42,6 +42,12 @@ struct __align__(16) Staged {
   float4 col;  // r, g, b, 1/opacity (preprocess)
 };
 
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // Stage Gaussian `id` into slot `slot` and return its 8-bit warp-block mask
 // for the tile whose top-left pixel is (tx0, ty0).
 __device__ __forceinline__ uint32_t stage(Staged* s, int slot, uint32_t id, int tx0, int ty0,
@@ -374,9 +380,11 @@ __global__ void __launch_bounds__(kBlock, DW_BWD_MIN_BLOCKS)
         const float4 co = sm[j].co;
         const float dx = g.x - pfx, dy = g.y - pfy;
         const float dxx = dx * dx, dxy = dx * dy, dyy = dy * dy;
-        const float power = -0.5f * (co.x * dxx + co.z * dyy) - co.y * dxy;
-        const float G = __expf(power);
-        const float alpha = fminf(0.99f, co.w * G);
+        // the packed forward's exact operation sequence (eval2), so this
+        // kernel walks exactly the forward's contributors
+        const float power = __fmaf_rn(-co.y, dxy, -0.5f * __fmaf_rn(co.z, dyy, co.x * dxx));
+        const float G = ex2_approx(power * 1.4426950408889634f);
+        const float alpha = fminf(0.99f, G * co.w);
         const bool act = inside && contributor < last_contributor && power <= 0.0f &&
                          alpha >= 1.0f / 255.0f;
         const unsigned ballot = __ballot_sync(kFull, act);
@@ -657,11 +665,6 @@ __device__ __forceinline__ float2 bc2(float a) { return make_float2(a, a); }
 __device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
 __device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
-__device__ __forceinline__ float ex2_approx(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 // 16-byte shared load from a 32-bit shared-window address held in a register
 // (ptxas otherwise re-derives the window base in every loop iteration).
 __device__ __forceinline__ float4 lds128(uint32_t a) {

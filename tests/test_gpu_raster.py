@@ -297,6 +297,58 @@ def test_render_views_host_reserve_overflow_redo(cuda, orc):
     assert np.linalg.norm(g - want_g) / np.linalg.norm(want_g) < GRAD_REL_L2
 
 
+def test_full_size_c3_properties(cuda):
+    """BASELINE configs[2] at full size (1M Gaussians, 1920x1080), where the
+    CPU oracle is too slow: size-independent properties. The (tile | depth)
+    keys are sorted, the tile ranges partition the instance list and hold
+    only their own tile; every reduction policy and threshold yields the same
+    contributing pairs, RED counts that follow the policy (native = 9 per
+    pair; SW-B monotone in t, t = 33 == native), and gradients equal to the
+    native-atomic ones up to fp32 summation order."""
+    import torch
+
+    from paper_2401_05345_b200 import _lib
+    from paper_2401_05345_b200 import warpred as wr
+    from paper_2401_05345_b200.rasterizer import GaussianRasterizer, lib
+    from paper_2401_05345_b200.scene import CONFIGS, make_camera, make_dL_dpixels, make_scene
+
+    P, W, H, hc, _ = CONFIGS["c3_1m_1080p"]
+    sc = {k: torch.from_numpy(v).to(cuda) for k, v in make_scene(P, W, H, seed=0).items()}
+    dL = torch.from_numpy(make_dL_dpixels(W, H, seed=1)).to(cuda)
+    r = GaussianRasterizer()
+    _, _, nr = r.render_forward(sc["means3D"], sc["scales"], sc["rotations"], sc["opacities"],
+                                sc["colors"], make_camera(W, H))
+    keys = r.buffer("keys")
+    assert keys.shape[0] == nr > 4_000_000
+    assert np.all(keys[1:] >= keys[:-1])
+    ranges = r.buffer("ranges")
+    tiles = (keys >> np.uint64(32)).astype(np.int64)
+    nonempty = ranges[:, 1] > ranges[:, 0]
+    assert ranges[nonempty, 0].min() == 0 and ranges[nonempty, 1].max() == nr
+    starts = np.repeat(np.nonzero(nonempty)[0], (ranges[nonempty, 1] - ranges[nonempty, 0]))
+    assert np.array_equal(starts, tiles)  # each instance sits in its own tile's range
+
+    def run(kind, t):
+        g, pairs = r.render_backward(dL, wr.Policy(kind, t), count_pairs=True)
+        reds = _lib.u64()
+        _lib.check(lib().dw_rasterizer_last_reds(r.handle, C.byref(reds)))
+        return g.double().cpu().numpy(), pairs, reds.value
+
+    g_nat, pairs, reds_nat = run(wr.PolicyKind.native, 0)
+    assert pairs > 100_000_000 and reds_nat == 9 * pairs
+    prev = 0
+    for t in (0, 8, 16, 33):
+        g, p2, reds = run(wr.PolicyKind.sw_b, t)
+        assert p2 == pairs  # same contributor set as the forward and the native kernel
+        assert reds >= prev
+        prev = reds
+        rel = np.linalg.norm(g - g_nat) / np.linalg.norm(g_nat)
+        assert rel < 1e-5, (t, rel)
+    # t = 33: nothing reduces; one RED per (active lane, param), a lane carrying its two
+    # pixels' sum -- at most the native kernel's one per (pixel, param)
+    assert prev <= reds_nat
+
+
 def test_empty_and_culled_scenes(cuda):
     import torch
 
