@@ -81,6 +81,49 @@ struct ReduceScatter {
   }
 };
 
+// N = 9 specialisation with the level sums done as packed FP32 pairs
+// (sm_100 FADD2): same slot algebra as ReduceScatter<9, 16> (bfly_slot<9>
+// applies unchanged), 8 adds instead of 12.
+__device__ __forceinline__ void reduce_scatter9(float (&v)[9], int lane) {
+  // level 16: 9 -> 5 slots
+  bool up = (lane & 16) != 0;
+  float sd[5], kp[5];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    sd[k] = up ? v[k] : v[k + 5];
+    kp[k] = up ? v[k + 5] : v[k];
+  }
+  sd[4] = up ? v[4] : 0.0f;
+  kp[4] = v[4];
+  float rv[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) rv[k] = __shfl_xor_sync(kFull, sd[k], 16);
+  const float2 s01 = __fadd2_rn(make_float2(kp[0], kp[1]), make_float2(rv[0], rv[1]));
+  const float2 s23 = __fadd2_rn(make_float2(kp[2], kp[3]), make_float2(rv[2], rv[3]));
+  const float s4 = kp[4] + rv[4];
+  // level 8: 5 -> 3
+  up = (lane & 8) != 0;
+  const float a0 = up ? s01.x : s23.y, a1 = up ? s01.y : s4, a2 = up ? s23.x : 0.0f;
+  const float b0 = up ? s23.y : s01.x, b1 = up ? s4 : s01.y, b2 = s23.x;
+  const float r0 = __shfl_xor_sync(kFull, a0, 8), r1 = __shfl_xor_sync(kFull, a1, 8),
+              r2 = __shfl_xor_sync(kFull, a2, 8);
+  const float2 t01 = __fadd2_rn(make_float2(b0, b1), make_float2(r0, r1));
+  const float t2 = b2 + r2;
+  // level 4: 3 -> 2
+  up = (lane & 4) != 0;
+  const float c0 = up ? t01.x : t2, c1 = up ? t01.y : 0.0f;
+  const float d0 = up ? t2 : t01.x, d1 = t01.y;
+  const float2 u = __fadd2_rn(make_float2(d0, d1),
+                              make_float2(__shfl_xor_sync(kFull, c0, 4), __shfl_xor_sync(kFull, c1, 4)));
+  // level 2: 2 -> 1
+  up = (lane & 2) != 0;
+  const float e0 = up ? u.x : u.y, f0 = up ? u.y : u.x;
+  float w = f0 + __shfl_xor_sync(kFull, e0, 2);
+  // level 1: plain butterfly
+  w += __shfl_xor_sync(kFull, w, 1);
+  v[0] = w;
+}
+
 // Which param lane `lane` holds after ReduceScatter<N,16>, and whether it is
 // the one designated lane that issues that param's RED.
 template <int N>
@@ -161,7 +204,10 @@ __device__ __forceinline__ void reduce_bfly_scaled(int idx, float* grad, float (
                                                    float lane_scale, const float (&scale)[N]) {
   const int cnt = __popc(ballot);
   if (cnt >= thr) {  // cnt > 0: callers skip empty ballots
-    ReduceScatter<N, 16>::run(v, lane);
+    if constexpr (N == 9)
+      reduce_scatter9(v, lane);
+    else
+      ReduceScatter<N, 16>::run(v, lane);
     if (issuer) {
       red_add(grad + static_cast<int64_t>(idx) * N + slot, v[0] * lane_scale);
       if (COUNT) nred += 1;
