@@ -75,12 +75,15 @@ struct dw_rasterizer {
   size_t cap_h[12] = {0};
   float* h_bufs[12] = {nullptr};
   cudaStream_t s_in = nullptr, s_out = nullptr;  // copy streams of the batched host path
-  cudaEvent_t ev[7] = {};
+  cudaStream_t s_aux = nullptr;  // second compute stream: odd views of a batch
+  dw_rasterizer* twin = nullptr;  // forward state of the odd views
+  cudaEvent_t ev[10] = {};
 
   void ensure_streams() {
     if (s_in) return;
     DW_CUDA(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
     DW_CUDA(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+    DW_CUDA(cudaStreamCreateWithFlags(&s_aux, cudaStreamNonBlocking));
     for (auto& e : ev) DW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
 
@@ -93,9 +96,11 @@ struct dw_rasterizer {
     for (float* p : h_bufs)
       if (p) cudaFree(p);
     if (h_total) cudaFreeHost(h_total);
+    delete twin;
     if (s_in) {
       cudaStreamDestroy(s_in);
       cudaStreamDestroy(s_out);
+      cudaStreamDestroy(s_aux);
       for (auto e : ev) cudaEventDestroy(e);
     }
   }
@@ -512,71 +517,85 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
   float* d_dl[2] = {r->host_scratch(5, 3 * npx), r->host_scratch(8, 3 * npx)};
   float* d_img[2] = {r->host_scratch(6, 3 * npx), r->host_scratch(9, 3 * npx)};
   cudaEvent_t e_scene = r->ev[0], e_in[2] = {r->ev[1], r->ev[2]},
-              e_used[2] = {r->ev[3], r->ev[4]}, e_img[2] = {r->ev[5], r->ev[6]};
+              e_used[2] = {r->ev[3], r->ev[4]}, e_img[2] = {r->ev[5], r->ev[6]},
+              e_start = r->ev[7], e_zero = r->ev[8], e_aux = r->ev[9];
+  // Views alternate between two forward states and two compute streams
+  // (R[k & 1], S[k & 1]), so view k+1's projection / sort -- latency-bound
+  // launches that leave most SMs idle -- overlaps view k's backward. Both
+  // backwards add into the one gradient buffer with RED atomics, whose order
+  // was never fixed, so the sum is the same up to fp32 reassociation.
+  if (V > 1 && !r->twin) r->twin = new dw_rasterizer();
+  dw_rasterizer* R[2] = {r, V > 1 ? r->twin : r};
+  cudaStream_t S[2] = {s, V > 1 ? r->s_aux : s};
   auto h2d = [&](float* d, const float* h, size_t n, cudaStream_t st) {
     if (n) DW_CUDA(cudaMemcpyAsync(d, h, n * sizeof(float), cudaMemcpyHostToDevice, st));
   };
-  // the copy streams must not run ahead of work already queued on `s`
-  DW_CUDA(cudaEventRecord(e_used[0], s));
-  DW_CUDA(cudaEventRecord(e_used[1], s));
-  DW_CUDA(cudaStreamWaitEvent(r->s_in, e_used[0], 0));
+  // nothing may run ahead of work already queued on `s`
+  DW_CUDA(cudaEventRecord(e_start, s));
+  DW_CUDA(cudaStreamWaitEvent(r->s_in, e_start, 0));
+  DW_CUDA(cudaStreamWaitEvent(r->s_out, e_start, 0));
+  DW_CUDA(cudaStreamWaitEvent(S[1], e_start, 0));
   h2d(d_m, m, 3 * size_t(P), r->s_in);
   h2d(d_sc, sc, 3 * size_t(P), r->s_in);
   h2d(d_rot, rot, 4 * size_t(P), r->s_in);
   h2d(d_op, op, size_t(P), r->s_in);
   h2d(d_col, col, 3 * size_t(P), r->s_in);
   DW_CUDA(cudaEventRecord(e_scene, r->s_in));
-  h2d(d_dl[0], dL, 3 * npx, r->s_in);
-  DW_CUDA(cudaEventRecord(e_in[0], r->s_in));
-  DW_CUDA(cudaMemsetAsync(d_g, 0, kNParam * np * sizeof(float), s));
   DW_CUDA(cudaStreamWaitEvent(s, e_scene, 0));
-  // View 0 reads its instance count back (one host sync) and reserves 1.5x
-  // that; views 1.. then keep the count on the device (no host sync per
-  // view, so the host runs ahead and the copy streams overlap freely). A view
-  // that outgrows the reserve raises the sticky overflow flag and the whole
-  // batch is redone with per-view host syncs.
-  bool nosync_ok = V > 1;
+  DW_CUDA(cudaStreamWaitEvent(S[1], e_scene, 0));
+  // Views 0 and 1 read their instance counts back (host sync on their own
+  // stream only) and size a 1.5x reserve for their forward state; later
+  // views keep the count on the device (no host sync: the host runs ahead
+  // and every copy overlaps). A view that outgrows its reserve raises the
+  // sticky overflow flag and the whole batch is redone with host-read counts.
+  bool nosync_ok = V > 2;
   for (int pass = 0; pass < 2; ++pass) {
-    if (pass == 1) {  // redo from the start: zero the gradients, re-upload view 0's dL/dpixel
-      DW_CUDA(cudaMemsetAsync(d_g, 0, kNParam * np * sizeof(float), s));
-      h2d(d_dl[0], dL, 3 * npx, r->s_in);
-      DW_CUDA(cudaEventRecord(e_in[0], r->s_in));
-    }
+    DW_CUDA(cudaMemsetAsync(d_g, 0, kNParam * np * sizeof(float), s));
+    DW_CUDA(cudaEventRecord(e_zero, s));
+    DW_CUDA(cudaStreamWaitEvent(S[1], e_zero, 0));
+    h2d(d_dl[0], dL, 3 * npx, r->s_in);
+    DW_CUDA(cudaEventRecord(e_in[0], r->s_in));
     for (int k = 0; k < V; ++k) {
       const int b = k & 1;
+      dw_rasterizer* Rb = R[b];
+      cudaStream_t Sb = S[b];
       if (k + 1 < V) {  // prefetch view k+1 once view k-1 released its buffer
-        DW_CUDA(cudaStreamWaitEvent(r->s_in, e_used[b ^ 1], 0));
+        if (k >= 1) DW_CUDA(cudaStreamWaitEvent(r->s_in, e_used[b ^ 1], 0));
         h2d(d_dl[b ^ 1], dL + static_cast<size_t>(k + 1) * 3 * npx, 3 * npx, r->s_in);
         DW_CUDA(cudaEventRecord(e_in[b ^ 1], r->s_in));
       }
-      DW_CUDA(cudaStreamWaitEvent(s, e_in[b], 0));
-      if (k >= 2) DW_CUDA(cudaStreamWaitEvent(s, e_img[b], 0));  // image k-2 downloaded
-      if (nosync_ok && k == 1) {  // view 0 is done with the buffers a reserve may move
-        const int64_t want = r->num_rendered + r->num_rendered / 2 + 4096;
-        if (static_cast<int64_t>(std::min(r->cap_i[0], r->cap_i[2])) < want) {
-          DW_CUDA(cudaStreamSynchronize(s));
-          r->reserve(P, cams[0].width, cams[0].height, want);
+      DW_CUDA(cudaStreamWaitEvent(Sb, e_in[b], 0));
+      if (k >= 2) DW_CUDA(cudaStreamWaitEvent(Sb, e_img[b], 0));  // image k-2 downloaded
+      if (nosync_ok && (k == 2 || k == 3)) {  // first reuse of R[b]: size its reserve
+        const int64_t want = Rb->num_rendered + Rb->num_rendered / 2 + 4096;
+        if (static_cast<int64_t>(std::min(Rb->cap_i[0], Rb->cap_i[2])) < want) {
+          DW_CUDA(cudaStreamSynchronize(Sb));  // view k-2 is done with the buffers a reserve moves
+          Rb->reserve(P, cams[0].width, cams[0].height, want);
         }
-        DW_CUDA(cudaMemsetAsync(r->overflow_dev, 0, sizeof(unsigned int), s));
+        DW_CUDA(cudaMemsetAsync(Rb->overflow_dev, 0, sizeof(unsigned int), Sb));
       }
-      const bool nosync = nosync_ok && k > 0;
-      r->forward(P, d_m, d_sc, d_rot, d_op, d_col, cams[k], d_img[b], nullptr, s, nosync,
-                 /*sticky_overflow=*/true);
-      r->backward(d_dl[b], policy, thr, d_g, nullptr, s);
-      DW_CUDA(cudaEventRecord(e_used[b], s));
+      const bool nosync = nosync_ok && k >= 2;
+      Rb->forward(P, d_m, d_sc, d_rot, d_op, d_col, cams[k], d_img[b], nullptr, Sb, nosync,
+                  /*sticky_overflow=*/true);
+      Rb->backward(d_dl[b], policy, thr, d_g, nullptr, Sb);
+      DW_CUDA(cudaEventRecord(e_used[b], Sb));
       if (out_images) {
         DW_CUDA(cudaStreamWaitEvent(r->s_out, e_used[b], 0));
         DW_CUDA(cudaMemcpyAsync(out_images + static_cast<size_t>(k) * 3 * npx, d_img[b],
                                 3 * npx * sizeof(float), cudaMemcpyDeviceToHost, r->s_out));
         DW_CUDA(cudaEventRecord(e_img[b], r->s_out));
       } else {
-        DW_CUDA(cudaEventRecord(e_img[b], s));
+        DW_CUDA(cudaEventRecord(e_img[b], Sb));
       }
     }
+    DW_CUDA(cudaEventRecord(e_aux, S[1]));
+    DW_CUDA(cudaStreamWaitEvent(s, e_aux, 0));
     if (!nosync_ok) break;
-    bool ovf = false;
-    r->resolve_count(&ovf);  // synchronous: the batch's sticky flag
-    if (!ovf) break;
+    DW_CUDA(cudaStreamSynchronize(s));  // both compute streams (S[1] joined into s)
+    bool ovf0 = false, ovf1 = false;
+    R[0]->resolve_count(&ovf0);  // the batch's sticky flags
+    R[1]->resolve_count(&ovf1);
+    if (!ovf0 && !ovf1) break;
     nosync_ok = false;  // redo every view with host-read instance counts
   }
   if (P > 0)
