@@ -4,10 +4,46 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
 
 #include "../../include/distwar.h"
 
 namespace dw {
+
+// Programmatic dependent launch (sm_90+): a kernel launched with launch_pdl may
+// be scheduled while its predecessor in the stream drains; it must execute
+// pdl_wait() before touching global memory the predecessor reads or writes
+// (it returns once the predecessor grid has completed and flushed). Each PDL
+// kernel then releases its own dependents at once (pdl_trigger), so the
+// short, latency-bound binning kernels of the forward do not pay a full
+// launch + ramp-up gap each.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+#ifndef DW_PDL
+#define DW_PDL 1
+#endif
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = DW_PDL ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("launch: ") + cudaGetErrorString(e));
+}
 
 constexpr int kTile = 16;         // 16x16-pixel tiles, one 256-thread CTA each
 constexpr int kBlock = kTile * kTile;

@@ -710,6 +710,8 @@ __global__ void __launch_bounds__(128)
                  const float4* __restrict__ conic_opacity, const float4* __restrict__ rgb,
                  float* __restrict__ final_T, uint32_t* __restrict__ n_contrib,
                  float* __restrict__ out_color) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
   __shared__ Staged sm[kBlock];
   __shared__ uint8_t s_mask[kBlock];
   const int tile = blockIdx.x, t = threadIdx.x, w = t >> 5, lane = t & 31;
@@ -801,6 +803,8 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
                   const float* __restrict__ final_Ts, const uint32_t* __restrict__ n_contrib,
                   const float* __restrict__ dL_dpixels, int thr, float* __restrict__ grad,
                   unsigned long long* __restrict__ counters, const TapBuf tap) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
   static_assert(POL != kNative, "native runs the thread-per-pixel kernel");
   constexpr int NW = 4;
   __shared__ Staged sm[2][kBlock];  // double buffer: batch i+1 lands while batch i is walked
@@ -1025,10 +1029,10 @@ void launch_bwd(bool count, const CamParams& cam, const uint2* ranges, const uin
   if constexpr (POL != kNative) {
     if (DW_BLEND_X2) {
       if (count)
-        k_backward_x2<POL, true><<<grid, 128, 0, s>>>(cam, ranges, values, means2D, co, rgb, fT,
+        launch_pdl(k_backward_x2<POL, true>, grid, 128, 0, s, cam, ranges, values, means2D, co, rgb, fT,
                                                       nc, dL, thr, grad, ctr, TapBuf{});
       else
-        k_backward_x2<POL, false><<<grid, 128, 0, s>>>(cam, ranges, values, means2D, co, rgb, fT,
+        launch_pdl(k_backward_x2<POL, false>, grid, 128, 0, s, cam, ranges, values, means2D, co, rgb, fT,
                                                        nc, dL, thr, grad, nullptr, TapBuf{});
       return;
     }
@@ -1057,7 +1061,7 @@ void launch_backward_tap(const CamParams& cam, const uint2* ranges, const uint32
                          float* grad, const TapBuf& tap, cudaStream_t s) {
   const int grid = cam.tiles_x * cam.tiles_y;
   if (DW_BLEND_X2)
-    k_backward_x2<kSwB, false, true><<<grid, 128, 0, s>>>(
+    launch_pdl(k_backward_x2<kSwB, false, true>, grid, 128, 0, s, 
         cam, ranges, values, means2D, co, rgb, final_T, n_contrib, dL, thr, grad, nullptr, tap);
   else
     k_backward_multi<DW_BWD_PPT, kSwB, false, true><<<grid, 256 / DW_BWD_PPT, 0, s>>>(
@@ -1075,7 +1079,7 @@ void launch_forward_impl(const CamParams& cam, const uint2* ranges, const uint32
 #define DW_FWD_PPT 2  // A/B on C3: 0.527 vs 0.558 ms (profiles/r01/ab_fwd2.jsonl)
 #endif
   if (DW_BLEND_X2)
-    k_forward_x2<<<grid, 128, 0, s>>>(cam, ranges, values, means2D, conic_opacity, rgb, final_T,
+    launch_pdl(k_forward_x2, grid, 128, 0, s, cam, ranges, values, means2D, conic_opacity, rgb, final_T,
                                       n_contrib, out_color);
   else if (DW_FWD_PPT == 2)
     k_forward_ppt2<<<grid, 128, 0, s>>>(cam, ranges, values, means2D, conic_opacity, rgb, final_T,

@@ -51,6 +51,8 @@ __global__ void __launch_bounds__(kBlock)
                  float2* __restrict__ means2D, float* __restrict__ depths,
                  int* __restrict__ radii, float4* __restrict__ conic_opacity,
                  float4* __restrict__ rgb, uint32_t* __restrict__ tiles_touched) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
   __shared__ __align__(16) float s_mean[3 * kBlock];
   __shared__ __align__(16) float s_scale[3 * kBlock];
   __shared__ __align__(16) float s_col[3 * kBlock];
@@ -170,11 +172,11 @@ void launch_preprocess(int P, const float* means3D, const float* scales, const f
   const bool vec = aligned(means3D) && aligned(scales) && aligned(colors) && aligned(rotations);
   const int grid = (P + kBlock - 1) / kBlock;
   if (vec)
-    k_preprocess<true><<<grid, kBlock, 0, s>>>(P, means3D, scales, rotations, opacities, colors,
+    launch_pdl(k_preprocess<true>, grid, kBlock, 0, s, P, means3D, scales, rotations, opacities, colors,
                                                cam, means2D, depths, radii, conic_opacity, rgb,
                                                tiles_touched);
   else
-    k_preprocess<false><<<grid, kBlock, 0, s>>>(P, means3D, scales, rotations, opacities, colors,
+    launch_pdl(k_preprocess<false>, grid, kBlock, 0, s, P, means3D, scales, rotations, opacities, colors,
                                                 cam, means2D, depths, radii, conic_opacity, rgb,
                                                 tiles_touched);
   DW_CUDA(cudaGetLastError());

@@ -74,6 +74,8 @@ __global__ void __launch_bounds__(kSortThreads)
     k_upsweep(const uint32_t* __restrict__ keys, int64_t n, int shift, uint32_t mask,
               int bits, uint32_t* __restrict__ counts, int64_t tiles,
               const unsigned long long* __restrict__ n_dev) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
   __shared__ uint32_t hist[kWarps][256];
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
   n = live_n(n, n_dev);
@@ -107,6 +109,8 @@ __global__ void __launch_bounds__(kSortThreads)
 // to digit_total[d].
 __global__ void __launch_bounds__(1024)
     k_scan_rows(uint32_t* __restrict__ counts, int64_t tiles, uint32_t* __restrict__ digit_total) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
   __shared__ uint32_t warp_sums[32];
   __shared__ uint32_t carry;
   uint32_t* row = counts + static_cast<int64_t>(blockIdx.x) * tiles;
@@ -144,6 +148,8 @@ __global__ void __launch_bounds__(1024)
 }
 
 __global__ void k_scan_digits(uint32_t* __restrict__ digit_total, int ndigits) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
   // 256 threads, exclusive scan in place (<= 256 digits)
   __shared__ uint32_t s[256];
   const int t = threadIdx.x;
@@ -173,6 +179,8 @@ __global__ void __launch_bounds__(kSortThreads)
                 int64_t tiles, const uint32_t* __restrict__ digit_base,
                 uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
                 const unsigned long long* __restrict__ n_dev) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
   constexpr int TILE = ITEMS * kSortThreads;
   __shared__ uint32_t s_cnt[kWarps][256];  // warp digit counts -> tile-local offsets
   __shared__ uint32_t s_dstart[256];       // tile-local start of each digit's run
@@ -260,6 +268,8 @@ __global__ void __launch_bounds__(kSortThreads)
 __global__ void __launch_bounds__(kSortThreads)
     k_scan_tile_sums(const uint32_t* __restrict__ in, const uint32_t* __restrict__ order,
                      int64_t n, unsigned long long* __restrict__ tile_sums) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
   __shared__ unsigned long long ws[kSortThreads / 32];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kSortTile;
@@ -280,6 +290,8 @@ __global__ void __launch_bounds__(kSortThreads)
 }
 
 __global__ void k_scan_tile_prefix(unsigned long long* __restrict__ tile_sums, int64_t tiles) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
   // single block of 1024: exclusive scan of tile sums in place (loop)
   __shared__ unsigned long long warp_sums[32];
   __shared__ unsigned long long carry;
@@ -318,6 +330,8 @@ __global__ void __launch_bounds__(kSortThreads)
     k_scan_tile_apply(const uint32_t* __restrict__ in, const uint32_t* __restrict__ order,
                       int64_t n, const unsigned long long* __restrict__ tile_prefix,
                       uint64_t* __restrict__ out) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
   // thread-blocked: thread t owns elements [16t, 16t+16) of the tile
   __shared__ unsigned long long ws[kSortThreads / 32];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -350,6 +364,8 @@ __global__ void __launch_bounds__(kSortThreads)
 
 __global__ void k_iota_depthkey(int P, const float* __restrict__ depths, const int* __restrict__ radii,
                                 uint32_t* __restrict__ dkey, uint32_t* __restrict__ ids) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
   dkey[i] = radii[i] > 0 ? __float_as_uint(depths[i]) : 0xffffffffu;
@@ -374,6 +390,8 @@ __global__ void __launch_bounds__(256)
                        const int* __restrict__ radii, const uint64_t* __restrict__ offsets,
                        int tiles_x, int tiles_y, uint32_t* __restrict__ tile_ids,
                        uint32_t* __restrict__ values, uint64_t cap) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   int r[4] = {0, 0, 0, 0};
@@ -424,6 +442,8 @@ __global__ void __launch_bounds__(256)
 __global__ void k_clamp_total(const uint64_t* __restrict__ offsets, int P, uint64_t cap,
                               unsigned long long* __restrict__ n_live,
                               unsigned int* __restrict__ overflow) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
   const uint64_t total = P > 0 ? offsets[P - 1] : 0;
   const bool fits = total <= cap;
   *n_live = fits ? total : 0ull;
@@ -432,6 +452,8 @@ __global__ void k_clamp_total(const uint64_t* __restrict__ offsets, int P, uint6
 
 __global__ void k_ranges_u32(int64_t L, const uint32_t* __restrict__ tiles, uint2* __restrict__ ranges,
                              const unsigned long long* __restrict__ n_dev) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   L = live_n(L, n_dev);
   if (idx >= L) return;
@@ -494,30 +516,30 @@ int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* 
     const uint32_t mask = (1u << b) - 1u;
     switch (items) {
       case 16:
-        k_upsweep<16><<<grid, kSortThreads, 0, s>>>(k[cur], n, shift, mask, b, counts, tiles,
+        launch_pdl(k_upsweep<16>, grid, kSortThreads, 0, s, k[cur], n, shift, mask, b, counts, tiles,
                                                     n_dev);
         break;
       case 8:
-        k_upsweep<8><<<grid, kSortThreads, 0, s>>>(k[cur], n, shift, mask, b, counts, tiles,
+        launch_pdl(k_upsweep<8>, grid, kSortThreads, 0, s, k[cur], n, shift, mask, b, counts, tiles,
                                                    n_dev);
         break;
       default:
-        k_upsweep<4><<<grid, kSortThreads, 0, s>>>(k[cur], n, shift, mask, b, counts, tiles,
+        launch_pdl(k_upsweep<4>, grid, kSortThreads, 0, s, k[cur], n, shift, mask, b, counts, tiles,
                                                    n_dev);
     }
-    k_scan_rows<<<256, 1024, 0, s>>>(counts, tiles, digit);
-    k_scan_digits<<<1, 256, 0, s>>>(digit, 256);
+    launch_pdl(k_scan_rows, 256, 1024, 0, s, counts, tiles, digit);
+    launch_pdl(k_scan_digits, 1, 256, 0, s, digit, 256);
     switch (items) {
       case 16:
-        k_downsweep<16><<<grid, kSortThreads, 0, s>>>(k[cur], v[cur], n, shift, mask, b, counts,
+        launch_pdl(k_downsweep<16>, grid, kSortThreads, 0, s, k[cur], v[cur], n, shift, mask, b, counts,
                                                       tiles, digit, k[cur ^ 1], v[cur ^ 1], n_dev);
         break;
       case 8:
-        k_downsweep<8><<<grid, kSortThreads, 0, s>>>(k[cur], v[cur], n, shift, mask, b, counts,
+        launch_pdl(k_downsweep<8>, grid, kSortThreads, 0, s, k[cur], v[cur], n, shift, mask, b, counts,
                                                      tiles, digit, k[cur ^ 1], v[cur ^ 1], n_dev);
         break;
       default:
-        k_downsweep<4><<<grid, kSortThreads, 0, s>>>(k[cur], v[cur], n, shift, mask, b, counts,
+        launch_pdl(k_downsweep<4>, grid, kSortThreads, 0, s, k[cur], v[cur], n, shift, mask, b, counts,
                                                      tiles, digit, k[cur ^ 1], v[cur ^ 1], n_dev);
     }
     cur ^= 1;
@@ -531,16 +553,16 @@ void inclusive_scan_gather(const uint32_t* in, const uint32_t* order, int64_t n,
   if (n <= 0) return;
   const int64_t tiles = (n + kSortTile - 1) / kSortTile;
   auto* sums = static_cast<unsigned long long*>(temp);
-  k_scan_tile_sums<<<static_cast<unsigned>(tiles), kSortThreads, 0, s>>>(in, order, n, sums);
-  k_scan_tile_prefix<<<1, 1024, 0, s>>>(sums, tiles);
-  k_scan_tile_apply<<<static_cast<unsigned>(tiles), kSortThreads, 0, s>>>(in, order, n, sums, out);
+  launch_pdl(k_scan_tile_sums, static_cast<unsigned>(tiles), kSortThreads, 0, s, in, order, n, sums);
+  launch_pdl(k_scan_tile_prefix, 1, 1024, 0, s, sums, tiles);
+  launch_pdl(k_scan_tile_apply, static_cast<unsigned>(tiles), kSortThreads, 0, s, in, order, n, sums, out);
   DW_CUDA(cudaGetLastError());
 }
 
 void launch_depth_keys(int P, const float* depths, const int* radii, uint32_t* dkey, uint32_t* ids,
                        cudaStream_t s) {
   if (P <= 0) return;
-  k_iota_depthkey<<<blocks_for(P, 256), 256, 0, s>>>(P, depths, radii, dkey, ids);
+  launch_pdl(k_iota_depthkey, blocks_for(P, 256), 256, 0, s, P, depths, radii, dkey, ids);
   DW_CUDA(cudaGetLastError());
 }
 
@@ -548,7 +570,7 @@ void launch_duplicate_sorted(int P, const uint32_t* order, const float2* means2D
                              const uint64_t* offsets, const CamParams& cam, uint32_t* tile_ids,
                              uint32_t* values, uint64_t cap, cudaStream_t s) {
   if (P <= 0) return;
-  k_duplicate_sorted<<<blocks_for(P, 256), 256, 0, s>>>(P, order, means2D, radii, offsets,
+  launch_pdl(k_duplicate_sorted, blocks_for(P, 256), 256, 0, s, P, order, means2D, radii, offsets,
                                                         cam.tiles_x, cam.tiles_y, tile_ids, values,
                                                         cap);
   DW_CUDA(cudaGetLastError());
@@ -557,13 +579,13 @@ void launch_duplicate_sorted(int P, const uint32_t* order, const float2* means2D
 void launch_ranges_u32(int64_t L, const uint32_t* tiles, uint2* ranges, cudaStream_t s,
                        const unsigned long long* n_dev) {
   if (L <= 0) return;
-  k_ranges_u32<<<blocks_for(L, 256), 256, 0, s>>>(L, tiles, ranges, n_dev);
+  launch_pdl(k_ranges_u32, blocks_for(L, 256), 256, 0, s, L, tiles, ranges, n_dev);
   DW_CUDA(cudaGetLastError());
 }
 
 void launch_clamp_total(const uint64_t* offsets, int P, uint64_t cap, unsigned long long* n_live,
                         unsigned int* overflow, cudaStream_t s) {
-  k_clamp_total<<<1, 1, 0, s>>>(offsets, P, cap, n_live, overflow);
+  launch_pdl(k_clamp_total, 1, 1, 0, s, offsets, P, cap, n_live, overflow);
   DW_CUDA(cudaGetLastError());
 }
 
