@@ -227,7 +227,7 @@ struct dw_rasterizer {
     count_pending = false;
     if (P > 0) {
       // 1. Gaussians in (depth, id) order: stable 32-bit LSD sort
-      dw::launch_depth_keys(P, depths, radii, dkey[0], dids[0], s);
+      dw::launch_depth_keys(P, depths, radii, dkey[0], dids[0], ranges, ntiles, s);
       ensure_tmp(dw::radix_sort_temp_bytes(P));
       order = dids[dw::radix_sort_pairs(dkey, dids, P, 32, tmp, s)];
       // instance offsets in that order
@@ -236,9 +236,8 @@ struct dw_rasterizer {
         if (cap_i[0] == 0 || cap_i[2] == 0)
           throw std::invalid_argument("no-sync forward needs dw_rasterizer_reserve first");
         n_grid = static_cast<int64_t>(std::min(cap_i[0], cap_i[2]));
-        if (!sticky_overflow) DW_CUDA(cudaMemsetAsync(overflow_dev, 0, sizeof(unsigned int), s));
         dw::launch_clamp_total(offsets, P, static_cast<uint64_t>(n_grid), live_dev, overflow_dev,
-                               s);
+                               sticky_overflow, s);
         n_dev = live_dev;
         count_pending = true;
       } else {
@@ -266,7 +265,7 @@ struct dw_rasterizer {
       tiles_sorted = itile[cur];
       vals = ivals[cur];
     }
-    DW_CUDA(cudaMemsetAsync(ranges, 0, sizeof(uint2) * ntiles, s));
+    if (P == 0) DW_CUDA(cudaMemsetAsync(ranges, 0, sizeof(uint2) * ntiles, s));
     dw::launch_ranges_u32(n_grid, tiles_sorted, ranges, s, n_dev);
     dw::launch_forward_impl(cam, ranges, vals, means2D, conic_opacity, rgb, radii, final_T,
                             n_contrib, out_color, s);

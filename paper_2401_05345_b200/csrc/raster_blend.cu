@@ -1029,11 +1029,11 @@ void launch_bwd(bool count, const CamParams& cam, const uint2* ranges, const uin
   if constexpr (POL != kNative) {
     if (DW_BLEND_X2) {
       if (count)
-        launch_pdl(k_backward_x2<POL, true>, grid, 128, 0, s, cam, ranges, values, means2D, co, rgb, fT,
-                                                      nc, dL, thr, grad, ctr, TapBuf{});
+        launch_pdl(k_backward_x2<POL, true>, grid, 128, 0, s, cam, ranges, values, means2D, co, rgb,
+                   fT, nc, dL, thr, grad, ctr, TapBuf{});
       else
-        launch_pdl(k_backward_x2<POL, false>, grid, 128, 0, s, cam, ranges, values, means2D, co, rgb, fT,
-                                                       nc, dL, thr, grad, nullptr, TapBuf{});
+        launch_pdl(k_backward_x2<POL, false>, grid, 128, 0, s, cam, ranges, values, means2D, co,
+                   rgb, fT, nc, dL, thr, grad, nullptr, TapBuf{});
       return;
     }
     constexpr int NT = 256 / DW_BWD_PPT;
@@ -1061,8 +1061,8 @@ void launch_backward_tap(const CamParams& cam, const uint2* ranges, const uint32
                          float* grad, const TapBuf& tap, cudaStream_t s) {
   const int grid = cam.tiles_x * cam.tiles_y;
   if (DW_BLEND_X2)
-    launch_pdl(k_backward_x2<kSwB, false, true>, grid, 128, 0, s, 
-        cam, ranges, values, means2D, co, rgb, final_T, n_contrib, dL, thr, grad, nullptr, tap);
+    launch_pdl(k_backward_x2<kSwB, false, true>, grid, 128, 0, s, cam, ranges, values, means2D, co,
+               rgb, final_T, n_contrib, dL, thr, grad, nullptr, tap);
   else
     k_backward_multi<DW_BWD_PPT, kSwB, false, true><<<grid, 256 / DW_BWD_PPT, 0, s>>>(
         cam, ranges, values, means2D, co, rgb, final_T, n_contrib, dL, thr, grad, nullptr, tap);
@@ -1079,8 +1079,8 @@ void launch_forward_impl(const CamParams& cam, const uint2* ranges, const uint32
 #define DW_FWD_PPT 2  // A/B on C3: 0.527 vs 0.558 ms (profiles/r01/ab_fwd2.jsonl)
 #endif
   if (DW_BLEND_X2)
-    launch_pdl(k_forward_x2, grid, 128, 0, s, cam, ranges, values, means2D, conic_opacity, rgb, final_T,
-                                      n_contrib, out_color);
+    launch_pdl(k_forward_x2, grid, 128, 0, s, cam, ranges, values, means2D, conic_opacity, rgb,
+               final_T, n_contrib, out_color);
   else if (DW_FWD_PPT == 2)
     k_forward_ppt2<<<grid, 128, 0, s>>>(cam, ranges, values, means2D, conic_opacity, rgb, final_T,
                                         n_contrib, out_color);

@@ -172,13 +172,11 @@ void launch_preprocess(int P, const float* means3D, const float* scales, const f
   const bool vec = aligned(means3D) && aligned(scales) && aligned(colors) && aligned(rotations);
   const int grid = (P + kBlock - 1) / kBlock;
   if (vec)
-    launch_pdl(k_preprocess<true>, grid, kBlock, 0, s, P, means3D, scales, rotations, opacities, colors,
-                                               cam, means2D, depths, radii, conic_opacity, rgb,
-                                               tiles_touched);
+    launch_pdl(k_preprocess<true>, grid, kBlock, 0, s, P, means3D, scales, rotations, opacities,
+               colors, cam, means2D, depths, radii, conic_opacity, rgb, tiles_touched);
   else
-    launch_pdl(k_preprocess<false>, grid, kBlock, 0, s, P, means3D, scales, rotations, opacities, colors,
-                                                cam, means2D, depths, radii, conic_opacity, rgb,
-                                                tiles_touched);
+    launch_pdl(k_preprocess<false>, grid, kBlock, 0, s, P, means3D, scales, rotations, opacities,
+               colors, cam, means2D, depths, radii, conic_opacity, rgb, tiles_touched);
   DW_CUDA(cudaGetLastError());
 }
 

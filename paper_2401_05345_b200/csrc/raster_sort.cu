@@ -25,6 +25,8 @@
 //              a running per-digit base orders the rounds; then scatter.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "distwar.cuh"
 #include "dw_internal.h"
 #include "raster.cuh"
@@ -362,11 +364,15 @@ __global__ void __launch_bounds__(kSortThreads)
   }
 }
 
+// Also clears the tile ranges (k_ranges_u32 writes only the non-empty ones),
+// so no memset node breaks the forward's programmatic-launch chain.
 __global__ void k_iota_depthkey(int P, const float* __restrict__ depths, const int* __restrict__ radii,
-                                uint32_t* __restrict__ dkey, uint32_t* __restrict__ ids) {
+                                uint32_t* __restrict__ dkey, uint32_t* __restrict__ ids,
+                                uint2* __restrict__ ranges, int ntiles) {
   pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < ntiles) ranges[i] = make_uint2(0u, 0u);
   if (i >= P) return;
   dkey[i] = radii[i] > 0 ? __float_as_uint(depths[i]) : 0xffffffffu;
   ids[i] = static_cast<uint32_t>(i);
@@ -441,13 +447,15 @@ __global__ void __launch_bounds__(256)
 // flag is raised for the host to read later.
 __global__ void k_clamp_total(const uint64_t* __restrict__ offsets, int P, uint64_t cap,
                               unsigned long long* __restrict__ n_live,
-                              unsigned int* __restrict__ overflow) {
+                              unsigned int* __restrict__ overflow, int sticky) {
   pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
   const uint64_t total = P > 0 ? offsets[P - 1] : 0;
   const bool fits = total <= cap;
   *n_live = fits ? total : 0ull;
-  if (!fits) *overflow = 1u;  // sticky: cleared by the caller (per forward, or per view batch)
+  // sticky: the flag accumulates over a view batch (cleared by the caller)
+  if (!fits) *overflow = 1u;
+  else if (!sticky) *overflow = 0u;
 }
 
 __global__ void k_ranges_u32(int64_t L, const uint32_t* __restrict__ tiles, uint2* __restrict__ ranges,
@@ -516,31 +524,31 @@ int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* 
     const uint32_t mask = (1u << b) - 1u;
     switch (items) {
       case 16:
-        launch_pdl(k_upsweep<16>, grid, kSortThreads, 0, s, k[cur], n, shift, mask, b, counts, tiles,
-                                                    n_dev);
+        launch_pdl(k_upsweep<16>, grid, kSortThreads, 0, s, k[cur], n, shift, mask, b, counts,
+                   tiles, n_dev);
         break;
       case 8:
         launch_pdl(k_upsweep<8>, grid, kSortThreads, 0, s, k[cur], n, shift, mask, b, counts, tiles,
-                                                   n_dev);
+                   n_dev);
         break;
       default:
         launch_pdl(k_upsweep<4>, grid, kSortThreads, 0, s, k[cur], n, shift, mask, b, counts, tiles,
-                                                   n_dev);
+                   n_dev);
     }
     launch_pdl(k_scan_rows, 256, 1024, 0, s, counts, tiles, digit);
     launch_pdl(k_scan_digits, 1, 256, 0, s, digit, 256);
     switch (items) {
       case 16:
-        launch_pdl(k_downsweep<16>, grid, kSortThreads, 0, s, k[cur], v[cur], n, shift, mask, b, counts,
-                                                      tiles, digit, k[cur ^ 1], v[cur ^ 1], n_dev);
+        launch_pdl(k_downsweep<16>, grid, kSortThreads, 0, s, k[cur], v[cur], n, shift, mask, b,
+                   counts, tiles, digit, k[cur ^ 1], v[cur ^ 1], n_dev);
         break;
       case 8:
-        launch_pdl(k_downsweep<8>, grid, kSortThreads, 0, s, k[cur], v[cur], n, shift, mask, b, counts,
-                                                     tiles, digit, k[cur ^ 1], v[cur ^ 1], n_dev);
+        launch_pdl(k_downsweep<8>, grid, kSortThreads, 0, s, k[cur], v[cur], n, shift, mask, b,
+                   counts, tiles, digit, k[cur ^ 1], v[cur ^ 1], n_dev);
         break;
       default:
-        launch_pdl(k_downsweep<4>, grid, kSortThreads, 0, s, k[cur], v[cur], n, shift, mask, b, counts,
-                                                     tiles, digit, k[cur ^ 1], v[cur ^ 1], n_dev);
+        launch_pdl(k_downsweep<4>, grid, kSortThreads, 0, s, k[cur], v[cur], n, shift, mask, b,
+                   counts, tiles, digit, k[cur ^ 1], v[cur ^ 1], n_dev);
     }
     cur ^= 1;
   }
@@ -553,16 +561,19 @@ void inclusive_scan_gather(const uint32_t* in, const uint32_t* order, int64_t n,
   if (n <= 0) return;
   const int64_t tiles = (n + kSortTile - 1) / kSortTile;
   auto* sums = static_cast<unsigned long long*>(temp);
-  launch_pdl(k_scan_tile_sums, static_cast<unsigned>(tiles), kSortThreads, 0, s, in, order, n, sums);
+  launch_pdl(k_scan_tile_sums, static_cast<unsigned>(tiles), kSortThreads, 0, s, in, order, n,
+             sums);
   launch_pdl(k_scan_tile_prefix, 1, 1024, 0, s, sums, tiles);
-  launch_pdl(k_scan_tile_apply, static_cast<unsigned>(tiles), kSortThreads, 0, s, in, order, n, sums, out);
+  launch_pdl(k_scan_tile_apply, static_cast<unsigned>(tiles), kSortThreads, 0, s, in, order, n,
+             sums, out);
   DW_CUDA(cudaGetLastError());
 }
 
 void launch_depth_keys(int P, const float* depths, const int* radii, uint32_t* dkey, uint32_t* ids,
-                       cudaStream_t s) {
-  if (P <= 0) return;
-  launch_pdl(k_iota_depthkey, blocks_for(P, 256), 256, 0, s, P, depths, radii, dkey, ids);
+                       uint2* ranges, int ntiles, cudaStream_t s) {
+  if (P <= 0 && ntiles <= 0) return;
+  launch_pdl(k_iota_depthkey, blocks_for(std::max(P, ntiles), 256), 256, 0, s, P, depths, radii,
+             dkey, ids, ranges, ntiles);
   DW_CUDA(cudaGetLastError());
 }
 
@@ -571,8 +582,7 @@ void launch_duplicate_sorted(int P, const uint32_t* order, const float2* means2D
                              uint32_t* values, uint64_t cap, cudaStream_t s) {
   if (P <= 0) return;
   launch_pdl(k_duplicate_sorted, blocks_for(P, 256), 256, 0, s, P, order, means2D, radii, offsets,
-                                                        cam.tiles_x, cam.tiles_y, tile_ids, values,
-                                                        cap);
+             cam.tiles_x, cam.tiles_y, tile_ids, values, cap);
   DW_CUDA(cudaGetLastError());
 }
 
@@ -584,8 +594,8 @@ void launch_ranges_u32(int64_t L, const uint32_t* tiles, uint2* ranges, cudaStre
 }
 
 void launch_clamp_total(const uint64_t* offsets, int P, uint64_t cap, unsigned long long* n_live,
-                        unsigned int* overflow, cudaStream_t s) {
-  launch_pdl(k_clamp_total, 1, 1, 0, s, offsets, P, cap, n_live, overflow);
+                        unsigned int* overflow, bool sticky, cudaStream_t s) {
+  launch_pdl(k_clamp_total, 1, 1, 0, s, offsets, P, cap, n_live, overflow, sticky ? 1 : 0);
   DW_CUDA(cudaGetLastError());
 }
 

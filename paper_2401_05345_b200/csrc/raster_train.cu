@@ -29,6 +29,8 @@ __global__ void __launch_bounds__(256)
                           const float* __restrict__ rotations, const int* __restrict__ radii,
                           const CamParams cam, const float* __restrict__ grad2d,
                           float* __restrict__ grad3d) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P || radii[i] <= 0) return;
   const float* g2 = grad2d + static_cast<int64_t>(i) * kNParam;
@@ -176,6 +178,8 @@ __global__ void __launch_bounds__(256)
            const float* __restrict__ grad, float* __restrict__ m, float* __restrict__ v,
            float lr0, float lr1, float lr2, float lr3, float lr4, float b1, float b2, float eps,
            float bc1, float bc2) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const int64_t i = k / kNParam3D;
@@ -201,8 +205,8 @@ void launch_preprocess_backward(int P, const float* means3D, const float* scales
                                 const float* rotations, const int* radii, const CamParams& cam,
                                 const float* grad2d, float* grad3d, cudaStream_t s) {
   if (P <= 0) return;
-  k_preprocess_backward<<<(P + 255) / 256, 256, 0, s>>>(P, means3D, scales, rotations, radii, cam,
-                                                        grad2d, grad3d);
+  launch_pdl(k_preprocess_backward, (P + 255) / 256, 256, 0, s, P, means3D, scales, rotations,
+             radii, cam, grad2d, grad3d);
   DW_CUDA(cudaGetLastError());
 }
 
@@ -212,9 +216,9 @@ void launch_adam(int P, float* means3D, float* scales, float* rotations, float* 
   if (P <= 0) return;
   const int64_t n = static_cast<int64_t>(P) * kNParam3D;
   const float bc1 = 1.f - powf(b1, (float)step), bc2 = 1.f - powf(b2, (float)step);
-  k_adam<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
-      n, means3D, scales, rotations, opacities, colors, grad, m, v, lr[0], lr[1], lr[2], lr[3],
-      lr[4], b1, b2, eps, bc1, bc2);
+  launch_pdl(k_adam, static_cast<unsigned>((n + 255) / 256), 256, 0, s, n, means3D, scales,
+             rotations, opacities, colors, grad, m, v, lr[0], lr[1], lr[2], lr[3], lr[4], b1, b2,
+             eps, bc1, bc2);
   DW_CUDA(cudaGetLastError());
 }
 
