@@ -227,7 +227,7 @@ struct dw_rasterizer {
     count_pending = false;
     if (P > 0) {
       // 1. Gaussians in (depth, id) order: stable 32-bit LSD sort
-      dw::launch_depth_keys(P, depths, radii, dkey[0], dids[0], ranges, ntiles, s);
+      dw::launch_depth_keys(P, depths, radii, dkey[0], dids[0], s);
       ensure_tmp(dw::radix_sort_temp_bytes(P));
       order = dids[dw::radix_sort_pairs(dkey, dids, P, 32, tmp, s)];
       // instance offsets in that order
@@ -265,8 +265,7 @@ struct dw_rasterizer {
       tiles_sorted = itile[cur];
       vals = ivals[cur];
     }
-    if (P == 0) DW_CUDA(cudaMemsetAsync(ranges, 0, sizeof(uint2) * ntiles, s));
-    dw::launch_ranges_u32(n_grid, tiles_sorted, ranges, s, n_dev);
+    dw::launch_ranges_u32(n_grid, tiles_sorted, ranges, ntiles, s, n_dev);
     dw::launch_forward_impl(cam, ranges, vals, means2D, conic_opacity, rgb, radii, final_T,
                             n_contrib, out_color, s);
     if (radii_out && P > 0)

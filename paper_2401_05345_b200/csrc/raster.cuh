@@ -109,14 +109,14 @@ int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* 
                      cudaStream_t s, const unsigned long long* n_dev = nullptr);
 void inclusive_scan_gather(const uint32_t* in, const uint32_t* order, int64_t n, uint64_t* out,
                            void* temp, cudaStream_t s);
-// depth keys + ids, and clears ranges[ntiles]
 void launch_depth_keys(int P, const float* depths, const int* radii, uint32_t* dkey, uint32_t* ids,
-                       uint2* ranges, int ntiles, cudaStream_t s);
+                       cudaStream_t s);
 void launch_duplicate_sorted(int P, const uint32_t* order, const float2* means2D, const int* radii,
                              const uint64_t* offsets, const CamParams& cam, uint32_t* tile_ids,
                              uint32_t* values, uint64_t cap, cudaStream_t s);
-void launch_ranges_u32(int64_t L, const uint32_t* tiles, uint2* ranges, cudaStream_t s,
-                       const unsigned long long* n_dev = nullptr);
+// ranges[0, ntiles) of the sorted tile ids (every range written)
+void launch_ranges_u32(int64_t L, const uint32_t* tiles, uint2* ranges, int ntiles,
+                       cudaStream_t s, const unsigned long long* n_dev = nullptr);
 void launch_clamp_total(const uint64_t* offsets, int P, uint64_t cap, unsigned long long* n_live,
                         unsigned int* overflow, bool sticky, cudaStream_t s);
 void launch_make_keys(int64_t L, const uint32_t* tiles, const uint32_t* values, const float* depths,

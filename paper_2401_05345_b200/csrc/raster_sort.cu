@@ -59,10 +59,8 @@ __device__ __forceinline__ unsigned digit_peers(uint32_t d, int bits, bool valid
   return peers;
 }
 
-// Per-tile digit histogram. A tile is ITEMS*256 consecutive elements; warp w
-// owns the contiguous chunk [w*ITEMS*32, (w+1)*ITEMS*32) and counts it into
-// a warp-private smem histogram, one update per distinct digit per warp
-// instruction (ballot multi-split aggregation: no atomics, no contention).
+// Per-tile digit histogram of ITEMS*256 consecutive elements (the same tiles
+// the downsweep ranks).
 // n_dev (nullable): element count read on the device, capped by n -- the
 // no-host-sync forward sizes the grid for the capacity n.
 __device__ __forceinline__ int64_t live_n(int64_t n, const unsigned long long* n_dev) {
@@ -79,27 +77,48 @@ __global__ void __launch_bounds__(kSortThreads)
   pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
   __shared__ uint32_t hist[kWarps][256];
-  const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+  const int t = threadIdx.x, w = t >> 5;
   n = live_n(n, n_dev);
 #pragma unroll
   for (int k = 0; k < kWarps; ++k) hist[k][t] = 0;
   __syncthreads();
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * (ITEMS * kSortThreads) +
-                       static_cast<int64_t>(w) * ITEMS * 32;
+  (void)bits;
+  // Thread-blocked: thread t counts the ITEMS consecutive keys
+  // [tile0 + t*ITEMS, +ITEMS) (16-byte loads), run-length aggregated in
+  // registers and flushed with one shared atomic per run into its warp's
+  // histogram. Sorted-ish inputs (the instance list is generated in
+  // (depth, row, column) order: runs of equal high digits) need few atomics;
+  // random digits cost one uncontended shared atomic per key.
+  const int64_t first = static_cast<int64_t>(blockIdx.x) * (ITEMS * kSortThreads) +
+                        static_cast<int64_t>(t) * ITEMS;
   uint32_t key[ITEMS];
+  if (first + ITEMS <= n) {
+#pragma unroll
+    for (int k = 0; k < ITEMS; k += 4) {
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(keys + first + k));
+      key[k] = q.x;
+      key[k + 1] = q.y;
+      key[k + 2] = q.z;
+      key[k + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) key[k] = first + k < n ? __ldg(keys + first + k) : 0u;
+  }
+  uint32_t prev = 0xffffffffu, run = 0;
 #pragma unroll
   for (int k = 0; k < ITEMS; ++k) {
-    const int64_t e = base + k * 32 + lane;
-    key[k] = e < n ? __ldg(keys + e) : 0u;
+    if (first + k < n) {
+      const uint32_t d = (key[k] >> shift) & mask;
+      if (d != prev) {
+        if (run) atomicAdd(&hist[w][prev], run);
+        prev = d;
+        run = 0;
+      }
+      ++run;
+    }
   }
-#pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    const bool valid = base + k * 32 + lane < n;
-    const uint32_t d = (key[k] >> shift) & mask;
-    const unsigned peers = digit_peers(d, bits, valid);
-    if (valid && (__ffs(peers) - 1) == lane) hist[w][d] += __popc(peers);
-    __syncwarp();
-  }
+  if (run) atomicAdd(&hist[w][prev], run);
   __syncthreads();
   uint32_t s = 0;
 #pragma unroll
@@ -364,15 +383,11 @@ __global__ void __launch_bounds__(kSortThreads)
   }
 }
 
-// Also clears the tile ranges (k_ranges_u32 writes only the non-empty ones),
-// so no memset node breaks the forward's programmatic-launch chain.
 __global__ void k_iota_depthkey(int P, const float* __restrict__ depths, const int* __restrict__ radii,
-                                uint32_t* __restrict__ dkey, uint32_t* __restrict__ ids,
-                                uint2* __restrict__ ranges, int ntiles) {
+                                uint32_t* __restrict__ dkey, uint32_t* __restrict__ ids) {
   pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < ntiles) ranges[i] = make_uint2(0u, 0u);
   if (i >= P) return;
   dkey[i] = radii[i] > 0 ? __float_as_uint(depths[i]) : 0xffffffffu;
   ids[i] = static_cast<uint32_t>(i);
@@ -458,24 +473,40 @@ __global__ void k_clamp_total(const uint64_t* __restrict__ offsets, int P, uint6
   else if (!sticky) *overflow = 0u;
 }
 
-__global__ void k_ranges_u32(int64_t L, const uint32_t* __restrict__ tiles, uint2* __restrict__ ranges,
-                             const unsigned long long* __restrict__ n_dev) {
+// Tile ranges from the sorted tile ids by search rather than by a pass over
+// every instance: warp t finds B(t) and B(t+1), B(x) = #ids < x (lower
+// bounds, 32-ary: six rounds of 32 probes for 10^9 instances), and writes
+// ranges[t] = [B(t), B(t+1)), or (0, 0) for an empty tile as the reference
+// layout has it.
+__device__ __forceinline__ int64_t lower_bound_warp(const uint32_t* __restrict__ a, int64_t L,
+                                                    uint32_t x, int lane) {
+  int64_t lo = 0, hi = L;  // the bound lies in [lo, hi]
+  while (hi - lo > 32) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t p = lo + static_cast<int64_t>(lane) * step;
+    const int c = __popc(__ballot_sync(kFull, p < hi && __ldg(a + p) < x));
+    const int64_t nlo = c > 0 ? lo + static_cast<int64_t>(c - 1) * step + 1 : lo;
+    hi = min(hi, lo + static_cast<int64_t>(c) * step);
+    lo = nlo;
+  }
+  const int64_t p = lo + lane;
+  return lo + __popc(__ballot_sync(kFull, p < hi && __ldg(a + p) < x));
+}
+
+__global__ void k_ranges_search(int64_t L, const uint32_t* __restrict__ tiles,
+                                uint2* __restrict__ ranges, int ntiles,
+                                const unsigned long long* __restrict__ n_dev) {
   pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
-  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int t = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+  if (t >= ntiles) return;
   L = live_n(L, n_dev);
-  if (idx >= L) return;
-  const uint32_t tile = tiles[idx];
-  if (idx == 0) {
-    ranges[tile].x = 0;
-  } else {
-    const uint32_t prev = tiles[idx - 1];
-    if (tile != prev) {
-      ranges[prev].y = static_cast<uint32_t>(idx);
-      ranges[tile].x = static_cast<uint32_t>(idx);
-    }
-  }
-  if (idx == L - 1) ranges[tile].y = static_cast<uint32_t>(L);
+  const int64_t b0 = lower_bound_warp(tiles, L, static_cast<uint32_t>(t), lane);
+  const int64_t b1 = lower_bound_warp(tiles, L, static_cast<uint32_t>(t) + 1u, lane);
+  if (lane == 0)
+    ranges[t] = b1 > b0 ? make_uint2(static_cast<uint32_t>(b0), static_cast<uint32_t>(b1))
+                        : make_uint2(0u, 0u);
 }
 
 __global__ void k_make_keys(int64_t L, const uint32_t* __restrict__ tiles,
@@ -570,10 +601,9 @@ void inclusive_scan_gather(const uint32_t* in, const uint32_t* order, int64_t n,
 }
 
 void launch_depth_keys(int P, const float* depths, const int* radii, uint32_t* dkey, uint32_t* ids,
-                       uint2* ranges, int ntiles, cudaStream_t s) {
-  if (P <= 0 && ntiles <= 0) return;
-  launch_pdl(k_iota_depthkey, blocks_for(std::max(P, ntiles), 256), 256, 0, s, P, depths, radii,
-             dkey, ids, ranges, ntiles);
+                       cudaStream_t s) {
+  if (P <= 0) return;
+  launch_pdl(k_iota_depthkey, blocks_for(P, 256), 256, 0, s, P, depths, radii, dkey, ids);
   DW_CUDA(cudaGetLastError());
 }
 
@@ -586,10 +616,11 @@ void launch_duplicate_sorted(int P, const uint32_t* order, const float2* means2D
   DW_CUDA(cudaGetLastError());
 }
 
-void launch_ranges_u32(int64_t L, const uint32_t* tiles, uint2* ranges, cudaStream_t s,
-                       const unsigned long long* n_dev) {
-  if (L <= 0) return;
-  launch_pdl(k_ranges_u32, blocks_for(L, 256), 256, 0, s, L, tiles, ranges, n_dev);
+void launch_ranges_u32(int64_t L, const uint32_t* tiles, uint2* ranges, int ntiles,
+                       cudaStream_t s, const unsigned long long* n_dev) {
+  if (ntiles <= 0) return;
+  launch_pdl(k_ranges_search, blocks_for(static_cast<int64_t>(ntiles) * 32, 256), 256, 0, s,
+             L, tiles, ranges, ntiles, n_dev);
   DW_CUDA(cudaGetLastError());
 }
 
