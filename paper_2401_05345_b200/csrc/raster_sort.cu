@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "distwar.cuh"
 #include "dw_internal.h"
@@ -47,6 +48,23 @@ constexpr int kWarps = kSortThreads / 32;
 #ifndef DW_SORT_MATCH
 #define DW_SORT_MATCH 0  // 1: one __match_any_sync instead of `bits` ballots
 #endif
+// Compile-time digit width and a FULL (every lane valid) fast path.
+template <int BITS, bool FULL>
+__device__ __forceinline__ unsigned digit_peers_t(uint32_t d, bool valid) {
+  unsigned peers = kFull;
+  if (!FULL) {
+    peers = __ballot_sync(kFull, valid);
+    if (!valid) peers = ~peers;
+  }
+#pragma unroll
+  for (int b = 0; b < BITS; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const unsigned m = __ballot_sync(kFull, bit);
+    peers &= bit ? m : ~m;
+  }
+  return peers;
+}
+
 __device__ __forceinline__ unsigned digit_peers(uint32_t d, int bits, bool valid) {
   if (DW_SORT_MATCH) return __match_any_sync(kFull, valid ? d : 0xffffffffu);
   unsigned peers = __ballot_sync(kFull, valid);
@@ -193,7 +211,7 @@ __global__ void k_scan_digits(uint32_t* __restrict__ digit_total, int ndigits) {
 // order) turns warp-local ranks into global positions. Element order inside
 // the tile is (warp, step, lane) = index order, so the pass is stable.
 // Three block barriers per tile.
-template <int ITEMS>
+template <int ITEMS, int BITS>
 __global__ void __launch_bounds__(kSortThreads)
     k_downsweep(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, int64_t n,
                 int shift, uint32_t mask, int bits, const uint32_t* __restrict__ counts,
@@ -216,29 +234,46 @@ __global__ void __launch_bounds__(kSortThreads)
   s_gbase[t] = digit_base[t] + counts[static_cast<int64_t>(t) * tiles + blockIdx.x];
   const int64_t tile0 = static_cast<int64_t>(blockIdx.x) * TILE;
   const int64_t base = tile0 + static_cast<int64_t>(w) * ITEMS * 32;
+  (void)bits;
   uint32_t key[ITEMS], val[ITEMS], rank[ITEMS];
+  const bool full = tile0 + TILE <= n;  // block-uniform: every element of the tile is live
+  if (full) {
 #pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    const int64_t e = base + k * 32 + lane;
-    key[k] = e < n ? __ldg(keys + e) : 0u;
-    val[k] = e < n ? __ldg(vals + e) : 0u;
+    for (int k = 0; k < ITEMS; ++k) {
+      key[k] = __ldg(keys + base + k * 32 + lane);
+      val[k] = __ldg(vals + base + k * 32 + lane);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      const int64_t e = base + k * 32 + lane;
+      key[k] = e < n ? __ldg(keys + e) : 0u;
+      val[k] = e < n ? __ldg(vals + e) : 0u;
+    }
   }
   __syncthreads();
   // 1. rank inside the warp's contiguous chunk (warp-private counters)
+  auto rank_items = [&](auto full_tag) {
+    constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
-  for (int k = 0; k < ITEMS; ++k) {
-    const bool valid = base + k * 32 + lane < n;
-    const uint32_t d = (key[k] >> shift) & mask;
-    const unsigned peers = digit_peers(d, bits, valid);
-    const int leader = __ffs(peers) - 1;
-    uint32_t old = 0;
-    if (valid && leader == lane) {
-      old = s_cnt[w][d];
-      s_cnt[w][d] = old + __popc(peers);
+    for (int k = 0; k < ITEMS; ++k) {
+      const bool valid = FULL || base + k * 32 + lane < n;
+      const uint32_t d = (key[k] >> shift) & mask;
+      const unsigned peers = digit_peers_t<BITS, FULL>(d, valid);
+      const int leader = __ffs(peers) - 1;
+      uint32_t old = 0;
+      if (valid && leader == lane) {
+        old = s_cnt[w][d];
+        s_cnt[w][d] = old + __popc(peers);
+      }
+      rank[k] = __shfl_sync(kFull, old, leader) + __popc(peers & lt);
+      __syncwarp();
     }
-    rank[k] = __shfl_sync(kFull, old, leader) + __popc(peers & lt);
-    __syncwarp();
-  }
+  };
+  if (full)
+    rank_items(std::true_type{});
+  else
+    rank_items(std::false_type{});
   __syncthreads();
   // 2. thread t owns digit t: tile total, exclusive scan over digits
   uint32_t tot = 0;
@@ -540,6 +575,31 @@ size_t scan_temp_bytes(int64_t n) {
 
 // Stable LSD sort of (k[cur], v[cur]) on bits [0, bits); returns the index
 // (0/1) of the double buffer holding the result.
+template <int ITEMS>
+void launch_downsweep(int bits, unsigned grid, cudaStream_t s, const uint32_t* k, const uint32_t* v,
+                      int64_t n, int shift, uint32_t mask, const uint32_t* counts, int64_t tiles,
+                      const uint32_t* digit, uint32_t* ko, uint32_t* vo,
+                      const unsigned long long* n_dev) {
+#define DW_DOWN(B)                                                                            \
+  case B:                                                                                     \
+    launch_pdl(k_downsweep<ITEMS, B>, grid, kSortThreads, 0, s, k, v, n, shift, mask, bits,  \
+               counts, tiles, digit, ko, vo, n_dev);                                          \
+    break;
+  switch (bits) {
+    DW_DOWN(1)
+    DW_DOWN(2)
+    DW_DOWN(3)
+    DW_DOWN(4)
+    DW_DOWN(5)
+    DW_DOWN(6)
+    DW_DOWN(7)
+    default:
+      launch_pdl(k_downsweep<ITEMS, 8>, grid, kSortThreads, 0, s, k, v, n, shift, mask, bits,
+                 counts, tiles, digit, ko, vo, n_dev);
+  }
+#undef DW_DOWN
+}
+
 int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* temp,
                      cudaStream_t s, const unsigned long long* n_dev) {
   int cur = 0;
@@ -570,16 +630,16 @@ int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* 
     launch_pdl(k_scan_digits, 1, 256, 0, s, digit, 256);
     switch (items) {
       case 16:
-        launch_pdl(k_downsweep<16>, grid, kSortThreads, 0, s, k[cur], v[cur], n, shift, mask, b,
-                   counts, tiles, digit, k[cur ^ 1], v[cur ^ 1], n_dev);
+        launch_downsweep<16>(b, grid, s, k[cur], v[cur], n, shift, mask, counts, tiles, digit,
+                             k[cur ^ 1], v[cur ^ 1], n_dev);
         break;
       case 8:
-        launch_pdl(k_downsweep<8>, grid, kSortThreads, 0, s, k[cur], v[cur], n, shift, mask, b,
-                   counts, tiles, digit, k[cur ^ 1], v[cur ^ 1], n_dev);
+        launch_downsweep<8>(b, grid, s, k[cur], v[cur], n, shift, mask, counts, tiles, digit,
+                            k[cur ^ 1], v[cur ^ 1], n_dev);
         break;
       default:
-        launch_pdl(k_downsweep<4>, grid, kSortThreads, 0, s, k[cur], v[cur], n, shift, mask, b,
-                   counts, tiles, digit, k[cur ^ 1], v[cur ^ 1], n_dev);
+        launch_downsweep<4>(b, grid, s, k[cur], v[cur], n, shift, mask, counts, tiles, digit,
+                            k[cur ^ 1], v[cur ^ 1], n_dev);
     }
     cur ^= 1;
   }
