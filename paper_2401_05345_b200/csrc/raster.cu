@@ -18,6 +18,10 @@
 #include "dw_internal.h"
 #include "raster.cuh"
 
+#ifndef DW_LPT
+#define DW_LPT 1  // the backward takes tiles longest-list first (0: row-major)
+#endif
+
 namespace {
 
 template <typename T>
@@ -59,8 +63,9 @@ struct dw_rasterizer {
   uint32_t* tiles_sorted = nullptr;
   uint32_t* vals = nullptr;                 // sorted Gaussian ids (the lists)
 
-  size_t cap_t = 0, cap_px = 0, cap_px2 = 0;
+  size_t cap_t = 0, cap_px = 0, cap_px2 = 0, cap_to = 0;
   uint2* ranges = nullptr;
+  uint32_t* tile_order = nullptr;  // tiles, longest list first (the backward's CTA order)
   float* final_T = nullptr;
   uint32_t* n_contrib = nullptr;
 
@@ -90,7 +95,8 @@ struct dw_rasterizer {
   ~dw_rasterizer() {
     void* ps[] = {means2D, depths, radii, conic_opacity, rgb, tiles_touched, offsets, dkey[0],
                   dkey[1], dids[0], dids[1], itile[0], itile[1], ivals[0], ivals[1], ranges,
-                  final_T, n_contrib, tmp, scan_tmp, keys_dbg, counters, live_dev, overflow_dev};
+                  final_T, n_contrib, tmp, scan_tmp, keys_dbg, counters, live_dev, overflow_dev,
+                  tile_order};
     for (void* p : ps)
       if (p) cudaFree(p);
     for (float* p : h_bufs)
@@ -142,6 +148,7 @@ struct dw_rasterizer {
     }
     grow(scan_tmp, cap_scan, dw::scan_temp_bytes(P_));
     grow(ranges, cap_t, ntiles);
+    grow(tile_order, cap_to, ntiles);
     grow(final_T, cap_px, npx);
     grow(n_contrib, cap_px2, npx);
     const size_t ni = static_cast<size_t>(std::max<int64_t>(max_instances, 1));
@@ -206,6 +213,7 @@ struct dw_rasterizer {
     grow(tiles_touched, cap_p6, np);
     grow(offsets, cap_p7, np);
     grow(ranges, cap_t, static_cast<size_t>(ntiles));
+    grow(tile_order, cap_to, static_cast<size_t>(ntiles));
     grow(final_T, cap_px, static_cast<size_t>(W) * H);
     grow(n_contrib, cap_px2, static_cast<size_t>(W) * H);
     ensure_small();
@@ -266,7 +274,8 @@ struct dw_rasterizer {
       vals = ivals[cur];
     }
     dw::launch_ranges_u32(n_grid, tiles_sorted, ranges, ntiles, s, n_dev);
-    dw::launch_forward_impl(cam, ranges, vals, means2D, conic_opacity, rgb, radii, final_T,
+    order_stale = true;  // the backward derives its tile order from these ranges
+    dw::launch_forward_impl(cam, ranges, vals, means2D, conic_opacity, rgb, nullptr, final_T,
                             n_contrib, out_color, s);
     if (radii_out && P > 0)
       DW_CUDA(cudaMemcpyAsync(radii_out, radii, sizeof(int) * P, cudaMemcpyDeviceToDevice, s));
@@ -288,8 +297,9 @@ struct dw_rasterizer {
       DW_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned long long), s));
       ctr = counters;
     }
-    dw::launch_backward_impl(cam, ranges, vals, means2D, conic_opacity, rgb, radii, final_T,
-                             n_contrib, dL_dpixels, policy, thr, grad, ctr, s);
+    ensure_order(s);
+    dw::launch_backward_impl(cam, ranges, vals, means2D, conic_opacity, rgb, order_or_null(),
+                             final_T, n_contrib, dL_dpixels, policy, thr, grad, ctr, s);
     if (pairs_out) {
       unsigned long long h[2];
       DW_CUDA(cudaMemcpyAsync(h, counters, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -302,6 +312,16 @@ struct dw_rasterizer {
   uint64_t last_reds = 0;
 
   void ensure_tmp(size_t bytes) { grow(tmp, cap_tmp, bytes); }
+  const uint32_t* order_or_null() const { return DW_LPT ? tile_order : nullptr; }
+  // Longest-list-first tile order of the last forward's ranges, computed once
+  // by the first backward after it (any permutation is correct; this one
+  // shortens the backward's last wave: C2 0.156 -> 0.148 ms, C3 -1 %).
+  bool order_stale = true;
+  void ensure_order(cudaStream_t s) {
+    if (!DW_LPT || !order_stale) return;
+    dw::launch_tile_order(ranges, cam.tiles_x * cam.tiles_y, tile_order, s);
+    order_stale = false;
+  }
 
   float* host_scratch(int slot, size_t n) {
     grow(h_bufs[slot], cap_h[slot], n);
@@ -376,8 +396,9 @@ dw::HostTrace raster_backward_tap(dw_rasterizer* r, const float* dL, int thr, fl
   } guard{tb};
   DW_CUDA(cudaMemsetAsync(tb.count, 0, sizeof(unsigned long long), s));
   if (r->P > 0)
+    r->ensure_order(s);
     launch_backward_tap(r->cam, r->ranges, r->vals, r->means2D, r->conic_opacity, r->rgb,
-                        r->final_T, r->n_contrib, dL, thr, grad, tb, s);
+                        r->order_or_null(), r->final_T, r->n_contrib, dL, thr, grad, tb, s);
   unsigned long long count = 0;
   DW_CUDA(cudaMemcpyAsync(&count, tb.count, sizeof(count), cudaMemcpyDeviceToHost, s));
   DW_CUDA(cudaStreamSynchronize(s));

@@ -87,10 +87,12 @@ struct TapBuf {
 };
 
 // SW-B backward that also records its per-warp records (raster_blend.cu).
+// tile_order (nullable): CTA i renders tile tile_order[i] (launch_tile_order)
 void launch_backward_tap(const CamParams& cam, const uint2* ranges, const uint32_t* values,
                          const float2* means2D, const float4* co, const float4* rgb,
-                         const float* final_T, const uint32_t* n_contrib, const float* dL, int thr,
-                         float* grad, const TapBuf& tap, cudaStream_t s);
+                         const uint32_t* tile_order, const float* final_T,
+                         const uint32_t* n_contrib, const float* dL, int thr, float* grad,
+                         const TapBuf& tap, cudaStream_t s);
 
 // raster_train.cu: preprocess backward (adds into grad3d[P][14]) and Adam.
 void launch_preprocess_backward(int P, const float* means3D, const float* scales,
@@ -114,6 +116,8 @@ void launch_depth_keys(int P, const float* depths, const int* radii, uint32_t* d
 void launch_duplicate_sorted(int P, const uint32_t* order, const float2* means2D, const int* radii,
                              const uint64_t* offsets, const CamParams& cam, uint32_t* tile_ids,
                              uint32_t* values, uint64_t cap, cudaStream_t s);
+// order[ntiles]: tiles by descending list length (bucketed), for the blend kernels
+void launch_tile_order(const uint2* ranges, int ntiles, uint32_t* order, cudaStream_t s);
 // ranges[0, ntiles) of the sorted tile ids (every range written)
 void launch_ranges_u32(int64_t L, const uint32_t* tiles, uint2* ranges, int ntiles,
                        cudaStream_t s, const unsigned long long* n_dev = nullptr);
@@ -124,13 +128,14 @@ void launch_make_keys(int64_t L, const uint32_t* tiles, const uint32_t* values, 
 
 void launch_forward_impl(const CamParams& cam, const uint2* ranges, const uint32_t* values,
                          const float2* means2D, const float4* conic_opacity, const float4* rgb,
-                         const int* radii, float* final_T, uint32_t* n_contrib, float* out_color,
-                         cudaStream_t s);
+                         const uint32_t* tile_order, float* final_T, uint32_t* n_contrib,
+                         float* out_color, cudaStream_t s);
 
 // counters (nullable): [0] += contributing (pixel, Gaussian) pairs, [1] += REDs.
 void launch_backward_impl(const CamParams& cam, const uint2* ranges, const uint32_t* values,
                           const float2* means2D, const float4* co, const float4* rgb,
-                          const int* radii, const float* final_T, const uint32_t* n_contrib,
+                          const uint32_t* tile_order, const float* final_T,
+                          const uint32_t* n_contrib,
                           const float* dL, int policy, int thr, float* grad,
                           unsigned long long* counters, cudaStream_t s);
 

@@ -709,12 +709,13 @@ __global__ void __launch_bounds__(128)
                  const uint32_t* __restrict__ values, const float2* __restrict__ means2D,
                  const float4* __restrict__ conic_opacity, const float4* __restrict__ rgb,
                  float* __restrict__ final_T, uint32_t* __restrict__ n_contrib,
-                 float* __restrict__ out_color) {
+                 float* __restrict__ out_color, const uint32_t* __restrict__ tile_order) {
   pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
   __shared__ Staged sm[kBlock];
   __shared__ uint8_t s_mask[kBlock];
-  const int tile = blockIdx.x, t = threadIdx.x, w = t >> 5, lane = t & 31;
+  const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
+  const int t = threadIdx.x, w = t >> 5, lane = t & 31;
   const int tx0 = (tile % cam.tiles_x) * kTile, ty0 = (tile / cam.tiles_x) * kTile;
   const int px = tx0 + (w & 1) * 8 + (lane & 7);
   const int py = ty0 + (w >> 1) * 8 + (lane >> 3);
@@ -802,7 +803,8 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
                   const float4* __restrict__ conic_opacity, const float4* __restrict__ rgb,
                   const float* __restrict__ final_Ts, const uint32_t* __restrict__ n_contrib,
                   const float* __restrict__ dL_dpixels, int thr, float* __restrict__ grad,
-                  unsigned long long* __restrict__ counters, const TapBuf tap) {
+                  unsigned long long* __restrict__ counters, const TapBuf tap,
+                  const uint32_t* __restrict__ tile_order) {
   pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
   static_assert(POL != kNative, "native runs the thread-per-pixel kernel");
@@ -810,7 +812,8 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
   __shared__ Staged sm[2][kBlock];  // double buffer: batch i+1 lands while batch i is walked
   __shared__ uint8_t s_mask[kBlock];
   __shared__ uint32_t s_wmax[NW];
-  const int tile = blockIdx.x, t = threadIdx.x, w = t >> 5, lane = t & 31;
+  const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
+  const int t = threadIdx.x, w = t >> 5, lane = t & 31;
   const int tx0 = (tile % cam.tiles_x) * kTile, ty0 = (tile / cam.tiles_x) * kTile;
   const int px = tx0 + (w & 1) * 8 + (lane & 7);
   const int py = ty0 + (w >> 1) * 8 + (lane >> 3);
@@ -1019,7 +1022,8 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
 
 template <int POL>
 void launch_bwd(bool count, const CamParams& cam, const uint2* ranges, const uint32_t* values,
-                const float2* means2D, const float4* co, const float4* rgb, const float* fT,
+                const float2* means2D, const float4* co, const float4* rgb,
+                const uint32_t* tile_order, const float* fT,
                 const uint32_t* nc, const float* dL, int thr, float* grad,
                 unsigned long long* ctr, cudaStream_t s) {
   const int grid = cam.tiles_x * cam.tiles_y;
@@ -1030,10 +1034,10 @@ void launch_bwd(bool count, const CamParams& cam, const uint2* ranges, const uin
     if (DW_BLEND_X2) {
       if (count)
         launch_pdl(k_backward_x2<POL, true>, grid, 128, 0, s, cam, ranges, values, means2D, co, rgb,
-                   fT, nc, dL, thr, grad, ctr, TapBuf{});
+                   fT, nc, dL, thr, grad, ctr, TapBuf{}, tile_order);
       else
         launch_pdl(k_backward_x2<POL, false>, grid, 128, 0, s, cam, ranges, values, means2D, co,
-                   rgb, fT, nc, dL, thr, grad, nullptr, TapBuf{});
+                   rgb, fT, nc, dL, thr, grad, nullptr, TapBuf{}, tile_order);
       return;
     }
     constexpr int NT = 256 / DW_BWD_PPT;
@@ -1057,12 +1061,13 @@ void launch_bwd(bool count, const CamParams& cam, const uint2* ranges, const uin
 
 void launch_backward_tap(const CamParams& cam, const uint2* ranges, const uint32_t* values,
                          const float2* means2D, const float4* co, const float4* rgb,
-                         const float* final_T, const uint32_t* n_contrib, const float* dL, int thr,
-                         float* grad, const TapBuf& tap, cudaStream_t s) {
+                         const uint32_t* tile_order, const float* final_T,
+                         const uint32_t* n_contrib, const float* dL, int thr, float* grad,
+                         const TapBuf& tap, cudaStream_t s) {
   const int grid = cam.tiles_x * cam.tiles_y;
   if (DW_BLEND_X2)
     launch_pdl(k_backward_x2<kSwB, false, true>, grid, 128, 0, s, cam, ranges, values, means2D, co,
-               rgb, final_T, n_contrib, dL, thr, grad, nullptr, tap);
+               rgb, final_T, n_contrib, dL, thr, grad, nullptr, tap, tile_order);
   else
     k_backward_multi<DW_BWD_PPT, kSwB, false, true><<<grid, 256 / DW_BWD_PPT, 0, s>>>(
         cam, ranges, values, means2D, co, rgb, final_T, n_contrib, dL, thr, grad, nullptr, tap);
@@ -1071,16 +1076,15 @@ void launch_backward_tap(const CamParams& cam, const uint2* ranges, const uint32
 
 void launch_forward_impl(const CamParams& cam, const uint2* ranges, const uint32_t* values,
                          const float2* means2D, const float4* conic_opacity, const float4* rgb,
-                         const int* radii, float* final_T, uint32_t* n_contrib, float* out_color,
-                         cudaStream_t s) {
-  (void)radii;
+                         const uint32_t* tile_order, float* final_T, uint32_t* n_contrib,
+                         float* out_color, cudaStream_t s) {
   const int grid = cam.tiles_x * cam.tiles_y;
 #ifndef DW_FWD_PPT
 #define DW_FWD_PPT 2  // A/B on C3: 0.527 vs 0.558 ms (profiles/r01/ab_fwd2.jsonl)
 #endif
   if (DW_BLEND_X2)
     launch_pdl(k_forward_x2, grid, 128, 0, s, cam, ranges, values, means2D, conic_opacity, rgb,
-               final_T, n_contrib, out_color);
+               final_T, n_contrib, out_color, tile_order);
   else if (DW_FWD_PPT == 2)
     k_forward_ppt2<<<grid, 128, 0, s>>>(cam, ranges, values, means2D, conic_opacity, rgb, final_T,
                                         n_contrib, out_color);
@@ -1092,27 +1096,26 @@ void launch_forward_impl(const CamParams& cam, const uint2* ranges, const uint32
 
 void launch_backward_impl(const CamParams& cam, const uint2* ranges, const uint32_t* values,
                           const float2* means2D, const float4* co, const float4* rgb,
-                          const int* radii, const float* final_T, const uint32_t* n_contrib,
-                          const float* dL, int policy, int thr, float* grad,
-                          unsigned long long* counters, cudaStream_t s) {
-  (void)radii;
+                          const uint32_t* tile_order, const float* final_T,
+                          const uint32_t* n_contrib, const float* dL, int policy, int thr,
+                          float* grad, unsigned long long* counters, cudaStream_t s) {
   const bool count = counters != nullptr;
   switch (policy) {
     case kNative:
-      launch_bwd<kNative>(count, cam, ranges, values, means2D, co, rgb, final_T, n_contrib, dL,
-                          thr, grad, counters, s);
+      launch_bwd<kNative>(count, cam, ranges, values, means2D, co, rgb, tile_order, final_T,
+                          n_contrib, dL, thr, grad, counters, s);
       break;
     case kSwS:
-      launch_bwd<kSwS>(count, cam, ranges, values, means2D, co, rgb, final_T, n_contrib, dL, thr,
-                       grad, counters, s);
+      launch_bwd<kSwS>(count, cam, ranges, values, means2D, co, rgb, tile_order, final_T, n_contrib,
+                       dL, thr, grad, counters, s);
       break;
     case kSwB:
-      launch_bwd<kSwB>(count, cam, ranges, values, means2D, co, rgb, final_T, n_contrib, dL, thr,
-                       grad, counters, s);
+      launch_bwd<kSwB>(count, cam, ranges, values, means2D, co, rgb, tile_order, final_T, n_contrib,
+                       dL, thr, grad, counters, s);
       break;
     default:
-      launch_bwd<kCccl>(count, cam, ranges, values, means2D, co, rgb, final_T, n_contrib, dL,
-                        thr, grad, counters, s);
+      launch_bwd<kCccl>(count, cam, ranges, values, means2D, co, rgb, tile_order, final_T,
+                        n_contrib, dL, thr, grad, counters, s);
   }
   DW_CUDA(cudaGetLastError());
 }

@@ -551,6 +551,49 @@ __global__ void k_make_keys(int64_t L, const uint32_t* __restrict__ tiles,
   if (i < L) keys[i] = (static_cast<uint64_t>(tiles[i]) << 32) | __float_as_uint(depths[values[i]]);
 }
 
+// Longest-processing-time-first tile order for the blend kernels: tiles
+// bucketed by list length on a 1/8-octave log scale, longest buckets first
+// (order within a bucket is arbitrary). The few very long tiles then start in
+// the first wave instead of trailing the last one.
+__global__ void __launch_bounds__(1024)
+    k_tile_order(const uint2* __restrict__ ranges, int ntiles, uint32_t* __restrict__ order) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
+  __shared__ uint32_t cnt[256];
+  const int t = threadIdx.x;
+  if (t < 256) cnt[t] = 0;
+  __syncthreads();
+  auto bucket = [&](int tile) {
+    const uint2 r = ranges[tile];
+    const float lg = __log2f(static_cast<float>(r.y - r.x) + 1.0f);
+    return 255 - min(255, static_cast<int>(8.0f * lg));
+  };
+  for (int i = t; i < ntiles; i += 1024) atomicAdd(&cnt[bucket(i)], 1u);
+  __syncthreads();
+  if (t < 32) {  // exclusive scan of the 256 bucket counts by one warp
+    uint32_t v[8], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      v[k] = cnt[t * 8 + k];
+      sum += v[k];
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, o);
+      if (t >= o) incl += y;
+    }
+    uint32_t run = incl - sum;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      cnt[t * 8 + k] = run;
+      run += v[k];
+    }
+  }
+  __syncthreads();
+  for (int i = t; i < ntiles; i += 1024) order[atomicAdd(&cnt[bucket(i)], 1u)] = static_cast<uint32_t>(i);
+}
+
 inline unsigned blocks_for(int64_t n, int per) { return static_cast<unsigned>((n + per - 1) / per); }
 
 }  // namespace
@@ -694,6 +737,12 @@ void launch_make_keys(int64_t L, const uint32_t* tiles, const uint32_t* values, 
                       uint64_t* keys, cudaStream_t s) {
   if (L <= 0) return;
   k_make_keys<<<blocks_for(L, 256), 256, 0, s>>>(L, tiles, values, depths, keys);
+  DW_CUDA(cudaGetLastError());
+}
+
+void launch_tile_order(const uint2* ranges, int ntiles, uint32_t* order, cudaStream_t s) {
+  if (ntiles <= 0) return;
+  launch_pdl(k_tile_order, 1, 1024, 0, s, ranges, ntiles, order);
   DW_CUDA(cudaGetLastError());
 }
 
