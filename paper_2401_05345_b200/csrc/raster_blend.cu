@@ -128,185 +128,14 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
-__global__ void __launch_bounds__(kBlock)
-    k_forward(const CamParams cam, const uint2* __restrict__ ranges,
-              const uint32_t* __restrict__ values, const float2* __restrict__ means2D,
-              const float4* __restrict__ conic_opacity, const float4* __restrict__ rgb,
-              float* __restrict__ final_T, uint32_t* __restrict__ n_contrib,
-              float* __restrict__ out_color) {
-  __shared__ Staged sm[kBlock];
-  __shared__ uint8_t s_mask[kBlock];
-  const int tile = blockIdx.x, t = threadIdx.x, w = t >> 5, lane = t & 31;
-  const int tx0 = (tile % cam.tiles_x) * kTile, ty0 = (tile / cam.tiles_x) * kTile;
-  int px, py;
-  tile_pixel(tile, t, cam.tiles_x, &px, &py);
-  const bool inside = px < cam.W && py < cam.H;
-  const float pfx = (float)px, pfy = (float)py;
-  const uint2 range = ranges[tile];
-  const int rounds = (int)((range.y - range.x + kBlock - 1) / kBlock);
-  int todo = (int)(range.y - range.x);
-  bool done = !inside;
-  float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
-  uint32_t last = 0;
-  for (int i = 0; i < rounds; ++i, todo -= kBlock) {
-    if (__syncthreads_count(done) == kBlock) break;
-    const uint32_t progress = range.x + i * kBlock + t;
-    uint32_t mask = 0;
-    if (progress < range.y)
-      mask = stage(sm, t, values[progress], tx0, ty0, means2D, conic_opacity, rgb);
-    s_mask[t] = (uint8_t)mask;
-    __syncthreads();
-    const int n = min(kBlock, todo);
-    for (int k = 0; k * 32 < n; ++k) {
-      if (__all_sync(kFull, done)) break;
-      const int jl = k * 32 + lane;
-      unsigned bits = __ballot_sync(kFull, jl < n && ((s_mask[jl] >> w) & 1u));
-      while (bits) {
-        const int j = k * 32 + __ffs(bits) - 1;
-        bits &= bits - 1u;
-        if (done) continue;
-        const float4 g = sm[j].xyi;
-        const float4 co = sm[j].co;
-        const float dx = g.x - pfx, dy = g.y - pfy;
-        const float power = -0.5f * (co.x * dx * dx + co.z * dy * dy) - co.y * dx * dy;
-        if (power > 0.0f) continue;
-        const float alpha = fminf(0.99f, co.w * __expf(power));
-        if (alpha < 1.0f / 255.0f) continue;
-        const float test_T = T * (1.0f - alpha);
-        if (test_T < 0.0001f) {
-          done = true;
-          continue;
-        }
-        const float4 c = sm[j].col;
-        const float aT = alpha * T;
-        C0 += c.x * aT;
-        C1 += c.y * aT;
-        C2 += c.z * aT;
-        T = test_T;
-        last = (uint32_t)(i * kBlock + j + 1);  // 1-based list position
-      }
-    }
-  }
-  if (inside) {
-    const int pix = py * cam.W + px;
-    const int HW = cam.H * cam.W;
-    final_T[pix] = T;
-    n_contrib[pix] = last;
-    out_color[pix] = C0 + T * cam.bg[0];
-    out_color[HW + pix] = C1 + T * cam.bg[1];
-    out_color[2 * HW + pix] = C2 + T * cam.bg[2];
-  }
-}
-
-// Forward with two pixels per thread (128 threads per tile, warp = 8x8
-// block, lane pixels (l & 7, l >> 3) and 4 rows below), same staging and
-// masks; each pixel keeps its own early-termination state.
-struct FwdPix {
-  float pfx, pfy, T, C0, C1, C2;
-  uint32_t last;
-  bool done;
-};
-
-__device__ __forceinline__ void fwd_step(FwdPix& s, const float4& g, const float4& co,
-                                         const float4& c, uint32_t pos) {
-  if (s.done) return;
-  const float dx = g.x - s.pfx, dy = g.y - s.pfy;
-  const float power = -0.5f * (co.x * dx * dx + co.z * dy * dy) - co.y * dx * dy;
-  if (power > 0.0f) return;
-  const float alpha = fminf(0.99f, co.w * __expf(power));
-  if (alpha < 1.0f / 255.0f) return;
-  const float test_T = s.T * (1.0f - alpha);
-  if (test_T < 0.0001f) {
-    s.done = true;
-    return;
-  }
-  const float aT = alpha * s.T;
-  s.C0 += c.x * aT;
-  s.C1 += c.y * aT;
-  s.C2 += c.z * aT;
-  s.T = test_T;
-  s.last = pos;
-}
-
-__global__ void __launch_bounds__(128)
-    k_forward_ppt2(const CamParams cam, const uint2* __restrict__ ranges,
-                   const uint32_t* __restrict__ values, const float2* __restrict__ means2D,
-                   const float4* __restrict__ conic_opacity, const float4* __restrict__ rgb,
-                   float* __restrict__ final_T, uint32_t* __restrict__ n_contrib,
-                   float* __restrict__ out_color) {
-  __shared__ Staged sm[kBlock];
-  __shared__ uint8_t s_mask[kBlock];
-  const int tile = blockIdx.x, t = threadIdx.x, w = t >> 5, lane = t & 31;
-  const int tx0 = (tile % cam.tiles_x) * kTile, ty0 = (tile / cam.tiles_x) * kTile;
-  const int px = tx0 + (w & 1) * 8 + (lane & 7);
-  const int py = ty0 + (w >> 1) * 8 + (lane >> 3);
-  FwdPix p[2];
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    p[k].pfx = (float)px;
-    p[k].pfy = (float)(py + 4 * k);
-    p[k].T = 1.0f;
-    p[k].C0 = p[k].C1 = p[k].C2 = 0.0f;
-    p[k].last = 0;
-    p[k].done = !(px < cam.W && py + 4 * k < cam.H);
-  }
-  const uint32_t wbits = (1u << (4 * (w >> 1) + (w & 1))) | (1u << (4 * (w >> 1) + (w & 1) + 2));
-  const uint2 range = ranges[tile];
-  const int rounds = (int)((range.y - range.x + kBlock - 1) / kBlock);
-  int todo = (int)(range.y - range.x);
-  for (int i = 0; i < rounds; ++i, todo -= kBlock) {
-    if (__syncthreads_count(p[0].done && p[1].done) == 128) break;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int st = t + h * 128;
-      const uint32_t progress = range.x + i * kBlock + st;
-      uint32_t mask = 0;
-      if (progress < range.y)
-        mask = stage(sm, st, values[progress], tx0, ty0, means2D, conic_opacity, rgb);
-      s_mask[st] = (uint8_t)mask;
-    }
-    __syncthreads();
-    const int n = min(kBlock, todo);
-    for (int k = 0; k * 32 < n; ++k) {
-      if (__all_sync(kFull, p[0].done && p[1].done)) break;
-      const int jl = k * 32 + lane;
-      const uint32_t m = jl < n ? s_mask[jl] : 0u;
-      unsigned bits = __ballot_sync(kFull, (m & wbits) != 0u);
-      while (bits) {
-        const int j = k * 32 + __ffs(bits) - 1;
-        bits &= bits - 1u;
-        const float4 g = sm[j].xyi;
-        const float4 co = sm[j].co;
-        const float4 c = sm[j].col;
-        const uint32_t pos = (uint32_t)(i * kBlock + j + 1);  // 1-based list position
-        fwd_step(p[0], g, co, c, pos);
-        fwd_step(p[1], g, co, c, pos);
-      }
-    }
-  }
-  const int HW = cam.H * cam.W;
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const int y = py + 4 * k;
-    if (px < cam.W && y < cam.H) {
-      const int pix = y * cam.W + px;
-      final_T[pix] = p[k].T;
-      n_contrib[pix] = p[k].last;
-      out_color[pix] = p[k].C0 + p[k].T * cam.bg[0];
-      out_color[HW + pix] = p[k].C1 + p[k].T * cam.bg[1];
-      out_color[2 * HW + pix] = p[k].C2 + p[k].T * cam.bg[2];
-    }
-  }
-}
-
 #ifndef DW_BWD_MIN_BLOCKS
 #define DW_BWD_MIN_BLOCKS 5  // 5 x 256 threads/SM: <= 51 registers, no spills (ptxas -v)
 #endif
 
 // One pixel per thread -- the paper's GradComputation layout ("thread corr.
-// to pixel"). Production use: the native (naive-atomic)
-// baseline, whose fastest layout this is; the reduction policies run
-// k_backward_multi below (any policy compiles here, for A/B runs).
+// to pixel"): the native (naive-atomic) baseline, whose
+// fastest layout this is (7.8 vs 8.2 ms two-pixel on C3). The reduction
+// policies run k_backward_x2 below.
 template <int POL, bool COUNT>
 __global__ void __launch_bounds__(kBlock, DW_BWD_MIN_BLOCKS)
     k_backward(const CamParams cam, const uint2* __restrict__ ranges,
@@ -444,206 +273,10 @@ __global__ void __launch_bounds__(kBlock, DW_BWD_MIN_BLOCKS)
   }
 }
 
-// ---------------------------------------------------------------------------
-// Two pixels per thread (PPT = 2): 128 threads per 16x16 tile, warp w owns the
-// 8x8 block (column w & 1, row band w >> 1); lane l holds pixel (l & 7, l >> 3)
-// and the pixel 4 rows below. Per Gaussian, a lane first adds its two
-// pixels' 9 gradients in registers, then the warp runs the DISTWAR policy on
-// the lane sums (a lane is active if either pixel is). The mask / ballot /
-// staging overhead and the warp reduction are paid once per 64 pixels.
-// native keeps one RED per (active pixel, param): the paper's baseline.
-struct Pix {
-  float pfx, pfy, T, T_final, dLp0, dLp1, dLp2, bg_dot;
-  float acc0, acc1, acc2, lc0, lc1, lc2, last_alpha;
-  uint32_t last;
-  bool inside;
-};
-
-__device__ __forceinline__ void pix_init(Pix& s, int px, int py, const CamParams& cam,
-                                         const float* __restrict__ final_Ts,
-                                         const uint32_t* __restrict__ n_contrib,
-                                         const float* __restrict__ dL) {
-  s.inside = px < cam.W && py < cam.H;
-  const int pix = py * cam.W + px, HW = cam.H * cam.W;
-  s.pfx = (float)px;
-  s.pfy = (float)py;
-  s.T_final = s.inside ? final_Ts[pix] : 0.0f;
-  s.T = s.T_final;
-  s.last = s.inside ? n_contrib[pix] : 0u;
-  s.dLp0 = s.inside ? dL[pix] : 0.0f;
-  s.dLp1 = s.inside ? dL[HW + pix] : 0.0f;
-  s.dLp2 = s.inside ? dL[2 * HW + pix] : 0.0f;
-  s.bg_dot = cam.bg[0] * s.dLp0 + cam.bg[1] * s.dLp1 + cam.bg[2] * s.dLp2;
-  s.acc0 = s.acc1 = s.acc2 = s.lc0 = s.lc1 = s.lc2 = s.last_alpha = 0.0f;
-}
-
-// Activity test + (if active) gradient into v (added when ADD, else assigned).
-template <bool ADD>
-__device__ __forceinline__ bool pix_step(Pix& s, uint32_t contributor, const float4& g,
-                                         const float4& co, const float4& c, float hw, float hh,
-                                         float (&v)[kNParam]) {
-  const float dx = g.x - s.pfx, dy = g.y - s.pfy;
-  const float dxx = dx * dx, dxy = dx * dy, dyy = dy * dy;
-  const float power = -0.5f * (co.x * dxx + co.z * dyy) - co.y * dxy;
-  const float G = __expf(power);
-  const float alpha = fminf(0.99f, co.w * G);
-  const bool act = s.inside && contributor < s.last && power <= 0.0f && alpha >= 1.0f / 255.0f;
-  if (act) {
-    const float inv = __fdividef(1.0f, 1.0f - alpha);
-    s.T = s.T * inv;
-    const float dcd = alpha * s.T;
-    s.acc0 += s.last_alpha * (s.lc0 - s.acc0);
-    s.acc1 += s.last_alpha * (s.lc1 - s.acc1);
-    s.acc2 += s.last_alpha * (s.lc2 - s.acc2);
-    s.lc0 = c.x;
-    s.lc1 = c.y;
-    s.lc2 = c.z;
-    float dL_dalpha = (c.x - s.acc0) * s.dLp0;
-    dL_dalpha += (c.y - s.acc1) * s.dLp1;
-    dL_dalpha += (c.z - s.acc2) * s.dLp2;
-    dL_dalpha *= s.T;
-    s.last_alpha = alpha;
-    dL_dalpha += (-s.T_final * inv) * s.bg_dot;
-    const float q = G * (co.w * dL_dalpha);
-    const float qh = -0.5f * q;
-    const float r[kNParam] = {-q * (co.x * dx + co.y * dy) * hw, -q * (co.z * dy + co.y * dx) * hh,
-                              qh * dxx, qh * dxy, qh * dyy, G * dL_dalpha, dcd * s.dLp0,
-                              dcd * s.dLp1, dcd * s.dLp2};
-#pragma unroll
-    for (int p = 0; p < kNParam; ++p) v[p] = ADD ? v[p] + r[p] : r[p];
-  } else if (!ADD) {
-#pragma unroll
-    for (int p = 0; p < kNParam; ++p) v[p] = 0.0f;
-  }
-  return act;
-}
-
-// Pixels per lane of the reduction-policy kernel (A/B: -DDW_BWD_PPT=4).
-#ifndef DW_BWD_PPT
-#define DW_BWD_PPT 2
-#endif
-// CTAs per SM the register allocator must allow (ptxas -v: no spills):
-// PPT 2 -> 6 x 128 threads (<= 80 regs), PPT 4 -> 8 x 64 threads (<= 128 regs).
+// CTAs per SM the register allocator must allow for the packed kernels (ptxas -v: no spills).
 #ifndef DW_MULTI_MIN_BLOCKS
-#define DW_MULTI_MIN_BLOCKS (DW_BWD_PPT == 4 ? 8 : 6)
+#define DW_MULTI_MIN_BLOCKS 6
 #endif
-
-// PPT pixels per lane: 256/PPT threads per 16x16 tile; warp w owns the
-// 8 x 4PPT block (column w & 1, row band w >> 1) and lane l holds pixels
-// (l & 7, (l >> 3) + 4k), k < PPT. Per Gaussian a lane sums its pixels' 9
-// gradients in registers, then the warp runs the DISTWAR policy on the lane
-// sums (a lane is active if any of its pixels is). Mask / ballot / staging
-// overhead and the warp reduction are paid once per 32 PPT pixels.
-template <int PPT, int POL, bool COUNT, bool TAP = false>
-__global__ void __launch_bounds__(256 / PPT, DW_MULTI_MIN_BLOCKS)
-    k_backward_multi(const CamParams cam, const uint2* __restrict__ ranges,
-                     const uint32_t* __restrict__ values, const float2* __restrict__ means2D,
-                     const float4* __restrict__ conic_opacity, const float4* __restrict__ rgb,
-                     const float* __restrict__ final_Ts, const uint32_t* __restrict__ n_contrib,
-                     const float* __restrict__ dL_dpixels, int thr, float* __restrict__ grad,
-                     unsigned long long* __restrict__ counters, const TapBuf tap) {
-  static_assert(POL != kNative, "native runs the thread-per-pixel kernel");
-  constexpr int NT = 256 / PPT, NW = 8 / PPT;
-  __shared__ Staged sm[kBlock];
-  __shared__ uint8_t s_mask[kBlock];
-  __shared__ uint32_t s_wmax[NW];
-  const int tile = blockIdx.x, t = threadIdx.x, w = t >> 5, lane = t & 31;
-  const int tx0 = (tile % cam.tiles_x) * kTile, ty0 = (tile / cam.tiles_x) * kTile;
-  const int px = tx0 + (w & 1) * 8 + (lane & 7);
-  const int py = ty0 + (w >> 1) * (4 * PPT) + (lane >> 3);
-  Pix pxl[PPT];
-  uint32_t lmax = 0;
-#pragma unroll
-  for (int k = 0; k < PPT; ++k) {
-    pix_init(pxl[k], px, py + 4 * k, cam, final_Ts, n_contrib, dL_dpixels);
-    lmax = max(lmax, pxl[k].last);
-  }
-  const float hw = 0.5f * (float)cam.W, hh = 0.5f * (float)cam.H;
-  const uint2 range = ranges[tile];
-  const uint32_t wmax = __reduce_max_sync(kFull, lmax);
-  if (lane == 0) s_wmax[w] = wmax;
-  __syncthreads();
-  uint32_t bmax = 0;
-#pragma unroll
-  for (int k = 0; k < NW; ++k) bmax = max(bmax, s_wmax[k]);
-  // this warp's PPT 8x4 bands in the 8-bit staging mask (stage(): 8x4 layout)
-  uint32_t wbits = 0;
-#pragma unroll
-  for (int k = 0; k < PPT; ++k) wbits |= 1u << (2 * ((w >> 1) * PPT + k) + (w & 1));
-  uint32_t nred = 0, npairs = 0;
-  bool issuer;
-  const int slot = bfly_slot<kNParam>(lane, &issuer);
-  const int rounds = (int)((bmax + kBlock - 1) / kBlock);
-  int todo = (int)bmax;
-  const uint32_t top = range.x + bmax;
-  for (int i = 0; i < rounds; ++i, todo -= kBlock) {
-    __syncthreads();
-#pragma unroll
-    for (int h = 0; h < PPT; ++h) {
-      const int st = t + h * NT;
-      uint32_t mask = 0;
-      if (st < todo)
-        mask = stage(sm, st, values[top - 1 - (i * kBlock + st)], tx0, ty0, means2D,
-                     conic_opacity, rgb);
-      s_mask[st] = (uint8_t)mask;
-    }
-    __syncthreads();
-    const int n = min(kBlock, todo);
-    const uint32_t base = bmax - 1 - (uint32_t)(i * kBlock);
-    for (int k = 0; k * 32 < n; ++k) {
-      const int jl = k * 32 + lane;
-      const uint32_t m = jl < n ? s_mask[jl] : 0u;
-      unsigned bits = __ballot_sync(kFull, (m & wbits) != 0u && (base - (uint32_t)jl) < wmax);
-      while (bits) {
-        const int j = k * 32 + __ffs(bits) - 1;
-        bits &= bits - 1u;
-        const uint32_t contributor = base - (uint32_t)j;
-        const float4 g = sm[j].xyi;
-        const float4 co = sm[j].co;
-        const float4 c = sm[j].col;
-        float v[kNParam];
-        bool act = pix_step<false>(pxl[0], contributor, g, co, c, hw, hh, v);
-        uint32_t cnt = COUNT ? __popc(__ballot_sync(kFull, act)) : 0u;
-#pragma unroll
-        for (int q = 1; q < PPT; ++q) {
-          const bool a = pix_step<true>(pxl[q], contributor, g, co, c, hw, hh, v);
-          if (COUNT) cnt += __popc(__ballot_sync(kFull, a));
-          act = act || a;
-        }
-        const unsigned ballot = __ballot_sync(kFull, act);
-        if (ballot == 0u) continue;
-        const int id = (int)__float_as_uint(g.z);
-        if (COUNT && lane == 0) npairs += cnt;
-        if (TAP) {  // the record the policy reduces: lane value = its pixels' sum
-          unsigned long long rec = 0;
-          if (lane == 0) rec = atomicAdd(tap.count, 1ull);
-          rec = __shfl_sync(kFull, rec, 0);
-          if (rec < tap.cap) {
-            if (lane == 0) {
-              tap.warp_id[rec] = tile * NW + w;
-              tap.iteration[rec] = (int32_t)contributor;
-              tap.active[rec] = ballot;
-            }
-            tap.prim[rec * 32 + lane] = id;
-#pragma unroll
-            for (int p = 0; p < kNParam; ++p) tap.vals[(rec * kNParam + p) * 32 + lane] = v[p];
-          }
-        }
-        if (POL == kSwB) {
-          reduce_bfly<kNParam, COUNT, true>(id, grad, v, thr, act, lane, nred, ballot, slot, issuer);
-        } else if (POL == kSwS) {
-          reduce_serial<kNParam, COUNT>(id, grad, v, thr, act, lane, nred, ballot);
-        } else {
-          reduce_cccl<kNParam, COUNT>(id, grad, v, act, lane, nred, ballot);
-        }
-      }
-    }
-  }
-  if (COUNT) {
-    flush_count(counters, npairs, lane);
-    flush_count(counters + 1, nred, lane);
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Packed-FP32 two-pixel kernels (sm_100 FFMA2 / FMUL2 / FADD2).
@@ -794,8 +427,12 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-// Backward, packed two-pixel form of k_backward_multi<2, POL> (same tile /
-// warp / lane layout, staging, masks, list-position bound and policy calls).
+// Backward with two pixels per lane for the reduction policies: warp w owns
+// the 8x8 block (column w & 1, row band w >> 1), lane l the pixels
+// (l & 7, l >> 3) and 4 rows below; per Gaussian a lane sums its two pixels'
+// gradients before the warp runs the DISTWAR policy on the lane sums, so the
+// mask / ballot / staging overhead and the warp reduction are paid once per
+// 64 pixels.
 template <int POL, bool COUNT, bool TAP = false>
 __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
     k_backward_x2(const CamParams cam, const uint2* __restrict__ ranges,
@@ -1016,10 +653,6 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
   }
 }
 
-#ifndef DW_BLEND_X2
-#define DW_BLEND_X2 1  // packed f32x2 two-pixel kernels (0: k_backward_multi / k_forward_ppt2)
-#endif
-
 template <int POL>
 void launch_bwd(bool count, const CamParams& cam, const uint2* ranges, const uint32_t* values,
                 const float2* means2D, const float4* co, const float4* rgb,
@@ -1027,26 +660,15 @@ void launch_bwd(bool count, const CamParams& cam, const uint2* ranges, const uin
                 const uint32_t* nc, const float* dL, int thr, float* grad,
                 unsigned long long* ctr, cudaStream_t s) {
   const int grid = cam.tiles_x * cam.tiles_y;
-  // The reduction policies run two pixels per thread; native keeps the
-  // paper's thread-per-pixel kernel (its faster layout: 7.8 vs 8.2 ms on C3,
-  // profiles/r01/ab_ppt.jsonl), so the naive baseline is not handicapped.
+  // The reduction policies run two pixels per lane; native keeps the paper's
+  // thread-per-pixel kernel (profiles/r01/ab_ppt.jsonl).
   if constexpr (POL != kNative) {
-    if (DW_BLEND_X2) {
-      if (count)
-        launch_pdl(k_backward_x2<POL, true>, grid, 128, 0, s, cam, ranges, values, means2D, co, rgb,
-                   fT, nc, dL, thr, grad, ctr, TapBuf{}, tile_order);
-      else
-        launch_pdl(k_backward_x2<POL, false>, grid, 128, 0, s, cam, ranges, values, means2D, co,
-                   rgb, fT, nc, dL, thr, grad, nullptr, TapBuf{}, tile_order);
-      return;
-    }
-    constexpr int NT = 256 / DW_BWD_PPT;
     if (count)
-      k_backward_multi<DW_BWD_PPT, POL, true><<<grid, NT, 0, s>>>(
-          cam, ranges, values, means2D, co, rgb, fT, nc, dL, thr, grad, ctr, TapBuf{});
+      launch_pdl(k_backward_x2<POL, true>, grid, 128, 0, s, cam, ranges, values, means2D, co, rgb,
+                 fT, nc, dL, thr, grad, ctr, TapBuf{}, tile_order);
     else
-      k_backward_multi<DW_BWD_PPT, POL, false><<<grid, NT, 0, s>>>(
-          cam, ranges, values, means2D, co, rgb, fT, nc, dL, thr, grad, nullptr, TapBuf{});
+      launch_pdl(k_backward_x2<POL, false>, grid, 128, 0, s, cam, ranges, values, means2D, co,
+                 rgb, fT, nc, dL, thr, grad, nullptr, TapBuf{}, tile_order);
     return;
   }
   if (count)
@@ -1065,12 +687,8 @@ void launch_backward_tap(const CamParams& cam, const uint2* ranges, const uint32
                          const uint32_t* n_contrib, const float* dL, int thr, float* grad,
                          const TapBuf& tap, cudaStream_t s) {
   const int grid = cam.tiles_x * cam.tiles_y;
-  if (DW_BLEND_X2)
-    launch_pdl(k_backward_x2<kSwB, false, true>, grid, 128, 0, s, cam, ranges, values, means2D, co,
-               rgb, final_T, n_contrib, dL, thr, grad, nullptr, tap, tile_order);
-  else
-    k_backward_multi<DW_BWD_PPT, kSwB, false, true><<<grid, 256 / DW_BWD_PPT, 0, s>>>(
-        cam, ranges, values, means2D, co, rgb, final_T, n_contrib, dL, thr, grad, nullptr, tap);
+  launch_pdl(k_backward_x2<kSwB, false, true>, grid, 128, 0, s, cam, ranges, values, means2D, co,
+             rgb, final_T, n_contrib, dL, thr, grad, nullptr, tap, tile_order);
   DW_CUDA(cudaGetLastError());
 }
 
@@ -1079,18 +697,8 @@ void launch_forward_impl(const CamParams& cam, const uint2* ranges, const uint32
                          const uint32_t* tile_order, float* final_T, uint32_t* n_contrib,
                          float* out_color, cudaStream_t s) {
   const int grid = cam.tiles_x * cam.tiles_y;
-#ifndef DW_FWD_PPT
-#define DW_FWD_PPT 2  // A/B on C3: 0.527 vs 0.558 ms (profiles/r01/ab_fwd2.jsonl)
-#endif
-  if (DW_BLEND_X2)
-    launch_pdl(k_forward_x2, grid, 128, 0, s, cam, ranges, values, means2D, conic_opacity, rgb,
-               final_T, n_contrib, out_color, tile_order);
-  else if (DW_FWD_PPT == 2)
-    k_forward_ppt2<<<grid, 128, 0, s>>>(cam, ranges, values, means2D, conic_opacity, rgb, final_T,
-                                        n_contrib, out_color);
-  else
-    k_forward<<<grid, kBlock, 0, s>>>(cam, ranges, values, means2D, conic_opacity, rgb, final_T,
-                                      n_contrib, out_color);
+  launch_pdl(k_forward_x2, grid, 128, 0, s, cam, ranges, values, means2D, conic_opacity, rgb,
+             final_T, n_contrib, out_color, tile_order);
   DW_CUDA(cudaGetLastError());
 }
 
