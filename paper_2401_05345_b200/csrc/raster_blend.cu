@@ -354,15 +354,19 @@ __global__ void __launch_bounds__(128)
   const int py = ty0 + (w >> 1) * 8 + (lane >> 3);
   const float pfx = (float)px;
   const float2 npfy = make_float2(-(float)py, -(float)(py + 4));
-  float2 T = bc2(1.0f), C0 = bc2(0.0f), C1 = bc2(0.0f), C2 = bc2(0.0f);
+  // A pixel is live while T > 0; termination stores -T (the transmittance
+  // at termination, which final_T reports) so no separate done flag is kept.
+  // Pixels outside the image start terminated.
+  float2 T = make_float2(px < cam.W && py < cam.H ? 1.0f : -1.0f,
+                         px < cam.W && py + 4 < cam.H ? 1.0f : -1.0f);
+  float2 C0 = bc2(0.0f), C1 = bc2(0.0f), C2 = bc2(0.0f);
   uint32_t last0 = 0, last1 = 0;
-  bool done0 = !(px < cam.W && py < cam.H), done1 = !(px < cam.W && py + 4 < cam.H);
   const uint32_t wbits = (1u << (4 * (w >> 1) + (w & 1))) | (1u << (4 * (w >> 1) + (w & 1) + 2));
   const uint2 range = ranges[tile];
   const int rounds = (int)((range.y - range.x + kBlock - 1) / kBlock);
   int todo = (int)(range.y - range.x);
   for (int i = 0; i < rounds; ++i, todo -= kBlock) {
-    if (__syncthreads_count(done0 && done1) == 128) break;
+    if (__syncthreads_count(T.x < 0.0f && T.y < 0.0f) == 128) break;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int st = t + h * 128;
@@ -375,7 +379,7 @@ __global__ void __launch_bounds__(128)
     __syncthreads();
     const int n = min(kBlock, todo);
     for (int k = 0; k * 32 < n; ++k) {
-      if (__all_sync(kFull, done0 && done1)) break;
+      if (__all_sync(kFull, T.x < 0.0f && T.y < 0.0f)) break;
       const int jl = k * 32 + lane;
       const uint32_t m = jl < n ? s_mask[jl] : 0u;
       unsigned bits = __ballot_sync(kFull, (m & wbits) != 0u);
@@ -388,29 +392,26 @@ __global__ void __launch_bounds__(128)
         eval2(g, co, pfx, npfy, e);
         const float2 Go = mul2(e.G, bc2(co.w));
         const float2 alpha = make_float2(fminf(0.99f, Go.x), fminf(0.99f, Go.y));
-        const float2 om = fma2(alpha, bc2(-1.0f), bc2(1.0f));
-        const float2 test_T = mul2(T, om);
-        bool a0 = !done0 && e.power.x <= 0.0f && alpha.x >= 1.0f / 255.0f;
-        bool a1 = !done1 && e.power.y <= 0.0f && alpha.y >= 1.0f / 255.0f;
-        done0 = done0 || (a0 && test_T.x < 0.0001f);
-        done1 = done1 || (a1 && test_T.y < 0.0001f);
-        a0 = a0 && !done0;
-        a1 = a1 && !done1;
-        const float2 am = mul2(alpha, make_float2(a0 ? 1.0f : 0.0f, a1 ? 1.0f : 0.0f));
+        const float2 test_T = mul2(T, fma2(alpha, bc2(-1.0f), bc2(1.0f)));
+        const bool a0 = T.x > 0.0f && e.power.x <= 0.0f && alpha.x >= 1.0f / 255.0f;
+        const bool a1 = T.y > 0.0f && e.power.y <= 0.0f && alpha.y >= 1.0f / 255.0f;
+        const bool b0 = a0 && test_T.x >= 0.0001f;  // blends; a0 && !b0 terminates
+        const bool b1 = a1 && test_T.y >= 0.0001f;
+        const float2 am = make_float2(b0 ? alpha.x : 0.0f, b1 ? alpha.y : 0.0f);
         const float4 c = sm[j].col;
         const float2 aT = mul2(am, T);
         C0 = fma2(bc2(c.x), aT, C0);
         C1 = fma2(bc2(c.y), aT, C1);
         C2 = fma2(bc2(c.z), aT, C2);
-        T = mul2(T, fma2(am, bc2(-1.0f), bc2(1.0f)));  // == test_T when active, T when not
+        T = make_float2(b0 ? test_T.x : (a0 ? -T.x : T.x), b1 ? test_T.y : (a1 ? -T.y : T.y));
         const uint32_t pos = (uint32_t)(i * kBlock + j + 1);  // 1-based list position
-        last0 = a0 ? pos : last0;
-        last1 = a1 ? pos : last1;
+        last0 = b0 ? pos : last0;
+        last1 = b1 ? pos : last1;
       }
     }
   }
   const int HW = cam.H * cam.W;
-  const float Ts[2] = {T.x, T.y}, c0[2] = {C0.x, C0.y}, c1[2] = {C1.x, C1.y},
+  const float Ts[2] = {fabsf(T.x), fabsf(T.y)}, c0[2] = {C0.x, C0.y}, c1[2] = {C1.x, C1.y},
               c2[2] = {C2.x, C2.y};
   const uint32_t ls[2] = {last0, last1};
 #pragma unroll
