@@ -51,6 +51,7 @@ constexpr int kWarps = kSortThreads / 32;
 // Compile-time digit width and a FULL (every lane valid) fast path.
 template <int BITS, bool FULL>
 __device__ __forceinline__ unsigned digit_peers_t(uint32_t d, bool valid) {
+  if (DW_SORT_MATCH) return __match_any_sync(kFull, FULL || valid ? d : 0xffffffffu);
   unsigned peers = kFull;
   if (!FULL) {
     peers = __ballot_sync(kFull, valid);
