@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 
 #include "distwar.cuh"
@@ -66,6 +67,10 @@ struct dw_rasterizer {
   size_t cap_t = 0, cap_px = 0, cap_px2 = 0, cap_to = 0;
   uint2* ranges = nullptr;
   uint32_t* tile_order = nullptr;  // tiles, longest list first (the backward's CTA order)
+  bool dense = false;              // last forward used dense (tile-major) binning
+  uint2* rects = nullptr;          // dense binning: packed tile rectangle + id, depth order
+  int* diff = nullptr;             // dense binning: 2D difference grid of the rectangles
+  size_t cap_r = 0, cap_diff = 0;
   float* final_T = nullptr;
   uint32_t* n_contrib = nullptr;
 
@@ -96,7 +101,7 @@ struct dw_rasterizer {
     void* ps[] = {means2D, depths, radii, conic_opacity, rgb, tiles_touched, offsets, dkey[0],
                   dkey[1], dids[0], dids[1], itile[0], itile[1], ivals[0], ivals[1], ranges,
                   final_T, n_contrib, tmp, scan_tmp, keys_dbg, counters, live_dev, overflow_dev,
-                  tile_order};
+                  tile_order, rects, diff};
     for (void* p : ps)
       if (p) cudaFree(p);
     for (float* p : h_bufs)
@@ -264,7 +269,18 @@ struct dw_rasterizer {
     }
     tiles_sorted = itile[0];
     vals = ivals[0];
-    if (n_grid > 0) {
+    // Dense scenes (large tile rectangles: P x tiles <= 4 x instances) build the
+    // per-tile lists directly; the rest duplicate + radix-sort (same output).
+    const char* env = std::getenv("DW_DENSE_BINNING");  // "0" / "1" force a path
+    dense = n_grid > 0 && dw::dense_binning_fits(cam.tiles_x, cam.tiles_y) &&
+            (env && *env ? *env == '1'
+                         : static_cast<double>(P) * ntiles <= 4.0 * static_cast<double>(n_grid));
+    if (dense) {
+      grow(rects, cap_r, static_cast<size_t>(P));
+      grow(diff, cap_diff, dw::dense_diff_bytes(cam.tiles_x, cam.tiles_y) / sizeof(int));
+      dw::launch_dense_binning(P, order, means2D, radii, cam, rects, diff, ranges, ivals[0],
+                               n_dev, s);
+    } else if (n_grid > 0) {
       // 2. duplicate in depth order, 3. stable sort by tile id
       dw::launch_duplicate_sorted(P, order, means2D, radii, offsets, cam, itile[0], ivals[0],
                                   static_cast<uint64_t>(n_grid), s);
@@ -273,7 +289,7 @@ struct dw_rasterizer {
       tiles_sorted = itile[cur];
       vals = ivals[cur];
     }
-    dw::launch_ranges_u32(n_grid, tiles_sorted, ranges, ntiles, s, n_dev);
+    if (!dense) dw::launch_ranges_u32(n_grid, tiles_sorted, ranges, ntiles, s, n_dev);
     order_stale = true;  // the backward derives its tile order from these ranges
     dw::launch_forward_impl(cam, ranges, vals, means2D, conic_opacity, rgb, nullptr, final_T,
                             n_contrib, out_color, s);
@@ -465,7 +481,11 @@ void raster_buffer(const dw_rasterizer* r, int which, const void** p, int64_t* c
     case 5: {  // (tile << 32 | depth bits) of the sorted instances, built on request
       auto* m = const_cast<dw_rasterizer*>(r);
       grow(m->keys_dbg, m->cap_keys, static_cast<size_t>(std::max<int64_t>(I, 1)));
-      launch_make_keys(I, r->tiles_sorted, r->vals, r->depths, m->keys_dbg, nullptr);
+      if (r->dense)  // dense binning writes no tile-id array: derive it from the ranges
+        launch_tiles_from_ranges(r->ranges, r->cam.tiles_x * r->cam.tiles_y, r->itile[0],
+                                 nullptr);
+      launch_make_keys(I, r->dense ? r->itile[0] : r->tiles_sorted, r->vals, r->depths,
+                       m->keys_dbg, nullptr);
       DW_CUDA(cudaDeviceSynchronize());
       *p = r->keys_dbg;
       *count = I;

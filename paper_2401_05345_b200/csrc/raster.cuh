@@ -116,6 +116,14 @@ void launch_depth_keys(int P, const float* depths, const int* radii, uint32_t* d
 void launch_duplicate_sorted(int P, const uint32_t* order, const float2* means2D, const int* radii,
                              const uint64_t* offsets, const CamParams& cam, uint32_t* tile_ids,
                              uint32_t* values, uint64_t cap, cudaStream_t s);
+// Dense (tile-major) binning: per-tile lists built directly from the
+// depth-ordered Gaussians' tile rectangles (raster_sort.cu).
+size_t dense_diff_bytes(int tiles_x, int tiles_y);
+bool dense_binning_fits(int tiles_x, int tiles_y);
+void launch_dense_binning(int P, const uint32_t* order, const float2* means2D, const int* radii,
+                          const CamParams& cam, uint2* rects, int* diff, uint2* ranges,
+                          uint32_t* values, const unsigned long long* n_dev, cudaStream_t s);
+void launch_tiles_from_ranges(const uint2* ranges, int ntiles, uint32_t* tiles, cudaStream_t s);
 // order[ntiles]: tiles by descending list length (bucketed), for the blend kernels
 void launch_tile_order(const uint2* ranges, int ntiles, uint32_t* order, cudaStream_t s);
 // ranges[0, ntiles) of the sorted tile ids (every range written)

@@ -493,6 +493,176 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Dense binning (tile-major list construction) for scenes whose Gaussians
+// cover large tile rectangles (the high-contention C4 scene: ~4,500 tiles per
+// Gaussian, 0.9 G instances). Instead of duplicating every instance and
+// radix-sorting 0.9 G keys, each tile's list is built directly: the tile's
+// warp scans the Gaussians' packed rectangles in depth order and appends the
+// ones containing it (ballot compaction keeps the order), at an offset from
+// per-tile counts obtained with a 2D difference array. Output is identical
+// to the sort path -- per tile, Gaussians in (depth, index) order -- and costs
+// ~P x tiles / 32 rectangle tests instead of ~I log-passes; raster.cu picks it
+// when P x tiles <= 4 I.
+//
+// Packed rectangle (bytes): x0 | y0 << 8 | (x1-1) << 16 | (y1-1) << 24, so
+// "tile (tx, ty) inside" is one bytewise compare (x0, y0, tx, ty) <=
+// (tx, ty, x1-1, y1-1); an empty rectangle packs as x0 = 255, x1-1 = 0.
+constexpr uint32_t kEmptyRect = 0x000000ffu;
+
+__global__ void __launch_bounds__(256)
+    k_dense_rects(int P, const uint32_t* __restrict__ order, const float2* __restrict__ means2D,
+                  const int* __restrict__ radii, int tiles_x, int tiles_y,
+                  uint2* __restrict__ rects, int* __restrict__ diff) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
+  extern __shared__ int s_diff[];  // (tiles_y + 1) x (tiles_x + 1) corner counts
+  const int W1 = tiles_x + 1, cells = W1 * (tiles_y + 1);
+  for (int c = threadIdx.x; c < cells; c += blockDim.x) s_diff[c] = 0;
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
+    const uint32_t gid = order[i];
+    uint32_t packed = kEmptyRect;
+    const int rad = radii[gid];
+    if (rad > 0) {
+      int r[4];
+      rect_of(means2D[gid], rad, tiles_x, tiles_y, r);
+      if (r[2] > r[0] && r[3] > r[1]) {
+        packed = (uint32_t)r[0] | (uint32_t)r[1] << 8 | (uint32_t)(r[2] - 1) << 16 |
+                 (uint32_t)(r[3] - 1) << 24;
+        atomicAdd(&s_diff[r[1] * W1 + r[0]], 1);
+        atomicAdd(&s_diff[r[1] * W1 + r[2]], -1);
+        atomicAdd(&s_diff[r[3] * W1 + r[0]], -1);
+        atomicAdd(&s_diff[r[3] * W1 + r[2]], 1);
+      }
+    }
+    rects[i] = make_uint2(packed, gid);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < cells; c += blockDim.x)
+    if (s_diff[c]) atomicAdd(&diff[c], s_diff[c]);
+}
+
+// One block: 2D prefix sums of the corner counts -> per-tile counts ->
+// exclusive scan in tile order -> ranges ((0, 0) for empty tiles, as the
+// sort path and the reference layout have it). With a live-count bound
+// (n_dev, no-sync forward) an over-capacity frame renders empty.
+__global__ void __launch_bounds__(1024)
+    k_dense_ranges(const int* __restrict__ diff, int tiles_x, int tiles_y,
+                   uint2* __restrict__ ranges, const unsigned long long* __restrict__ n_dev) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
+  extern __shared__ int s_cnt2[];  // (tiles_y + 1) x (tiles_x + 1)
+  __shared__ uint32_t s_wsum[32];
+  __shared__ unsigned long long s_total;
+  const int W1 = tiles_x + 1, cells = W1 * (tiles_y + 1), t = threadIdx.x;
+  for (int c = t; c < cells; c += 1024) s_cnt2[c] = diff[c];
+  __syncthreads();
+  for (int y = t; y <= tiles_y; y += 1024) {  // prefix along x
+    int run = 0;
+    for (int x = 0; x <= tiles_x; ++x) {
+      run += s_cnt2[y * W1 + x];
+      s_cnt2[y * W1 + x] = run;
+    }
+  }
+  __syncthreads();
+  for (int x = t; x <= tiles_x; x += 1024) {  // prefix along y
+    int run = 0;
+    for (int y = 0; y <= tiles_y; ++y) {
+      run += s_cnt2[y * W1 + x];
+      s_cnt2[y * W1 + x] = run;
+    }
+  }
+  __syncthreads();
+  // tile (x, y) count = s_cnt2[y][x]; exclusive scan in tile order, 1024 x k
+  const int ntiles = tiles_x * tiles_y;
+  const int per = (ntiles + 1023) / 1024;
+  const int lane = t & 31, w = t >> 5;
+  uint32_t local = 0;
+  for (int k = 0; k < per; ++k) {
+    const int tile = t * per + k;
+    if (tile < ntiles) local += (uint32_t)s_cnt2[(tile / tiles_x) * W1 + tile % tiles_x];
+  }
+  uint32_t incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_wsum[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t v = s_wsum[lane], vi = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, vi, o);
+      if (lane >= o) vi += y;
+    }
+    s_wsum[lane] = vi - v;
+    if (lane == 31) s_total = vi;
+  }
+  __syncthreads();
+  const bool over = n_dev && *n_dev < s_total;
+  uint32_t run = s_wsum[w] + incl - local;
+  for (int k = 0; k < per; ++k) {
+    const int tile = t * per + k;
+    if (tile >= ntiles) break;
+    const uint32_t c = (uint32_t)s_cnt2[(tile / tiles_x) * W1 + tile % tiles_x];
+    ranges[tile] = (c == 0 || over) ? make_uint2(0u, 0u) : make_uint2(run, run + c);
+    run += c;
+  }
+}
+
+// Blocks of 8 warps = 8 consecutive tiles; Gaussian rectangles staged in
+// shared memory 1,024 at a time and tested by every warp against its tile.
+__global__ void __launch_bounds__(256)
+    k_dense_fill(int P, const uint2* __restrict__ rects, const uint2* __restrict__ ranges,
+                 int tiles_x, int ntiles, uint32_t* __restrict__ values) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
+  __shared__ uint2 s_r[1024];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tile = blockIdx.x * 8 + w;
+  const bool live = tile < ntiles;
+  const uint2 rg = live ? ranges[tile] : make_uint2(0u, 0u);
+  const bool work = __syncthreads_or(rg.y > rg.x);
+  if (!work) return;
+  const uint32_t tx = live ? (uint32_t)(tile % tiles_x) : 255u;
+  const uint32_t ty = live ? (uint32_t)(tile / tiles_x) : 255u;
+  const uint32_t T = tx | ty << 8 | tx << 16 | ty << 24;
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t pos = rg.x;
+  const bool mine = rg.y > rg.x;
+  for (int c0 = 0; c0 < P; c0 += 1024) {
+    const int nc = min(1024, P - c0);
+    __syncthreads();
+    for (int k = threadIdx.x; k < nc; k += 256) s_r[k] = rects[c0 + k];
+    __syncthreads();
+    if (!mine) continue;
+    for (int j = 0; j < nc; j += 32) {
+      const int k = j + lane;
+      const uint2 r = k < nc ? s_r[k] : make_uint2(kEmptyRect, 0u);
+      const uint32_t lo = (r.x & 0x0000ffffu) | (T & 0xffff0000u);
+      const uint32_t hi = (T & 0x0000ffffu) | (r.x & 0xffff0000u);
+      const bool in = __vcmpleu4(lo, hi) == 0xffffffffu;
+      const unsigned b = __ballot_sync(kFull, in);
+      if (in) values[pos + __popc(b & lt)] = r.y;
+      pos += __popc(b);
+    }
+  }
+}
+
+// Tile id of every list position (debug key materialisation after dense
+// binning, which writes no tile-id array): one warp per tile.
+__global__ void k_tiles_from_ranges(const uint2* __restrict__ ranges, int ntiles,
+                                    uint32_t* __restrict__ tiles) {
+  const int lane = threadIdx.x & 31;
+  const int tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (tile >= ntiles) return;
+  const uint2 r = ranges[tile];
+  for (uint32_t i = r.x + lane; i < r.y; i += 32) tiles[i] = (uint32_t)tile;
+}
+
 // No-host-sync sizing: the live instance count is the scan total when it fits
 // the reserved capacity, else 0 (the frame renders empty) and the overflow
 // flag is raised for the host to read later.
@@ -744,6 +914,45 @@ void launch_make_keys(int64_t L, const uint32_t* tiles, const uint32_t* values, 
 void launch_tile_order(const uint2* ranges, int ntiles, uint32_t* order, cudaStream_t s) {
   if (ntiles <= 0) return;
   launch_pdl(k_tile_order, 1, 1024, 0, s, ranges, ntiles, order);
+  DW_CUDA(cudaGetLastError());
+}
+
+size_t dense_diff_bytes(int tiles_x, int tiles_y) {
+  return static_cast<size_t>(tiles_x + 1) * (tiles_y + 1) * sizeof(int);
+}
+
+bool dense_binning_fits(int tiles_x, int tiles_y) {
+  return tiles_x <= 255 && tiles_y <= 255 && dense_diff_bytes(tiles_x, tiles_y) <= 96 * 1024;
+}
+
+void launch_dense_binning(int P, const uint32_t* order, const float2* means2D, const int* radii,
+                          const CamParams& cam, uint2* rects, int* diff, uint2* ranges,
+                          uint32_t* values, const unsigned long long* n_dev, cudaStream_t s) {
+  const size_t dbytes = dense_diff_bytes(cam.tiles_x, cam.tiles_y);
+  const int ntiles = cam.tiles_x * cam.tiles_y;
+  static bool attr_set = false;  // > 48 KB dynamic smem for 4K-class grids
+  if (!attr_set) {
+    DW_CUDA(cudaFuncSetAttribute(k_dense_rects, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 96 * 1024));
+    DW_CUDA(cudaFuncSetAttribute(k_dense_ranges, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 96 * 1024));
+    attr_set = true;
+  }
+  DW_CUDA(cudaMemsetAsync(diff, 0, dbytes, s));
+  if (P > 0)
+    launch_pdl(k_dense_rects, std::min<unsigned>(blocks_for(P, 256), 148 * 2), 256, dbytes, s, P,
+               order, means2D, radii, cam.tiles_x, cam.tiles_y, rects, diff);
+  launch_pdl(k_dense_ranges, 1, 1024, dbytes, s, diff, cam.tiles_x, cam.tiles_y, ranges, n_dev);
+  if (P > 0)
+    launch_pdl(k_dense_fill, blocks_for(ntiles, 8), 256, 0, s, P, rects, ranges, cam.tiles_x,
+               ntiles, values);
+  DW_CUDA(cudaGetLastError());
+}
+
+void launch_tiles_from_ranges(const uint2* ranges, int ntiles, uint32_t* tiles, cudaStream_t s) {
+  if (ntiles <= 0) return;
+  k_tiles_from_ranges<<<blocks_for(static_cast<int64_t>(ntiles) * 32, 256), 256, 0, s>>>(
+      ranges, ntiles, tiles);
   DW_CUDA(cudaGetLastError());
 }
 

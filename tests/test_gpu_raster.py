@@ -69,8 +69,17 @@ def cases(orc):
     return out
 
 
+@pytest.fixture(params=["auto", "sort", "dense"])
+def binning(request, monkeypatch):
+    """Both list constructions -- duplicate + radix sort, and dense
+    (tile-major) binning -- must give the oracle's lists bit for bit."""
+    if request.param != "auto":
+        monkeypatch.setenv("DW_DENSE_BINNING", "1" if request.param == "dense" else "0")
+    return request.param
+
+
 @pytest.mark.parametrize("name", [c[0] for c in CASES])
-def test_forward_bit_exact_binning_and_image(cuda, cases, name):
+def test_forward_bit_exact_binning_and_image(cuda, cases, name, binning):
     from paper_2401_05345_b200 import warpred as wr
 
     sc, cam, dL, ref = cases[name]
