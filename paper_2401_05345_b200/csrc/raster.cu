@@ -69,7 +69,7 @@ struct dw_rasterizer {
   uint32_t* tile_order = nullptr;  // tiles, longest list first (the backward's CTA order)
   bool dense = false;              // last forward used dense (tile-major) binning
   uint2* rects = nullptr;          // dense binning: packed tile rectangle + id, depth order
-  int* diff = nullptr;             // dense binning: 2D difference grid of the rectangles
+  int* diff = nullptr;             // dense binning: per-segment difference grids + offsets
   size_t cap_r = 0, cap_diff = 0;
   float* final_T = nullptr;
   uint32_t* n_contrib = nullptr;
@@ -277,9 +277,9 @@ struct dw_rasterizer {
                          : static_cast<double>(P) * ntiles <= 4.0 * static_cast<double>(n_grid));
     if (dense) {
       grow(rects, cap_r, static_cast<size_t>(P));
-      grow(diff, cap_diff, dw::dense_diff_bytes(cam.tiles_x, cam.tiles_y) / sizeof(int));
+      grow(diff, cap_diff, dw::dense_scratch_words(cam.tiles_x, cam.tiles_y));
       dw::launch_dense_binning(P, order, means2D, radii, cam, rects, diff, ranges, ivals[0],
-                               n_dev, s);
+                               n_dev, static_cast<uint64_t>(n_grid), s);
     } else if (n_grid > 0) {
       // 2. duplicate in depth order, 3. stable sort by tile id
       dw::launch_duplicate_sorted(P, order, means2D, radii, offsets, cam, itile[0], ivals[0],

@@ -119,10 +119,13 @@ void launch_duplicate_sorted(int P, const uint32_t* order, const float2* means2D
 // Dense (tile-major) binning: per-tile lists built directly from the
 // depth-ordered Gaussians' tile rectangles (raster_sort.cu).
 size_t dense_diff_bytes(int tiles_x, int tiles_y);
+size_t dense_scratch_words(int tiles_x, int tiles_y);
 bool dense_binning_fits(int tiles_x, int tiles_y);
+// n_dev (nullable): live instance count; with it, a count above cap renders empty
 void launch_dense_binning(int P, const uint32_t* order, const float2* means2D, const int* radii,
-                          const CamParams& cam, uint2* rects, int* diff, uint2* ranges,
-                          uint32_t* values, const unsigned long long* n_dev, cudaStream_t s);
+                          const CamParams& cam, uint2* rects, int* scratch, uint2* ranges,
+                          uint32_t* values, const unsigned long long* n_dev, uint64_t cap,
+                          cudaStream_t s);
 void launch_tiles_from_ranges(const uint2* ranges, int ntiles, uint32_t* tiles, cudaStream_t s);
 // order[ntiles]: tiles by descending list length (bucketed), for the blend kernels
 void launch_tile_order(const uint2* ranges, int ntiles, uint32_t* order, cudaStream_t s);

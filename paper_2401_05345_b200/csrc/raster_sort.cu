@@ -497,18 +497,23 @@ __global__ void __launch_bounds__(256)
 // Dense binning (tile-major list construction) for scenes whose Gaussians
 // cover large tile rectangles (the high-contention C4 scene: ~4,500 tiles per
 // Gaussian, 0.9 G instances). Instead of duplicating every instance and
-// radix-sorting 0.9 G keys, each tile's list is built directly: the tile's
-// warp scans the Gaussians' packed rectangles in depth order and appends the
-// ones containing it (ballot compaction keeps the order), at an offset from
-// per-tile counts obtained with a 2D difference array. Output is identical
-// to the sort path -- per tile, Gaussians in (depth, index) order -- and costs
-// ~P x tiles / 32 rectangle tests instead of ~I log-passes; raster.cu picks it
-// when P x tiles <= 4 I.
+// radix-sorting 0.9 G keys, each tile's list is built directly:
+//   1. k_dense_rects: the depth-ordered Gaussians' tile rectangles, packed,
+//      plus per SEGMENT of the depth order (kDenseSeg segments) a 2D
+//      difference grid of the rectangles (4 shared atomics per Gaussian);
+//   2. k_dense_ranges: 2D prefix sums -> per (segment, tile) counts -> tile
+//      ranges and each segment's write offset inside each tile's list;
+//   3. k_dense_fill: a warp owns (segment, 8 consecutive tiles of a row),
+//      turns each rectangle into an 8-bit mask of its tiles and appends the
+//      Gaussian to each tile by ballot compaction (order preserved).
+// Output is identical to the sort path -- per tile, Gaussians in (depth,
+// index) order -- for ~P x tiles / 256 warp steps instead of duplicating and
+// sorting I instances; raster.cu picks it when P x tiles <= 4 I.
 //
-// Packed rectangle (bytes): x0 | y0 << 8 | (x1-1) << 16 | (y1-1) << 24, so
-// "tile (tx, ty) inside" is one bytewise compare (x0, y0, tx, ty) <=
-// (tx, ty, x1-1, y1-1); an empty rectangle packs as x0 = 255, x1-1 = 0.
-constexpr uint32_t kEmptyRect = 0x000000ffu;
+// Packed rectangle: x0 | y0 << 8 | (x1-1) << 16 | (y1-1) << 24 (tile units
+// < 256); an empty rectangle packs as y0 = 255 > y1-1 = 0.
+constexpr uint32_t kEmptyRect = 0x0000ff00u;
+constexpr int kDenseSeg = 16;
 
 __global__ void __launch_bounds__(256)
     k_dense_rects(int P, const uint32_t* __restrict__ order, const float2* __restrict__ means2D,
@@ -518,9 +523,14 @@ __global__ void __launch_bounds__(256)
   pdl_trigger();
   extern __shared__ int s_diff[];  // (tiles_y + 1) x (tiles_x + 1) corner counts
   const int W1 = tiles_x + 1, cells = W1 * (tiles_y + 1);
+  const int per_seg = gridDim.x / kDenseSeg;  // blocks per segment
+  const int seg = blockIdx.x / per_seg, sub = blockIdx.x % per_seg;
+  const int64_t lo = static_cast<int64_t>(P) * seg / kDenseSeg;
+  const int64_t hi = static_cast<int64_t>(P) * (seg + 1) / kDenseSeg;
   for (int c = threadIdx.x; c < cells; c += blockDim.x) s_diff[c] = 0;
   __syncthreads();
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
+  for (int64_t i = lo + static_cast<int64_t>(sub) * blockDim.x + threadIdx.x; i < hi;
+       i += static_cast<int64_t>(per_seg) * blockDim.x) {
     const uint32_t gid = order[i];
     uint32_t packed = kEmptyRect;
     const int rad = radii[gid];
@@ -539,49 +549,59 @@ __global__ void __launch_bounds__(256)
     rects[i] = make_uint2(packed, gid);
   }
   __syncthreads();
+  int* d = diff + static_cast<int64_t>(seg) * cells;
+  int* dt = diff + static_cast<int64_t>(kDenseSeg) * cells;  // all segments
   for (int c = threadIdx.x; c < cells; c += blockDim.x)
-    if (s_diff[c]) atomicAdd(&diff[c], s_diff[c]);
+    if (s_diff[c]) {
+      atomicAdd(&d[c], s_diff[c]);
+      atomicAdd(&dt[c], s_diff[c]);
+    }
 }
 
-// One block: 2D prefix sums of the corner counts -> per-tile counts ->
-// exclusive scan in tile order -> ranges ((0, 0) for empty tiles, as the
-// sort path and the reference layout have it). With a live-count bound
-// (n_dev, no-sync forward) an over-capacity frame renders empty.
+// One block per segment and one for all of them: diff[g][cells] -> in place 2D
+// inclusive prefix sums in shared memory (the count of the segment's
+// rectangles containing each tile; g = kDenseSeg: all segments).
 __global__ void __launch_bounds__(1024)
-    k_dense_ranges(const int* __restrict__ diff, int tiles_x, int tiles_y,
+    k_dense_prefix2d(int* __restrict__ diff, int tiles_x, int tiles_y) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
+  extern __shared__ int s_g[];
+  const int W1 = tiles_x + 1, H1 = tiles_y + 1, cells = W1 * H1, t = threadIdx.x;
+  int* g = diff + static_cast<int64_t>(blockIdx.x) * cells;
+  for (int c = t; c < cells; c += 1024) s_g[c] = g[c];
+  __syncthreads();
+  for (int y = t; y < H1; y += 1024) {
+    int run = 0;
+    for (int x = 0; x < W1; ++x) s_g[y * W1 + x] = run += s_g[y * W1 + x];
+  }
+  __syncthreads();
+  for (int x = t; x < W1; x += 1024) {
+    int run = 0;
+    for (int y = 0; y < H1; ++y) s_g[y * W1 + x] = run += s_g[y * W1 + x];
+  }
+  __syncthreads();
+  for (int c = t; c < cells; c += 1024) g[c] = s_g[c];
+}
+
+// One block: tile ranges from the all-segment counts ((0, 0) when empty, the
+// reference layout). With a live-count bound (n_dev, no-sync forward) an
+// over-capacity frame renders empty.
+__global__ void __launch_bounds__(1024)
+    k_dense_ranges(const int* __restrict__ counts, int tiles_x, int tiles_y,
                    uint2* __restrict__ ranges, const unsigned long long* __restrict__ n_dev) {
   pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
-  extern __shared__ int s_cnt2[];  // (tiles_y + 1) x (tiles_x + 1)
   __shared__ uint32_t s_wsum[32];
   __shared__ unsigned long long s_total;
   const int W1 = tiles_x + 1, cells = W1 * (tiles_y + 1), t = threadIdx.x;
-  for (int c = t; c < cells; c += 1024) s_cnt2[c] = diff[c];
-  __syncthreads();
-  for (int y = t; y <= tiles_y; y += 1024) {  // prefix along x
-    int run = 0;
-    for (int x = 0; x <= tiles_x; ++x) {
-      run += s_cnt2[y * W1 + x];
-      s_cnt2[y * W1 + x] = run;
-    }
-  }
-  __syncthreads();
-  for (int x = t; x <= tiles_x; x += 1024) {  // prefix along y
-    int run = 0;
-    for (int y = 0; y <= tiles_y; ++y) {
-      run += s_cnt2[y * W1 + x];
-      s_cnt2[y * W1 + x] = run;
-    }
-  }
-  __syncthreads();
-  // tile (x, y) count = s_cnt2[y][x]; exclusive scan in tile order, 1024 x k
   const int ntiles = tiles_x * tiles_y;
+  const int* tot = counts + static_cast<int64_t>(kDenseSeg) * cells;
   const int per = (ntiles + 1023) / 1024;
   const int lane = t & 31, w = t >> 5;
   uint32_t local = 0;
   for (int k = 0; k < per; ++k) {
     const int tile = t * per + k;
-    if (tile < ntiles) local += (uint32_t)s_cnt2[(tile / tiles_x) * W1 + tile % tiles_x];
+    if (tile < ntiles) local += (uint32_t)tot[(tile / tiles_x) * W1 + tile % tiles_x];
   }
   uint32_t incl = local;
 #pragma unroll
@@ -592,7 +612,8 @@ __global__ void __launch_bounds__(1024)
   if (lane == 31) s_wsum[w] = incl;
   __syncthreads();
   if (w == 0) {
-    uint32_t v = s_wsum[lane], vi = v;
+    const uint32_t v = s_wsum[lane];
+    uint32_t vi = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(kFull, vi, o);
@@ -607,47 +628,75 @@ __global__ void __launch_bounds__(1024)
   for (int k = 0; k < per; ++k) {
     const int tile = t * per + k;
     if (tile >= ntiles) break;
-    const uint32_t c = (uint32_t)s_cnt2[(tile / tiles_x) * W1 + tile % tiles_x];
+    const uint32_t c = (uint32_t)tot[(tile / tiles_x) * W1 + tile % tiles_x];
     ranges[tile] = (c == 0 || over) ? make_uint2(0u, 0u) : make_uint2(run, run + c);
     run += c;
   }
 }
 
-// Blocks of 8 warps = 8 consecutive tiles; Gaussian rectangles staged in
-// shared memory 1,024 at a time and tested by every warp against its tile.
-__global__ void __launch_bounds__(256)
-    k_dense_fill(int P, const uint2* __restrict__ rects, const uint2* __restrict__ ranges,
-                 int tiles_x, int ntiles, uint32_t* __restrict__ values) {
+// Block = one depth-order segment x 8 warps; warp = 8 consecutive tiles of a
+// row. The segment's rectangles are staged 1,024 at a time; each lane turns
+// one rectangle into the 8-bit mask of the warp's tiles it covers and the warp
+// appends it to each of those tiles' lists by ballot compaction.
+__global__ void __launch_bounds__(256, 4)
+    k_dense_fill(int P, const uint2* __restrict__ rects, const int* __restrict__ counts,
+                 const uint2* __restrict__ ranges, int tiles_x, int tiles_y, int groups_x,
+                 uint32_t* __restrict__ values,
+                 const unsigned long long* __restrict__ n_dev, uint64_t total_cap) {
   pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
   __shared__ uint2 s_r[1024];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int tile = blockIdx.x * 8 + w;
-  const bool live = tile < ntiles;
-  const uint2 rg = live ? ranges[tile] : make_uint2(0u, 0u);
-  const bool work = __syncthreads_or(rg.y > rg.x);
-  if (!work) return;
-  const uint32_t tx = live ? (uint32_t)(tile % tiles_x) : 255u;
-  const uint32_t ty = live ? (uint32_t)(tile / tiles_x) : 255u;
-  const uint32_t T = tx | ty << 8 | tx << 16 | ty << 24;
+  const int ngroups = groups_x * tiles_y;
+  const int blocks_per_seg = (ngroups + 7) / 8;
+  const int seg = blockIdx.x / blocks_per_seg;
+  const int grp = (blockIdx.x % blocks_per_seg) * 8 + w;
+  const int ntiles = tiles_x * tiles_y;
+  // No-sync forward: the clamped live count is 0 when the instances exceed the
+  // reserve (the frame renders empty) -- and when there are none to write.
+  if (n_dev && *n_dev == 0ull) return;
+  (void)total_cap;
+  const int ty = grp / groups_x, tx0 = (grp % groups_x) * 8;
+  const bool live = grp < ngroups;
+  // where this segment starts in each of the warp's 8 tile lists: the tile's
+  // range start plus the earlier segments' counts (lanes 0-7, one tile each)
+  uint32_t off = 0;
+  if (live && lane < 8 && tx0 + lane < tiles_x) {
+    const int W1 = tiles_x + 1, cells = W1 * (tiles_y + 1);
+    const int cell = ty * W1 + tx0 + lane;
+    off = ranges[ty * tiles_x + tx0 + lane].x;
+    for (int sg = 0; sg < seg; ++sg) off += (uint32_t)counts[static_cast<int64_t>(sg) * cells + cell];
+  }
+  uint32_t* dst[8];  // next write position in each of the warp's 8 tile lists
+#pragma unroll
+  for (int k = 0; k < 8; ++k) dst[k] = values + __shfl_sync(kFull, off, k);
+  (void)ntiles;
+  const int64_t lo = static_cast<int64_t>(P) * seg / kDenseSeg;
+  const int64_t hi = static_cast<int64_t>(P) * (seg + 1) / kDenseSeg;
   const uint32_t lt = (1u << lane) - 1u;
-  uint32_t pos = rg.x;
-  const bool mine = rg.y > rg.x;
-  for (int c0 = 0; c0 < P; c0 += 1024) {
-    const int nc = min(1024, P - c0);
+  const uint32_t last = static_cast<uint32_t>(min(tiles_x - 1 - tx0, 7));  // last tile offset
+  for (int64_t c0 = lo; c0 < hi; c0 += 1024) {
+    const int nc = static_cast<int>(hi - c0 < 1024 ? hi - c0 : 1024);
     __syncthreads();
     for (int k = threadIdx.x; k < nc; k += 256) s_r[k] = rects[c0 + k];
     __syncthreads();
-    if (!mine) continue;
+    if (!live) continue;
     for (int j = 0; j < nc; j += 32) {
       const int k = j + lane;
       const uint2 r = k < nc ? s_r[k] : make_uint2(kEmptyRect, 0u);
-      const uint32_t lo = (r.x & 0x0000ffffu) | (T & 0xffff0000u);
-      const uint32_t hi = (T & 0x0000ffffu) | (r.x & 0xffff0000u);
-      const bool in = __vcmpleu4(lo, hi) == 0xffffffffu;
-      const unsigned b = __ballot_sync(kFull, in);
-      if (in) values[pos + __popc(b & lt)] = r.y;
-      pos += __popc(b);
+      const int x0 = (int)(r.x & 0xffu) - tx0, y0 = (int)((r.x >> 8) & 0xffu);
+      const int x1 = (int)((r.x >> 16) & 0xffu) - tx0, y1 = (int)(r.x >> 24);
+      const int a = max(x0, 0), b = min(x1, (int)last);
+      uint32_t m = 0;
+      if (y0 <= ty && ty <= y1 && a <= b) m = (0xffu >> (7 - b)) & (0xffu << a);
+      if (__ballot_sync(kFull, m != 0u) == 0u) continue;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const bool in = (m >> q) & 1u;
+        const unsigned bq = __ballot_sync(kFull, in);
+        if (in) dst[q][__popc(bq & lt)] = r.y;
+        dst[q] += __popc(bq);
+      }
     }
   }
 }
@@ -921,32 +970,41 @@ size_t dense_diff_bytes(int tiles_x, int tiles_y) {
   return static_cast<size_t>(tiles_x + 1) * (tiles_y + 1) * sizeof(int);
 }
 
+size_t dense_scratch_words(int tiles_x, int tiles_y) {  // per-segment + total count grids
+  return static_cast<size_t>(kDenseSeg + 1) * (tiles_x + 1) * (tiles_y + 1);
+}
+
 bool dense_binning_fits(int tiles_x, int tiles_y) {
   return tiles_x <= 255 && tiles_y <= 255 && dense_diff_bytes(tiles_x, tiles_y) <= 96 * 1024;
 }
 
 void launch_dense_binning(int P, const uint32_t* order, const float2* means2D, const int* radii,
-                          const CamParams& cam, uint2* rects, int* diff, uint2* ranges,
-                          uint32_t* values, const unsigned long long* n_dev, cudaStream_t s) {
+                          const CamParams& cam, uint2* rects, int* scratch, uint2* ranges,
+                          uint32_t* values, const unsigned long long* n_dev, uint64_t cap,
+                          cudaStream_t s) {
   const size_t dbytes = dense_diff_bytes(cam.tiles_x, cam.tiles_y);
   const int ntiles = cam.tiles_x * cam.tiles_y;
+  int* diff = scratch;  // kDenseSeg + 1 grids
   static bool attr_set = false;  // > 48 KB dynamic smem for 4K-class grids
   if (!attr_set) {
     DW_CUDA(cudaFuncSetAttribute(k_dense_rects, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  96 * 1024));
-    DW_CUDA(cudaFuncSetAttribute(k_dense_ranges, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    DW_CUDA(cudaFuncSetAttribute(k_dense_prefix2d, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  96 * 1024));
     attr_set = true;
   }
-  DW_CUDA(cudaMemsetAsync(diff, 0, dbytes, s));
-  if (P > 0)
-    launch_pdl(k_dense_rects, std::min<unsigned>(blocks_for(P, 256), 148 * 2), 256, dbytes, s, P,
-               order, means2D, radii, cam.tiles_x, cam.tiles_y, rects, diff);
-  launch_pdl(k_dense_ranges, 1, 1024, dbytes, s, diff, cam.tiles_x, cam.tiles_y, ranges, n_dev);
-  if (P > 0)
-    launch_pdl(k_dense_fill, blocks_for(ntiles, 8), 256, 0, s, P, rects, ranges, cam.tiles_x,
-               ntiles, values);
+  DW_CUDA(cudaMemsetAsync(diff, 0, (kDenseSeg + 1) * dbytes, s));
+  const int per_seg = std::max(1, std::min<int>(static_cast<int>(blocks_for(P, 256 * kDenseSeg)), 16));
+  launch_pdl(k_dense_rects, kDenseSeg * per_seg, 256, dbytes, s, P, order, means2D, radii,
+             cam.tiles_x, cam.tiles_y, rects, diff);
+  launch_pdl(k_dense_prefix2d, kDenseSeg + 1, 1024, dbytes, s, diff, cam.tiles_x, cam.tiles_y);
+  launch_pdl(k_dense_ranges, 1, 1024, 0, s, diff, cam.tiles_x, cam.tiles_y, ranges, n_dev);
+  const int groups_x = (cam.tiles_x + 7) / 8;
+  const int blocks_per_seg = (groups_x * cam.tiles_y + 7) / 8;
+  launch_pdl(k_dense_fill, kDenseSeg * blocks_per_seg, 256, 0, s, P, rects, diff, ranges,
+             cam.tiles_x, cam.tiles_y, groups_x, values, n_dev, cap);
   DW_CUDA(cudaGetLastError());
+  (void)ntiles;
 }
 
 void launch_tiles_from_ranges(const uint2* ranges, int ntiles, uint32_t* tiles, cudaStream_t s) {
