@@ -467,13 +467,41 @@ __global__ void __launch_bounds__(256)
   }
   if (area == 0) r[0] = r[1] = r[2] = r[3] = 0;
   const bool big = area > 32;
-  if (!big) {
-    for (int y = r[1]; y < r[3]; ++y)
-      for (int x = r[0]; x < r[2]; ++x) {
-        tile_ids[off] = static_cast<uint32_t>(y * tiles_x + x);
-        values[off] = gid;
-        ++off;
+  // Small rectangles, written by the whole warp: element e of the warp's
+  // small-rectangle instances belongs to the lane whose [excl, excl + area)
+  // holds it (5-step search over the lanes' exclusive scan), so consecutive
+  // lanes store consecutive list positions instead of 32 scattered streams.
+  {
+    const int sa = big ? 0 : area;
+    int incl = sa;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int excl = incl - sa;
+    const int total = __shfl_sync(kFull, incl, 31);
+    const int wdt = r[2] - r[0];
+    for (int e0 = 0; e0 < total; e0 += 32) {  // warp-uniform trips: shuffles need every lane
+      const int e = e0 + lane;
+      int owner = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int probe = owner + step;
+        if (__shfl_sync(kFull, excl, probe) <= e) owner = probe;  // probe <= 31
       }
+      // lanes of the same owner are contiguous; the shuffles below are per lane
+      const int k = e - __shfl_sync(kFull, excl, owner);
+      const int w = __shfl_sync(kFull, wdt, owner);
+      const int x0 = __shfl_sync(kFull, r[0], owner), y0 = __shfl_sync(kFull, r[1], owner);
+      const uint64_t o = __shfl_sync(kFull, off, owner);
+      const uint32_t g = __shfl_sync(kFull, gid, owner);
+      if (e < total) {
+        const int row = static_cast<int>((static_cast<float>(k) + 0.5f) / static_cast<float>(w));
+        tile_ids[o + k] = static_cast<uint32_t>((y0 + row) * tiles_x + x0 + (k - row * w));
+        values[o + k] = g;
+      }
+    }
   }
   unsigned todo = __ballot_sync(kFull, big);
   while (todo) {
