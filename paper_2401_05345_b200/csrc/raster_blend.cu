@@ -334,9 +334,10 @@ __device__ __forceinline__ void eval2(const float4& g, const float4& co, float p
   e.G = make_float2(ex2_approx(pl.x), ex2_approx(pl.y));
 }
 
-// The forward keeps synchronous staging: its tiles often terminate early
-// (opaque pixels), so a prefetched batch is frequently wasted -- A/B on C3:
-// 0.833 ms (this) vs 0.869 ms with the backward's cp.async double buffer.
+// The forward keeps synchronous staging: with the backward's cp.async double
+// buffer it is slower on C3 (0.869 vs 0.833 ms: early-terminating tiles waste
+// the prefetched batch) and on C4 too (3.49 vs 3.29 ms: the doubled shared
+// memory costs occupancy the latency hiding does not repay).
 __global__ void __launch_bounds__(128)
     k_forward_x2(const CamParams cam, const uint2* __restrict__ ranges,
                  const uint32_t* __restrict__ values, const float2* __restrict__ means2D,
