@@ -67,6 +67,8 @@ struct dw_rasterizer {
   size_t cap_t = 0, cap_px = 0, cap_px2 = 0, cap_to = 0;
   uint2* ranges = nullptr;
   uint32_t* tile_order = nullptr;  // tiles, longest list first (the backward's CTA order)
+  uint32_t* area_sorted = nullptr; // tiles_touched in depth order (the offsets scan's input)
+  size_t cap_as = 0;
   bool dense = false;              // last forward used dense (tile-major) binning
   uint2* rects = nullptr;          // dense binning: packed tile rectangle + id, depth order
   int* diff = nullptr;             // dense binning: per-segment difference grids + offsets
@@ -101,7 +103,7 @@ struct dw_rasterizer {
     void* ps[] = {means2D, depths, radii, conic_opacity, rgb, tiles_touched, offsets, dkey[0],
                   dkey[1], dids[0], dids[1], itile[0], itile[1], ivals[0], ivals[1], ranges,
                   final_T, n_contrib, tmp, scan_tmp, keys_dbg, counters, live_dev, overflow_dev,
-                  tile_order, rects, diff};
+                  tile_order, rects, diff, area_sorted};
     for (void* p : ps)
       if (p) cudaFree(p);
     for (float* p : h_bufs)
@@ -151,6 +153,7 @@ struct dw_rasterizer {
       grow(dkey[b], cap_d[b], np);
       grow(dids[b], cap_d[2 + b], np);
     }
+    grow(area_sorted, cap_as, np);
     grow(scan_tmp, cap_scan, dw::scan_temp_bytes(P_));
     grow(ranges, cap_t, ntiles);
     grow(tile_order, cap_to, ntiles);
@@ -227,6 +230,7 @@ struct dw_rasterizer {
       grow(dkey[b], cap_d[b], np);
       grow(dids[b], cap_d[2 + b], np);
     }
+    grow(area_sorted, cap_as, np);
     grow(scan_tmp, cap_scan, dw::scan_temp_bytes(P));
 
     dw::launch_preprocess(P, means3D, scales, rotations, opacities, colors, cam, means2D, depths,
@@ -242,9 +246,11 @@ struct dw_rasterizer {
       // 1. Gaussians in (depth, id) order: stable 32-bit LSD sort
       dw::launch_depth_keys(P, depths, radii, dkey[0], dids[0], s);
       ensure_tmp(dw::radix_sort_temp_bytes(P));
-      order = dids[dw::radix_sort_pairs(dkey, dids, P, 32, tmp, s)];
-      // instance offsets in that order
-      dw::inclusive_scan_gather(tiles_touched, order, P, offsets, scan_tmp, s);
+      // (its last pass also lays tiles_touched out in that order: area_sorted)
+      order = dids[dw::radix_sort_pairs(dkey, dids, P, 32, tmp, s, nullptr, tiles_touched,
+                                        area_sorted)];
+      // instance offsets in that order (a sequential scan, no gather)
+      dw::inclusive_scan_gather(area_sorted, nullptr, P, offsets, scan_tmp, s);
       if (nosync) {
         if (cap_i[0] == 0 || cap_i[2] == 0)
           throw std::invalid_argument("no-sync forward needs dw_rasterizer_reserve first");

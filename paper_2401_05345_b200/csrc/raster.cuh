@@ -107,8 +107,11 @@ size_t radix_sort_temp_bytes(int64_t n);
 size_t scan_temp_bytes(int64_t n);
 // n_dev (nullable): live element count read on the device (<= n, the
 // capacity the grids are sized for) -- the no-host-sync forward.
+// gather_src (nullable): the last pass also writes gather_out[i] =
+// gather_src[sorted value i] (a payload in sorted order, e.g. tiles touched).
 int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* temp,
-                     cudaStream_t s, const unsigned long long* n_dev = nullptr);
+                     cudaStream_t s, const unsigned long long* n_dev = nullptr,
+                     const uint32_t* gather_src = nullptr, uint32_t* gather_out = nullptr);
 void inclusive_scan_gather(const uint32_t* in, const uint32_t* order, int64_t n, uint64_t* out,
                            void* temp, cudaStream_t s);
 void launch_depth_keys(int P, const float* depths, const int* radii, uint32_t* dkey, uint32_t* ids,

@@ -218,7 +218,8 @@ __global__ void __launch_bounds__(kSortThreads)
                 int shift, uint32_t mask, int bits, const uint32_t* __restrict__ counts,
                 int64_t tiles, const uint32_t* __restrict__ digit_base,
                 uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
-                const unsigned long long* __restrict__ n_dev) {
+                const unsigned long long* __restrict__ n_dev,
+                const uint32_t* __restrict__ gather_src, uint32_t* __restrict__ gather_out) {
   pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
   constexpr int TILE = ITEMS * kSortThreads;
@@ -318,6 +319,7 @@ __global__ void __launch_bounds__(kSortThreads)
     const uint32_t g = s_gbase[d] + (static_cast<uint32_t>(i) - s_dstart[d]);
     keys_out[g] = kk;
     vals_out[g] = s_val[i];
+    if (gather_src) gather_out[g] = __ldg(gather_src + s_val[i]);  // sorted payload
   }
 }
 
@@ -870,11 +872,11 @@ template <int ITEMS>
 void launch_downsweep(int bits, unsigned grid, cudaStream_t s, const uint32_t* k, const uint32_t* v,
                       int64_t n, int shift, uint32_t mask, const uint32_t* counts, int64_t tiles,
                       const uint32_t* digit, uint32_t* ko, uint32_t* vo,
-                      const unsigned long long* n_dev) {
+                      const unsigned long long* n_dev, const uint32_t* gsrc, uint32_t* gout) {
 #define DW_DOWN(B)                                                                            \
   case B:                                                                                     \
     launch_pdl(k_downsweep<ITEMS, B>, grid, kSortThreads, 0, s, k, v, n, shift, mask, bits,  \
-               counts, tiles, digit, ko, vo, n_dev);                                          \
+               counts, tiles, digit, ko, vo, n_dev, gsrc, gout);                              \
     break;
   switch (bits) {
     DW_DOWN(1)
@@ -886,13 +888,14 @@ void launch_downsweep(int bits, unsigned grid, cudaStream_t s, const uint32_t* k
     DW_DOWN(7)
     default:
       launch_pdl(k_downsweep<ITEMS, 8>, grid, kSortThreads, 0, s, k, v, n, shift, mask, bits,
-                 counts, tiles, digit, ko, vo, n_dev);
+                 counts, tiles, digit, ko, vo, n_dev, gsrc, gout);
   }
 #undef DW_DOWN
 }
 
 int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* temp,
-                     cudaStream_t s, const unsigned long long* n_dev) {
+                     cudaStream_t s, const unsigned long long* n_dev, const uint32_t* gather_src,
+                     uint32_t* gather_out) {
   int cur = 0;
   if (n <= 0 || bits <= 0) return cur;
   const int items = sort_items(n);
@@ -904,6 +907,7 @@ int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* 
   for (int shift = 0; shift < bits; shift += 8) {
     const int b = bits - shift < 8 ? bits - shift : 8;
     const uint32_t mask = (1u << b) - 1u;
+    const bool last = shift + 8 >= bits;
     switch (items) {
       case 16:
         launch_pdl(k_upsweep<16>, grid, kSortThreads, 0, s, k[cur], n, shift, mask, b, counts,
@@ -922,15 +926,18 @@ int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* 
     switch (items) {
       case 16:
         launch_downsweep<16>(b, grid, s, k[cur], v[cur], n, shift, mask, counts, tiles, digit,
-                             k[cur ^ 1], v[cur ^ 1], n_dev);
+                             k[cur ^ 1], v[cur ^ 1], n_dev, last ? gather_src : nullptr,
+                             gather_out);
         break;
       case 8:
         launch_downsweep<8>(b, grid, s, k[cur], v[cur], n, shift, mask, counts, tiles, digit,
-                            k[cur ^ 1], v[cur ^ 1], n_dev);
+                            k[cur ^ 1], v[cur ^ 1], n_dev, last ? gather_src : nullptr,
+                            gather_out);
         break;
       default:
         launch_downsweep<4>(b, grid, s, k[cur], v[cur], n, shift, mask, counts, tiles, digit,
-                            k[cur ^ 1], v[cur ^ 1], n_dev);
+                            k[cur ^ 1], v[cur ^ 1], n_dev, last ? gather_src : nullptr,
+                            gather_out);
     }
     cur ^= 1;
   }
