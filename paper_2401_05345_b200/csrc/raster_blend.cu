@@ -42,6 +42,19 @@ struct __align__(16) Staged {
   float4 col;  // r, g, b, 1/opacity (preprocess)
 };
 
+// The staged conic is pre-scaled so the exponent of G = exp(-q/2) comes out
+// directly in log2 units: (a, b, c) -> (k a, 2 k b, k c), k = -log2(e)/2, and
+// log2 G = k a dx^2 + 2 k b dx dy + k c dy^2 = fma(2kb, dxy, fma(kc, dyy, ka dxx))
+// -- two fused multiply-adds where the unscaled form needs four operations
+// plus the log2(e) multiply. Every blend kernel evaluates exactly this
+// sequence (the packed backward stages the raw conic and forms the same scaled
+// coefficients itself), so forward and backward take identical alpha
+// decisions.
+constexpr float kConicScale = -0.5f * 1.4426950408889634f;
+__device__ __forceinline__ float4 scale_conic(const float4& co) {
+  return make_float4(kConicScale * co.x, 2.0f * kConicScale * co.y, kConicScale * co.z, co.w);
+}
+
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -57,7 +70,7 @@ __device__ __forceinline__ uint32_t stage(Staged* s, int slot, uint32_t id, int 
   const float2 m = __ldg(means2D + id);
   const float4 co = __ldg(conic_opacity + id);
   s[slot].xyi = make_float4(m.x, m.y, __uint_as_float(id), 0.0f);
-  s[slot].co = co;
+  s[slot].co = scale_conic(co);
   s[slot].col = __ldg(rgb + id);
   if (!(co.w * 255.0f > 1.0f)) return 0u;  // alpha < 1/255 everywhere
   const float det = co.x * co.z - co.y * co.y;
@@ -211,8 +224,8 @@ __global__ void __launch_bounds__(kBlock, DW_BWD_MIN_BLOCKS)
         const float dxx = dx * dx, dxy = dx * dy, dyy = dy * dy;
         // the packed forward's exact operation sequence (eval2), so this
         // kernel walks exactly the forward's contributors
-        const float power = __fmaf_rn(-co.y, dxy, -0.5f * __fmaf_rn(co.z, dyy, co.x * dxx));
-        const float G = ex2_approx(power * 1.4426950408889634f);
+        const float power = __fmaf_rn(co.y, dxy, __fmaf_rn(co.z, dyy, co.x * dxx));  // log2 G
+        const float G = ex2_approx(power);
         const float alpha = fminf(0.99f, G * co.w);
         const bool act = inside && contributor < last_contributor && power <= 0.0f &&
                          alpha >= 1.0f / 255.0f;
@@ -243,8 +256,11 @@ __global__ void __launch_bounds__(kBlock, DW_BWD_MIN_BLOCKS)
           // dL_dG * dG/d(delta) and -0.5 G d d^T dL_dG reuse power's products
           const float q = G * (co.w * dL_dalpha);
           const float qh = -0.5f * q;
-          v[0] = -q * (co.x * dx + co.y * dy) * ddelx_dx;
-          v[1] = -q * (co.z * dy + co.y * dx) * ddely_dy;
+          // unscaled conic (a, b, c) = (A, B/2, C) / k (scale_conic)
+          const float ca = co.x * (1.0f / kConicScale), cb = co.y * (0.5f / kConicScale),
+                      cc = co.z * (1.0f / kConicScale);
+          v[0] = -q * (ca * dx + cb * dy) * ddelx_dx;
+          v[1] = -q * (cc * dy + cb * dx) * ddely_dy;
           v[2] = qh * dxx;
           v[3] = qh * dxy;
           v[4] = qh * dyy;
@@ -320,18 +336,22 @@ struct Eval2 {
   float dx, dxx;
   float2 dy, dxy, dyy, power, G;
 };
-__device__ __forceinline__ void eval2(const float4& g, const float4& co, float pfx, float2 npfy,
+// STAGED_SCALED: co is already scale_conic()'d (the forward's and the native
+// backward's staging); otherwise it is the raw conic and the same three
+// scaled coefficients are formed here -- bit-identical values either way.
+template <bool STAGED_SCALED>
+__device__ __forceinline__ void eval2(const float4& g, const float4& co_in, float pfx, float2 npfy,
                                       Eval2& e) {
-  constexpr float kLog2e = 1.4426950408889634f;
+  const float4 co = STAGED_SCALED ? co_in : scale_conic(co_in);
   e.dx = g.x - pfx;
   e.dy = add2(bc2(g.y), npfy);
   e.dxx = e.dx * e.dx;
   e.dxy = mul2(bc2(e.dx), e.dy);
   e.dyy = mul2(e.dy, e.dy);
-  const float2 t = fma2(bc2(co.z), e.dyy, bc2(co.x * e.dxx));
-  e.power = fma2(bc2(-co.y), e.dxy, mul2(bc2(-0.5f), t));
-  const float2 pl = mul2(e.power, bc2(kLog2e));
-  e.G = make_float2(ex2_approx(pl.x), ex2_approx(pl.y));
+  // co is the staged (pre-scaled) conic: power = log2 G (its sign is the
+  // unscaled power's)
+  e.power = fma2(bc2(co.y), e.dxy, fma2(bc2(co.z), e.dyy, bc2(co.x * e.dxx)));
+  e.G = make_float2(ex2_approx(e.power.x), ex2_approx(e.power.y));
 }
 
 // The forward keeps synchronous staging: with the backward's cp.async double
@@ -390,7 +410,7 @@ __global__ void __launch_bounds__(128)
         const float4 g = sm[j].xyi;
         const float4 co = sm[j].co;
         Eval2 e;
-        eval2(g, co, pfx, npfy, e);
+        eval2<true>(g, co, pfx, npfy, e);
         const float2 Go = mul2(e.G, bc2(co.w));
         const float2 alpha = make_float2(fminf(0.99f, Go.x), fminf(0.99f, Go.y));
         const float2 test_T = mul2(T, fma2(alpha, bc2(-1.0f), bc2(1.0f)));
@@ -569,7 +589,7 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
         const float4 g = lds128(sbase + 48u * (uint32_t)j);
         const float4 co = lds128(sbase + 48u * (uint32_t)j + 16u);
         Eval2 e;
-        eval2(g, co, pfx, npfy, e);
+        eval2<false>(g, co, pfx, npfy, e);
         const float2 Go = mul2(e.G, bc2(co.w));
         const float2 alpha = make_float2(fminf(0.99f, Go.x), fminf(0.99f, Go.y));
         const bool a0 = contributor < last0 && e.power.x <= 0.0f && alpha.x >= 1.0f / 255.0f;
