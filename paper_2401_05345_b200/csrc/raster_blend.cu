@@ -61,43 +61,12 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-// Stage Gaussian `id` into slot `slot` and return its 8-bit warp-block mask
-// for the tile whose top-left pixel is (tx0, ty0).
-__device__ __forceinline__ uint32_t stage(Staged* s, int slot, uint32_t id, int tx0, int ty0,
-                                          const float2* __restrict__ means2D,
-                                          const float4* __restrict__ conic_opacity,
-                                          const float4* __restrict__ rgb) {
-  const float2 m = __ldg(means2D + id);
-  const float4 co = __ldg(conic_opacity + id);
-  s[slot].xyi = make_float4(m.x, m.y, __uint_as_float(id), 0.0f);
-  s[slot].co = scale_conic(co);
-  s[slot].col = __ldg(rgb + id);
-  if (!(co.w * 255.0f > 1.0f)) return 0u;  // alpha < 1/255 everywhere
-  const float det = co.x * co.z - co.y * co.y;
-  if (!(det > 0.0f) || !(co.x > 0.0f)) return 0xffu;  // degenerate: no culling
-  const float tau = 1.05f * 2.0f * __logf(255.0f * co.w) + 0.05f;
-  const float ex = sqrtf(tau * co.z / det), ey = sqrtf(tau * co.x / det);
-  uint32_t cx = 0, ry = 0;
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    const float lo = (float)(tx0 + 8 * c), hi = lo + 7.0f;
-    if (m.x + ex >= lo && m.x - ex <= hi) cx |= 1u << c;
-  }
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const float lo = (float)(ty0 + 4 * r), hi = lo + 3.0f;
-    if (m.y + ey >= lo && m.y - ey <= hi) ry |= 1u << r;
-  }
-  // warp w covers column (w & 1), row (w >> 1)
-  uint32_t mask = 0;
-#pragma unroll
-  for (int w = 0; w < 8; ++w)
-    if ((cx >> (w & 1) & 1u) && (ry >> (w >> 1) & 1u)) mask |= 1u << w;
-  return mask;
-}
-
-// Footprint mask of a Gaussian already in shared memory (the part of stage()
-// after the loads).
+// Footprint mask of a Gaussian: the 8x4 bands (8 per 16x16 tile; warp w of
+// the one-pixel kernel = band w, warp w of the two-pixel kernels = bands
+// 4 (w >> 1) + (w & 1) + {0, 2}) its alpha >= 1/255 ellipse can reach.
+#ifndef DW_EXACT_CULL
+#define DW_EXACT_CULL 1  // 0: bounding-box band test only
+#endif
 __device__ __forceinline__ uint32_t footprint_mask(float mx, float my, const float4& co, int tx0,
                                                    int ty0) {
   if (!(co.w * 255.0f > 1.0f)) return 0u;
@@ -122,6 +91,22 @@ __device__ __forceinline__ uint32_t footprint_mask(float mx, float my, const flo
     if ((cx >> (w & 1) & 1u) && (ry >> (w >> 1) & 1u)) mask |= 1u << w;
   return mask;
 }
+
+// Stage Gaussian `id` into slot `slot` (conic pre-scaled, scale_conic) and
+// return its 8-bit warp-block mask for the tile whose top-left pixel is
+// (tx0, ty0).
+__device__ __forceinline__ uint32_t stage(Staged* s, int slot, uint32_t id, int tx0, int ty0,
+                                          const float2* __restrict__ means2D,
+                                          const float4* __restrict__ conic_opacity,
+                                          const float4* __restrict__ rgb) {
+  const float2 m = __ldg(means2D + id);
+  const float4 co = __ldg(conic_opacity + id);
+  s[slot].xyi = make_float4(m.x, m.y, __uint_as_float(id), 0.0f);
+  s[slot].co = scale_conic(co);
+  s[slot].col = __ldg(rgb + id);
+  return footprint_mask(m.x, m.y, co, tx0, ty0);
+}
+
 
 // Asynchronous (cp.async, no register staging) gather of Gaussian `id` into
 // slot `s`: means2D -> xyi.xy, conic/opacity -> co, rgb (+ 1/opacity) -> col.
