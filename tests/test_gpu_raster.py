@@ -237,16 +237,21 @@ def test_render_host_e2e(cuda, cases):
     assert rel < GRAD_REL_L2
 
 
-def test_render_views_host_matches_per_view(cuda, orc):
-    """Batched host path (one scene upload, overlapped per-view copies) ==
-    the sum over views of the oracle's per-view gradients; images per view."""
+@pytest.mark.parametrize("binning", ["auto", "dense"])
+def test_render_views_host_matches_per_view(cuda, orc, binning, monkeypatch):
+    """Batched host path (one scene upload, views alternating over two
+    forward states and compute streams, overlapped per-view copies) == the sum
+    over views of the oracle's per-view gradients; images per view."""
     import torch
+
+    if binning == "dense":
+        monkeypatch.setenv("DW_DENSE_BINNING", "1")
 
     from paper_2401_05345_b200 import warpred as wr
     from paper_2401_05345_b200.rasterizer import GaussianRasterizer, render_views_host
     from paper_2401_05345_b200.scene import make_dL_dpixels, make_scene, orbit_cameras
 
-    P, W, H, V = 5000, 200, 144, 3
+    P, W, H, V = 5000, 200, 144, 5
     sc = make_scene(P, W, H, seed=31)
     cams = orbit_cameras(W, H, V)
     dL = np.stack([make_dL_dpixels(W, H, seed=40 + k) for k in range(V)])
