@@ -130,6 +130,10 @@ void launch_dense_binning(int P, const uint32_t* order, const float2* means2D, c
                           uint32_t* values, const unsigned long long* n_dev, uint64_t cap,
                           cudaStream_t s);
 void launch_tiles_from_ranges(const uint2* ranges, int ntiles, uint32_t* tiles, cudaStream_t s);
+// Per-tile stable depth sort of index-ordered tile lists (tile-first binning);
+// scratch: 2 x instances u64 (used by lists longer than the shared-memory cap).
+void launch_segsort_depth(const uint2* ranges, const float* depths, uint32_t* values,
+                          unsigned long long* scratch, int ntiles, cudaStream_t s);
 // order[ntiles]: tiles by descending list length (bucketed), for the blend kernels
 void launch_tile_order(const uint2* ranges, int ntiles, uint32_t* order, cudaStream_t s);
 // ranges[0, ntiles) of the sorted tile ids (every range written)

@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(256)
   uint32_t gid = 0;
   int area = 0;
   if (i < P) {
-    gid = order[i];
+    gid = order ? order[i] : static_cast<uint32_t>(i);
     const int rad = radii[gid];
     if (rad > 0) {
       rect_of(means2D[gid], rad, tiles_x, tiles_y, r);
@@ -521,6 +521,97 @@ __global__ void __launch_bounds__(256)
       values[o + k] = g;
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Tile-first binning: duplicate the instances in Gaussian-index order, stable
+// radix-sort them by tile (each tile's list then holds its Gaussians in index
+// order), then sort every tile's list by depth in shared memory. A stable
+// depth order over index order is the (depth, index) order -- the list the
+// depth-first pipeline (global depth sort, then duplicate, then tile sort)
+// produces -- without four LSD passes over all P Gaussians. The per-tile
+// sort is a bitonic network on the 64-bit keys (depth bits << 32 | id), a
+// total order equal to that one; lists longer than kSegCap are sorted in
+// kSegCap chunks and merged pairwise in global scratch by the same CTA.
+constexpr int kSegCap = 2048;
+
+__device__ __forceinline__ void bitonic_smem(unsigned long long* a, int npad) {
+  for (int k = 2; k <= npad; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < npad; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const unsigned long long x = a[i], y = a[l];
+          const bool up = (i & k) == 0;
+          if ((x > y) == up) {
+            a[i] = y;
+            a[l] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_segsort_depth(const uint2* __restrict__ ranges, const float* __restrict__ depths,
+                    uint32_t* __restrict__ values, unsigned long long* __restrict__ scratch,
+                    int ntiles) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
+  __shared__ unsigned long long s_k[kSegCap];
+  const int tile = blockIdx.x;
+  if (tile >= ntiles) return;
+  const uint2 r = ranges[tile];
+  const int n = static_cast<int>(r.y - r.x);
+  if (n <= 1) return;
+  auto key_of = [&](int i) {
+    const uint32_t id = values[r.x + i];
+    return static_cast<unsigned long long>(__float_as_uint(__ldg(depths + id))) << 32 | id;
+  };
+  if (n <= kSegCap) {
+    int npad = 32;
+    while (npad < n) npad <<= 1;
+    for (int i = threadIdx.x; i < npad; i += blockDim.x) s_k[i] = i < n ? key_of(i) : ~0ull;
+    __syncthreads();
+    bitonic_smem(s_k, npad);
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+      values[r.x + i] = static_cast<uint32_t>(s_k[i]);
+    return;
+  }
+  // long list: sorted chunks into scratch[r.x ..], then pairwise merges
+  unsigned long long* bufs[2] = {scratch + r.x, scratch + static_cast<size_t>(r.x) + n};
+  for (int c0 = 0; c0 < n; c0 += kSegCap) {
+    const int m = min(kSegCap, n - c0);
+    for (int i = threadIdx.x; i < kSegCap; i += blockDim.x) s_k[i] = i < m ? key_of(c0 + i) : ~0ull;
+    __syncthreads();
+    bitonic_smem(s_k, kSegCap);
+    for (int i = threadIdx.x; i < m; i += blockDim.x) bufs[0][c0 + i] = s_k[i];
+    __syncthreads();
+  }
+  int cur = 0;
+  for (int run = kSegCap; run < n; run <<= 1, cur ^= 1) {
+    const unsigned long long* in = bufs[cur];
+    unsigned long long* out = bufs[cur ^ 1];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int a0 = (i / (2 * run)) * 2 * run;  // pair of runs [a0, a0+run), [a0+run, a0+2run)
+      const int b0 = min(a0 + run, n), b1 = min(a0 + 2 * run, n);
+      const unsigned long long x = in[i];
+      // rank in the other run (keys are distinct): elements of the other run below x
+      const bool inA = i < b0;
+      int lo = inA ? b0 : a0, hi = inA ? b1 : b0;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (in[mid] < x) lo = mid + 1; else hi = mid;
+      }
+      const int rank = inA ? (i - a0) + (lo - b0) : (i - b0) + (lo - a0);
+      out[a0 + rank] = x;
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    values[r.x + i] = static_cast<uint32_t>(bufs[cur][i]);
 }
 
 // ---------------------------------------------------------------------------
@@ -1046,6 +1137,13 @@ void launch_tiles_from_ranges(const uint2* ranges, int ntiles, uint32_t* tiles, 
   if (ntiles <= 0) return;
   k_tiles_from_ranges<<<blocks_for(static_cast<int64_t>(ntiles) * 32, 256), 256, 0, s>>>(
       ranges, ntiles, tiles);
+  DW_CUDA(cudaGetLastError());
+}
+
+void launch_segsort_depth(const uint2* ranges, const float* depths, uint32_t* values,
+                          unsigned long long* scratch, int ntiles, cudaStream_t s) {
+  if (ntiles <= 0) return;
+  launch_pdl(k_segsort_depth, ntiles, 256, 0, s, ranges, depths, values, scratch, ntiles);
   DW_CUDA(cudaGetLastError());
 }
 

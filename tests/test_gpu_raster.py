@@ -69,12 +69,17 @@ def cases(orc):
     return out
 
 
-@pytest.fixture(params=["auto", "sort", "dense"])
+@pytest.fixture(params=["auto", "depth-first", "tile-first", "dense"])
 def binning(request, monkeypatch):
-    """Both list constructions -- duplicate + radix sort, and dense
-    (tile-major) binning -- must give the oracle's lists bit for bit."""
-    if request.param != "auto":
-        monkeypatch.setenv("DW_DENSE_BINNING", "1" if request.param == "dense" else "0")
+    """Every list construction -- depth-first (global depth sort, duplicate,
+    sort by tile), tile-first (duplicate by index, sort by tile, per-tile
+    depth sort) and dense (tile-major) binning -- must give the oracle's
+    lists bit for bit."""
+    if request.param in ("depth-first", "tile-first"):
+        monkeypatch.setenv("DW_DENSE_BINNING", "0")
+        monkeypatch.setenv("DW_TILE_FIRST", "1" if request.param == "tile-first" else "0")
+    elif request.param == "dense":
+        monkeypatch.setenv("DW_DENSE_BINNING", "1")
     return request.param
 
 
