@@ -335,7 +335,7 @@ struct dw_rasterizer {
     if (!dense && tile_first && n_grid > 0) {
       // 4. every tile's list (index order) -> (depth, index) order
       grow(seg_scratch, cap_seg, 2 * static_cast<size_t>(n_grid));
-      dw::launch_segsort_depth(ranges, depths, vals, seg_scratch, ntiles, s);
+      dw::launch_segsort_depth(ranges, depths, vals, seg_scratch, n_grid, ntiles, s);
     }
     order_stale = true;  // the backward derives its tile order from these ranges
     dw::launch_forward_impl(cam, ranges, vals, means2D, conic_opacity, rgb, nullptr, final_T,

@@ -133,7 +133,8 @@ void launch_tiles_from_ranges(const uint2* ranges, int ntiles, uint32_t* tiles, 
 // Per-tile stable depth sort of index-ordered tile lists (tile-first binning);
 // scratch: 2 x instances u64 (used by lists longer than the shared-memory cap).
 void launch_segsort_depth(const uint2* ranges, const float* depths, uint32_t* values,
-                          unsigned long long* scratch, int ntiles, cudaStream_t s);
+                          unsigned long long* scratch, int64_t capacity, int ntiles,
+                          cudaStream_t s);
 // order[ntiles]: tiles by descending list length (bucketed), for the blend kernels
 void launch_tile_order(const uint2* ranges, int ntiles, uint32_t* order, cudaStream_t s);
 // ranges[0, ntiles) of the sorted tile ids (every range written)

@@ -557,7 +557,7 @@ __device__ __forceinline__ void bitonic_smem(unsigned long long* a, int npad) {
 __global__ void __launch_bounds__(256)
     k_segsort_depth(const uint2* __restrict__ ranges, const float* __restrict__ depths,
                     uint32_t* __restrict__ values, unsigned long long* __restrict__ scratch,
-                    int ntiles) {
+                    int ntiles, int64_t half) {
   pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
   __shared__ unsigned long long s_k[kSegCap];
@@ -581,7 +581,8 @@ __global__ void __launch_bounds__(256)
     return;
   }
   // long list: sorted chunks into scratch[r.x ..], then pairwise merges
-  unsigned long long* bufs[2] = {scratch + r.x, scratch + static_cast<size_t>(r.x) + n};
+  // per-tile ping-pong halves: [r.x, r.y) of scratch[0, half) and of scratch[half, 2 half)
+  unsigned long long* bufs[2] = {scratch + r.x, scratch + half + r.x};
   for (int c0 = 0; c0 < n; c0 += kSegCap) {
     const int m = min(kSegCap, n - c0);
     for (int i = threadIdx.x; i < kSegCap; i += blockDim.x) s_k[i] = i < m ? key_of(c0 + i) : ~0ull;
@@ -1141,9 +1142,11 @@ void launch_tiles_from_ranges(const uint2* ranges, int ntiles, uint32_t* tiles, 
 }
 
 void launch_segsort_depth(const uint2* ranges, const float* depths, uint32_t* values,
-                          unsigned long long* scratch, int ntiles, cudaStream_t s) {
+                          unsigned long long* scratch, int64_t capacity, int ntiles,
+                          cudaStream_t s) {
   if (ntiles <= 0) return;
-  launch_pdl(k_segsort_depth, ntiles, 256, 0, s, ranges, depths, values, scratch, ntiles);
+  launch_pdl(k_segsort_depth, ntiles, 256, 0, s, ranges, depths, values, scratch, ntiles,
+             capacity);
   DW_CUDA(cudaGetLastError());
 }
 

@@ -281,6 +281,38 @@ def test_render_views_host_matches_per_view(cuda, orc, binning, monkeypatch):
         assert np.linalg.norm(g - want_g) / np.linalg.norm(want_g) < GRAD_REL_L2
 
 
+def test_binning_paths_agree_on_long_lists(cuda, monkeypatch):
+    """Lists longer than the per-tile sort's shared-memory block (tile-first
+    sorts them in chunks and merges in global scratch) and dense binning:
+    every path gives the depth-first lists bit for bit."""
+    import torch
+
+    from paper_2401_05345_b200.rasterizer import GaussianRasterizer
+    from paper_2401_05345_b200.scene import make_camera, make_scene
+
+    P, W, H = 6000, 160, 128
+    sc = {k: torch.from_numpy(v).to(cuda)
+          for k, v in make_scene(P, W, H, seed=7, high_contention=True).items()}
+    cam = make_camera(W, H)
+    out = {}
+    for path, env in (("depth-first", ("0", "0")), ("tile-first", ("0", "1")),
+                      ("dense", ("1", "0"))):
+        monkeypatch.setenv("DW_DENSE_BINNING", env[0])
+        monkeypatch.setenv("DW_TILE_FIRST", env[1])
+        r = GaussianRasterizer()
+        img, _, nr = r.render_forward(*[sc[k] for k in ("means3D", "scales", "rotations",
+                                                        "opacities", "colors")], cam)
+        out[path] = (r.buffer("values"), r.buffer("ranges"), img.cpu().numpy(), nr)
+    ref = out["depth-first"]
+    lens = ref[1][:, 1] - ref[1][:, 0]
+    assert lens.max() > 4096  # the chunked-merge path runs
+    for path in ("tile-first", "dense"):
+        assert out[path][3] == ref[3]
+        assert np.array_equal(out[path][0], ref[0]), path
+        assert np.array_equal(out[path][1], ref[1]), path
+        assert np.array_equal(out[path][2], ref[2]), path
+
+
 def test_render_views_host_reserve_overflow_redo(cuda, orc):
     """Views after the first keep their instance count on the device against
     a reserve of 1.5x view 0's count; a later view that outgrows it (view 0
