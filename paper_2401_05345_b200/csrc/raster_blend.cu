@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(128)
         eval2<true>(g, co, pfx, npfy, e);
         const float2 Go = mul2(e.G, bc2(co.w));
         const float2 alpha = make_float2(fminf(0.99f, Go.x), fminf(0.99f, Go.y));
-        const float2 test_T = mul2(T, fma2(alpha, bc2(-1.0f), bc2(1.0f)));
+        const float2 test_T = mul2(T, add2(bc2(1.0f), make_float2(-alpha.x, -alpha.y)));
         const bool a0 = T.x > 0.0f && e.power.x <= 0.0f && alpha.x >= 1.0f / 255.0f;
         const bool a1 = T.y > 0.0f && e.power.y <= 0.0f && alpha.y >= 1.0f / 255.0f;
         const bool b0 = a0 && test_T.x >= 0.0001f;  // blends; a0 && !b0 terminates
