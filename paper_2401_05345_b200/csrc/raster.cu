@@ -38,6 +38,14 @@ void grow(T*& p, size_t& cap, size_t want) {
   cap = n;
 }
 
+// grow() for state that kernels expect zeroed (and leave zeroed) between calls
+template <typename T>
+void grow_zeroed(T*& p, size_t& cap, size_t want) {
+  if (want <= cap && p) return;
+  grow(p, cap, want);
+  DW_CUDA(cudaMemset(p, 0, cap * sizeof(T)));
+}
+
 }  // namespace
 
 struct dw_rasterizer {
@@ -162,7 +170,7 @@ struct dw_rasterizer {
       grow(dids[b], cap_d[2 + b], np);
     }
     grow(area_sorted, cap_as, np);
-    grow(scan_tmp, cap_scan, dw::scan_temp_bytes(P_));
+    grow_zeroed(scan_tmp, cap_scan, dw::scan_temp_bytes(P_));
     grow(ranges, cap_t, ntiles);
     grow(tile_order, cap_to, ntiles);
     grow(final_T, cap_px, npx);
@@ -245,17 +253,8 @@ struct dw_rasterizer {
       grow(dids[b], cap_d[2 + b], np);
     }
     grow(area_sorted, cap_as, np);
-    grow(scan_tmp, cap_scan, dw::scan_temp_bytes(P));
+    grow_zeroed(scan_tmp, cap_scan, dw::scan_temp_bytes(P));
 
-    dw::launch_preprocess(P, means3D, scales, rotations, opacities, colors, cam, means2D, depths,
-                          radii, conic_opacity, rgb, tiles_touched, s);
-    // Instance count: read back (one host sync) to size the buffers, or --
-    // nosync -- kept on the device against the reserved capacity
-    // (dw_rasterizer_reserve), so the whole forward is graph-capturable.
-    int64_t n_grid = 0;                        // element count the grids are sized for
-    const unsigned long long* n_dev = nullptr;  // live count on the device (nosync)
-    num_rendered = 0;
-    count_pending = false;
     // Tile-first binning (default): instances duplicated in index order, sorted
     // by tile, each tile's list then depth-sorted on chip. Depth-first: all P
     // Gaussians depth-sorted first (also what dense binning needs).
@@ -266,9 +265,21 @@ struct dw_rasterizer {
     tile_first = tf_env && *tf_env ? *tf_env == '1'
                                    : DW_TILE_FIRST != 0 && last_list_mean >= 0.0 &&
                                          last_list_mean < kTileFirstMaxMean;
+    // the depth-first paths' sort keys come straight out of the preprocess
+    const bool keys_ready = !tile_first;
+    dw::launch_preprocess(P, means3D, scales, rotations, opacities, colors, cam, means2D, depths,
+                          radii, conic_opacity, rgb, tiles_touched, keys_ready ? dkey[0] : nullptr,
+                          keys_ready ? dids[0] : nullptr, s);
+    // Instance count: read back (one host sync) to size the buffers, or --
+    // nosync -- kept on the device against the reserved capacity
+    // (dw_rasterizer_reserve), so the whole forward is graph-capturable.
+    int64_t n_grid = 0;                        // element count the grids are sized for
+    const unsigned long long* n_dev = nullptr;  // live count on the device (nosync)
+    num_rendered = 0;
+    count_pending = false;
     bool depth_sorted = false;
     auto depth_sort = [&](bool with_area) {
-      dw::launch_depth_keys(P, depths, radii, dkey[0], dids[0], s);
+      if (!keys_ready) dw::launch_depth_keys(P, depths, radii, dkey[0], dids[0], s);
       ensure_tmp(dw::radix_sort_temp_bytes(P));
       // (its last pass can also lay tiles_touched out in that order: area_sorted)
       order = dids[dw::radix_sort_pairs(dkey, dids, P, 32, tmp, s, nullptr,

@@ -73,7 +73,8 @@ __device__ __forceinline__ void tile_pixel(int tile, int t, int tiles_x, int* px
 void launch_preprocess(int P, const float* means3D, const float* scales, const float* rotations,
                        const float* opacities, const float* colors, const CamParams& cam,
                        float2* means2D, float* depths, int* radii, float4* conic_opacity,
-                       float4* rgb, uint32_t* tiles_touched, cudaStream_t s);
+                       float4* rgb, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* dids,
+                       cudaStream_t s);  // dkey/dids (nullable): depth-sort keys and ids
 
 // Device buffers of the backward's WarpRecord tap (SoA like dw_device_trace).
 struct TapBuf {

@@ -50,7 +50,8 @@ __global__ void __launch_bounds__(kBlock)
                  const float* __restrict__ colors, const CamParams cam,
                  float2* __restrict__ means2D, float* __restrict__ depths,
                  int* __restrict__ radii, float4* __restrict__ conic_opacity,
-                 float4* __restrict__ rgb, uint32_t* __restrict__ tiles_touched) {
+                 float4* __restrict__ rgb, uint32_t* __restrict__ tiles_touched,
+                 uint32_t* __restrict__ dkey, uint32_t* __restrict__ dids) {
   pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
   __shared__ __align__(16) float s_mean[3 * kBlock];
@@ -66,6 +67,11 @@ __global__ void __launch_bounds__(kBlock)
   if (i >= P) return;
   radii[i] = 0;
   tiles_touched[i] = 0;
+  // depth-sort input (nullable): (depth bits, id), culled Gaussians last
+  if (dkey) {
+    dkey[i] = 0xffffffffu;
+    dids[i] = static_cast<uint32_t>(i);
+  }
 
   const float px = s_mean[3 * t], py = s_mean[3 * t + 1], pz = s_mean[3 * t + 2];
   const float* vm = cam.vm;
@@ -152,6 +158,7 @@ __global__ void __launch_bounds__(kBlock)
   const int area = (rmaxx - rminx) * (rmaxy - rminy);
   if (area == 0) return;
   depths[i] = tv2;
+  if (dkey && radius > 0) dkey[i] = __float_as_uint(tv2);
   radii[i] = radius;
   means2D[i] = make_float2(ix, iy);
   const float op = __ldg(opacities + i);
@@ -166,17 +173,18 @@ __global__ void __launch_bounds__(kBlock)
 void launch_preprocess(int P, const float* means3D, const float* scales, const float* rotations,
                        const float* opacities, const float* colors, const CamParams& cam,
                        float2* means2D, float* depths, int* radii, float4* conic_opacity,
-                       float4* rgb, uint32_t* tiles_touched, cudaStream_t s) {
+                       float4* rgb, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* dids,
+                       cudaStream_t s) {
   if (P <= 0) return;
   auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   const bool vec = aligned(means3D) && aligned(scales) && aligned(colors) && aligned(rotations);
   const int grid = (P + kBlock - 1) / kBlock;
   if (vec)
     launch_pdl(k_preprocess<true>, grid, kBlock, 0, s, P, means3D, scales, rotations, opacities,
-               colors, cam, means2D, depths, radii, conic_opacity, rgb, tiles_touched);
+               colors, cam, means2D, depths, radii, conic_opacity, rgb, tiles_touched, dkey, dids);
   else
     launch_pdl(k_preprocess<false>, grid, kBlock, 0, s, P, means3D, scales, rotations, opacities,
-               colors, cam, means2D, depths, radii, conic_opacity, rgb, tiles_touched);
+               colors, cam, means2D, depths, radii, conic_opacity, rgb, tiles_touched, dkey, dids);
   DW_CUDA(cudaGetLastError());
 }
 

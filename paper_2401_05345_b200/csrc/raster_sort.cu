@@ -323,84 +323,60 @@ __global__ void __launch_bounds__(kSortThreads)
   }
 }
 
-// Inclusive scan u32 -> u64 of in[order[i]] (order may be null).
-__global__ void __launch_bounds__(kSortThreads)
-    k_scan_tile_sums(const uint32_t* __restrict__ in, const uint32_t* __restrict__ order,
-                     int64_t n, unsigned long long* __restrict__ tile_sums) {
-  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
-  pdl_trigger();
-  __shared__ unsigned long long ws[kSortThreads / 32];
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kSortTile;
-  unsigned long long s = 0;
-  for (int r = 0; r < kSortItems; ++r) {
-    const int64_t e = base + r * kSortThreads + t;
-    if (e < n) s += __ldg(in + (order ? __ldg(order + e) : e));
-  }
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-  if (lane == 0) ws[w] = s;
-  __syncthreads();
-  if (t == 0) {
-    unsigned long long tot = 0;
-    for (int k = 0; k < kSortThreads / 32; ++k) tot += ws[k];
-    tile_sums[blockIdx.x] = tot;
-  }
-}
+// Inclusive scan u32 -> u64 of in[order[i]] (order may be null), one pass
+// with decoupled look-back: each CTA takes the next tile id from a counter
+// (so every predecessor is already running: the spin cannot deadlock),
+// publishes its tile aggregate, walks back over its predecessors' flags 32 at
+// a time until one holds an inclusive prefix, and publishes its own inclusive
+// prefix. Flag word = status (2 bits: 1 aggregate, 2 inclusive) | value (62
+// bits) so one relaxed 64-bit store publishes both. The last CTA to finish
+// zeroes the flags and counters again: the state is clean between calls
+// without a memset (and inside a captured graph).
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kSortThreads * kScanItems;  // 2048 elements
+constexpr unsigned long long kScanAgg = 1ull << 62, kScanInc = 2ull << 62;
+constexpr unsigned long long kScanVal = kScanAgg - 1ull;
 
-__global__ void k_scan_tile_prefix(unsigned long long* __restrict__ tile_sums, int64_t tiles) {
-  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
-  pdl_trigger();
-  // single block of 1024: exclusive scan of tile sums in place (loop)
-  __shared__ unsigned long long warp_sums[32];
-  __shared__ unsigned long long carry;
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  if (t == 0) carry = 0;
-  __syncthreads();
-  for (int64_t b = 0; b < tiles; b += 1024) {
-    const int64_t i = b + t;
-    const unsigned long long v = i < tiles ? tile_sums[i] : 0ull;
-    unsigned long long incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long y = __shfl_up_sync(kFull, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) warp_sums[w] = incl;
-    __syncthreads();
-    if (w == 0) {
-      unsigned long long s = warp_sums[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long y = __shfl_up_sync(kFull, s, o);
-        if (lane >= o) s += y;
-      }
-      warp_sums[lane] = s;
-    }
-    __syncthreads();
-    if (i < tiles) tile_sums[i] = carry + (w ? warp_sums[w - 1] : 0ull) + incl - v;
-    __syncthreads();
-    if (t == 0) carry += warp_sums[31];
-    __syncthreads();
-  }
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 __global__ void __launch_bounds__(kSortThreads)
-    k_scan_tile_apply(const uint32_t* __restrict__ in, const uint32_t* __restrict__ order,
-                      int64_t n, const unsigned long long* __restrict__ tile_prefix,
-                      uint64_t* __restrict__ out) {
+    k_scan_chained(const uint32_t* __restrict__ in, const uint32_t* __restrict__ order, int64_t n,
+                   unsigned long long* __restrict__ state, uint64_t* __restrict__ out) {
   pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
-  // thread-blocked: thread t owns elements [16t, 16t+16) of the tile
-  __shared__ unsigned long long ws[kSortThreads / 32];
+  __shared__ uint32_t s_in[kScanTile + kScanTile / 32];          // padded: conflict-free transpose
+  __shared__ unsigned long long s_out[kScanTile + kScanTile / 16];
+  __shared__ unsigned long long s_wsum[kSortThreads / 32];
+  __shared__ unsigned long long s_excl;
+  __shared__ uint32_t s_tile;
+  unsigned* ctr = reinterpret_cast<unsigned*>(state);  // [0] next tile id, [1] tiles done
+  unsigned long long* flags = state + 1;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const int64_t first = static_cast<int64_t>(blockIdx.x) * kSortTile + t * kSortItems;
-  uint32_t v[kSortItems];
+  if (t == 0) s_tile = atomicAdd(ctr, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t tile0 = tile * kScanTile;
+  // coalesced load (element k*256 + t), transposed so thread t scans [8t, 8t+8)
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int i = k * kSortThreads + t;
+    const int64_t e = tile0 + i;
+    s_in[i + (i >> 5)] = e < n ? __ldg(in + (order ? __ldg(order + e) : e)) : 0u;
+  }
+  __syncthreads();
+  uint32_t v[kScanItems];
   unsigned long long tot = 0;
 #pragma unroll
-  for (int k = 0; k < kSortItems; ++k) {
-    const int64_t e = first + k;
-    v[k] = e < n ? __ldg(in + (order ? __ldg(order + e) : e)) : 0u;
+  for (int k = 0; k < kScanItems; ++k) {
+    const int i = t * kScanItems + k;
+    v[k] = s_in[i + (i >> 5)];
     tot += v[k];
   }
   unsigned long long incl = tot;
@@ -409,15 +385,63 @@ __global__ void __launch_bounds__(kSortThreads)
     const unsigned long long y = __shfl_up_sync(kFull, incl, o);
     if (lane >= o) incl += y;
   }
-  if (lane == 31) ws[w] = incl;
+  if (lane == 31) s_wsum[w] = incl;
   __syncthreads();
-  unsigned long long wbase = 0;
-  for (int k = 0; k < w; ++k) wbase += ws[k];
-  unsigned long long run = tile_prefix[blockIdx.x] + wbase + incl - tot;
+  unsigned long long wbase = 0, agg = 0;
 #pragma unroll
-  for (int k = 0; k < kSortItems; ++k) {
+  for (int k = 0; k < kSortThreads / 32; ++k) {
+    const unsigned long long x = s_wsum[k];
+    wbase += k < w ? x : 0ull;
+    agg += x;
+  }
+  if (w == 0) {
+    unsigned long long excl = 0;
+    if (tile == 0) {
+      if (lane == 0) st_relaxed_gpu(flags, kScanInc | agg);
+    } else {
+      if (lane == 0) st_relaxed_gpu(flags + tile, kScanAgg | agg);
+      int64_t end = tile - 1;  // window [end - 31, end]
+      while (true) {
+        const int64_t j = end - lane;
+        const unsigned long long f = j >= 0 ? ld_relaxed_gpu(flags + j) : kScanInc;
+        if (__any_sync(kFull, (f >> 62) == 0ull)) continue;  // a predecessor not published yet
+        const unsigned inc = __ballot_sync(kFull, (f >> 62) == 2ull);
+        const int stop = inc ? __ffs(inc) - 1 : 31;  // nearest inclusive prefix
+        unsigned long long x = lane <= stop ? (f & kScanVal) : 0ull;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+        excl += x;
+        if (inc) break;
+        end -= 32;
+      }
+      if (lane == 0) st_relaxed_gpu(flags + tile, kScanInc | (excl + agg));
+    }
+    if (lane == 0) s_excl = excl;
+  }
+  __syncthreads();
+  unsigned long long run = s_excl + wbase + incl - tot;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
     run += v[k];
-    if (first + k < n) out[first + k] = run;
+    const int i = t * kScanItems + k;
+    s_out[i + (i >> 4)] = run;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int i = k * kSortThreads + t;
+    const int64_t e = tile0 + i;
+    if (e < n) out[e] = s_out[i + (i >> 4)];
+  }
+  // the last CTA out resets the state for the next call
+  if (t == 0) {
+    const unsigned tiles = gridDim.x;
+    s_tile = atomicAdd(ctr + 1, 1u) == tiles - 1 ? 1u : 0u;
+  }
+  __syncthreads();
+  if (s_tile) {
+    for (unsigned i = t; i < gridDim.x; i += kSortThreads) flags[i] = 0ull;
+    if (t == 0) state[0] = 0ull;
   }
 }
 
@@ -954,8 +978,8 @@ size_t radix_sort_temp_bytes(int64_t n) {
   return (static_cast<size_t>(tiles) * 256 + 256) * sizeof(uint32_t) + 256;
 }
 
-size_t scan_temp_bytes(int64_t n) {
-  return static_cast<size_t>((n + kSortTile - 1) / kSortTile + 1) * sizeof(unsigned long long);
+size_t scan_temp_bytes(int64_t n) {  // look-back state: counters + one flag per tile
+  return static_cast<size_t>((n + kScanTile - 1) / kScanTile + 1) * sizeof(unsigned long long);
 }
 
 // Stable LSD sort of (k[cur], v[cur]) on bits [0, bits); returns the index
@@ -1040,13 +1064,9 @@ int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* 
 void inclusive_scan_gather(const uint32_t* in, const uint32_t* order, int64_t n, uint64_t* out,
                            void* temp, cudaStream_t s) {
   if (n <= 0) return;
-  const int64_t tiles = (n + kSortTile - 1) / kSortTile;
-  auto* sums = static_cast<unsigned long long*>(temp);
-  launch_pdl(k_scan_tile_sums, static_cast<unsigned>(tiles), kSortThreads, 0, s, in, order, n,
-             sums);
-  launch_pdl(k_scan_tile_prefix, 1, 1024, 0, s, sums, tiles);
-  launch_pdl(k_scan_tile_apply, static_cast<unsigned>(tiles), kSortThreads, 0, s, in, order, n,
-             sums, out);
+  const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+  launch_pdl(k_scan_chained, static_cast<unsigned>(tiles), kSortThreads, 0, s, in, order, n,
+             static_cast<unsigned long long*>(temp), out);
   DW_CUDA(cudaGetLastError());
 }
 
