@@ -409,6 +409,30 @@ def main() -> None:
     clocks = sampler.stop()
 
     ms_per_step = total_ms / args.steps
+
+    # ---- the step's one exchange, timed alone: NCCL all-reduce
+    # of grad[P, 9] fp32, device events, max over ranks; bus bandwidth uses
+    # the ring-equivalent factor 2 (n - 1) / n
+    allreduce = None
+    if dist is not None:
+        reps = 10
+        for _ in range(3):
+            dist.all_reduce(grad)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            dist.all_reduce(grad)
+        e1.record()
+        torch.cuda.synchronize()
+        ar = torch.tensor([e0.elapsed_time(e1) / reps], device=dev, dtype=torch.float64)
+        dist.all_reduce(ar, op=dist.ReduceOp.MAX)
+        ar_ms = float(ar.item())
+        nbytes = grad.numel() * grad.element_size()
+        allreduce = {"bytes": nbytes, "ms": ar_ms, "share_of_step": ar_ms / ms_per_step,
+                     "busbw_GBps": nbytes * 2 * (world - 1) / world / (ar_ms * 1e-3) / 1e9,
+                     "backend": dist.get_backend()}
     contrib_job = contrib_rank * world
     if dist is not None:
         c = torch.tensor([contrib_rank], device=dev, dtype=torch.float64)
@@ -540,6 +564,7 @@ def main() -> None:
                     "path": "dw_render_views_host: pinned H2D scene + V dL/dpixel, forward + "
                             "backward of V views, D2H V images + grad (copy streams "
                             "double-buffered against compute)"},
+            "allreduce": allreduce,
             "cpu_baseline": cpu,
             "cpu_port": cpu_port,
             "trace_family": tfam,
