@@ -399,8 +399,10 @@ __global__ void __launch_bounds__(128)
         const float2 Go = mul2(e.G, bc2(co.w));
         const float2 alpha = make_float2(fminf(0.99f, Go.x), fminf(0.99f, Go.y));
         const float2 test_T = mul2(T, add2(bc2(1.0f), make_float2(-alpha.x, -alpha.y)));
-        const bool a0 = T.x > 0.0f && e.power.x <= 0.0f && alpha.x >= 1.0f / 255.0f;
-        const bool a1 = T.y > 0.0f && e.power.y <= 0.0f && alpha.y >= 1.0f / 255.0f;
+        // a terminated pixel (T < 0) has test_T < 0, so the T > 0 check is
+        // folded into test_T >= 1e-4 and the termination store into -|T|
+        const bool a0 = e.power.x <= 0.0f && alpha.x >= 1.0f / 255.0f;
+        const bool a1 = e.power.y <= 0.0f && alpha.y >= 1.0f / 255.0f;
         const bool b0 = a0 && test_T.x >= 0.0001f;  // blends; a0 && !b0 terminates
         const bool b1 = a1 && test_T.y >= 0.0001f;
         const float2 am = make_float2(b0 ? alpha.x : 0.0f, b1 ? alpha.y : 0.0f);
@@ -409,7 +411,8 @@ __global__ void __launch_bounds__(128)
         C0 = fma2(bc2(c.x), aT, C0);
         C1 = fma2(bc2(c.y), aT, C1);
         C2 = fma2(bc2(c.z), aT, C2);
-        T = make_float2(b0 ? test_T.x : (a0 ? -T.x : T.x), b1 ? test_T.y : (a1 ? -T.y : T.y));
+        T = make_float2(b0 ? test_T.x : (a0 ? -fabsf(T.x) : T.x),
+                        b1 ? test_T.y : (a1 ? -fabsf(T.y) : T.y));
         const uint32_t pos = (uint32_t)(i * kBlock + j + 1);  // 1-based list position
         last0 = b0 ? pos : last0;
         last1 = b1 ? pos : last1;
