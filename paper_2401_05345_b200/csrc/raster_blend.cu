@@ -44,7 +44,7 @@ struct __align__(16) Staged {
 
 // The staged conic is pre-scaled so the exponent of G = exp(-q/2) comes out
 // directly in log2 units: (a, b, c) -> (k a, 2 k b, k c), k = -log2(e)/2, and
-// log2 G = k a dx^2 + 2 k b dx dy + k c dy^2 = fma(2kb, dxy, fma(kc, dyy, ka dxx))
+// log2 G = k a dx^2 + 2 k b dx dy + k c dy^2 = fma(fma(kc, dy, 2kb dx), dy, ka dxx)
 // -- two fused multiply-adds where the unscaled form needs four operations
 // plus the log2(e) multiply. Every blend kernel evaluates exactly this
 // sequence (the packed backward stages the raw conic and forms the same scaled
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kBlock, DW_BWD_MIN_BLOCKS)
         const float dxx = dx * dx, dxy = dx * dy, dyy = dy * dy;
         // the packed forward's exact operation sequence (eval2), so this
         // kernel walks exactly the forward's contributors
-        const float power = __fmaf_rn(co.y, dxy, __fmaf_rn(co.z, dyy, co.x * dxx));  // log2 G
+        const float power = __fmaf_rn(__fmaf_rn(co.z, dy, co.y * dx), dy, co.x * dxx);  // log2 G
         const float G = ex2_approx(power);
         const float alpha = fminf(0.99f, G * co.w);
         const bool act = inside && contributor < last_contributor && power <= 0.0f &&
@@ -319,7 +319,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // alpha decisions.
 struct Eval2 {
   float dx, dxx;
-  float2 dy, dxy, dyy, power, G;
+  float2 dy, power, G;
 };
 // STAGED_SCALED: co is already scale_conic()'d (the forward's and the native
 // backward's staging); otherwise it is the raw conic and the same three
@@ -331,11 +331,10 @@ __device__ __forceinline__ void eval2(const float4& g, const float4& co_in, floa
   e.dx = g.x - pfx;
   e.dy = add2(bc2(g.y), npfy);
   e.dxx = e.dx * e.dx;
-  e.dxy = mul2(bc2(e.dx), e.dy);
-  e.dyy = mul2(e.dy, e.dy);
   // co is the staged (pre-scaled) conic: power = log2 G (its sign is the
-  // unscaled power's)
-  e.power = fma2(bc2(co.y), e.dxy, fma2(bc2(co.z), e.dyy, bc2(co.x * e.dxx)));
+  // unscaled power's), in Horner form over dy -- the lane's two pixels share
+  // dx: power = (k a dx^2) + dy (2 k b dx + k c dy)
+  e.power = fma2(fma2(bc2(co.z), e.dy, bc2(co.y * e.dx)), e.dy, bc2(co.x * e.dxx));
   e.G = make_float2(ex2_approx(e.power.x), ex2_approx(e.power.y));
 }
 
