@@ -26,6 +26,7 @@
 // are all inactive for a Gaussian (ballot == 0) issues nothing, as the
 // reference policies emit no request for an empty active mask
 // (reducers.cpp:154-156).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "distwar.cuh"
@@ -37,9 +38,9 @@ namespace dw {
 namespace {
 
 struct __align__(16) Staged {
-  float4 xyi;  // x, y, id (uint bits), -
+  float4 xyi;  // x, y, id (uint bits), 1/opacity (packed backward's mask phase)
   float4 co;   // conic a, b, c, opacity
-  float4 col;  // r, g, b, 1/opacity (preprocess)
+  float4 col;  // r, g, b, footprint extents (preprocess: half2 bits)
 };
 
 // The staged conic is pre-scaled so the exponent of G = exp(-q/2) comes out
@@ -67,13 +68,15 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // bounding box. (An exact ellipse-rectangle test per band is slower: C3
 // backward 0.835 vs 0.780 ms -- its cost at staging exceeds the walks it
 // saves; the remaining empty walks are mostly misses between pixel centres.)
-__device__ __forceinline__ uint32_t footprint_mask(float mx, float my, const float4& co, int tx0,
+// The half-extents (ex, ey) come precomputed from the preprocess (rgb.w, a
+// half2 rounded up: raster_preprocess.cu), so staging does compares only;
+// -inf marks a Gaussian that can never reach alpha 1/255, +inf a degenerate
+// conic (no culling).
+__device__ __forceinline__ uint32_t footprint_mask(float mx, float my, float ext_bits, int tx0,
                                                    int ty0) {
-  if (!(co.w * 255.0f > 1.0f)) return 0u;
-  const float det = co.x * co.z - co.y * co.y;
-  if (!(det > 0.0f) || !(co.x > 0.0f)) return 0xffu;
-  const float tau = 1.05f * 2.0f * __logf(255.0f * co.w) + 0.05f;
-  const float ex = sqrtf(tau * co.z / det), ey = sqrtf(tau * co.x / det);
+  const uint32_t eb = __float_as_uint(ext_bits);
+  const float2 e = __half22float2(*reinterpret_cast<const __half2*>(&eb));
+  const float ex = e.x, ey = e.y;
   uint32_t cx = 0, ry = 0;
 #pragma unroll
   for (int c = 0; c < 2; ++c) {
@@ -103,13 +106,14 @@ __device__ __forceinline__ uint32_t stage(Staged* s, int slot, uint32_t id, int 
   const float4 co = __ldg(conic_opacity + id);
   s[slot].xyi = make_float4(m.x, m.y, __uint_as_float(id), 0.0f);
   s[slot].co = scale_conic(co);
-  s[slot].col = __ldg(rgb + id);
-  return footprint_mask(m.x, m.y, co, tx0, ty0);
+  const float4 c = __ldg(rgb + id);
+  s[slot].col = c;
+  return footprint_mask(m.x, m.y, c.w, tx0, ty0);
 }
 
 
 // Asynchronous (cp.async, no register staging) gather of Gaussian `id` into
-// slot `s`: means2D -> xyi.xy, conic/opacity -> co, rgb (+ 1/opacity) -> col.
+// slot `s`: means2D -> xyi.xy, conic/opacity -> co, rgb (+ extents) -> col.
 __device__ __forceinline__ void stage_async(Staged* s, uint32_t id,
                                             const float2* __restrict__ means2D,
                                             const float4* __restrict__ conic_opacity,
@@ -299,15 +303,6 @@ __device__ __forceinline__ float2 bc2(float a) { return make_float2(a, a); }
 __device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
 __device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
-// 16-byte shared load from a 32-bit shared-window address held in a register
-// (ptxas otherwise re-derives the window base in every loop iteration).
-__device__ __forceinline__ float4 lds128(uint32_t a) {
-  float4 v;
-  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(a));
-  return v;
-}
 __device__ __forceinline__ float rcp_approx(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -514,8 +509,6 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
     if (slot == p) lane_scale = scale[p];
   // keep it in a register: ptxas otherwise re-derives it in every reducing iteration
   asm volatile("" : "+f"(lane_scale));
-  uint32_t sbase0 = (uint32_t)__cvta_generic_to_shared(&sm[0][0]);
-  asm volatile("" : "+r"(sbase0));
   const int rounds = (int)((bmax + kBlock - 1) / kBlock);
   int todo = (int)bmax;
   const uint32_t top = range.x + bmax;
@@ -551,8 +544,10 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
       uint32_t mask = 0;
       if (cur_v[h]) {
         const float4 xy = cur[st].xyi;
-        mask = footprint_mask(xy.x, xy.y, cur[st].co, tx0, ty0);
-        cur[st].xyi.z = __uint_as_float(cur_id[h]);
+        mask = footprint_mask(xy.x, xy.y, cur[st].col.w, tx0, ty0);
+        // xyi.zw = (id, 1/opacity) for the RED address and the opacity gradient
+        *reinterpret_cast<float2*>(&cur[st].xyi.z) =
+            make_float2(__uint_as_float(cur_id[h]), rcp_approx(cur[st].co.w));
       }
       s_mask[st] = (uint8_t)mask;
       cur_id[h] = nxt_id[h];
@@ -562,7 +557,6 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
       nxt_id[h] = nxt_v[h] ? values[top - 1 - st2] : 0u;
     }
     __syncthreads();
-    const uint32_t sbase = sbase0 + (uint32_t)((i & 1) * kBlock * (int)sizeof(Staged));
     const int n = min(kBlock, todo);
     const uint32_t base = bmax - 1 - (uint32_t)(i * kBlock);
     for (int k = 0; k * 32 < n; ++k) {
@@ -573,8 +567,8 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
         const int j = k * 32 + __ffs(bits) - 1;
         bits &= bits - 1u;
         const uint32_t contributor = base - (uint32_t)j;
-        const float4 g = lds128(sbase + 48u * (uint32_t)j);
-        const float4 co = lds128(sbase + 48u * (uint32_t)j + 16u);
+        const float4 g = cur[j].xyi;
+        const float4 co = cur[j].co;
         Eval2 e;
         eval2<false>(g, co, pfx, npfy, e);
         const float2 Go = mul2(e.G, bc2(co.w));
@@ -585,7 +579,7 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
         const unsigned ballot = __ballot_sync(kFull, act);
         if (ballot == 0u) continue;
         const float2 msk = make_float2(a0 ? 1.0f : 0.0f, a1 ? 1.0f : 0.0f);
-        const float4 c = lds128(sbase + 48u * (uint32_t)j + 32u);
+        const float4 c = cur[j].col;
         const float2 am = mul2(alpha, msk);
         const float2 om = add2(bc2(1.0f), make_float2(-am.x, -am.y));
         const float2 inv = make_float2(rcp_approx(om.x), rcp_approx(om.y));
@@ -616,7 +610,7 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
                             e.dxx * Q,
                             e.dx * Qy,
                             Qyy,
-                            Q * c.w,
+                            Q * g.w,
                             fmaf(dcd.y, dL0.y, dcd.x * dL0.x),
                             fmaf(dcd.y, dL1.y, dcd.x * dL1.x),
                             fmaf(dcd.y, dL2.y, dcd.x * dL2.x)};

@@ -11,6 +11,7 @@
 // The P x 3 inputs (means3D, scales, colors) are not 16 B aligned per
 // Gaussian, so each CTA stages its 256 Gaussians' 768 floats through shared
 // memory with 192 coalesced float4 loads, then each thread reads its triple.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "dw_internal.h"
@@ -19,6 +20,30 @@
 namespace dw {
 
 namespace {
+
+// Half-extents of the alpha >= 1/255 ellipse: alpha = min(0.99, o G) with
+// G = exp(-q/2), q = d^T Q d (Q = conic) needs q <= tau = 2 ln(255 o); the
+// ellipse q <= tau lies in |dx| <= sqrt(tau Q^-1_xx), |dy| <= sqrt(tau Q^-1_yy)
+// with Q^-1_xx = c / (ac - b^2), Q^-1_yy = a / (ac - b^2). tau is inflated by
+// 5 % + 0.05 (the blend's exp2 approximation and FMA rounding) and the half2
+// is rounded up: -inf = never visible (o <= 1/255), +inf = degenerate conic.
+__device__ __forceinline__ uint32_t footprint_extents(const float4& co) {
+  float ex, ey;
+  if (!(co.w * 255.0f > 1.0f)) {
+    ex = ey = -INFINITY;
+  } else {
+    const float det = co.x * co.z - co.y * co.y;
+    if (!(det > 0.0f) || !(co.x > 0.0f)) {
+      ex = ey = INFINITY;
+    } else {
+      const float tau = 1.05f * 2.0f * __logf(255.0f * co.w) + 0.05f;
+      ex = sqrtf(tau * co.z / det) * 1.001f;
+      ey = sqrtf(tau * co.x / det) * 1.001f;
+    }
+  }
+  const __half2 h = __halves2half2(__float2half_ru(ex), __float2half_ru(ey));
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
 
 template <bool VEC>
 __device__ __forceinline__ void stage3(const float* __restrict__ src, float* sm, int64_t first,
@@ -162,9 +187,13 @@ __global__ void __launch_bounds__(kBlock)
   radii[i] = radius;
   means2D[i] = make_float2(ix, iy);
   const float op = __ldg(opacities + i);
-  conic_opacity[i] = make_float4(cv2 * det_inv, -cv1 * det_inv, cv0 * det_inv, op);
-  // w: 1/opacity for the backward's opacity gradient (sum q / o, raster_blend.cu)
-  rgb[i] = make_float4(s_col[3 * t], s_col[3 * t + 1], s_col[3 * t + 2], op > 0.0f ? 1.0f / op : 0.0f);
+  const float4 co = make_float4(cv2 * det_inv, -cv1 * det_inv, cv0 * det_inv, op);
+  conic_opacity[i] = co;
+  // w: the blend kernels' footprint half-extents (raster_blend.cu
+  // footprint_mask) as a half2, rounded up with a margin so the mask stays a
+  // superset of the alpha >= 1/255 ellipse's pixel bands
+  rgb[i] = make_float4(s_col[3 * t], s_col[3 * t + 1], s_col[3 * t + 2],
+                       __uint_as_float(footprint_extents(co)));
   tiles_touched[i] = static_cast<uint32_t>(area);
 }
 
