@@ -38,9 +38,10 @@ namespace dw {
 namespace {
 
 struct __align__(16) Staged {
-  float4 xyi;  // x, y, id (uint bits), 1/opacity (packed backward's mask phase)
+  float4 xyi;  // x, y, id (uint bits), - (packed backward: k b, see its mask phase)
   float4 co;   // conic a, b, c, opacity
-  float4 col;  // r, g, b, footprint extents (preprocess: half2 bits)
+  float4 col;  // r, g, b, footprint extents (preprocess: half2 bits; packed
+               // backward: 1/opacity after its mask phase)
 };
 
 // The staged conic is pre-scaled so the exponent of G = exp(-q/2) comes out
@@ -48,9 +49,9 @@ struct __align__(16) Staged {
 // log2 G = k a dx^2 + 2 k b dx dy + k c dy^2 = fma(fma(kc, dy, 2kb dx), dy, ka dxx)
 // -- two fused multiply-adds where the unscaled form needs four operations
 // plus the log2(e) multiply. Every blend kernel evaluates exactly this
-// sequence (the packed backward stages the raw conic and forms the same scaled
-// coefficients itself), so forward and backward take identical alpha
-// decisions.
+// sequence on the same scale_conic() values (the packed backward gathers the
+// raw conic with cp.async and scales it in place in its mask phase), so
+// forward and backward take identical alpha decisions.
 constexpr float kConicScale = -0.5f * 1.4426950408889634f;
 __device__ __forceinline__ float4 scale_conic(const float4& co) {
   return make_float4(kConicScale * co.x, 2.0f * kConicScale * co.y, kConicScale * co.z, co.w);
@@ -491,7 +492,9 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
   }
   float2 acc0 = bc2(0.0f), acc1 = bc2(0.0f), acc2 = bc2(0.0f);
   const float hw = 0.5f * (float)cam.W, hh = 0.5f * (float)cam.H;
-  const float scale[kNParam] = {-hw, -hh, -0.5f, -0.5f, -0.5f, 1.0f, 1.0f, 1.0f, 1.0f};
+  // mean2D lane values carry the staged conic's factor k (below): 1/k here
+  const float scale[kNParam] = {-hw / kConicScale, -hh / kConicScale, -0.5f, -0.5f, -0.5f,
+                                1.0f, 1.0f, 1.0f, 1.0f};
   const uint2 range = ranges[tile];
   const uint32_t wmax = __reduce_max_sync(kFull, max(last0, last1));
   if (lane == 0) s_wmax[w] = wmax;
@@ -544,10 +547,14 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
       uint32_t mask = 0;
       if (cur_v[h]) {
         const float4 xy = cur[st].xyi;
+        const float4 co = cur[st].co;
         mask = footprint_mask(xy.x, xy.y, cur[st].col.w, tx0, ty0);
-        // xyi.zw = (id, 1/opacity) for the RED address and the opacity gradient
+        // xyi.zw = (id, k b): RED address, mean2D gradient; co = the walk's
+        // exponent coefficients (scale_conic); col.w = 1/opacity
         *reinterpret_cast<float2*>(&cur[st].xyi.z) =
-            make_float2(__uint_as_float(cur_id[h]), rcp_approx(cur[st].co.w));
+            make_float2(__uint_as_float(cur_id[h]), kConicScale * co.y);
+        cur[st].co = scale_conic(co);
+        cur[st].col.w = rcp_approx(co.w);
       }
       s_mask[st] = (uint8_t)mask;
       cur_id[h] = nxt_id[h];
@@ -570,7 +577,7 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
         const float4 g = cur[j].xyi;
         const float4 co = cur[j].co;
         Eval2 e;
-        eval2<false>(g, co, pfx, npfy, e);
+        eval2<true>(g, co, pfx, npfy, e);
         const float2 Go = mul2(e.G, bc2(co.w));
         const float2 alpha = make_float2(fminf(0.99f, Go.x), fminf(0.99f, Go.y));
         const bool a0 = contributor < last0 && e.power.x <= 0.0f && alpha.x >= 1.0f / 255.0f;
@@ -605,12 +612,13 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
         const float Q = q.x + q.y, Qy = qdy.x + qdy.y;
         const float Qyy = fmaf(qdy.y, e.dy.y, qdy.x * e.dy.x);
         const float tq = e.dx * Q;
-        float v[kNParam] = {fmaf(co.x, tq, co.y * Qy),
-                            fmaf(co.z, Qy, co.y * tq),
+        // co = (k a, 2 k b, k c), g.w = k b: mean2D = k (a dx Q + b Qy, c Qy + b dx Q)
+        float v[kNParam] = {fmaf(co.x, tq, g.w * Qy),
+                            fmaf(co.z, Qy, g.w * tq),
                             e.dxx * Q,
                             e.dx * Qy,
                             Qyy,
-                            Q * g.w,
+                            Q * c.w,
                             fmaf(dcd.y, dL0.y, dcd.x * dL0.x),
                             fmaf(dcd.y, dL1.y, dcd.x * dL1.x),
                             fmaf(dcd.y, dL2.y, dcd.x * dL2.x)};
