@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
     last0 = ls[0];
     last1 = ls[1];
   }
-  float2 acc0 = bc2(0.0f), acc1 = bc2(0.0f), acc2 = bc2(0.0f);
+  float2 accd = bc2(0.0f);  // per pixel: (accumulated colour behind) . dL/dpixel
   const float hw = 0.5f * (float)cam.W, hh = 0.5f * (float)cam.H;
   // mean2D lane values carry the staged conic's factor k (below): 1/k here
   const float scale[kNParam] = {-hw / kConicScale, -hh / kConicScale, -0.5f, -0.5f, -0.5f,
@@ -592,14 +592,13 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
         const float2 inv = make_float2(rcp_approx(om.x), rcp_approx(om.y));
         T = mul2(T, inv);
         const float2 dcd = mul2(am, T);
-        const float2 d0 = fma2(acc0, bc2(-1.0f), bc2(c.x));  // c - acc
-        const float2 d1 = fma2(acc1, bc2(-1.0f), bc2(c.y));
-        const float2 d2 = fma2(acc2, bc2(-1.0f), bc2(c.z));
-        float2 dLa = fma2(d2, dL2, fma2(d1, dL1, mul2(d0, dL0)));
-        dLa = fma2(dLa, T, mul2(nTb, inv));
-        acc0 = fma2(am, d0, acc0);
-        acc1 = fma2(am, d1, acc1);
-        acc2 = fma2(am, d2, acc2);
+        // dL/dalpha's colour term sum_ch (c_ch - acc_ch) dL_ch = CD - S with
+        // CD = c . dL and S = acc . dL carried instead of the three colour
+        // accumulators: acc += am (c - acc) gives S += am (CD - S)
+        const float2 CD = fma2(bc2(c.z), dL2, fma2(bc2(c.y), dL1, mul2(bc2(c.x), dL0)));
+        const float2 dcol = add2(CD, make_float2(-accd.x, -accd.y));
+        accd = fma2(am, dcol, accd);
+        const float2 dLa = fma2(dcol, T, mul2(nTb, inv));
         // Lane sums of the nine gradients with the factors -W/2, -H/2 (mean2D)
         // and -1/2 (conic) left for after the warp sum. With q = o G dL/dalpha
         // per pixel and dx shared by the lane's two pixels:
