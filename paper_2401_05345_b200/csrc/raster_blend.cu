@@ -317,18 +317,14 @@ struct Eval2 {
   float dx, dxx;
   float2 dy, power, G;
 };
-// STAGED_SCALED: co is already scale_conic()'d (the forward's and the native
-// backward's staging); otherwise it is the raw conic and the same three
-// scaled coefficients are formed here -- bit-identical values either way.
-template <bool STAGED_SCALED>
-__device__ __forceinline__ void eval2(const float4& g, const float4& co_in, float pfx, float2 npfy,
+// co is the staged scale_conic() conic (every blend kernel stages or
+// rewrites it so), g.xy the mean.
+__device__ __forceinline__ void eval2(const float4& g, const float4& co, float pfx, float2 npfy,
                                       Eval2& e) {
-  const float4 co = STAGED_SCALED ? co_in : scale_conic(co_in);
   e.dx = g.x - pfx;
   e.dy = add2(bc2(g.y), npfy);
   e.dxx = e.dx * e.dx;
-  // co is the staged (pre-scaled) conic: power = log2 G (its sign is the
-  // unscaled power's), in Horner form over dy -- the lane's two pixels share
+  // power = log2 G (its sign is the unscaled power's), in Horner form over dy -- the lane's two pixels share
   // dx: power = (k a dx^2) + dy (2 k b dx + k c dy)
   e.power = fma2(fma2(bc2(co.z), e.dy, bc2(co.y * e.dx)), e.dy, bc2(co.x * e.dxx));
   e.G = make_float2(ex2_approx(e.power.x), ex2_approx(e.power.y));
@@ -390,7 +386,7 @@ __global__ void __launch_bounds__(128)
         const float4 g = sm[j].xyi;
         const float4 co = sm[j].co;
         Eval2 e;
-        eval2<true>(g, co, pfx, npfy, e);
+        eval2(g, co, pfx, npfy, e);
         const float2 Go = mul2(e.G, bc2(co.w));
         const float2 alpha = make_float2(fminf(0.99f, Go.x), fminf(0.99f, Go.y));
         const float2 test_T = mul2(T, add2(bc2(1.0f), make_float2(-alpha.x, -alpha.y)));
@@ -577,7 +573,7 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
         const float4 g = cur[j].xyi;
         const float4 co = cur[j].co;
         Eval2 e;
-        eval2<true>(g, co, pfx, npfy, e);
+        eval2(g, co, pfx, npfy, e);
         const float2 Go = mul2(e.G, bc2(co.w));
         const float2 alpha = make_float2(fminf(0.99f, Go.x), fminf(0.99f, Go.y));
         const bool a0 = contributor < last0 && e.power.x <= 0.0f && alpha.x >= 1.0f / 255.0f;
