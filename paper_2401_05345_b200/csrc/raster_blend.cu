@@ -575,12 +575,13 @@ __global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
         Eval2 e;
         eval2(g, co, pfx, npfy, e);
         const float2 Go = mul2(e.G, bc2(co.w));
-        const float2 alpha = make_float2(fminf(0.99f, Go.x), fminf(0.99f, Go.y));
-        const bool a0 = contributor < last0 && e.power.x <= 0.0f && alpha.x >= 1.0f / 255.0f;
-        const bool a1 = contributor < last1 && e.power.y <= 0.0f && alpha.y >= 1.0f / 255.0f;
+        // min(0.99, Go) >= 1/255 <=> Go >= 1/255: the clamp waits for the active path
+        const bool a0 = contributor < last0 && e.power.x <= 0.0f && Go.x >= 1.0f / 255.0f;
+        const bool a1 = contributor < last1 && e.power.y <= 0.0f && Go.y >= 1.0f / 255.0f;
         const bool act = a0 || a1;
         const unsigned ballot = __ballot_sync(kFull, act);
         if (ballot == 0u) continue;
+        const float2 alpha = make_float2(fminf(0.99f, Go.x), fminf(0.99f, Go.y));
         const float2 msk = make_float2(a0 ? 1.0f : 0.0f, a1 ? 1.0f : 0.0f);
         const float4 c = cur[j].col;
         const float2 am = mul2(alpha, msk);
