@@ -13,10 +13,12 @@
 // Footprint bound. alpha = min(0.99, o G) >= 1/255 with G = exp(-q/2),
 // q = d^T Q d (Q = conic), needs q <= tau = 2 ln(255 o). The ellipse
 // q <= tau lies in |dx| <= sqrt(tau Q^-1_xx), |dy| <= sqrt(tau Q^-1_yy), with
-// Q^-1_xx = c / (ac - b^2), Q^-1_yy = a / (ac - b^2). The kernel inflates tau
-// by 5 % + 0.05 to cover __expf and FMA rounding, so culling never drops a
-// pair the per-lane test would keep (o <= 1/255 -> never active; a
-// degenerate conic falls back to no culling).
+// Q^-1_xx = c / (ac - b^2), Q^-1_yy = a / (ac - b^2). The preprocess computes
+// these half-extents once per Gaussian (raster_preprocess.cu
+// footprint_extents), inflating tau by 5 % + 0.05 to cover the exp2
+// approximation and FMA rounding and rounding up to half precision, so
+// culling never drops a pair the per-lane test would keep (o <= 1/255 ->
+// never active; a degenerate conic falls back to no culling).
 //
 // Backward: the GradComputation loop of PAPER.md:1481-1504 -- each pixel
 // thread walks its Gaussians back to front, cond1/cond2 are the
