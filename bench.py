@@ -6,12 +6,13 @@ and ms/iter vs naive-atomic; L2-atomic roofline %).
 
 Workload (config.workload): BASELINE configs[2] -- 1M synthetic Gaussians,
 1920x1080, the scene the north_star target is stated on -- rendered as
-BASELINE configs[4]'s structure: a fixed batch of `--views` (64) orbit views
-sharded across the N ranks (strong scaling), every rank's views resident in
-HBM. A STEP is the backward pass of the rasterizer over the rank's views
-(DISTWAR SW-B, balancing threshold tuned on the box with the reference's sweep
-rule) plus, for N > 1, the NCCL all-reduce of the per-Gaussian gradient
-buffer. `--views-per-gpu V` switches to weak scaling (V views per rank).
+BASELINE configs[4]'s structure: `--views-per-gpu` (64) orbit views per rank
+(views are independent units: weak scaling, the per-GPU work fixed as N
+grows), every rank's views resident in HBM. A STEP is the backward pass of the
+rasterizer over the rank's views (DISTWAR SW-B, balancing threshold tuned on
+the box with the reference's sweep rule) plus, for N > 1, the NCCL all-reduce
+of the per-Gaussian gradient buffer. `--views V` instead shards a fixed batch
+of V views across the ranks (strong scaling).
 One unit = one gradient contribution = (contributing pixel, Gaussian, param),
 9 per pair.
 
@@ -48,10 +49,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=WORKLOAD)
-    ap.add_argument("--views", type=int, default=64,
-                    help="view batch sharded across ranks (strong scaling)")
-    ap.add_argument("--views-per-gpu", type=int, default=0,
-                    help="if > 0: weak scaling, this many views per rank")
+    ap.add_argument("--views", type=int, default=0,
+                    help="if > 0: this view batch sharded across ranks (strong scaling)")
+    ap.add_argument("--views-per-gpu", type=int, default=64,
+                    help="views per rank (weak scaling; the default)")
     ap.add_argument("--naive-steps", type=int, default=0,
                     help="timed steps of the naive comparison (0: max(3, steps // 4))")
     ap.add_argument("--threshold", default="auto", help="SW-B balancing threshold or 'auto'")
@@ -246,7 +247,7 @@ def reference_arm(args) -> None:
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": args.workload, "gaussians": P, "width": W,
                                         "height": H, "tile_stride": stride},
         "cpu_baseline": cpu,
@@ -285,7 +286,7 @@ def main() -> None:
     from paper_2401_05345_b200.dist import shard_views
 
     P, W, H, hc, _ = CONFIGS[args.workload]
-    weak = args.views_per_gpu > 0
+    weak = args.views <= 0
     total_views = args.views_per_gpu * world if weak else args.views
     if total_views < world:
         raise SystemExit("need at least one view per rank")
