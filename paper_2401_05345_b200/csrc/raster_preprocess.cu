@@ -36,9 +36,12 @@ __device__ __forceinline__ uint32_t footprint_extents(const float4& co) {
     if (!(det > 0.0f) || !(co.x > 0.0f)) {
       ex = ey = INFINITY;
     } else {
+      // fast-math reciprocal / rsqrt: the 0.2 % margin covers their few-ulp error
       const float tau = 1.05f * 2.0f * __logf(255.0f * co.w) + 0.05f;
-      ex = sqrtf(tau * co.z / det) * 1.001f;
-      ey = sqrtf(tau * co.x / det) * 1.001f;
+      const float rdet = __fdividef(1.0f, det);
+      const float x = tau * co.z * rdet, y = tau * co.x * rdet;
+      ex = x * rsqrtf(x) * 1.002f;
+      ey = y * rsqrtf(y) * 1.002f;
     }
   }
   const __half2 h = __halves2half2(__float2half_ru(ex), __float2half_ru(ey));
