@@ -283,7 +283,13 @@ __global__ void __launch_bounds__(kBlock, DW_BWD_MIN_BLOCKS)
 
 // CTAs per SM the register allocator must allow for the packed kernels (ptxas -v: no spills).
 #ifndef DW_MULTI_MIN_BLOCKS
-#define DW_MULTI_MIN_BLOCKS 8  // A/B on C3: 0.782 vs 0.786 ms (6)
+#define DW_MULTI_MIN_BLOCKS 8
+#endif
+// The timed SW-B instantiation is bounded for 7 CTAs/SM: ptxas then takes 64
+// registers, still 8 CTAs/SM resident (C3 0.711 vs 0.717 ms bounded for 8,
+// 0.750 for 6); the others stay bounded for 8 (SW-S would take 72 registers)
+#ifndef DW_SWB_MIN_BLOCKS
+#define DW_SWB_MIN_BLOCKS 7
 #endif
 
 // ---------------------------------------------------------------------------
@@ -336,7 +342,12 @@ __device__ __forceinline__ void eval2(const float4& g, const float4& co, float p
 // buffer it is slower on C3 (0.869 vs 0.833 ms: early-terminating tiles waste
 // the prefetched batch) and on C4 too (3.49 vs 3.29 ms: the doubled shared
 // memory costs occupancy the latency hiding does not repay).
-__global__ void __launch_bounds__(128)
+#ifdef DW_FWD_MIN_BLOCKS  // A/B hook; by default ptxas picks 48 registers (10 CTAs/SM)
+#define DW_FWD_BOUNDS __launch_bounds__(128, DW_FWD_MIN_BLOCKS)
+#else
+#define DW_FWD_BOUNDS __launch_bounds__(128)
+#endif
+__global__ void DW_FWD_BOUNDS
     k_forward_x2(const CamParams cam, const uint2* __restrict__ ranges,
                  const uint32_t* __restrict__ values, const float2* __restrict__ means2D,
                  const float4* __restrict__ conic_opacity, const float4* __restrict__ rgb,
@@ -437,7 +448,8 @@ __global__ void __launch_bounds__(128)
 // mask / ballot / staging overhead and the warp reduction are paid once per
 // 64 pixels.
 template <int POL, bool COUNT, bool TAP = false>
-__global__ void __launch_bounds__(128, DW_MULTI_MIN_BLOCKS)
+__global__ void __launch_bounds__(128, (POL == kSwB && !COUNT && !TAP) ? DW_SWB_MIN_BLOCKS
+                                                                      : DW_MULTI_MIN_BLOCKS)
     k_backward_x2(const CamParams cam, const uint2* __restrict__ ranges,
                   const uint32_t* __restrict__ values, const float2* __restrict__ means2D,
                   const float4* __restrict__ conic_opacity, const float4* __restrict__ rgb,
