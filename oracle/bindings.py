@@ -104,6 +104,32 @@ class _GsState(C.Structure):
     ]
 
 
+class GsFlip(C.Structure):
+    _fields_ = [("pixel", C.c_int32), ("position", C.c_uint32), ("gaussian", C.c_int32),
+                ("kind", C.c_int32)]
+
+
+class GsVerifyReport(C.Structure):
+    _fields_ = [(k, C.c_int64) for k in (
+        "pairs", "pairs_default", "amb_alpha", "amb_term", "pix_ambiguous", "pix_flipped",
+        "flips", "pix_unresolved", "pix_nomatch", "pix_world_cap")] + [
+        ("max_worlds", C.c_int32), ("nflip_rec", C.c_int32)]
+
+    def as_dict(self):
+        return {k: int(getattr(self, k)) for k, _ in self._fields_}
+
+
+class GsVerifyOut(C.Structure):
+    _fields_ = [("grad", C.c_void_p), ("grad_bound", C.c_void_p), ("grad_abs", C.c_void_p),
+                ("grad_slack", C.c_void_p), ("npix", C.c_void_p), ("image", C.c_void_p),
+                ("image_mag", C.c_void_p), ("image_slack", C.c_void_p), ("final_T", C.c_void_p), ("epix", C.c_void_p),
+                ("n_contrib", C.c_void_p), ("status", C.c_void_p), ("flips", C.c_void_p),
+                ("flip_cap", C.c_int32), ("nflip_rec", C.c_int32)]
+
+
+U_F32 = 2.0 ** -24
+
+
 def _arr(ptr, n, dtype):
     if n == 0:
         return np.zeros(0, dtype=dtype)
@@ -172,9 +198,21 @@ class Oracle:
                                   C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,
                                   C.POINTER(C.c_int64)]
 
+        L.gs_forward_lists.argtypes = [C.POINTER(_GsState), C.c_int32] + [C.c_void_p] * 5 + [
+            C.POINTER(Camera), C.c_int, C.c_int]
+        L.gs_verify_last_error.restype = C.c_char_p
+        L.gs_verify.argtypes = [C.POINTER(_GsState), C.POINTER(Camera), C.c_void_p, C.c_void_p,
+                                C.c_void_p, C.c_void_p, C.c_double, C.POINTER(GsVerifyOut),
+                                C.POINTER(GsVerifyReport), C.c_int]
+
     def _check(self, rc):
         if rc != 0:
             raise RuntimeError(self.L.or_last_error().decode())
+
+    # -- decision-matched verification (gs_verify.c) ---------------------
+    def gs_view(self, scene, cam: "Camera", threads=8, with_keys=True) -> "GsView":
+        """Projection + per-tile lists (gs_forward_lists), no blend."""
+        return GsView(self, scene, cam, threads, with_keys)
 
     # -- traces ---------------------------------------------------------
     def _to_numpy(self, tp) -> Trace:
@@ -382,6 +420,95 @@ class Oracle:
                        _arr(s.tap_prim, 32 * r, np.int32),
                        _arr(s.tap_grads, 32 * NPARAM * r, np.float64))
         return dt, int(pairs.value), tr
+
+
+class GsView:
+    """One view's oracle state built by gs_forward_lists; verify() runs the
+    decision-matched blend + backward (gs_verify.c)."""
+
+    def __init__(self, orc: Oracle, scene, cam: Camera, threads: int, with_keys: bool):
+        self.orc, self.cam, self.threads = orc, cam, threads
+        L = orc.L
+        self.st = L.gs_state_new()
+        self.P = int(scene["means3D"].shape[0])
+        ins = [np.ascontiguousarray(scene[k], np.float32)
+               for k in ("means3D", "scales", "rotations", "opacities", "colors")]
+        if L.gs_forward_lists(self.st, self.P, *[a.ctypes.data for a in ins], C.byref(cam),
+                              threads, 1 if with_keys else 0):
+            msg = L.gs_verify_last_error().decode()
+            L.gs_state_free(self.st)
+            self.st = None
+            raise RuntimeError(msg)
+        s = self.st.contents
+        self.W, self.H = s.W, s.H
+        self.num_rendered = int(s.num_rendered)
+        self.with_keys = with_keys
+
+    def __del__(self):
+        if getattr(self, "st", None) is not None:
+            self.orc.L.gs_state_free(self.st)
+            self.st = None
+
+    def lists(self):
+        s = self.st.contents
+        P, nr, ntiles = self.P, self.num_rendered, s.tiles_x * s.tiles_y
+        out = {
+            "means2D": _arr(s.means2D, 2 * P, np.float32).reshape(P, 2),
+            "depths": _arr(s.depths, P, np.float32),
+            "radii": _arr(s.radii, P, np.int32),
+            "conic_opacity": _arr(s.conic_opacity, 4 * P, np.float32).reshape(P, 4),
+            "tiles_touched": _arr(s.tiles_touched, P, np.uint32),
+            "num_rendered": nr,
+            "values": _arr(s.values, nr, np.uint32),
+            "ranges": _arr(s.ranges, 2 * ntiles, np.uint32).reshape(ntiles, 2),
+        }
+        if self.with_keys:
+            out["keys"] = _arr(s.keys, nr, np.uint64)
+        return out
+
+    def verify(self, dL_dpixels=None, gpu=None, kappa=1.0, flip_cap=4096):
+        """gpu: None or (n_contrib [H*W] u32, final_T [H*W] f32, image [3,H,W] f32).
+        Returns (dict of arrays, report dict, flips list)."""
+        P, W, H = self.P, self.W, self.H
+        HW = W * H
+        o = {
+            "grad": np.zeros(P * NPARAM), "grad_bound": np.zeros(P * NPARAM),
+            "grad_abs": np.zeros(P * NPARAM), "grad_slack": np.zeros(P * NPARAM),
+            "npix": np.zeros(P, np.int32), "image": np.zeros(3 * HW),
+            "image_mag": np.zeros(3 * HW), "image_slack": np.zeros(3 * HW), "final_T": np.zeros(HW), "epix": np.zeros(HW),
+            "n_contrib": np.zeros(HW, np.uint32), "status": np.zeros(HW, np.uint8),
+        }
+        flips = (GsFlip * max(flip_cap, 1))()
+        out = GsVerifyOut(**{k: v.ctypes.data for k, v in o.items()}, flips=C.addressof(flips),
+                          flip_cap=flip_cap, nflip_rec=0)
+        rep = GsVerifyReport()
+        keep = []
+        dl = None
+        if dL_dpixels is not None:
+            dl = np.ascontiguousarray(dL_dpixels, np.float32)
+            keep.append(dl)
+        g = [None, None, None]
+        if gpu is not None:
+            g = [np.ascontiguousarray(gpu[0], np.uint32).reshape(-1),
+                 np.ascontiguousarray(gpu[1], np.float32).reshape(-1),
+                 np.ascontiguousarray(gpu[2], np.float32).reshape(-1)]
+            assert g[0].size == HW and g[1].size == HW and g[2].size == 3 * HW
+        L = self.orc.L
+        rc = L.gs_verify(self.st, C.byref(self.cam), dl.ctypes.data if dl is not None else None,
+                         *[a.ctypes.data if a is not None else None for a in g], float(kappa),
+                         C.byref(out), C.byref(rep), self.threads)
+        if rc:
+            raise RuntimeError(L.gs_verify_last_error().decode())
+        o["grad"] = o["grad"].reshape(P, NPARAM)
+        for k in ("grad_bound", "grad_abs", "grad_slack"):
+            o[k] = o[k].reshape(P, NPARAM)
+        o["image"] = o["image"].reshape(3, H, W)
+        o["image_mag"] = o["image_mag"].reshape(3, H, W)
+        o["image_slack"] = o["image_slack"].reshape(3, H, W)
+        for k in ("final_T", "epix", "n_contrib", "status"):
+            o[k] = o[k].reshape(H, W)
+        fl = [(f.pixel, f.position, f.gaussian, f.kind) for f in flips[:out.nflip_rec]]
+        return o, rep.as_dict(), fl
 
 
 def scene_spec_for(num_prims: int, n: int) -> SceneSpec:

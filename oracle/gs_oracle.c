@@ -20,6 +20,7 @@
  * compared under a stated tolerance (tests/test_gpu_raster.py).
  */
 #include "gs_oracle.h"
+#include "gs_internal.h"
 
 #include <math.h>
 #include <pthread.h>
@@ -117,7 +118,7 @@ static void cov2d(const float* tv, float fx, float fy, float tfx, float tfy,
   out3[2] = c + 0.3f;
 }
 
-static void preprocess_one(int i, const float* means3D, const float* scales,
+void gs_i_preprocess_one(int i, const float* means3D, const float* scales,
                            const float* rotations, const float* opacities,
                            const float* colors, const gs_camera* cam, gs_state* s) {
   s->radii[i] = 0;
@@ -173,7 +174,7 @@ static void preprocess_one(int i, const float* means3D, const float* scales,
   s->tiles_touched[i] = (uint32_t)area;
 }
 
-static void rect_of(const gs_state* s, int i, int* r) {
+void gs_i_rect_of(const gs_state* s, int i, int* r) {
   const float ix = s->means2D[2 * i], iy = s->means2D[2 * i + 1];
   const float fr = (float)s->radii[i];
   int v[4] = {(int)((ix - fr) / (float)GS_TILE), (int)((iy - fr) / (float)GS_TILE),
@@ -290,7 +291,7 @@ int gs_forward(gs_state* s, int32_t P, const float* means3D, const float* scales
   s->final_T = calloc(npix, sizeof(float));
   s->n_contrib = calloc(npix, sizeof(uint32_t));
   for (int i = 0; i < P; ++i)
-    preprocess_one(i, means3D, scales, rotations, opacities, colors, cam, s);
+    gs_i_preprocess_one(i, means3D, scales, rotations, opacities, colors, cam, s);
   /* duplicate keys in (Gaussian, row, column) order */
   int64_t total = 0;
   for (int i = 0; i < P; ++i) total += s->tiles_touched[i];
@@ -301,7 +302,7 @@ int gs_forward(gs_state* s, int32_t P, const float* means3D, const float* scales
   for (int i = 0; i < P; ++i) {
     if (s->radii[i] <= 0) continue;
     int r[4];
-    rect_of(s, i, r);
+    gs_i_rect_of(s, i, r);
     uint32_t dbits;
     memcpy(&dbits, &s->depths[i], 4);
     for (int y = r[1]; y < r[3]; ++y)

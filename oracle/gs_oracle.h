@@ -80,6 +80,67 @@ int gs_preprocess_backward(const gs_state* s, int32_t P, const float* means3D,
 void gs_adam(int64_t n, double* param, const double* grad, double* m, double* v, double lr,
              double beta1, double beta2, double eps, int step);
 
+
+/* ---- decision-matched verification (gs_verify.c) -------------------------- */
+
+/* Projection + per-tile lists by (depth, index) bucketing: the lists of
+ * gs_forward without its blend (out_color / final_T / n_contrib stay zero);
+ * keys only when with_keys (C4 has 0.9 G instances). */
+int gs_forward_lists(gs_state* s, int32_t P, const float* means3D, const float* scales,
+                     const float* rotations, const float* opacities, const float* colors,
+                     const gs_camera* cam, int threads, int with_keys);
+
+typedef struct gs_flip {
+  int32_t pixel;      /* y * W + x */
+  uint32_t position;  /* tile-list position of the decision */
+  int32_t gaussian;   /* Gaussian id */
+  int32_t kind;       /* 0 alpha >= 1/255 test, 1 T >= 1e-4 termination test */
+} gs_flip;
+
+typedef struct gs_verify_report {
+  int64_t pairs;          /* blended (pixel, Gaussian) pairs in the matched worlds */
+  int64_t pairs_default;  /* ... in the oracle's own world (no flips) */
+  int64_t amb_alpha;      /* ambiguous alpha decisions met (default world) */
+  int64_t amb_term;       /* ambiguous termination decisions met (default world) */
+  int64_t pix_ambiguous;  /* pixels with >= 2 worlds */
+  int64_t pix_flipped;    /* pixels whose matched world is not the default */
+  int64_t flips;          /* flipped decisions in the matched worlds */
+  int64_t pix_unresolved; /* the GPU outputs fit >1 world (grad_slack covers) */
+  int64_t pix_nomatch;    /* no world fits the GPU outputs: FAILURE */
+  int64_t pix_world_cap;  /* world enumeration truncated: FAILURE */
+  int32_t max_worlds;
+  int32_t nflip_rec;
+} gs_verify_report;
+
+typedef struct gs_verify_out {
+  double* grad;        /* P*9 gradients of the matched worlds (float64 arithmetic) */
+  double* grad_bound;  /* P*9 sum of E_pix * |term| magnitude, units of u = 2^-24 */
+  double* grad_abs;    /* P*9 sum of |term| */
+  double* grad_slack;  /* P*9 world spread of unresolved pixels (normally 0) */
+  int32_t* npix;       /* P contributing pixels per Gaussian */
+  double* image;       /* 3*H*W */
+  double* image_mag;   /* 3*H*W sum |c alpha T| + T |bg| */
+  double* image_slack; /* 3*H*W without GPU outputs: spread over the worlds (else 0) */
+  double* final_T;     /* H*W */
+  double* epix;        /* H*W E_pix, units of u */
+  uint32_t* n_contrib; /* H*W */
+  uint8_t* status;     /* H*W 0 unambiguous, 1 ambiguous-default, 2 flipped, 3 unresolved,
+                          4 no match, 5 world cap */
+  gs_flip* flips;
+  int32_t flip_cap;
+  int32_t nflip_rec;
+} gs_verify_out;
+
+/* Needs the lists of gs_forward or gs_forward_lists. Any output pointer may
+ * be NULL. gpu_* (all three or none): the GPU's per-pixel n_contrib, final_T
+ * and image [3][H][W]; without them every pixel takes the default world and
+ * the spread of the other worlds goes to grad_slack / image_slack.
+ * kappa scales the per-pixel tolerance used to match worlds. */
+int gs_verify(const gs_state* s, const gs_camera* cam, const float* dL_dpixels,
+              const uint32_t* gpu_n_contrib, const float* gpu_final_T, const float* gpu_image,
+              double kappa, gs_verify_out* out, gs_verify_report* rep, int threads);
+const char* gs_verify_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif

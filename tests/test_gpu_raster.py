@@ -1,26 +1,21 @@
-"""GPU parity of the Gaussian-splatting path against the CPU oracle.
-
-Bars (north_star): tile keys, sort order and per-tile ranges BIT-EXACT (the
-preprocess kernel is built -fmad=false and the oracle -ffp-contract=off, in
-the same operation order, so means2D/depths/radii/conics match bit for bit);
-images within 1e-3 absolute (GPU __expf vs CPU expf, FMA contraction in the
-blend); accumulated gradients within a relative L2 error of 2e-3 of the
-oracle's f64 sums, and per element within 1e-3 * (sum of |terms|) + 1e-5 --
-atomic summation order is nondeterministic and single pixels can flip across
-the alpha >= 1/255 / T >= 1e-4 thresholds, so the bound is stated on the
-per-address absolute term sum the oracle also returns.
+"""GPU rasterizer tests around the parity suite (tests/test_gpu_parity_full.py
+holds the decision-matched oracle comparisons at every BASELINE config; the
+bars are stated in tests/parity.py): the reduction tap against the
+reference policies, the host-buffer entry points, reuse, binning-path
+agreement at sizes the oracle sweep does not cover, and argument errors.
 """
 import ctypes as C
 
 import numpy as np
 import pytest
 
+from parity import oracle_views
+
 pytestmark = pytest.mark.gpu
 
-IMG_ATOL = 1e-3
+# legacy-oracle comparisons below (the tap) use the 3DGS-standard exp form
+# of gs_oracle.c, whose decisions can differ from the GPU's log2 form
 GRAD_REL_L2 = 2e-3
-GRAD_ELEM_RTOL = 1e-3
-GRAD_ELEM_ATOL = 1e-5
 
 
 def _ocam(cam):
@@ -30,94 +25,6 @@ def _ocam(cam):
     cc = cam.to_c()
     C.memmove(C.byref(oc), C.byref(cc), C.sizeof(oc))
     return oc
-
-
-def _render(cuda, sc, cam, dL, policy, count=True):
-    import torch
-
-    from paper_2401_05345_b200.rasterizer import GaussianRasterizer
-
-    r = GaussianRasterizer()
-    t = {k: torch.from_numpy(v).to(cuda) for k, v in sc.items()}
-    img, radii, nr = r.render_forward(t["means3D"], t["scales"], t["rotations"], t["opacities"],
-                                      t["colors"], cam)
-    out = r.render_backward(torch.from_numpy(dL).to(cuda), policy, count_pairs=count)
-    grad, pairs = out if count else (out, None)
-    torch.cuda.synchronize()
-    return r, img.cpu().numpy(), radii.cpu().numpy(), nr, grad.cpu().numpy(), pairs
-
-
-CASES = [
-    ("tiny_odd", 300, 61, 47, False, 0),
-    ("c1_10k_256", 10_000, 256, 256, False, 0),
-    ("c2_100k_800", 100_000, 800, 800, False, 0),
-    ("contention_small", 2_000, 320, 200, True, 5),
-]
-
-
-@pytest.fixture(scope="module")
-def cases(orc):
-    from paper_2401_05345_b200.scene import make_camera, make_dL_dpixels, make_scene
-
-    out = {}
-    for name, P, W, H, hc, seed in CASES:
-        sc = make_scene(P, W, H, seed=seed, high_contention=hc)
-        cam = make_camera(W, H)
-        dL = make_dL_dpixels(W, H, seed=seed + 1)
-        ref = orc.gs_render(sc, _ocam(cam), dL, threads=8)
-        out[name] = (sc, cam, dL, ref)
-    return out
-
-
-@pytest.fixture(params=["auto", "depth-first", "tile-first", "dense"])
-def binning(request, monkeypatch):
-    """Every list construction -- depth-first (global depth sort, duplicate,
-    sort by tile), tile-first (duplicate by index, sort by tile, per-tile
-    depth sort) and dense (tile-major) binning -- must give the oracle's
-    lists bit for bit."""
-    if request.param in ("depth-first", "tile-first"):
-        monkeypatch.setenv("DW_DENSE_BINNING", "0")
-        monkeypatch.setenv("DW_TILE_FIRST", "1" if request.param == "tile-first" else "0")
-    elif request.param == "dense":
-        monkeypatch.setenv("DW_DENSE_BINNING", "1")
-    return request.param
-
-
-@pytest.mark.parametrize("name", [c[0] for c in CASES])
-def test_forward_bit_exact_binning_and_image(cuda, cases, name, binning):
-    from paper_2401_05345_b200 import warpred as wr
-
-    sc, cam, dL, ref = cases[name]
-    r, img, radii, nr, _, _ = _render(cuda, sc, cam, dL, wr.Policy(wr.PolicyKind.sw_b, 0))
-    assert np.array_equal(radii, ref["radii"])
-    assert np.array_equal(r.buffer("means2D"), ref["means2D"])
-    assert np.array_equal(r.buffer("depths")[ref["radii"] > 0], ref["depths"][ref["radii"] > 0])
-    assert np.array_equal(r.buffer("conic_opacity")[ref["radii"] > 0],
-                          ref["conic_opacity"][ref["radii"] > 0])
-    assert np.array_equal(r.buffer("tiles_touched"), ref["tiles_touched"])
-    assert nr == ref["num_rendered"]
-    assert np.array_equal(r.buffer("keys"), ref["keys"])
-    assert np.array_equal(r.buffer("values"), ref["values"])
-    assert np.array_equal(r.buffer("ranges"), ref["ranges"])
-    assert np.abs(img - ref["image"]).max() < IMG_ATOL
-    nc = r.buffer("n_contrib").reshape(cam.height, cam.width)
-    assert np.mean(nc != ref["n_contrib"]) < 1e-3
-
-
-@pytest.mark.parametrize("policy", [(0, 0), (2, 0), (2, 8), (2, 33), (1, 0), (1, 16), (3, 0)])
-@pytest.mark.parametrize("name", [c[0] for c in CASES])
-def test_backward_gradients(cuda, cases, name, policy):
-    from paper_2401_05345_b200 import warpred as wr
-
-    sc, cam, dL, ref = cases[name]
-    _, _, _, _, grad, pairs = _render(cuda, sc, cam, dL, wr.Policy(wr.PolicyKind(policy[0]), policy[1]))
-    g = grad.astype(np.float64)
-    want, gabs = ref["grad"], ref["grad_abs"]
-    rel = np.linalg.norm(g - want) / max(np.linalg.norm(want), 1e-30)
-    assert rel < GRAD_REL_L2, rel
-    bad = np.abs(g - want) > GRAD_ELEM_RTOL * gabs + GRAD_ELEM_ATOL
-    assert bad.mean() < 1e-3, (bad.sum(), np.argwhere(bad)[:5])
-    assert abs(pairs - ref["pairs"]) <= max(2, ref["pairs"] // 10_000)
 
 
 def test_red_count_matches_reference_policy_on_tapped_trace(cuda, orc):
@@ -231,15 +138,21 @@ def _reds_of_last_backward(r):
     return val.value
 
 
-def test_render_host_e2e(cuda, cases):
+def test_render_host_e2e(cuda, orc):
+    """dw_render_host from host buffers == the oracle (image and gradients
+    within the parity bounds of tests/parity.py)."""
     from paper_2401_05345_b200 import warpred as wr
     from paper_2401_05345_b200.rasterizer import GaussianRasterizer
+    from paper_2401_05345_b200.scene import make_camera, make_dL_dpixels, make_scene
 
-    sc, cam, dL, ref = cases["c1_10k_256"]
+    P, W, H = 10_000, 256, 256
+    sc = make_scene(P, W, H, seed=2)
+    cam = make_camera(W, H)
+    dL = make_dL_dpixels(W, H, seed=3)
+    imgs, ib, want, tol = oracle_views(orc, sc, [cam], [dL])
     img, grad = GaussianRasterizer().render_host(sc, cam, dL, wr.Policy(wr.PolicyKind.sw_b, 0))
-    assert np.abs(img - ref["image"]).max() < IMG_ATOL
-    rel = np.linalg.norm(grad - ref["grad"]) / np.linalg.norm(ref["grad"])
-    assert rel < GRAD_REL_L2
+    assert np.all(np.abs(img - imgs[0]) <= ib[0])
+    assert np.all(np.abs(grad.astype(np.float64) - want) <= tol)
 
 
 @pytest.mark.parametrize("binning", ["auto", "dense"])
@@ -260,12 +173,9 @@ def test_render_views_host_matches_per_view(cuda, orc, binning, monkeypatch):
     sc = make_scene(P, W, H, seed=31)
     cams = orbit_cameras(W, H, V)
     dL = np.stack([make_dL_dpixels(W, H, seed=40 + k) for k in range(V)])
-    want_g = np.zeros((P, 9))
-    want_img = []
-    for k in range(V):
-        ref = orc.gs_render(sc, _ocam(cams[k]), dL[k], threads=8)
-        want_g += ref["grad"]
-        want_img.append(ref["image"])
+    want_img, ib, want_g, tol = oracle_views(orc, sc, cams, list(dL))
+    # one fp32 addition per view on top of the per-view bounds
+    tol = tol + V * 2.0 ** -24 * np.abs(want_g)
     pin = {k: torch.from_numpy(v).pin_memory() for k, v in sc.items()}
     dL_h = torch.from_numpy(dL.astype(np.float32)).pin_memory()
     img = torch.empty((V, 3, H, W), dtype=torch.float32).pin_memory()
@@ -276,9 +186,9 @@ def test_render_views_host_matches_per_view(cuda, orc, binning, monkeypatch):
         render_views_host(r, ptrs, P, cams, dL_h.data_ptr(), wr.Policy(wr.PolicyKind.sw_b, 8),
                           img.data_ptr(), grad.data_ptr())
         for k in range(V):
-            assert np.abs(img[k].numpy() - want_img[k]).max() < IMG_ATOL
+            assert np.all(np.abs(img[k].numpy() - want_img[k]) <= ib[k])
         g = grad.numpy().astype(np.float64)
-        assert np.linalg.norm(g - want_g) / np.linalg.norm(want_g) < GRAD_REL_L2
+        assert np.all(np.abs(g - want_g) <= tol)
 
 
 def test_binning_paths_agree_on_long_lists(cuda, monkeypatch):
@@ -358,11 +268,10 @@ def test_render_views_host_reserve_overflow_redo(cuda, orc):
     cams = [make_camera(W, H, fov_x_deg=150.0), make_camera(W, H), make_camera(W, H, yaw_deg=5.0)]
     V = len(cams)
     dL = np.stack([make_dL_dpixels(W, H, seed=60 + k) for k in range(V)])
-    want_g = np.zeros((P, 9))
-    refs = [orc.gs_render(sc, _ocam(cams[k]), dL[k], threads=8) for k in range(V)]
-    for ref in refs:
-        want_g += ref["grad"]
-    assert refs[1]["num_rendered"] > refs[0]["num_rendered"] * 3 // 2 + 4096
+    nrs = [orc.gs_view(sc, _ocam(c), threads=8).num_rendered for c in cams]
+    assert nrs[1] > nrs[0] * 3 // 2 + 4096
+    want_img, ib, want_g, tol = oracle_views(orc, sc, cams, list(dL))
+    tol = tol + V * 2.0 ** -24 * np.abs(want_g)
     pin = {k: torch.from_numpy(v).pin_memory() for k, v in sc.items()}
     dL_h = torch.from_numpy(dL.astype(np.float32)).pin_memory()
     img = torch.empty((V, 3, H, W), dtype=torch.float32).pin_memory()
@@ -372,14 +281,15 @@ def test_render_views_host_reserve_overflow_redo(cuda, orc):
     render_views_host(r, ptrs, P, cams, dL_h.data_ptr(), wr.Policy(wr.PolicyKind.sw_b, 8),
                       img.data_ptr(), grad.data_ptr())
     for k in range(V):
-        assert np.abs(img[k].numpy() - refs[k]["image"]).max() < IMG_ATOL
+        assert np.all(np.abs(img[k].numpy() - want_img[k]) <= ib[k])
     g = grad.numpy().astype(np.float64)
-    assert np.linalg.norm(g - want_g) / np.linalg.norm(want_g) < GRAD_REL_L2
+    assert np.all(np.abs(g - want_g) <= tol)
 
 
 def test_full_size_c3_properties(cuda):
-    """BASELINE configs[2] at full size (1M Gaussians, 1920x1080), where the
-    CPU oracle is too slow: size-independent properties. The (tile | depth)
+    """BASELINE configs[2] at full size (1M Gaussians, 1920x1080): the
+    size-independent properties, beside the oracle comparison of
+    test_gpu_parity_full.py. The (tile | depth)
     keys are sorted, the tile ranges partition the instance list and hold
     only their own tile; every reduction policy and threshold yields the same
     contributing pairs, RED counts that follow the policy (native = 9 per
