@@ -536,6 +536,7 @@ class Ref:
         L.ref_num_primitives.argtypes = [C.c_void_p]
         L.ref_num_primitives.restype = C.c_int32
         L.ref_export.argtypes = [C.c_void_p] + [C.c_void_p] * 5
+        L.ref_criterion1_draws.argtypes = [C.c_int32, C.c_void_p, C.c_void_p]
         L.ref_oracle_sum.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
         L.ref_apply_policy.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int32, C.c_void_p,
                                        C.c_void_p]
@@ -599,6 +600,19 @@ class Ref:
         touched = np.zeros(num_prims * n, np.uint8)
         self._check(self.L.ref_oracle_sum(h, num_prims, sums.ctypes.data, touched.ctypes.data))
         return sums, touched.astype(bool)
+
+    def criterion1_draws(self, ntraces: int):
+        """The (SceneSpec, thresholds) sequence of the reference's acceptance
+        criterion 1 (tests/acceptance.cpp:93-146); thresholds[p] = (sw_s, sw_b)
+        of preset p."""
+        specs = (SceneSpec * ntraces)()
+        thr = np.zeros(ntraces * 6, np.int32)
+        self._check(self.L.ref_criterion1_draws(ntraces, C.addressof(specs), thr.ctypes.data))
+        out = []
+        for i in range(ntraces):
+            d = {k: getattr(specs[i], k) for k, _ in SceneSpec._fields_}
+            out.append((d, thr[6 * i:6 * i + 6].reshape(3, 2).tolist()))
+        return out
 
     def apply_policy(self, h, kind, threshold, num_prims):
         n = self.L.ref_params(h)

@@ -13,6 +13,11 @@ Outputs (committed, small):
                                 its per-address sums.
   tests/golden/records.json     single-record request streams (apply_policy)
                                 for random convergent / divergent records.
+  tests/golden/criterion1.json  the first CRIT1_TRACES traces of the
+                                reference's acceptance criterion 1 (its own
+                                mt19937_64 draw sequence, acceptance.cpp:93-146):
+                                spec, and per (policy, threshold) drawn the
+                                reference's request count and sums sha256.
 The BASELINE trace family (C1..C4) is recorded by hash only.
 """
 from __future__ import annotations
@@ -65,6 +70,7 @@ FAMILY_T = [
                 locality=1.0, activity_prob=0.9, seed=1)),
 ]
 THRESHOLDS = [0, 1, 8, 16, 24, 32, 33]
+CRIT1_TRACES = 200
 
 
 def sha(a: np.ndarray) -> str:
@@ -143,7 +149,34 @@ def main() -> None:
                                  threshold=t, requests=reqs, instructions=ins, fp_adds=fp))
     with open(os.path.join(OUT, "records.json"), "w") as f:
         json.dump(recs, f)
+    write_criterion1(ref)
     print("wrote", OUT)
+
+
+def write_criterion1(ref: Ref) -> None:
+    traces = []
+    for spec_kw, thr in ref.criterion1_draws(CRIT1_TRACES):
+        spec = scene(**spec_kw)
+        h = ref.generate(spec)
+        P = spec.num_primitives
+        sums, _ = ref.oracle_sum(h, P)
+        runs = {}
+        # per preset, the acceptance loop runs native, sw_s, sw_b, cccl (and
+        # hw_atomred, which has no core policy); thresholds as drawn
+        for ss, sb in thr:
+            for kind, name, t in ((NATIVE, "native", 0), (SW_S, "sw_s", ss), (SW_B, "sw_b", sb),
+                                  (CCCL, "cccl", 0)):
+                key = f"{name}:{t}"
+                if key in runs:
+                    continue
+                s, c = ref.apply_policy(h, kind, t, P)
+                runs[key] = {"requests": c["requests"], "sums_sha256": sha(s)}
+        traces.append({"spec": spec_kw, "records": ref.to_numpy(h).num_records,
+                       "oracle_sum_sha256": sha(sums), "runs": runs})
+        ref.free(h)
+    with open(os.path.join(OUT, "criterion1.json"), "w") as f:
+        json.dump({"generated_by": "oracle/gen_golden.py (reference acceptance criterion-1 draws)",
+                   "traces": traces}, f, indent=0, sort_keys=True)
 
 
 if __name__ == "__main__":

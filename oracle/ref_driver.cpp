@@ -12,6 +12,7 @@
 // `--impl reference` arm. No reference source is copied into this repo; the
 // driver only includes the reference headers in place.
 
+#include <random>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -21,6 +22,7 @@
 #include <thread>
 #include <vector>
 
+#include "warpred/hwsim.hpp"
 #include "warpred/reducers.hpp"
 #include "warpred/trace_io.hpp"
 #include "warpred/workload.hpp"
@@ -270,6 +272,37 @@ int ref_time_policy(const void* h, int kind, int threshold, int32_t num_prims,
     for (int i = 0; i < threads; ++i) qq += q[i];
     *contributions = c;
     *requests = qq;
+  });
+}
+
+// The draw sequence of the reference's acceptance criterion 1
+// (tests/acceptance.cpp:93-146): one mt19937_64(20240801) stream; per trace
+// the nine SceneSpec draws in source order, then per preset (3) and policy
+// (native, sw_s, sw_b, cccl, hw_atomred) a threshold draw for the threshold
+// policies only (reducers::policy_uses_threshold). thresholds[i*6 + 2*p + k]
+// is preset p's sw_s (k = 0) / sw_b (k = 1) threshold of trace i.
+int ref_criterion1_draws(int32_t ntraces, RefScene* specs, int32_t* thresholds) {
+  return guarded([&] {
+    std::mt19937_64 mix(20240801);
+    const int npresets = static_cast<int>(hwsim::preset_names().size());
+    if (npresets != 3) throw std::runtime_error("expected 3 presets");
+    for (int32_t i = 0; i < ntraces; ++i) {
+      RefScene& s = specs[i];
+      s.num_primitives = 50 + static_cast<int32_t>(mix() % 400);
+      s.params_per_primitive = 1 + static_cast<int>(mix() % 4);
+      s.image_width = 32 + 8 * static_cast<int>(mix() % 5);
+      s.image_height = 16 + 4 * static_cast<int>(mix() % 5);
+      s.mean_fragment_span = 8.0 + static_cast<double>(mix() % 48);
+      s.fragments_per_pixel_mean = 1.0 + 0.25 * static_cast<double>(mix() % 5);
+      s.locality = 0.5 + 0.5 * static_cast<double>(mix() % 101) / 100.0;
+      s.activity_prob = 0.3 + 0.7 * static_cast<double>(mix() % 101) / 100.0;
+      s.seed = mix();
+      s.quantized_values = 1;
+      for (int p = 0; p < npresets; ++p) {
+        thresholds[i * 6 + 2 * p + 0] = static_cast<int32_t>(mix() % 33);  // sw_s
+        thresholds[i * 6 + 2 * p + 1] = static_cast<int32_t>(mix() % 33);  // sw_b
+      }
+    }
   });
 }
 

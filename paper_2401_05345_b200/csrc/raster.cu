@@ -38,12 +38,15 @@ void grow(T*& p, size_t& cap, size_t want) {
   cap = n;
 }
 
-// grow() for state that kernels expect zeroed (and leave zeroed) between calls
+// grow() for state that kernels expect zeroed (and leave zeroed) between
+// calls; the zeroing is ordered on the stream that will use the buffer (a
+// synchronous cudaMemset runs on the legacy default stream, which does not
+// order with non-blocking streams)
 template <typename T>
-void grow_zeroed(T*& p, size_t& cap, size_t want) {
+void grow_zeroed(T*& p, size_t& cap, size_t want, cudaStream_t s) {
   if (want <= cap && p) return;
   grow(p, cap, want);
-  DW_CUDA(cudaMemset(p, 0, cap * sizeof(T)));
+  DW_CUDA(cudaMemsetAsync(p, 0, cap * sizeof(T), s));
 }
 
 }  // namespace
@@ -139,13 +142,13 @@ struct dw_rasterizer {
   unsigned int* overflow_dev = nullptr;
   bool count_pending = false;  // num_rendered not read back yet (no-sync forward)
 
-  void ensure_small() {
+  void ensure_small(cudaStream_t s) {
     if (!counters) DW_CUDA(cudaMalloc(&counters, 2 * sizeof(unsigned long long)));
     if (!h_total) DW_CUDA(cudaMallocHost(&h_total, sizeof(uint64_t)));
     if (!live_dev) DW_CUDA(cudaMalloc(&live_dev, sizeof(unsigned long long)));
     if (!overflow_dev) {
       DW_CUDA(cudaMalloc(&overflow_dev, sizeof(unsigned int)));
-      DW_CUDA(cudaMemset(overflow_dev, 0, sizeof(unsigned int)));
+      DW_CUDA(cudaMemsetAsync(overflow_dev, 0, sizeof(unsigned int), s));
     }
   }
 
@@ -170,7 +173,7 @@ struct dw_rasterizer {
       grow(dids[b], cap_d[2 + b], np);
     }
     grow(area_sorted, cap_as, np);
-    grow_zeroed(scan_tmp, cap_scan, dw::scan_temp_bytes(P_));
+    grow_zeroed(scan_tmp, cap_scan, dw::scan_temp_bytes(P_), nullptr);
     grow(ranges, cap_t, ntiles);
     grow(tile_order, cap_to, ntiles);
     grow(final_T, cap_px, npx);
@@ -188,7 +191,10 @@ struct dw_rasterizer {
     }
     ensure_tmp(std::max(dw::radix_sort_temp_bytes(P_),
                         dw::radix_sort_temp_bytes(static_cast<int64_t>(std::min(cap_i[0], cap_i[2])))));
-    ensure_small();
+    ensure_small(nullptr);
+    // reserve() takes no stream: the zeroing above ran on the legacy stream,
+    // so complete it before any stream (blocking or not) uses the buffers
+    DW_CUDA(cudaDeviceSynchronize());
   }
 
   // Host view of the instance count (reads the device value back after a
@@ -246,14 +252,14 @@ struct dw_rasterizer {
     grow(tile_order, cap_to, static_cast<size_t>(ntiles));
     grow(final_T, cap_px, static_cast<size_t>(W) * H);
     grow(n_contrib, cap_px2, static_cast<size_t>(W) * H);
-    ensure_small();
+    ensure_small(s);
 
     for (int b = 0; b < 2; ++b) {
       grow(dkey[b], cap_d[b], np);
       grow(dids[b], cap_d[2 + b], np);
     }
     grow(area_sorted, cap_as, np);
-    grow_zeroed(scan_tmp, cap_scan, dw::scan_temp_bytes(P));
+    grow_zeroed(scan_tmp, cap_scan, dw::scan_temp_bytes(P), s);
 
     // Tile-first binning (default): instances duplicated in index order, sorted
     // by tile, each tile's list then depth-sorted on chip. Depth-first: all P
@@ -469,10 +475,11 @@ dw::HostTrace raster_backward_tap(dw_rasterizer* r, const float* dL, int thr, fl
     }
   } guard{tb};
   DW_CUDA(cudaMemsetAsync(tb.count, 0, sizeof(unsigned long long), s));
-  if (r->P > 0)
+  if (r->P > 0) {  // an empty scene has no lists (and no tile order) to walk
     r->ensure_order(s);
     launch_backward_tap(r->cam, r->ranges, r->vals, r->means2D, r->conic_opacity, r->rgb,
                         r->order_or_null(), r->final_T, r->n_contrib, dL, thr, grad, tb, s);
+  }
   unsigned long long count = 0;
   DW_CUDA(cudaMemcpyAsync(&count, tb.count, sizeof(count), cudaMemcpyDeviceToHost, s));
   DW_CUDA(cudaStreamSynchronize(s));

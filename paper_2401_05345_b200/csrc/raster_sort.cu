@@ -23,6 +23,7 @@
 //              element order; __match_any_sync ranks lanes within a warp,
 //              an smem per-digit prefix over the 8 warps orders the warps,
 //              a running per-digit base orders the rounds; then scatter.
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1132,13 +1133,18 @@ void launch_dense_binning(int P, const uint32_t* order, const float2* means2D, c
   const size_t dbytes = dense_diff_bytes(cam.tiles_x, cam.tiles_y);
   const int ntiles = cam.tiles_x * cam.tiles_y;
   int* diff = scratch;  // kDenseSeg + 1 grids
-  static bool attr_set = false;  // > 48 KB dynamic smem for 4K-class grids
-  if (!attr_set) {
+  // > 48 KB dynamic smem for 4K-class grids: a per-device, per-kernel
+  // attribute, so the opt-in is cached per device (a racing first call just
+  // sets it twice)
+  static std::atomic<bool> attr_set[64];
+  int dev = 0;
+  DW_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64 || !attr_set[dev].load(std::memory_order_acquire)) {
     DW_CUDA(cudaFuncSetAttribute(k_dense_rects, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  96 * 1024));
     DW_CUDA(cudaFuncSetAttribute(k_dense_prefix2d, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  96 * 1024));
-    attr_set = true;
+    if (dev >= 0 && dev < 64) attr_set[dev].store(true, std::memory_order_release);
   }
   DW_CUDA(cudaMemsetAsync(diff, 0, (kDenseSeg + 1) * dbytes, s));
   const int per_seg = std::max(1, std::min<int>(static_cast<int>(blocks_for(P, 256 * kDenseSeg)), 16));

@@ -49,12 +49,12 @@ class Adam:
         self.t += 1
         s = self.scene
         f32 = torch.float32
+        P, sp = _scene_ptrs(s["means3D"], s["scales"], s["rotations"], s["opacities"],
+                            s["colors"])
         check(lib().dw_adam_step(
-            int(s["means3D"].shape[0]), _ptr(s["means3D"], "means3D", f32),
-            _ptr(s["scales"], "scales", f32), _ptr(s["rotations"], "rotations", f32),
-            _ptr(s["opacities"], "opacities", f32), _ptr(s["colors"], "colors", f32),
-            _ptr(grad3d, "grad3d", f32), _ptr(self.exp_avg, "exp_avg", f32),
-            _ptr(self.exp_avg_sq, "exp_avg_sq", f32), C.byref(self.cfg), self.t,
+            P, *sp, _ptr(grad3d, "grad3d", f32, min_numel=NPARAM3D * P),
+            _ptr(self.exp_avg, "exp_avg", f32, NPARAM3D * P),
+            _ptr(self.exp_avg_sq, "exp_avg_sq", f32, NPARAM3D * P), C.byref(self.cfg), self.t,
             _stream(stream)))
 
 # dw_rasterizer_buffer ids
@@ -65,18 +65,38 @@ BUFFERS = {"means2D": (0, np.float32, 2), "depths": (1, np.float32, 1),
            "final_T": (8, np.float32, 1), "n_contrib": (9, np.uint32, 1)}
 
 
-def _ptr(t, name, dtype=None):
+def _ptr(t, name, dtype=None, numel=None, min_numel=None):
+    """Raw device pointer of a tensor the C side will trust blindly: type,
+    device (the current one), contiguity, dtype and element count are
+    checked here, so a wrong-shaped buffer raises instead of corrupting HBM."""
     import torch
 
     if not isinstance(t, torch.Tensor):
         raise TypeError(f"{name} must be a torch.Tensor")
     if not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor")
+    if t.device.index != torch.cuda.current_device():
+        raise ValueError(f"{name} is on {t.device}, the current device is "
+                         f"cuda:{torch.cuda.current_device()}")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
     if dtype is not None and t.dtype != dtype:
         raise ValueError(f"{name} must be {dtype}")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"{name} must have {numel} elements, has {t.numel()}")
+    if min_numel is not None and t.numel() < min_numel:
+        raise ValueError(f"{name} must have at least {min_numel} elements, has {t.numel()}")
     return t.data_ptr()
+
+
+def _scene_ptrs(means3D, scales, rotations, opacities, colors):
+    import torch
+
+    f32 = torch.float32
+    P = int(means3D.shape[0])
+    return P, (_ptr(means3D, "means3D", f32, 3 * P), _ptr(scales, "scales", f32, 3 * P),
+               _ptr(rotations, "rotations", f32, 4 * P), _ptr(opacities, "opacities", f32, P),
+               _ptr(colors, "colors", f32, 3 * P))
 
 
 def _stream(stream):
@@ -116,7 +136,7 @@ class GaussianRasterizer:
         import torch
 
         f32 = torch.float32
-        P = int(means3D.shape[0])
+        P, sp = _scene_ptrs(means3D, scales, rotations, opacities, colors)
         if out_color is None:
             out_color = torch.empty((3, camera.height, camera.width), dtype=f32,
                                     device=means3D.device)
@@ -125,10 +145,9 @@ class GaussianRasterizer:
         nr = C.c_int64()
         cam = camera.to_c()
         check(lib().dw_render_forward(
-            self._h, P, _ptr(means3D, "means3D", f32), _ptr(scales, "scales", f32),
-            _ptr(rotations, "rotations", f32), _ptr(opacities, "opacities", f32),
-            _ptr(colors, "colors", f32), C.byref(cam), _ptr(out_color, "out_color", f32),
-            _ptr(radii, "radii", torch.int32), C.byref(nr), _stream(stream)))
+            self._h, P, *sp, C.byref(cam),
+            _ptr(out_color, "out_color", f32, 3 * camera.height * camera.width),
+            _ptr(radii, "radii", torch.int32, P), C.byref(nr), _stream(stream)))
         self.P, self.num_rendered, self.camera = P, nr.value, camera
         return out_color, radii, nr.value
 
@@ -146,13 +165,12 @@ class GaussianRasterizer:
         import torch
 
         f32 = torch.float32
-        P = int(means3D.shape[0])
+        P, sp = _scene_ptrs(means3D, scales, rotations, opacities, colors)
         cam = camera.to_c()
         check(lib().dw_render_forward_async(
-            self._h, P, _ptr(means3D, "means3D", f32), _ptr(scales, "scales", f32),
-            _ptr(rotations, "rotations", f32), _ptr(opacities, "opacities", f32),
-            _ptr(colors, "colors", f32), C.byref(cam), _ptr(out_color, "out_color", f32),
-            _ptr(radii, "radii", torch.int32), _stream(stream)))
+            self._h, P, *sp, C.byref(cam),
+            _ptr(out_color, "out_color", f32, 3 * camera.height * camera.width),
+            _ptr(radii, "radii", torch.int32, P), _stream(stream)))
         self.P, self.num_rendered, self.camera = P, None, camera
         return out_color, radii
 
@@ -169,13 +187,17 @@ class GaussianRasterizer:
         (grad, pairs) when count_pairs (a separate counting instantiation)."""
         import torch
 
-        if grad is None:
-            grad = torch.zeros((self.P, NPARAM), dtype=torch.float32, device=dL_dpixels.device)
+        alloc = grad is None
+        if alloc:  # >= 1 row: an empty scene still passes a non-null buffer
+            grad = torch.zeros((max(self.P, 1), NPARAM), dtype=torch.float32,
+                               device=dL_dpixels.device)
         pairs = C.c_uint64()
         check(lib().dw_render_backward(
-            self._h, _ptr(dL_dpixels, "dL_dpixels", torch.float32), int(policy.kind),
-            policy.threshold, _ptr(grad, "grad", torch.float32),
+            self._h, _ptr(dL_dpixels, "dL_dpixels", torch.float32, self._npix3()),
+            int(policy.kind), policy.threshold,
+            _ptr(grad, "grad", torch.float32, min_numel=NPARAM * self.P),
             C.byref(pairs) if count_pairs else None, _stream(stream)))
+        grad = grad[:self.P] if alloc else grad
         return (grad, pairs.value) if count_pairs else grad
 
     def render_backward_tap(self, dL_dpixels, threshold: int = 0, grad=None,
@@ -187,13 +209,17 @@ class GaussianRasterizer:
 
         from .warpred import Trace
 
-        if grad is None:
-            grad = torch.zeros((self.P, NPARAM), dtype=torch.float32, device=dL_dpixels.device)
+        alloc = grad is None
+        if alloc:  # >= 1 row: an empty scene still passes a non-null buffer
+            grad = torch.zeros((max(self.P, 1), NPARAM), dtype=torch.float32,
+                               device=dL_dpixels.device)
         h, total = C.c_void_p(), C.c_int64()
         check(lib().dw_render_backward_tap(
-            self._h, _ptr(dL_dpixels, "dL_dpixels", torch.float32), threshold,
-            _ptr(grad, "grad", torch.float32), max_records, C.byref(h), C.byref(total),
+            self._h, _ptr(dL_dpixels, "dL_dpixels", torch.float32, self._npix3()), threshold,
+            _ptr(grad, "grad", torch.float32, min_numel=NPARAM * self.P), max_records,
+            C.byref(h), C.byref(total),
             _stream(stream)))
+        grad = grad[:self.P] if alloc else grad
         return grad, Trace(h.value), total.value
 
     def preprocess_backward(self, means3D, scales, rotations, grad2d, grad3d=None, stream=None):
@@ -204,11 +230,18 @@ class GaussianRasterizer:
         if grad3d is None:
             grad3d = torch.zeros((self.P, NPARAM3D), dtype=torch.float32, device=grad2d.device)
         f32 = torch.float32
+        P = self.P
         check(lib().dw_preprocess_backward(
-            self._h, _ptr(means3D, "means3D", f32), _ptr(scales, "scales", f32),
-            _ptr(rotations, "rotations", f32), _ptr(grad2d, "grad2d", f32),
-            _ptr(grad3d, "grad3d", f32), _stream(stream)))
+            self._h, _ptr(means3D, "means3D", f32, 3 * P), _ptr(scales, "scales", f32, 3 * P),
+            _ptr(rotations, "rotations", f32, 4 * P),
+            _ptr(grad2d, "grad2d", f32, min_numel=NPARAM * P),
+            _ptr(grad3d, "grad3d", f32, min_numel=NPARAM3D * P), _stream(stream)))
         return grad3d
+
+    def _npix3(self) -> int:
+        if self.camera is None:
+            raise _lib.InvalidArgument(1, "render_backward before render_forward")
+        return 3 * self.camera.height * self.camera.width
 
     def buffer(self, name: str) -> np.ndarray:
         """Host copy of an intermediate buffer (parity tests)."""
@@ -226,7 +259,13 @@ class GaussianRasterizer:
         P = int(scene["means3D"].shape[0])
         arrs = [np.ascontiguousarray(scene[k], np.float32)
                 for k in ("means3D", "scales", "rotations", "opacities", "colors")]
+        for a, k, w in zip(arrs, ("means3D", "scales", "rotations", "opacities", "colors"),
+                           (3, 3, 4, 1, 3)):
+            if a.size != w * P:
+                raise ValueError(f"{k} must have {w * P} elements, has {a.size}")
         dL = np.ascontiguousarray(dL_dpixels, np.float32)
+        if dL.size != 3 * camera.height * camera.width:
+            raise ValueError(f"dL_dpixels must have {3 * camera.height * camera.width} elements")
         img = np.zeros((3, camera.height, camera.width), np.float32)
         grad = np.zeros((P, NPARAM), np.float32)
         cam = camera.to_c()

@@ -416,3 +416,56 @@ def test_invalid_arguments(cuda):
     dL = torch.zeros((3, 8, 8), device=cuda)
     with pytest.raises(_lib.InvalidArgument, match="before render_forward"):
         r.render_backward(dL, wr.Policy(wr.PolicyKind.sw_b, 0), grad=torch.zeros((1, 9), device=cuda))
+
+
+def test_wrong_sized_buffers_raise(cuda):
+    """The C side trusts buffer sizes: the Python boundary checks every
+    element count against P / H / W before a pointer crosses it."""
+    import torch
+
+    from paper_2401_05345_b200 import warpred as wr
+    from paper_2401_05345_b200.rasterizer import GaussianRasterizer
+    from paper_2401_05345_b200.scene import make_camera, make_scene
+
+    P, W, H = 64, 48, 32
+    t = {k: torch.from_numpy(v).to(cuda) for k, v in make_scene(P, W, H, seed=1).items()}
+    cam = make_camera(W, H)
+    r = GaussianRasterizer()
+    with pytest.raises(ValueError, match="rotations"):
+        r.render_forward(t["means3D"], t["scales"], t["rotations"][:-1].contiguous(),
+                         t["opacities"], t["colors"], cam)
+    with pytest.raises(ValueError, match="out_color"):
+        r.render_forward(t["means3D"], t["scales"], t["rotations"], t["opacities"], t["colors"],
+                         cam, out_color=torch.empty((3, H, W - 1), device=cuda))
+    r.render_forward(t["means3D"], t["scales"], t["rotations"], t["opacities"], t["colors"], cam)
+    pol = wr.Policy(wr.PolicyKind.sw_b, 0)
+    with pytest.raises(ValueError, match="dL_dpixels"):
+        r.render_backward(torch.zeros((3, H, W + 1), device=cuda), pol)
+    with pytest.raises(ValueError, match="grad"):
+        r.render_backward(torch.zeros((3, H, W), device=cuda), pol,
+                          grad=torch.zeros((P - 1, 9), device=cuda))
+    with pytest.raises(ValueError, match="grad3d"):
+        r.preprocess_backward(t["means3D"], t["scales"], t["rotations"],
+                              torch.zeros((P, 9), device=cuda),
+                              torch.zeros((P, 13), device=cuda))
+
+
+def test_tap_on_empty_scene(cuda):
+    """The tap backward after an empty-scene forward walks nothing (no stale
+    lists or tile order are read) and returns no records."""
+    import torch
+
+    from paper_2401_05345_b200.rasterizer import GaussianRasterizer
+    from paper_2401_05345_b200.scene import make_camera, make_dL_dpixels, make_scene
+
+    cam = make_camera(64, 48)
+    r = GaussianRasterizer()
+    # a non-empty frame first, so stale per-tile state exists
+    t = {k: torch.from_numpy(v).to(cuda) for k, v in make_scene(500, 64, 48, seed=2).items()}
+    r.render_forward(t["means3D"], t["scales"], t["rotations"], t["opacities"], t["colors"], cam)
+    z = {k: v[:0].contiguous() for k, v in t.items()}
+    r.render_forward(z["means3D"], z["scales"], z["rotations"], z["opacities"], z["colors"], cam)
+    dL = torch.from_numpy(make_dL_dpixels(64, 48)).to(cuda)
+    grad, tr, total = r.render_backward_tap(dL, threshold=0)
+    torch.cuda.synchronize()
+    assert total == 0 and tr.record_count() == 0 and grad.numel() == 0

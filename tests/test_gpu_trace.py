@@ -109,7 +109,7 @@ def test_golden_traces(orc, cuda, name):
         assert np.array_equal(sums.astype(np.float64), want), key
 
 
-@pytest.mark.parametrize("name", ["C1", "C4"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
 def test_baseline_family_full_size(orc, cuda, name):
     """BASELINE-size traces: bit-exact sums and exact RED counts vs the golden
     request counts the reference produced (tests/golden/golden.json)."""
@@ -128,6 +128,37 @@ def test_baseline_family_full_size(orc, cuda, name):
         sums, m = wr.gpu_run(d, wr.Policy(wr.parse_policy_kind(k), int(t)))
         assert m.atomic_requests_to_l2 == c["requests"], key
         assert np.array_equal(sums.astype(np.float64), want), key
+
+
+def test_criterion1_randomized_differential(cuda):
+    """The reference's acceptance criterion 1 on the GPU: its first 200
+    seeded traces (the reference's own mt19937_64 draw sequence,
+    /root/reference/proj/tests/acceptance.cpp:93-146, fixture written by the
+    reference: tests/golden/criterion1.json) through every core policy at the
+    thresholds it draws. Per run: GPU RED count == the reference's request
+    count, and the sha256 of the GPU's per-address sums (as f64, Address
+    order) == the reference's (reducers.cpp:208-220 sums; all policies equal
+    the oracle on the quantized grid)."""
+    import hashlib
+
+    from paper_2401_05345_b200 import warpred as wr
+
+    g = json.load(open(os.path.join(GOLDEN, "criterion1.json")))["traces"]
+    assert len(g) == 200
+    runs = 0
+    for i, rec in enumerate(g):
+        tr = wr.generate(_spec(**rec["spec"]))
+        assert tr.record_count() == rec["records"], i
+        d = wr.DeviceTrace(tr)
+        for key, want in rec["runs"].items():
+            k, t = key.split(":")
+            sums, m = wr.gpu_run(d, wr.Policy(wr.parse_policy_kind(k), int(t)))
+            assert m.atomic_requests_to_l2 == want["requests"], (i, key)
+            h = hashlib.sha256(np.ascontiguousarray(sums.astype(np.float64)).tobytes())
+            assert h.hexdigest() == want["sums_sha256"], (i, key)
+            assert want["sums_sha256"] == rec["oracle_sum_sha256"]
+            runs += 1
+    assert runs >= 1000
 
 
 def test_reduce_records_raw_pointers_and_stream(orc, cuda):

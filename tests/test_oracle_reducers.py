@@ -306,3 +306,25 @@ def test_random_differential_vs_reference(orc, ref):
             y, cy = ref.apply_policy(h, kind, t, P)
             assert np.array_equal(x, y) and cx == cy, (kw, kind, t)
         ref.free(h)
+
+
+def test_criterion1_golden_against_restatement(orc):
+    """The C restatement on the reference's own criterion-1 traces
+    (tests/golden/criterion1.json, written by the reference from
+    acceptance.cpp:93-146's draw sequence): oracle_sum and every drawn
+    (policy, threshold) run -- request counts and per-address sums -- equal
+    the reference's, hash for hash."""
+    from oracle.bindings import scene
+
+    g = json.load(open(os.path.join(GOLDEN, "criterion1.json")))["traces"]
+    for i, rec in enumerate(g):
+        tr = orc.generate(scene(**rec["spec"]))
+        assert tr.num_records == rec["records"], i
+        P = rec["spec"]["num_primitives"]
+        sums, _ = orc.oracle_sum(tr, P)
+        assert _sha(sums) == rec["oracle_sum_sha256"], i
+        for key, want in rec["runs"].items():
+            k, t = key.split(":")
+            s, c = orc.apply_policy(tr, {"native": 0, "sw_s": 1, "sw_b": 2, "cccl": 3}[k], int(t), P)
+            assert c["requests"] == want["requests"], (i, key)
+            assert _sha(s) == want["sums_sha256"], (i, key)
