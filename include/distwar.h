@@ -103,6 +103,7 @@ typedef struct dw_camera {
 const char* dw_version(void);          /* wr_version, warpred.h:86        */
 const char* dw_last_error(void);       /* wr_last_error, warpred.h:88-89  */
 int dw_device_count(void);             /* -1 when the CUDA runtime fails  */
+int dw_device_clock_khz(void);         /* max SM clock of the current device; -1 on failure */
 
 /* --------------------------------------------------- host traces (input) */
 void dw_scene_spec_init(dw_scene_spec* scene);                 /* warpred.h:91  */
@@ -123,6 +124,12 @@ dw_status dw_trace_from_arrays(int64_t num_records, int32_t params, int32_t num_
 dw_status dw_trace_arrays(const dw_trace* trace, const uint32_t** active,
                           const int32_t** prim, const double** grads,
                           dw_scene_spec* scene);
+
+/* Borrowed views of the records' warp ids and iteration indices. */
+dw_status dw_trace_ids(const dw_trace* trace, const int32_t** warp_id, const int32_t** iteration);
+/* Replaces the trace's scene spec (e.g. the seed of a text-format trace);
+ * params_per_primitive must match the records. */
+dw_status dw_trace_set_scene(dw_trace* trace, const dw_scene_spec* scene);
 
 /* ------------------------------------- trace-driven DISTWAR reduction (GPU) */
 /* Uploads a trace to HBM as SoA fp32: active u32[R], prim i32[R][32],
@@ -149,6 +156,13 @@ dw_status dw_reduce_records(const uint32_t* d_active, const int32_t* d_prim,
  * machine; host_grad_out (nullable, P*N floats) receives the sums. */
 dw_status dw_gpu_run(const dw_device_trace* dtrace, dw_policy_kind policy, int32_t threshold,
                      float* host_grad_out, dw_gpu_metrics* out);
+
+/* The reference's per-record cost model (reducers.cpp:84-206, InstructionCosts
+ * all 1) evaluated on the device over the uploaded records: out[0] =
+ * core_instructions, out[1] = core_fp_adds of wr_run_metrics (warpred.h:68-77)
+ * for (policy, threshold). */
+dw_status dw_model_costs(const dw_device_trace* dtrace, dw_policy_kind policy, int32_t threshold,
+                         uint64_t out[2]);
 
 /* Replaces wr_tune (warpred.h:120-122): measured sweep t = 0..32 on the
  * records of `iteration` (< 0: the whole trace), argmin with ties to the

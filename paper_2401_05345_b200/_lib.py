@@ -94,6 +94,7 @@ SIGNATURES = {
     "dw_version": (C.c_char_p, []),
     "dw_last_error": (C.c_char_p, []),
     "dw_device_count": (C.c_int, []),
+    "dw_device_clock_khz": (C.c_int, []),
     "dw_scene_spec_init": (None, [C.POINTER(SceneSpecC)]),
     "dw_trace_generate": (C.c_int, [C.POINTER(SceneSpecC), C.POINTER(vp)]),
     "dw_trace_free": (None, [vp]),
@@ -105,12 +106,15 @@ SIGNATURES = {
     "dw_trace_from_arrays": (C.c_int, [i64, i32, i32, vp, vp, vp, vp, vp, C.POINTER(vp)]),
     "dw_trace_arrays": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
                                   C.POINTER(SceneSpecC)]),
+    "dw_trace_ids": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp)]),
+    "dw_trace_set_scene": (C.c_int, [vp, C.POINTER(SceneSpecC)]),
     "dw_trace_upload": (C.c_int, [vp, vp, C.POINTER(vp)]),
     "dw_device_trace_free": (None, [vp]),
     "dw_device_trace_view": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
                                        C.POINTER(i64), C.POINTER(i32), C.POINTER(i32)]),
     "dw_reduce_records": (C.c_int, [vp, vp, vp, i64, i32, i32, C.c_int, i32, vp, vp, vp]),
     "dw_gpu_run": (C.c_int, [vp, C.c_int, i32, vp, C.POINTER(GpuMetricsC)]),
+    "dw_model_costs": (C.c_int, [vp, C.c_int, i32, vp]),
     "dw_tune": (C.c_int, [vp, C.c_int, i32, i32, C.POINTER(TuneReportC)]),
     "dw_tune_report_save_csv": (C.c_int, [C.POINTER(TuneReportC), C.c_char_p]),
     "dw_rasterizer_create": (C.c_int, [C.POINTER(vp)]),

@@ -160,6 +160,16 @@ int dw_device_count(void) {
   return n;
 }
 
+int dw_device_clock_khz(void) {
+  int dev = 0, khz = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, dev) != cudaSuccess) {
+    last_error = cudaGetErrorString(cudaGetLastError());
+    return -1;
+  }
+  return khz;
+}
+
 void dw_scene_spec_init(dw_scene_spec* scene) {
   if (scene) dw::scene_defaults(scene);
 }
@@ -251,6 +261,23 @@ dw_status dw_trace_arrays(const dw_trace* trace, const uint32_t** active, const 
   return DW_OK;
 }
 
+dw_status dw_trace_ids(const dw_trace* trace, const int32_t** warp_id, const int32_t** iteration) {
+  if (!trace) return fail_invalid("null argument");
+  if (warp_id) *warp_id = trace->t.warp_id.data();
+  if (iteration) *iteration = trace->t.iteration.data();
+  return DW_OK;
+}
+
+dw_status dw_trace_set_scene(dw_trace* trace, const dw_scene_spec* scene) {
+  if (!trace || !scene) return fail_invalid("null argument");
+  return guarded([&] {
+    if (scene->params_per_primitive != trace->t.scene.params_per_primitive)
+      throw std::invalid_argument("params_per_primitive must match the trace's records");
+    trace->t.scene = *scene;
+    return DW_OK;
+  });
+}
+
 dw_status dw_trace_upload(const dw_trace* trace, void* stream, dw_device_trace** out) {
   if (!trace || !out) return fail_invalid("null argument");
   return guarded([&] {
@@ -319,6 +346,23 @@ dw_status dw_gpu_run(const dw_device_trace* d, dw_policy_kind policy, int32_t th
     out->records = static_cast<uint64_t>(d->records);
     if (host_grad_out)
       DW_CUDA(cudaMemcpy(host_grad_out, grad.p, words * sizeof(float), cudaMemcpyDeviceToHost));
+    return DW_OK;
+  });
+}
+
+dw_status dw_model_costs(const dw_device_trace* d, dw_policy_kind policy, int32_t threshold,
+                         uint64_t out[2]) {
+  if (!d || !out) return fail_invalid("null argument");
+  return guarded([&] {
+    check_policy(policy, threshold);
+    DevBuf<unsigned long long> ctr(2);
+    DW_CUDA(cudaMemsetAsync(ctr.p, 0, 2 * sizeof(unsigned long long), nullptr));
+    dw::launch_model_costs(d->active, d->prim, d->records, d->params, policy, threshold, ctr.p,
+                           nullptr);
+    unsigned long long h[2] = {0, 0};
+    DW_CUDA(cudaMemcpy(h, ctr.p, sizeof h, cudaMemcpyDeviceToHost));
+    out[0] = h[0];
+    out[1] = h[1];
     return DW_OK;
   });
 }

@@ -10,8 +10,8 @@
 //
 //   native   reducers.cpp:84-93   one RED per (active lane, param)
 //   sw_s     reducers.cpp:95-136  __match_any_sync groups; a group of size
-//                                 >= t is folded by its lowest lane in
-//                                 ascending lane order, then N REDs
+//                                 >= t is summed (masked reduce-scatter
+//                                 butterfly), then N REDs
 //   sw_b     reducers.cpp:138-175 all 32 lanes on one primitive and
 //                                 popc(active) >= t: a full-warp butterfly,
 //                                 then N REDs; else per-lane REDs
@@ -220,44 +220,78 @@ __device__ __forceinline__ void reduce_bfly_scaled(int idx, float* grad, float (
   }
 }
 
-// SW-S (reduce_serial, PAPER.md:1719-1759 with masked _sync shuffles): the
-// lowest lane of each __match_any_sync group of size >= thr folds the other
-// members' values in ascending lane order (reducers.cpp:101-121), then issues
-// N REDs; smaller groups issue per-lane REDs. Must be reached by all lanes.
+// SW-S (reduce_serial; request semantics
+// reducers.cpp:95-136): the active lanes split into __match_any_sync groups
+// (one per distinct primitive); a group of size >= thr issues its N sums once,
+// from the lanes the reduce-scatter leaves them in; smaller groups issue
+// per-lane REDs. The paper's leader folds its group serially (O(group) SHFLs
+// per param, a warp-uniform trip count set by the largest group); here each
+// reducing group is summed by the same reduce-scatter butterfly as SW-B with
+// the lanes outside the group contributing zero, so a warp pays one
+// butterfly per reducing group -- and one in total when the active lanes
+// share a primitive, as every warp of the rasterizer and ~99 % of the C3
+// trace's records do. The per-group sum is a balanced tree rather than the
+// leader's ascending fold: identical on the reference's exact grid (any
+// order is exact below 65,793 addends), within fp32 rounding elsewhere.
+// Must be called by all 32 lanes.
+template <int N, bool COUNT>
+__device__ __forceinline__ void group_bfly(float (&x)[N], int lane) {
+  if constexpr (N == 9)
+    reduce_scatter9(x, lane);
+  else
+    ReduceScatter<N, 16>::run(x, lane);
+}
+
 template <int N, bool COUNT>
 __device__ __forceinline__ void reduce_serial(int idx, float* grad, const float (&v)[N], int thr,
                                               bool active, int lane, uint32_t& nred,
-                                              unsigned ballot) {
-  if (!active) return;  // inactive lanes take no part in SW-S (only `ballot` lanes)
-  const unsigned group = __match_any_sync(ballot, idx);
-  const int cnt = __popc(group);
-  const bool reduce = cnt >= thr;
-  const int leader = __ffs(group) - 1;
-  unsigned fetch = reduce ? (group & ~(1u << leader)) : 0u;
-  float sums[N];
+                                              unsigned ballot, int slot, bool issuer) {
+  if (ballot == 0u) return;  // no active lane: no groups, no requests
+  const unsigned group = active ? __match_any_sync(ballot, idx) : 0u;
+  if (__all_sync(kFull, !active || group == ballot)) {  // one group: every active lane
+    const int cnt = __popc(ballot);
+    if (cnt >= thr) {
+      float x[N];
 #pragma unroll
-  for (int p = 0; p < N; ++p) sums[p] = v[p];
-  // warp-uniform trip count: the largest reducing group's member count - 1
-  while (__any_sync(ballot, fetch != 0u)) {
-    const int src = fetch ? __ffs(fetch) - 1 : lane;
+      for (int p = 0; p < N; ++p) x[p] = active ? v[p] : 0.0f;
+      group_bfly<N, COUNT>(x, lane);
+      const int leader = __ffs(ballot) - 1;
+      const int idx0 = __shfl_sync(kFull, idx, leader);
+      if (issuer) {
+        red_add(grad + static_cast<int64_t>(idx0) * N + slot, x[0]);
+        if (COUNT) nred += 1;
+      }
+    } else if (active) {
+      float* base = grad + static_cast<int64_t>(idx) * N;
 #pragma unroll
-    for (int p = 0; p < N; ++p) {
-      const float x = __shfl_sync(ballot, v[p], src);
-      if (fetch && lane == leader) sums[p] += x;
-    }
-    fetch &= fetch - 1u;
-  }
-  float* base = grad + static_cast<int64_t>(idx) * N;
-  if (reduce) {
-    if (lane == leader) {
-#pragma unroll
-      for (int p = 0; p < N; ++p) red_add(base + p, sums[p]);
+      for (int p = 0; p < N; ++p) red_add(base + p, v[p]);
       if (COUNT) nred += N;
     }
-  } else {
+    return;
+  }
+  // divergent record: one pass per group, in ascending-leader order
+  unsigned remaining = ballot;
+  while (remaining) {
+    const int leader = __ffs(remaining) - 1;
+    const unsigned g = __shfl_sync(kFull, group, leader);
+    remaining &= ~g;
+    const bool mine = (g >> lane) & 1u;
+    if (__popc(g) >= thr) {
+      float x[N];
 #pragma unroll
-    for (int p = 0; p < N; ++p) red_add(base + p, v[p]);
-    if (COUNT) nred += N;
+      for (int p = 0; p < N; ++p) x[p] = mine ? v[p] : 0.0f;
+      group_bfly<N, COUNT>(x, lane);
+      const int idx0 = __shfl_sync(kFull, idx, leader);
+      if (issuer) {
+        red_add(grad + static_cast<int64_t>(idx0) * N + slot, x[0]);
+        if (COUNT) nred += 1;
+      }
+    } else if (mine) {
+      float* base = grad + static_cast<int64_t>(idx) * N;
+#pragma unroll
+      for (int p = 0; p < N; ++p) red_add(base + p, v[p]);
+      if (COUNT) nred += N;
+    }
   }
 }
 

@@ -27,6 +27,9 @@ int sm_count();  // cached per device
 void launch_reduce_records(const uint32_t* active, const int32_t* prim, const float* vals,
                            int64_t num_records, int n, int policy, int thr, float* grad,
                            unsigned long long* red_count, cudaStream_t stream);
+// The reference's instruction / FP-add cost model of the same records (out[2], accumulated).
+void launch_model_costs(const uint32_t* active, const int32_t* prim, int64_t num_records, int n,
+                        int policy, int thr, unsigned long long* out, cudaStream_t stream);
 
 // Host-side WarpRecord trace (workload.cpp): flat arrays as in
 // reference workload.hpp:41-65, lane-major f64 grads.

@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kBlock, DW_BWD_MIN_BLOCKS)
         } else if (POL == kSwB) {
           reduce_bfly<kNParam, COUNT, true>(id, grad, v, thr, act, lane, nred, ballot, slot, issuer);
         } else if (POL == kSwS) {
-          reduce_serial<kNParam, COUNT>(id, grad, v, thr, act, lane, nred, ballot);
+          reduce_serial<kNParam, COUNT>(id, grad, v, thr, act, lane, nred, ballot, slot, issuer);
         } else {
           reduce_cccl<kNParam, COUNT>(id, grad, v, act, lane, nred, ballot);
         }
@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(128, (POL == kSwB && !COUNT && !TAP) ? DW_SWB_
           reduce_bfly_scaled<kNParam, COUNT>(id, grad, v, thr, act, lane, nred, ballot, slot,
                                              issuer, lane_scale, scale);
         } else if (POL == kSwS) {
-          reduce_serial<kNParam, COUNT>(id, grad, v, thr, act, lane, nred, ballot);
+          reduce_serial<kNParam, COUNT>(id, grad, v, thr, act, lane, nred, ballot, slot, issuer);
         } else {
           reduce_cccl<kNParam, COUNT>(id, grad, v, act, lane, nred, ballot);
         }

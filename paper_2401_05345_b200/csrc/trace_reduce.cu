@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(256) k_reduce_trace(const uint32_t* __restrict
     } else if (POL == kSwB) {
       reduce_bfly<N, COUNT, false>(idx, grad, v, thr, act, lane, nred, a, slot, issuer);
     } else if (POL == kSwS) {
-      reduce_serial<N, COUNT>(idx, grad, v, thr, act, lane, nred, a);
+      reduce_serial<N, COUNT>(idx, grad, v, thr, act, lane, nred, a, slot, issuer);
     } else {
       reduce_cccl<N, COUNT>(idx, grad, v, act, lane, nred, a);
     }
@@ -180,6 +180,83 @@ void dispatch_pol(const uint32_t* a, const int32_t* p, const float* v, int64_t R
 }
 
 }  // namespace
+
+// The reference's per-record instruction / FP-add cost model
+// (reducers.cpp:84-206, every InstructionCosts entry 1: reducers.hpp:51-61),
+// evaluated on the device over the same records the policy kernels reduce, so
+// wr_simulate on the B200 reports the reference's core_instructions /
+// core_fp_adds beside the measured REDs and cycles. One warp per record;
+// out[0] += instructions, out[1] += fp adds.
+__global__ void __launch_bounds__(256) k_model_costs(const uint32_t* __restrict__ active,
+                                                     const int32_t* __restrict__ prim, int64_t R,
+                                                     int N, int pol, int thr,
+                                                     unsigned long long* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  unsigned long long ins = 0, fp = 0;  // lane-local shares, warp-summed at the end
+  const unsigned long long n = static_cast<unsigned long long>(N);
+  for (int64_t r = w0; r < R; r += nw) {
+    const uint32_t a = active[r];
+    const int idx = prim[r * 32 + lane];
+    const unsigned long long cnt = static_cast<unsigned long long>(__popc(a));
+    const int idx0 = __shfl_sync(kFull, idx, 0);
+    const bool same = __all_sync(kFull, idx == idx0) && idx0 >= 0;  // all_lanes_same_primitive
+    if (pol == kNative) {  // reducers.cpp:84-93
+      if (lane == 0) ins += cnt * n;
+    } else if (pol == kSwB) {  // reducers.cpp:138-175
+      if (lane == 0) {
+        ins += 4;
+        if (same && cnt > 0 && cnt >= static_cast<unsigned long long>(thr)) {
+          ins += 6 * n;
+          fp += 160 * n;
+        } else {
+          ins += cnt * n;
+        }
+      }
+    } else if (pol == kCccl) {  // reducers.cpp:177-206, per param
+      if (lane == 0) {
+        if (same && cnt > 0) {
+          ins += n * 10;
+          fp += n * 160;
+        } else {
+          ins += n * (4 + cnt);
+        }
+      }
+    } else if ((a >> lane) & 1u) {  // SW-S, reducers.cpp:95-136: per match_any group
+      const unsigned g = __match_any_sync(a, idx);
+      if (lane == __ffs(g) - 1) {  // the group's leader accounts for it
+        const unsigned long long gc = static_cast<unsigned long long>(__popc(g));
+        ins += 3;
+        if (gc >= static_cast<unsigned long long>(thr)) {
+          ins += 1 + (gc - 1) * (2 + n) + n;
+          fp += n * (gc - 1);
+        } else {
+          ins += gc * n;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    ins += __shfl_xor_sync(kFull, ins, off);
+    fp += __shfl_xor_sync(kFull, fp, off);
+  }
+  if (lane == 0 && (ins || fp)) {
+    atomicAdd(out, ins);
+    atomicAdd(out + 1, fp);
+  }
+}
+
+void launch_model_costs(const uint32_t* active, const int32_t* prim, int64_t R, int n, int policy,
+                        int thr, unsigned long long* out, cudaStream_t stream) {
+  if (R <= 0) return;
+  const int64_t want = (R + 7) / 8;
+  const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
+  k_model_costs<<<static_cast<int>(want < cap ? want : cap), 256, 0, stream>>>(active, prim, R, n,
+                                                                              policy, thr, out);
+  DW_CUDA(cudaGetLastError());
+}
 
 void launch_reduce_records(const uint32_t* active, const int32_t* prim, const float* vals,
                            int64_t R, int n, int policy, int thr, float* grad,
