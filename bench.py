@@ -4,22 +4,22 @@ and ms/iter vs naive-atomic; L2-atomic roofline %).
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
-Workload (config.workload): BASELINE configs[2] -- 1M synthetic Gaussians,
-1920x1080, the scene the north_star target is stated on -- rendered as
-BASELINE configs[4]'s structure: `--views-per-gpu` (64) orbit views per rank
-(views are independent units: weak scaling, the per-GPU work fixed as N
-grows), every rank's views resident in HBM. A STEP is the backward pass of the
-rasterizer over the rank's views (DISTWAR SW-B, balancing threshold tuned on
-the box with the reference's sweep rule) plus, for N > 1, the NCCL all-reduce
-of the per-Gaussian gradient buffer. `--views V` instead shards a fixed batch
-of V views across the ranks (strong scaling).
-One unit = one gradient contribution = (contributing pixel, Gaussian, param),
-9 per pair.
+Workload (config.workload): BASELINE configs[4] -- 3M synthetic Gaussians,
+1920x1080, a 64-view orbit batch sharded across the ranks (strong scaling:
+the batch is fixed, each of N ranks renders 64/N views; `--views-per-gpu V`
+switches to weak scaling). Every rank's views are resident in HBM. A STEP is
+the backward pass of the rasterizer over the rank's views (DISTWAR SW-B,
+balancing threshold tuned on the box with the reference's sweep rule) plus,
+for N > 1, the NCCL all-reduce of the per-Gaussian gradient buffer -- run
+through paper_2401_05345_b200.dist.view_parallel_backward. One unit = one
+gradient contribution = (contributing pixel, Gaussian, param), 9 per pair
+(SURVEY.md §8(d)). The north_star's >= 2x target scene (configs[2], 1M
+Gaussians, one 1080p view) is timed beside it (`target_config`).
 
 Printed on rank 0 as ONE JSON line; `value` = all ranks' contributions / the
 max over ranks of the device-timed steps; `e2e` = the same metric through the
-host-buffer C-ABI call dw_render_views_host (pinned H2D of the scene and
-dL/dpixel, forward + backward, D2H of images and gradients), the figure to
+host-buffer C-ABI calls (dw_render_views_host at N = 1; dw_render_views +
+NCCL all-reduce of the device gradient + one D2H at N > 1), the figure to
 compare with the reference arm.
 """
 from __future__ import annotations
@@ -37,7 +37,12 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WORKLOAD = "c3_1m_1080p"  # paper_2401_05345_b200.scene.CONFIGS key (BASELINE configs[2])
+# paper_2401_05345_b200.scene.CONFIGS keys: the benchmarked batch is BASELINE
+# configs[4] (3M Gaussians, a 64-view batch sharded across 1/2/4/8 GPUs); the
+# north_star's >= 2x target is stated on configs[2] (1M, one 1080p view),
+# reported beside it as `target_config`
+WORKLOAD = "c5_3m_1080p_64views"
+TARGET = "c3_1m_1080p"
 METRIC = "backward grad-contributions/sec & ms/iter vs naive-atomic; L2 atomic roofline %"
 UNIT = "contributions/s"
 
@@ -49,10 +54,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=WORKLOAD)
-    ap.add_argument("--views", type=int, default=0,
-                    help="if > 0: this view batch sharded across ranks (strong scaling)")
-    ap.add_argument("--views-per-gpu", type=int, default=64,
-                    help="views per rank (weak scaling; the default)")
+    ap.add_argument("--views", type=int, default=64,
+                    help="the view batch, sharded across ranks (strong scaling; the default)")
+    ap.add_argument("--views-per-gpu", type=int, default=0,
+                    help="if > 0: this many views per rank instead (weak scaling)")
     ap.add_argument("--naive-steps", type=int, default=0,
                     help="timed steps of the naive comparison (0: max(3, steps // 4))")
     ap.add_argument("--threshold", default="auto", help="SW-B balancing threshold or 'auto'")
@@ -169,7 +174,7 @@ def to_ocam(cam):
 
 
 # ----------------------------------------------------------- CPU baselines
-def cpu_port_baseline(sc, cam, dL, stride: int) -> dict:
+def cpu_port_baseline(sc, cam, dL, stride: int, workload: str) -> dict:
     """The oracle port's CPU backward (gradient math + per-address
     accumulation) on this box's host cores: the cpu_baseline of our arm."""
     from oracle.bindings import Oracle
@@ -183,12 +188,12 @@ def cpu_port_baseline(sc, cam, dL, stride: int) -> dict:
     finally:
         orc.gs_free(st)
     return {"value": 9 * pairs / secs, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"view 0 of {WORKLOAD}, every {stride} tile(s): {pairs} pairs "
+            "sample": f"view 0 of {workload}, every {stride} tile(s): {pairs} pairs "
                       f"({9 * pairs} contributions) in {secs:.2f} s, oracle/gs_oracle.c "
                       f"backward on {threads} threads"}
 
 
-def reference_measure(workload: str, steps: int, warmup: int, stride: int):
+def reference_measure(workload: str, steps: int, warmup: int, stride: int, cam=None):
     """The reference's own CPU implementation of the path on this box's host
     cores. The reference (warpred) implements the reduction stage only
     (reducers::apply_policy + per-address summation, oracle/_ref built from
@@ -203,7 +208,7 @@ def reference_measure(workload: str, steps: int, warmup: int, stride: int):
 
     P, W, H, hc, _ = CONFIGS[workload]
     sc = make_scene(P, W, H, seed=0, high_contention=hc)
-    cam = make_camera(W, H)
+    cam = cam or make_camera(W, H)
     dL = make_dL_dpixels(W, H, seed=1)
     orc = Oracle()
     threads = host_threads()
@@ -240,16 +245,23 @@ def reference_arm(args) -> None:
     """--impl reference: reference_measure() over the arm's --steps/--warmup."""
     from paper_2401_05345_b200.scene import CONFIGS
 
+    from paper_2401_05345_b200.scene import orbit_cameras
+
     P, W, H, _, _ = CONFIGS[args.workload]
     stride = max(args.cpu_tile_stride, 16)
-    cpu, total = reference_measure(args.workload, args.steps, args.warmup, stride)
+    # view 0 of the arm's batch (the orbit camera our arm's rank 0 renders first)
+    views = args.views_per_gpu * args.gpus if args.views_per_gpu > 0 else args.views
+    cam0 = orbit_cameras(W, H, views)[0] if views > 1 else None
+    cpu, total = reference_measure(args.workload, args.steps, args.warmup, stride, cam0)
     v = cpu["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": args.workload, "gaussians": P, "width": W,
-                                        "height": H, "tile_stride": stride},
+        "higher_is_better": True,
+        "scaling": "weak" if args.views_per_gpu > 0 else "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "gaussians": P, "width": W, "height": H,
+                   "views_total": views, "sample": f"every {stride}th tile of view 0"},
         "cpu_baseline": cpu,
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -257,6 +269,46 @@ def reference_arm(args) -> None:
 
 
 # ----------------------------------------------------------------- our arm
+def stage_breakdown(t, cam, P, H, W) -> dict:
+    """Per-stage forward times of one view (CUDA events between the stages,
+    dw_rasterizer_stage_timing) with each stage's algorithmic bytes and HBM
+    fraction; the events serialise the programmatic-dependent launches, so
+    the stages sum to slightly more than the untimed forward."""
+    import torch
+
+    from paper_2401_05345_b200.rasterizer import GaussianRasterizer
+
+    r = GaussianRasterizer()
+    r.stage_timing(True)
+    best = None
+    for _ in range(3):
+        r.render_forward(t["means3D"], t["scales"], t["rotations"], t["opacities"],
+                         t["colors"], cam)
+        ms = r.stage_ms()
+        best = ms if best is None else {k: min(best[k], ms[k]) for k in ms}
+    torch.cuda.synchronize()
+    I = r.num_rendered
+    vis = int((r.buffer("radii") > 0).sum())
+    hbm, _ = measured_peaks()
+    # algorithmic bytes per stage (DESIGN.md §4): reads + writes the stage
+    # cannot avoid, counted once
+    alg = {"preprocess": 56 * P + 60 * P,           # scene in; means2D..keys out
+           "depth_sort": 4 * 16 * vis,              # 4 LSD passes, 8 B in + 8 B out each
+           "offsets": 12 * P,                       # areas in, u64 offsets out
+           "binning": 20 * vis + 8 * I + 2 * 16 * I,  # duplicate + 2 tile-sort passes
+           "ranges": 4 * I + 8 * (W // 16 + 1) * (H // 16 + 1),
+           "blend": 4 * I + 44 * vis + 20 * H * W}
+    out = {}
+    for k, ms in best.items():
+        gbs = alg[k] / (ms * 1e-3) / 1e9 if ms > 0 else None
+        out[k] = {"ms": ms, "alg_bytes": alg[k], "GBps": gbs,
+                  "hbm_frac": gbs / hbm if gbs else None}
+    out["_sum_ms"] = sum(best.values())
+    out["_note"] = ("CUDA events between stages (serialises the PDL chain); blend is "
+                    "issue-bound, the others latency/HBM")
+    return out
+
+
 def main() -> None:
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -267,11 +319,13 @@ def main() -> None:
             reference_arm(args)
         return
 
-    import numpy as np
     import torch
 
+    from paper_2401_05345_b200 import _lib
     from paper_2401_05345_b200 import warpred as wr
-    from paper_2401_05345_b200.rasterizer import GaussianRasterizer, microbench_red
+    from paper_2401_05345_b200.dist import shard_views, view_parallel_backward
+    from paper_2401_05345_b200.rasterizer import (GaussianRasterizer, microbench_red,
+                                                  render_views, render_views_host)
     from paper_2401_05345_b200.scene import CONFIGS, make_camera, make_dL_dpixels, make_scene, \
         orbit_cameras
 
@@ -283,11 +337,10 @@ def main() -> None:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
-    from paper_2401_05345_b200.dist import shard_views
 
-    P, W, H, hc, _ = CONFIGS[args.workload]
-    weak = args.views <= 0
-    total_views = args.views_per_gpu * world if weak else args.views
+    P, W, H, hc, cfg_views = CONFIGS[args.workload]
+    weak = args.views_per_gpu > 0
+    total_views = args.views_per_gpu * world if weak else (args.views or max(cfg_views, 64))
     if total_views < world:
         raise SystemExit("need at least one view per rank")
     my_views = list(shard_views(total_views, world, rank))
@@ -298,13 +351,17 @@ def main() -> None:
     t = {k: torch.from_numpy(v).to(dev) for k, v in sc.items()}
     dLs = [torch.from_numpy(make_dL_dpixels(W, H, seed=1 + i)).to(dev) for i in my_views]
     stream = torch.cuda.current_stream()
+    local_of = {g: i for i, g in enumerate(my_views)}
+
+    def ev():
+        return torch.cuda.Event(enable_timing=True)
 
     # ---- forward: resident per-view states (timed for forward fps) -------
     rasts = [GaussianRasterizer() for _ in range(V)]
     fwd_ms = []
     for i, r in enumerate(rasts):
         for rep in range(2):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0, e1 = ev(), ev()
             e0.record()
             r.render_forward(t["means3D"], t["scales"], t["rotations"], t["opacities"],
                              t["colors"], cams[i])
@@ -312,11 +369,11 @@ def main() -> None:
             torch.cuda.synchronize()
             if rep == 1:
                 fwd_ms.append(e0.elapsed_time(e1))
+    stages = stage_breakdown(t, cams[0], P, H, W) if rank == 0 else None
     grad = torch.zeros((P, 9), dtype=torch.float32, device=dev)
 
     # ---- contributions per step (counting instantiation, untimed) --------
     pairs_per_view = []
-    reds = {}
     for r, dL in zip(rasts, dLs):
         _, pairs = r.render_backward(dL, wr.Policy(wr.PolicyKind.native, 0), grad=grad,
                                      count_pairs=True)
@@ -327,27 +384,25 @@ def main() -> None:
     red_peaks = {name: microbench_red(p, 1 << 28) for p, name in
                  ((0, "distinct"), (1, "same_address_warp"), (2, "v4"), (3, "distwar_9lane"))}
 
-    # ---- balancing threshold: measured sweep 0..32 (tuner.cpp:29-52) -----
-    def time_backward(policy, reps=3, views=None):
-        views = range(V) if views is None else views
+    def time_view(i, policy, reps=3):
         ms = []
         for _ in range(reps):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0, e1 = ev(), ev()
             grad.zero_()
             e0.record()
-            for i in views:
-                rasts[i].render_backward(dLs[i], policy, grad=grad)
+            rasts[i].render_backward(dLs[i], policy, grad=grad)
             e1.record()
             torch.cuda.synchronize()
             ms.append(e0.elapsed_time(e1))
         return statistics.median(ms)
 
+    # ---- balancing threshold: measured sweep 0..32 on view 0 (tuner.cpp:29-52)
     sweep = {}
     if args.threshold == "auto":
-        time_backward(wr.Policy(wr.PolicyKind.sw_b, 0), reps=2, views=[0])
+        time_view(0, wr.Policy(wr.PolicyKind.sw_b, 0), reps=2)
         best = None
         for thr in range(33):
-            sweep[thr] = time_backward(wr.Policy(wr.PolicyKind.sw_b, thr), reps=3, views=[0])
+            sweep[thr] = time_view(0, wr.Policy(wr.PolicyKind.sw_b, thr))
             if best is None or sweep[thr] < sweep[best]:
                 best = thr
         thr = best
@@ -358,7 +413,6 @@ def main() -> None:
     else:
         thr = int(args.threshold)
     policy = wr.Policy(wr.PolicyKind.sw_b, thr)
-    from paper_2401_05345_b200 import _lib
 
     def last_reds(r):
         v = C.c_uint64()
@@ -370,46 +424,63 @@ def main() -> None:
         r.render_backward(dL, policy, grad=grad, count_pairs=True)
         reds_distwar += last_reds(r)
 
-    # ---- the timed loop ---------------------------------------------------
+    # ---- the timed loop: dist.view_parallel_backward over the batch --------
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    def run_steps(pol, steps, warmup, sampler=None):
-        per_step, per_launch = [], []
+    def run_steps(pol, steps, warmup):
+        per_step, per_launch, view0 = [], [], []
         for s in range(warmup + steps):
             flush.fill_(float(s))  # L2 flush (256 MiB > 126 MB L2), outside the events
             torch.cuda.synchronize()
             if dist is not None:
                 dist.barrier()
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * V + 2)]
-            ev[0].record()
+            marks = []
+
+            def backward_view(g, out):
+                e0, e1 = ev(), ev()
+                e0.record()
+                rasts[local_of[g]].render_backward(dLs[local_of[g]], pol, grad=out)
+                e1.record()
+                marks.append((g, e0, e1))
+
+            e_start, e_end = ev(), ev()
+            e_start.record()
             grad.zero_()
-            for i in range(V):
-                ev[1 + 2 * i].record()
-                rasts[i].render_backward(dLs[i], pol, grad=grad)
-                ev[2 + 2 * i].record()
-            if dist is not None:
-                dist.all_reduce(grad)
-            ev[-1].record()
+            view_parallel_backward(backward_view, list(range(total_views)), grad,
+                                   all_reduce=dist is not None)
+            e_end.record()
             torch.cuda.synchronize()
             if s >= warmup:
-                per_step.append(ev[0].elapsed_time(ev[-1]))
-                per_launch += [ev[1 + 2 * i].elapsed_time(ev[2 + 2 * i]) for i in range(V)]
+                per_step.append(e_start.elapsed_time(e_end))
+                for g, e0, e1 in marks:
+                    per_launch.append(e0.elapsed_time(e1))
+                    if g == my_views[0]:
+                        view0.append(e0.elapsed_time(e1))
         total = sum(per_step)
         if dist is not None:
             tt = torch.tensor([total], device=dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             total = float(tt.item())
-        return total, per_launch
+        return total, per_launch, view0
 
     sampler = ClockSampler(local)
     time.sleep(0.3)
-    total_ms, launches = run_steps(policy, args.steps, args.warmup)
+    total_ms, launches, launches_v0 = run_steps(policy, args.steps, args.warmup)
     nv_steps = args.naive_steps or max(3, args.steps // 4)
-    total_nv_ms, launches_nv = run_steps(wr.Policy(wr.PolicyKind.native, 0), nv_steps,
-                                         min(args.warmup, 3))
+    total_nv_ms, launches_nv, _ = run_steps(wr.Policy(wr.PolicyKind.native, 0), nv_steps,
+                                            min(args.warmup, 3))
     clocks = sampler.stop()
-
     ms_per_step = total_ms / args.steps
+
+    # ---- where the speed-up comes from (view 0): the naive one-pixel kernel,
+    # the two-pixel kernel with no warp reduction (SW-B at t = 33: every lane
+    # issues its own REDs), and SW-B at the tuned t (PAPER.md:1481-1504 loop)
+    dec = {"native_1px_ms": time_view(0, wr.Policy(wr.PolicyKind.native, 0), reps=5),
+           "x2_no_reduction_ms": time_view(0, wr.Policy(wr.PolicyKind.sw_b, 33), reps=5),
+           "sw_b_tuned_ms": time_view(0, policy, reps=5)}
+    dec["layout_factor"] = dec["native_1px_ms"] / dec["x2_no_reduction_ms"]
+    dec["distwar_factor"] = dec["x2_no_reduction_ms"] / dec["sw_b_tuned_ms"]
+    dec["total_factor"] = dec["native_1px_ms"] / dec["sw_b_tuned_ms"]
 
     # ---- the step's one exchange, timed alone: NCCL all-reduce
     # of grad[P, 9] fp32, device events, max over ranks; bus bandwidth uses
@@ -421,7 +492,7 @@ def main() -> None:
             dist.all_reduce(grad)
         torch.cuda.synchronize()
         dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0, e1 = ev(), ev()
         e0.record()
         for _ in range(reps):
             dist.all_reduce(grad)
@@ -433,8 +504,8 @@ def main() -> None:
         nbytes = grad.numel() * grad.element_size()
         allreduce = {"bytes": nbytes, "ms": ar_ms, "share_of_step": ar_ms / ms_per_step,
                      "busbw_GBps": nbytes * 2 * (world - 1) / world / (ar_ms * 1e-3) / 1e9,
-                     "backend": dist.get_backend()}
-    contrib_job = contrib_rank * world
+                     "backend": dist.get_backend(), "world": world}
+    contrib_job = float(contrib_rank)
     if dist is not None:
         c = torch.tensor([contrib_rank], device=dev, dtype=torch.float64)
         dist.all_reduce(c)
@@ -442,27 +513,29 @@ def main() -> None:
     value = contrib_job * args.steps / (total_ms * 1e-3)
     naive_value = contrib_job * nv_steps / (total_nv_ms * 1e-3)
 
-    # ---- e2e through the host-buffer C-ABI call (dw_render_views_host) ---
-    # per step: pinned H2D of the scene + the V views' dL/dpixel, forward +
-    # backward of every view, D2H of the V images and of the gradients; at
-    # N > 1 the host gradients are summed across ranks (H2D, NCCL, D2H).
-    from paper_2401_05345_b200.rasterizer import render_views_host
-
+    # ---- e2e through the host-buffer C-ABI calls -------------------------
+    # per step: pinned H2D of the scene + the rank's dL/dpixel, forward +
+    # backward of every view, D2H of the images; N = 1: dw_render_views_host
+    # (gradient D2H inside); N > 1: dw_render_views leaves the gradient in
+    # HBM, NCCL all-reduces it over NVLink, then ONE D2H of the sum
     pin = {k: torch.from_numpy(v).pin_memory() for k, v in sc.items()}
     dL_h = torch.stack([d.cpu() for d in dLs]).pin_memory()
     img_h = torch.empty((V, 3, H, W), dtype=torch.float32).pin_memory()
     grad_h = torch.empty((P, 9), dtype=torch.float32).pin_memory()
+    grad_d = torch.empty((P, 9), dtype=torch.float32, device=dev)
     e2e_r = GaussianRasterizer()
     scene_ptrs = [pin[k].data_ptr() for k in ("means3D", "scales", "rotations", "opacities",
                                                "colors")]
 
     def e2e_step():
-        render_views_host(e2e_r, scene_ptrs, P, cams, dL_h.data_ptr(), policy, img_h.data_ptr(),
-                          grad_h.data_ptr(), stream)
-        if dist is not None:
-            g = grad_h.to(dev, non_blocking=True)
-            dist.all_reduce(g)
-            grad_h.copy_(g)
+        if dist is None:
+            render_views_host(e2e_r, scene_ptrs, P, cams, dL_h.data_ptr(), policy,
+                              img_h.data_ptr(), grad_h.data_ptr(), stream)
+        else:
+            render_views(e2e_r, scene_ptrs, P, cams, dL_h.data_ptr(), policy, img_h.data_ptr(),
+                         grad_d, stream)
+            dist.all_reduce(grad_d)
+            grad_h.copy_(grad_d, non_blocking=True)
             torch.cuda.synchronize()
 
     e2e_step()  # warm-up (allocations)
@@ -479,39 +552,77 @@ def main() -> None:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
     e2e_value = contrib_job * args.e2e_steps / e2e_s
-    h2d = sum(v.nbytes for v in sc.values()) + 3 * H * W * 4 * V + (P * 9 * 4 if world > 1 else 0)
-    d2h = 3 * H * W * 4 * V + P * 9 * 4 * (2 if world > 1 else 1)
+    h2d = sum(v.nbytes for v in sc.values()) + 3 * H * W * 4 * V
+    d2h = 3 * H * W * 4 * V + P * 9 * 4
 
-    # ---- roofline of the dominant kernel (render_backward, one launch/view)
+    # ---- rooflines of the dominant kernel (k_backward_x2<sw_b>) ----------
     hbm_peak, peak_src = measured_peaks()
     mean_launch_ms = statistics.mean(launches)
+    v0_launch_ms = statistics.mean(launches_v0)
     inst = statistics.mean(r.num_rendered for r in rasts)
-    vis = int(sum(int((r.buffer("radii") > 0).sum()) for r in rasts) / V)
+    vis = statistics.mean(int((r.buffer("radii") > 0).sum()) for r in rasts)
     alg_bytes = 4 * inst + 44 * vis + 20 * H * W + 36 * P
     achieved_gbs = alg_bytes / (mean_launch_ms * 1e-3) / 1e9
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "backward_dram_bytes.json")
-    if os.path.exists(prof):
-        traffic = json.load(open(prof)).get(args.workload)
-    # issue roofline: warp instructions per launch (ncu, committed sweep at the
-    # nearest profiled threshold) over the measured launch time, against
-    # 148 SMs x 4 schedulers x 1 inst/cycle at the SM clock seen in the run
+    prof_key = f"{args.workload}@view{my_views[0]}/{total_views}"
+    spec = f"sw_b:{thr}"
+
+    def prof(name):
+        p = os.path.join(ROOT, "profiles", name)
+        return json.load(open(p)).get(prof_key, {}) if os.path.exists(p) else {}
+
+    inst_t, dram_t = prof("backward_inst.json"), prof("backward_dram_bytes.json")
+    traffic = dram_t.get(spec)
     issue = None
-    inst_file = os.path.join(ROOT, "profiles", "backward_inst.json")
-    if os.path.exists(inst_file):
-        table = json.load(open(inst_file)).get(args.workload, {})
-        sw_b = {int(k.split(":")[1]): v for k, v in table.items() if k.startswith("sw_b:")}
-        if sw_b and clocks.get("sm_mhz"):
-            t_near = min(sw_b, key=lambda t: abs(t - thr))
-            ach = sw_b[t_near] / (mean_launch_ms * 1e-3)
-            peak = 148 * 4 * clocks["sm_mhz"] * 1e6
-            issue = {"bound": "issue", "achieved": ach, "peak": peak, "unit": "warp-inst/s",
-                     "frac": ach / peak, "inst_per_launch": sw_b[t_near],
-                     "inst_source": f"ncu sm__inst_executed.sum at sw_b:{t_near}"}
+    if inst_t.get(spec) and clocks.get("sm_mhz"):
+        ach = inst_t[spec] / (v0_launch_ms * 1e-3)
+        peak = 148 * 4 * clocks["sm_mhz"] * 1e6
+        issue = {"bound": "issue", "achieved": ach, "peak": peak, "unit": "warp-inst/s",
+                 "frac": ach / peak, "inst_per_launch": inst_t[spec],
+                 "launch_ms": v0_launch_ms,
+                 "inst_source": f"ncu sm__inst_executed.sum, {prof_key} {spec} "
+                                f"(profiles/backward_inst.json: {inst_t.get('csv')})",
+                 "peak_source": "148 SMs x 4 schedulers x 1 warp-inst/cycle x median SM clock "
+                                "of this run"}
     reds_per_launch = reds_distwar / V
     red_rate = reds_per_launch / (mean_launch_ms * 1e-3)
     naive_launch_ms = statistics.mean(launches_nv)
     naive_red_rate = (contrib_rank / V) / (naive_launch_ms * 1e-3)
+
+    # ---- the north_star target scene (BASELINE configs[2]): one view, naive
+    # vs DISTWAR at its own tuned threshold
+    target = None
+    if rank == 0 and args.workload != TARGET:
+        Pc, Wc, Hc, hcc, _ = CONFIGS[TARGET]
+        tc = {k: torch.from_numpy(v).to(dev)
+              for k, v in make_scene(Pc, Wc, Hc, seed=0, high_contention=hcc).items()}
+        rc = GaussianRasterizer()
+        rc.render_forward(tc["means3D"], tc["scales"], tc["rotations"], tc["opacities"],
+                          tc["colors"], make_camera(Wc, Hc))
+        dLc = torch.from_numpy(make_dL_dpixels(Wc, Hc, seed=1)).to(dev)
+        gc = torch.zeros((Pc, 9), device=dev)
+
+        def tc_ms(pol, reps=5):
+            ms = []
+            for _ in range(reps):
+                e0, e1 = ev(), ev()
+                e0.record()
+                rc.render_backward(dLc, pol, grad=gc)
+                e1.record()
+                torch.cuda.synchronize()
+                ms.append(e0.elapsed_time(e1))
+            return statistics.median(ms)
+
+        _, pc = rc.render_backward(dLc, wr.Policy(wr.PolicyKind.native, 0), grad=gc,
+                                   count_pairs=True)
+        sw = {tt: tc_ms(wr.Policy(wr.PolicyKind.sw_b, tt), reps=3) for tt in range(33)}
+        tbest = min(sw, key=lambda k: (sw[k], k))
+        nat = tc_ms(wr.Policy(wr.PolicyKind.native, 0))
+        swb = tc_ms(wr.Policy(wr.PolicyKind.sw_b, tbest))
+        target = {"workload": TARGET, "pairs": pc, "threshold": tbest, "native_ms": nat,
+                  "sw_b_ms": swb, "speedup": nat / swb,
+                  "sw_b_contributions_per_s": 9 * pc / (swb * 1e-3),
+                  "north_star_target": ">= 2x naive-atomic"}
+        del rc, tc, gc, dLc
 
     tfam = None
     if rank == 0 and not args.no_trace_family:
@@ -519,11 +630,11 @@ def main() -> None:
 
     cpu = cpu_port = None
     if rank == 0 and not args.no_cpu_baseline:
-        # the reference's CPU path (oracle/_ref) on a bounded sample, and the
-        # oracle port's whole backward on every tile, both on this box's cores
-        cpu, _ = reference_measure(args.workload, 3, 1, 16)
-        cpu_port = cpu_port_baseline(sc, make_camera(W, H), make_dL_dpixels(W, H, seed=1),
-                                     args.cpu_tile_stride)
+        # the reference's CPU path (oracle/_ref) on a bounded sample of view 0,
+        # and the oracle port's whole backward of view 0, on this box's cores
+        cpu, _ = reference_measure(args.workload, 3, 1, 16, cams[0])
+        cpu_port = cpu_port_baseline(sc, cams[0], make_dL_dpixels(W, H, seed=1 + my_views[0]),
+                                     args.cpu_tile_stride, args.workload)
 
     if rank == 0:
         line = {
@@ -542,15 +653,19 @@ def main() -> None:
             "naive": {"value": naive_value, "ms_per_step": total_nv_ms / nv_steps,
                       "steps": nv_steps,
                       "speedup_distwar_vs_naive": naive_value and value / naive_value},
+            "decomposition_view0": dec,
+            "target_config": target,
             "forward": {"ms_per_view": statistics.mean(fwd_ms),
-                        "fps": 1e3 / statistics.mean(fwd_ms)},
+                        "fps": 1e3 / statistics.mean(fwd_ms), "stages_view0": stages},
             "contributions_per_step": contrib_job, "pairs_per_view": pairs_per_view,
             "instances_per_view": [r.num_rendered for r in rasts],
             "threshold_sweep_ms": sweep,
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak,
-                         "unit": "GB/s", "frac": achieved_gbs / hbm_peak, "traffic": traffic,
-                         "kernel": "k_backward<sw_b>", "alg_bytes_per_launch": alg_bytes,
+                         "unit": "GB/s", "frac": achieved_gbs / hbm_peak,
+                         "traffic": traffic, "traffic_source": f"ncu dram bytes, {prof_key} {spec}",
+                         "kernel": "k_backward_x2<sw_b>", "alg_bytes_per_launch": alg_bytes,
                          "mean_launch_ms": mean_launch_ms, "peak_source": peak_src},
+            "roofline_binding": "issue",
             "roofline_issue": issue,
             "roofline_l2_atomic": {
                 "distwar": {"reds_per_launch": reds_per_launch, "achieved": red_rate,
@@ -562,9 +677,10 @@ def main() -> None:
                 "measured_red_peaks_per_s": red_peaks, "unit": "REDs/s"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-                    "path": "dw_render_views_host: pinned H2D scene + V dL/dpixel, forward + "
-                            "backward of V views, D2H V images + grad (copy streams "
-                            "double-buffered against compute)"},
+                    "path": ("dw_render_views_host" if dist is None else
+                             "dw_render_views + NCCL all-reduce of the device gradient + one D2H")
+                            + ": pinned H2D scene + V dL/dpixel, forward + backward of V views, "
+                              "D2H V images + grad"},
             "allreduce": allreduce,
             "cpu_baseline": cpu,
             "cpu_port": cpu_port,

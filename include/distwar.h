@@ -251,6 +251,13 @@ dw_status dw_adam_step(int32_t P, float* means3D, float* scales, float* rotation
 
 /* Number of global REDs issued by the last render_backward called with a
  * non-NULL pairs_out (the counting instantiation). */
+/* Per-stage timing of later forwards (diagnostic: CUDA events between the
+ * stages serialise the programmatic-dependent launches): after a forward,
+ * dw_rasterizer_stage_ms returns *count (6) stage times in ms -- preprocess,
+ * depth sort, instance offsets (+ count read-back), binning (duplicate + tile
+ * sort, or dense), tile ranges (+ per-tile sort), blend. */
+dw_status dw_rasterizer_stage_timing(dw_rasterizer* r, int32_t enable);
+dw_status dw_rasterizer_stage_ms(dw_rasterizer* r, double out_ms[6], int32_t* count);
 dw_status dw_rasterizer_last_reds(const dw_rasterizer* r, uint64_t* out);
 
 /* Device views of the rasterizer's intermediate buffers (parity tests):
@@ -285,6 +292,16 @@ dw_status dw_render_views_host(dw_rasterizer* r, int32_t P, const float* means3D
                                const dw_camera* cams, int32_t num_views,
                                const float* dL_dpixels, dw_policy_kind policy, int32_t threshold,
                                float* out_images, float* grad, void* stream);
+/* dw_render_views_host with the gradient left in HBM: d_grad is a device
+ * buffer of P*9 floats (overwritten, complete when the call returns), so a
+ * multi-GPU caller all-reduces it over NVLink before ONE device-to-host copy
+ * (SURVEY §8(b) wr_gs_allreduce_grads: the reduction is the caller's NCCL call
+ * on this buffer). */
+dw_status dw_render_views(dw_rasterizer* r, int32_t P, const float* means3D, const float* scales,
+                          const float* rotations, const float* opacities, const float* colors,
+                          const dw_camera* cams, int32_t num_views, const float* dL_dpixels,
+                          dw_policy_kind policy, int32_t threshold, float* out_images,
+                          float* d_grad, void* stream);
 
 /* --------------------------------------------------- roofline microbenchmarks */
 /* Measured f32 RED throughput (REDs/s) for `pattern`: 0 distinct addresses,

@@ -537,6 +537,8 @@ class Ref:
         L.ref_num_primitives.restype = C.c_int32
         L.ref_export.argtypes = [C.c_void_p] + [C.c_void_p] * 5
         L.ref_criterion1_draws.argtypes = [C.c_int32, C.c_void_p, C.c_void_p]
+        L.ref_read_metrics_csv.argtypes = [C.c_char_p, C.c_int32, C.POINTER(C.c_int64),
+                                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.ref_oracle_sum.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
         L.ref_apply_policy.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int32, C.c_void_p,
                                        C.c_void_p]
@@ -600,6 +602,23 @@ class Ref:
         touched = np.zeros(num_prims * n, np.uint8)
         self._check(self.L.ref_oracle_sum(h, num_prims, sums.ctypes.data, touched.ctypes.data))
         return sums, touched.astype(bool)
+
+    def read_metrics_csv(self, path: str, max_rows: int = 4096):
+        """The reference's experiment::read_metrics_csv on a file: list of
+        (policy kind, threshold or None, 7 integer RunMetrics, energy_proxy,
+        grad_speedup, end_to_end_speedup)."""
+        n = C.c_int64()
+        pol = np.zeros(max_rows, np.int32)
+        thr = np.zeros(max_rows, np.int32)
+        ints = np.zeros(7 * max_rows, np.uint64)
+        dbl = np.zeros(3 * max_rows, np.float64)
+        self._check(self.L.ref_read_metrics_csv(path.encode(), max_rows, C.byref(n),
+                                                pol.ctypes.data, thr.ctypes.data,
+                                                ints.ctypes.data, dbl.ctypes.data))
+        k = min(n.value, max_rows)
+        return [(int(pol[i]), None if thr[i] < 0 else int(thr[i]),
+                 ints[7 * i:7 * i + 7].tolist(), *dbl[3 * i:3 * i + 3].tolist())
+                for i in range(k)]
 
     def criterion1_draws(self, ntraces: int):
         """The (SceneSpec, thresholds) sequence of the reference's acceptance

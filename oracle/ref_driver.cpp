@@ -16,12 +16,14 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <fstream>
 #include <map>
 #include <stdexcept>
 #include <string>
 #include <thread>
 #include <vector>
 
+#include "warpred/experiment.hpp"
 #include "warpred/hwsim.hpp"
 #include "warpred/reducers.hpp"
 #include "warpred/trace_io.hpp"
@@ -262,8 +264,18 @@ int ref_time_policy(const void* h, int kind, int threshold, int32_t num_prims,
       });
     }
     for (auto& th : pool) th.join();
-    for (int i = 1; i < threads; ++i)
-      for (size_t w = 0; w < words; ++w) bufs[0][w] += bufs[i][w];
+    // merge the per-thread buffers in parallel, each thread one slice of the
+    // addresses (a serial merge would cost O(threads * P * N) whatever the
+    // sample size)
+    pool.clear();
+    for (int i = 0; i < threads; ++i) {
+      const size_t b = words * i / threads, e = words * (i + 1) / threads;
+      pool.emplace_back([&, b, e] {
+        for (int k = 1; k < threads; ++k)
+          for (size_t w = b; w < e; ++w) bufs[0][w] += bufs[k][w];
+      });
+    }
+    for (auto& th : pool) th.join();
     const auto t1 = std::chrono::steady_clock::now();
     *seconds = std::chrono::duration<double>(t1 - t0).count();
     uint64_t c = 0, qq = 0;
@@ -272,6 +284,34 @@ int ref_time_policy(const void* h, int kind, int threshold, int32_t num_prims,
     for (int i = 0; i < threads; ++i) qq += q[i];
     *contributions = c;
     *requests = qq;
+  });
+}
+
+// experiment::read_metrics_csv (experiment.cpp:319-336) over a metrics.csv
+// file: the reference's own reader accepting a file this repo writes
+// (tools/metrics_csv.py). Copies up to max_rows rows out:
+// policy kind, threshold (-1 when "-"), the 7 integer RunMetrics fields, and
+// energy_proxy / grad_speedup / end_to_end_speedup.
+int ref_read_metrics_csv(const char* path, int32_t max_rows, int64_t* nrows, int32_t* policy,
+                         int32_t* threshold, uint64_t* ints7, double* doubles3) {
+  return guarded([&] {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw std::runtime_error(std::string("cannot open ") + path);
+    const auto rows = experiment::read_metrics_csv(in);
+    *nrows = static_cast<int64_t>(rows.size());
+    for (size_t i = 0; i < rows.size() && static_cast<int32_t>(i) < max_rows; ++i) {
+      const auto& c = rows[i];
+      policy[i] = static_cast<int32_t>(c.policy);
+      threshold[i] = c.threshold ? *c.threshold : -1;
+      const auto& m = c.metrics;
+      const uint64_t v[7] = {m.total_cycles, m.stalls_lsu, m.stalls_other,
+                             m.atomic_requests_to_l2, m.core_instructions, m.core_fp_adds,
+                             m.interconnect_packets};
+      std::memcpy(ints7 + 7 * i, v, sizeof v);
+      doubles3[3 * i + 0] = m.energy_proxy;
+      doubles3[3 * i + 1] = c.grad_speedup;
+      doubles3[3 * i + 2] = c.end_to_end_speedup;
+    }
   });
 }
 

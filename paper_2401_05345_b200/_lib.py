@@ -127,6 +127,8 @@ SIGNATURES = {
     "dw_rasterizer_reserve": (C.c_int, [vp, i32, i32, i32, i64]),
     "dw_rasterizer_num_rendered": (C.c_int, [vp, C.POINTER(i64), C.POINTER(C.c_int)]),
     "dw_rasterizer_last_reds": (C.c_int, [vp, C.POINTER(u64)]),
+    "dw_rasterizer_stage_timing": (C.c_int, [vp, i32]),
+    "dw_rasterizer_stage_ms": (C.c_int, [vp, vp, C.POINTER(i32)]),
     "dw_preprocess_backward": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
     "dw_render_backward_tap": (C.c_int, [vp, vp, i32, vp, i64, C.POINTER(vp), C.POINTER(i64),
                                          vp]),
@@ -136,6 +138,8 @@ SIGNATURES = {
                                  i32, vp, vp, vp]),
     "dw_render_views_host": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, vp, i32, vp, C.c_int, i32,
                                        vp, vp, vp]),
+    "dw_render_views": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, vp, i32, vp, C.c_int, i32,
+                                  vp, vp, vp]),
     "dw_copy_to_host": (C.c_int, [vp, vp, C.c_size_t]),
     "dw_microbench_red": (C.c_int, [i32, i64, C.POINTER(C.c_double), vp]),
 }

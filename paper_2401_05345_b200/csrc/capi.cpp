@@ -23,6 +23,8 @@ int64_t raster_resolve(dw_rasterizer* r, bool* overflowed);
 void raster_backward(dw_rasterizer* r, const float* dL, int policy, int thr, float* grad,
                      uint64_t* pairs, cudaStream_t s);
 uint64_t raster_last_reds(const dw_rasterizer* r);
+void raster_stage_timing(dw_rasterizer* r, bool on);
+int raster_stage_ms(dw_rasterizer* r, double* out, int cap);
 void raster_buffer(const dw_rasterizer* r, int which, const void** p, int64_t* count);
 void raster_host(dw_rasterizer* r, int32_t P, const float* m, const float* sc, const float* rot,
                  const float* op, const float* col, const dw_camera* cam, const float* dL,
@@ -30,7 +32,7 @@ void raster_host(dw_rasterizer* r, int32_t P, const float* m, const float* sc, c
 void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float* sc,
                        const float* rot, const float* op, const float* col, const dw_camera* cams,
                        int32_t V, const float* dL, int policy, int thr, float* out_images,
-                       float* grad, cudaStream_t s);
+                       float* grad, cudaStream_t s, bool grad_on_device);
 void raster_preprocess_backward(dw_rasterizer* r, const float* means3D, const float* scales,
                                 const float* rotations, const float* grad2d, float* grad3d,
                                 cudaStream_t s);
@@ -549,6 +551,20 @@ dw_status dw_rasterizer_last_reds(const dw_rasterizer* r, uint64_t* out) {
   return DW_OK;
 }
 
+dw_status dw_rasterizer_stage_timing(dw_rasterizer* r, int32_t enable) {
+  if (!r) return fail_invalid("null argument");
+  dw::raster_stage_timing(r, enable != 0);
+  return DW_OK;
+}
+
+dw_status dw_rasterizer_stage_ms(dw_rasterizer* r, double out_ms[6], int32_t* count) {
+  if (!r || !out_ms || !count) return fail_invalid("null argument");
+  return guarded([&] {
+    *count = dw::raster_stage_ms(r, out_ms, 6);
+    return DW_OK;
+  });
+}
+
 dw_status dw_rasterizer_buffer(const dw_rasterizer* r, int32_t which, const void** dptr,
                                int64_t* count) {
   if (!r || !dptr || !count) return fail_invalid("null argument");
@@ -586,7 +602,24 @@ dw_status dw_render_views_host(dw_rasterizer* r, int32_t P, const float* means3D
     check_policy(policy, threshold);
     dw::raster_views_host(r, P, means3D, scales, rotations, opacities, colors, cams, num_views,
                           dL_dpixels, policy, threshold, out_images, grad,
-                          dw::as_stream(stream));
+                          dw::as_stream(stream), false);
+    return DW_OK;
+  });
+}
+
+dw_status dw_render_views(dw_rasterizer* r, int32_t P, const float* means3D, const float* scales,
+                          const float* rotations, const float* opacities, const float* colors,
+                          const dw_camera* cams, int32_t num_views, const float* dL_dpixels,
+                          dw_policy_kind policy, int32_t threshold, float* out_images,
+                          float* d_grad, void* stream) {
+  if (!r || !cams || !dL_dpixels || (P > 0 && !d_grad) ||
+      (P > 0 && (!means3D || !scales || !rotations || !opacities || !colors)))
+    return fail_invalid("null argument");
+  return guarded([&] {
+    check_policy(policy, threshold);
+    dw::raster_views_host(r, P, means3D, scales, rotations, opacities, colors, cams, num_views,
+                          dL_dpixels, policy, threshold, out_images, d_grad,
+                          dw::as_stream(stream), true);
     return DW_OK;
   });
 }

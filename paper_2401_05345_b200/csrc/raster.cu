@@ -110,6 +110,21 @@ struct dw_rasterizer {
   dw_rasterizer* twin = nullptr;  // forward state of the odd views
   cudaEvent_t ev[10] = {};
 
+  // Per-stage forward timing (dw_rasterizer_stage_timing): events recorded
+  // between the forward's stages. Diagnostic only: an event between two
+  // programmatic-dependent launches serialises them, so the stages add up
+  // to a little more than the untimed forward.
+  static constexpr int kStages = 6;  // preprocess, depth sort, offsets, binning, ranges, blend
+  bool stage_timing = false;
+  bool stage_valid = false;
+  cudaEvent_t st_ev[kStages + 1] = {};
+  void stage_mark(int i, cudaStream_t s) {
+    if (!stage_timing) return;
+    if (!st_ev[0])
+      for (auto& e : st_ev) DW_CUDA(cudaEventCreate(&e));
+    DW_CUDA(cudaEventRecord(st_ev[i], s));
+  }
+
   void ensure_streams() {
     if (s_in) return;
     DW_CUDA(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
@@ -128,6 +143,8 @@ struct dw_rasterizer {
     for (float* p : h_bufs)
       if (p) cudaFree(p);
     if (h_total) cudaFreeHost(h_total);
+    if (st_ev[0])
+      for (auto& e : st_ev) cudaEventDestroy(e);
     delete twin;
     if (s_in) {
       cudaStreamDestroy(s_in);
@@ -273,9 +290,12 @@ struct dw_rasterizer {
                                          last_list_mean < kTileFirstMaxMean;
     // the depth-first paths' sort keys come straight out of the preprocess
     const bool keys_ready = !tile_first;
+    stage_valid = stage_timing;
+    stage_mark(0, s);
     dw::launch_preprocess(P, means3D, scales, rotations, opacities, colors, cam, means2D, depths,
                           radii, conic_opacity, rgb, tiles_touched, keys_ready ? dkey[0] : nullptr,
                           keys_ready ? dids[0] : nullptr, s);
+    stage_mark(1, s);
     // Instance count: read back (one host sync) to size the buffers, or --
     // nosync -- kept on the device against the reserved capacity
     // (dw_rasterizer_reserve), so the whole forward is graph-capturable.
@@ -294,11 +314,13 @@ struct dw_rasterizer {
     };
     if (P > 0) {
       if (tile_first) {
+        stage_mark(2, s);  // no depth sort on this path
         // instance offsets in index order
         dw::inclusive_scan_gather(tiles_touched, nullptr, P, offsets, scan_tmp, s);
       } else {
         // 1. Gaussians in (depth, id) order: stable 32-bit LSD sort
         depth_sort(true);
+        stage_mark(2, s);
         // instance offsets in that order (a sequential scan, no gather)
         dw::inclusive_scan_gather(area_sorted, nullptr, P, offsets, scan_tmp, s);
       }
@@ -319,6 +341,10 @@ struct dw_rasterizer {
         last_list_mean = static_cast<double>(num_rendered) / ntiles;
       }
     }
+    if (P == 0) {
+      stage_mark(2, s);
+    }
+    stage_mark(3, s);
     if (n_grid >= (int64_t(1) << 32)) throw std::runtime_error("more than 2^32 tile instances");
     const size_t ni = static_cast<size_t>(std::max<int64_t>(n_grid, 1));
     for (int b = 0; b < 2; ++b) {
@@ -348,6 +374,7 @@ struct dw_rasterizer {
       tiles_sorted = itile[cur];
       vals = ivals[cur];
     }
+    stage_mark(4, s);
     if (!dense) dw::launch_ranges_u32(n_grid, tiles_sorted, ranges, ntiles, s, n_dev);
     if (!dense && tile_first && n_grid > 0) {
       // 4. every tile's list (index order) -> (depth, index) order
@@ -355,8 +382,10 @@ struct dw_rasterizer {
       dw::launch_segsort_depth(ranges, depths, vals, seg_scratch, n_grid, ntiles, s);
     }
     order_stale = true;  // the backward derives its tile order from these ranges
+    stage_mark(5, s);
     dw::launch_forward_impl(cam, ranges, vals, means2D, conic_opacity, rgb, nullptr, final_T,
                             n_contrib, out_color, s);
+    stage_mark(6, s);
     if (radii_out && P > 0)
       DW_CUDA(cudaMemcpyAsync(radii_out, radii, sizeof(int) * P, cudaMemcpyDeviceToDevice, s));
     forward_done = true;
@@ -443,6 +472,20 @@ void raster_backward(dw_rasterizer* r, const float* dL, int policy, int thr, flo
 }
 
 uint64_t raster_last_reds(const dw_rasterizer* r) { return r->last_reds; }
+
+void raster_stage_timing(dw_rasterizer* r, bool on) { r->stage_timing = on; }
+
+int raster_stage_ms(dw_rasterizer* r, double* out, int cap) {
+  if (!r->stage_valid || !r->st_ev[0]) throw std::invalid_argument("no stage-timed forward");
+  DW_CUDA(cudaEventSynchronize(r->st_ev[dw_rasterizer::kStages]));
+  const int n = std::min(cap, dw_rasterizer::kStages);
+  for (int i = 0; i < n; ++i) {
+    float ms = 0;
+    DW_CUDA(cudaEventElapsedTime(&ms, r->st_ev[i], r->st_ev[i + 1]));
+    out[i] = ms;
+  }
+  return n;
+}
 
 void raster_reserve(dw_rasterizer* r, int32_t P, int32_t W, int32_t H, int64_t max_instances) {
   r->reserve(P, W, H, max_instances);
@@ -601,10 +644,14 @@ void raster_host(dw_rasterizer* r, int32_t P, const float* m, const float* sc, c
 // buffer. dL/dpixel uploads (copy stream s_in) and image downloads (copy
 // stream s_out) are double-buffered against the compute stream, so with
 // pinned host memory the PCIe traffic of view k+1 / k-1 overlaps view k.
+// grad_on_device: `grad` is a device buffer of P*9 floats that receives the
+// batch's gradient (overwritten) and stays in HBM -- for a caller that reduces
+// it across GPUs before the one device-to-host copy; otherwise `grad` is host
+// memory and the gradient is copied there.
 void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float* sc,
                        const float* rot, const float* op, const float* col, const dw_camera* cams,
                        int32_t V, const float* dL, int policy, int thr, float* out_images,
-                       float* grad, cudaStream_t s) {
+                       float* grad, cudaStream_t s, bool grad_on_device) {
   if (V < 1) throw std::invalid_argument("need at least one view");
   for (int k = 1; k < V; ++k)
     if (cams[k].width != cams[0].width || cams[k].height != cams[0].height)
@@ -617,7 +664,7 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
   float* d_rot = r->host_scratch(2, 4 * np);
   float* d_op = r->host_scratch(3, np);
   float* d_col = r->host_scratch(4, 3 * np);
-  float* d_g = r->host_scratch(7, kNParam * np);
+  float* d_g = grad_on_device ? grad : r->host_scratch(7, kNParam * np);
   float* d_dl[2] = {r->host_scratch(5, 3 * npx), r->host_scratch(8, 3 * npx)};
   float* d_img[2] = {r->host_scratch(6, 3 * npx), r->host_scratch(9, 3 * npx)};
   cudaEvent_t e_scene = r->ev[0], e_in[2] = {r->ev[1], r->ev[2]},
@@ -702,7 +749,7 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
     if (!ovf0 && !ovf1) break;
     nosync_ok = false;  // redo every view with host-read instance counts
   }
-  if (P > 0)
+  if (P > 0 && !grad_on_device)
     DW_CUDA(cudaMemcpyAsync(grad, d_g, kNParam * size_t(P) * sizeof(float),
                             cudaMemcpyDeviceToHost, s));
   DW_CUDA(cudaStreamSynchronize(s));

@@ -238,6 +238,19 @@ class GaussianRasterizer:
             _ptr(grad3d, "grad3d", f32, min_numel=NPARAM3D * P), _stream(stream)))
         return grad3d
 
+    STAGES = ("preprocess", "depth_sort", "offsets", "binning", "ranges", "blend")
+
+    def stage_timing(self, enable: bool = True):
+        """Record CUDA events between the stages of later forwards (diagnostic)."""
+        check(lib().dw_rasterizer_stage_timing(self._h, 1 if enable else 0))
+
+    def stage_ms(self) -> dict:
+        """Per-stage ms of the last stage-timed forward (synchronises)."""
+        out = (C.c_double * 6)()
+        n = C.c_int32()
+        check(lib().dw_rasterizer_stage_ms(self._h, out, C.byref(n)))
+        return {self.STAGES[i]: out[i] for i in range(n.value)}
+
     def _npix3(self) -> int:
         if self.camera is None:
             raise _lib.InvalidArgument(1, "render_backward before render_forward")
@@ -337,6 +350,21 @@ def render_views_host(rast: "GaussianRasterizer", scene_ptrs, P: int, cams, dL_p
     check(lib().dw_render_views_host(rast.handle, P, *scene_ptrs, arr, len(cams), dL_ptr,
                                      int(policy.kind), policy.threshold, images_ptr, grad_ptr,
                                      None if stream is None else _stream(stream)))
+
+
+def render_views(rast: "GaussianRasterizer", scene_ptrs, P: int, cams, dL_ptr: int,
+                 policy: Policy, images_ptr, grad, stream=None):
+    """dw_render_views: render_views_host with the gradient left on the
+    device in `grad` (a CUDA tensor of P*9 fp32, overwritten) -- the multi-GPU
+    path all-reduces it over NCCL before one device-to-host copy."""
+    import torch
+
+    arr = (_lib.CameraC * len(cams))(*[c.to_c() for c in cams])
+    check(lib().dw_render_views(rast.handle, P, *scene_ptrs, arr, len(cams), dL_ptr,
+                                int(policy.kind), policy.threshold, images_ptr,
+                                _ptr(grad, "grad", torch.float32, NPARAM * P),
+                                None if stream is None else _stream(stream)))
+    return grad
 
 
 def microbench_red(pattern: int, ops: int = 1 << 28, stream=None) -> float:

@@ -1,50 +1,70 @@
 """Regenerate profiles/backward_inst.json and profiles/backward_dram_bytes.json
-(read by bench.py for its issue roofline and `traffic`) from the per-policy
-ncu CSVs of tools/threshold_sweep_ncu.sh.
+(read by bench.py for its issue roofline and roofline `traffic`) from an ncu
+CSV of tools/profile_sweep.py (one k_backward launch per spec, in spec order).
 
-    python tools/profile_json.py c3_1m_1080p profiles/r01/thr_sweep_csv/*.csv
+    python tools/profile_json.py gpurun_out/specs.json gpurun_out/sweep.csv
+
+Entries are keyed "<workload>@view<k>/<views>" -> {spec: value}; other keys in
+the files are kept.
 """
+import csv
+import io
 import json
 import os
-import re
 import sys
-
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
-from threshold_sweep_summary import load  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def main(workload, paths):
-    inst, dram = {}, {}
-    for p in paths:
-        m = re.search(r"thr_sweep_(\w+?)_(\d+)\.csv$", p)
-        if not m:
-            continue
-        d = load(p)
-        if not d:
-            continue
-        key = f"{m.group(1)}:{m.group(2)}"
-        if "sm__inst_executed.sum" in d:
-            inst[key] = d["sm__inst_executed.sum"]
-        if "dram__bytes_read.sum" in d and "dram__bytes_write.sum" in d:
-            dram[key] = d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"]
-    src = os.path.relpath(os.path.dirname(os.path.abspath(paths[0])), ROOT)
-    out_i = {"_source": f"ncu sm__inst_executed.sum (warp instructions) of one backward launch "
-                        f"per policy:threshold, {workload} view 0, {src}",
-             workload: dict(sorted(inst.items()))}
-    json.dump(out_i, open(os.path.join(ROOT, "profiles", "backward_inst.json"), "w"), indent=1)
-    # traffic of the SW-B launch nearest the bench's usual threshold (10-12)
-    swb = {int(k.split(":")[1]): v for k, v in dram.items() if k.startswith("sw_b:")}
-    if swb:
-        t = min(swb, key=lambda x: abs(x - 10))
-        out_d = {"_source": f"ncu dram__bytes_read.sum + dram__bytes_write.sum of one SW-B "
-                            f"backward launch (t = {t}), {workload} view 0, {src}",
-                 workload: swb[t], "per_threshold": {f"sw_b:{k}": v for k, v in sorted(swb.items())}}
-        json.dump(out_d, open(os.path.join(ROOT, "profiles", "backward_dram_bytes.json"), "w"),
-                  indent=1)
-    print(f"{len(inst)} instruction counts, {len(dram)} traffic figures")
+def launches(path):
+    """[{metric: value}] per kernel launch, in launch order."""
+    text = open(path).read()
+    start = text.find('"ID"')
+    rows = list(csv.DictReader(io.StringIO(text[start:])))
+    out, order = {}, []
+    for row in rows:
+        i = int(row["ID"])
+        if i not in out:
+            out[i] = {"kernel": row["Kernel Name"]}
+            order.append(i)
+        v = row["Metric Value"].replace(",", "")
+        try:
+            out[i][row["Metric Name"]] = float(v)
+        except ValueError:
+            pass
+    return [out[i] for i in order]
+
+
+def main(specs_path, csv_path):
+    sp = json.load(open(specs_path))
+    ls = launches(csv_path)
+    if len(ls) != len(sp["specs"]):
+        raise SystemExit(f"{len(ls)} launches for {len(sp['specs'])} specs")
+    key = f"{sp['workload']}@view{sp['view']}/{sp['views']}"
+    src = os.path.relpath(os.path.abspath(csv_path), ROOT)
+    files = {"inst": os.path.join(ROOT, "profiles", "backward_inst.json"),
+             "dram": os.path.join(ROOT, "profiles", "backward_dram_bytes.json"),
+             "time": os.path.join(ROOT, "profiles", "backward_ncu_ms.json")}
+    tables = {}
+    for name, p in files.items():
+        tables[name] = json.load(open(p)) if os.path.exists(p) else {}
+    inst, dram, tms = {}, {}, {}
+    for spec, l in zip(sp["specs"], ls):
+        inst[spec] = l.get("sm__inst_executed.sum")
+        if "dram__bytes_read.sum" in l and "dram__bytes_write.sum" in l:
+            dram[spec] = l["dram__bytes_read.sum"] + l["dram__bytes_write.sum"]
+        if "gpu__time_duration.sum" in l:
+            tms[spec] = l["gpu__time_duration.sum"] * 1e-6  # ns -> ms
+    tables["inst"]["_source"] = ("ncu sm__inst_executed.sum (warp instructions) of one backward "
+                                 "launch per policy:threshold (tools/profile_sweep.py)")
+    tables["dram"]["_source"] = ("ncu dram__bytes_read.sum + dram__bytes_write.sum of one "
+                                 "backward launch per policy:threshold (tools/profile_sweep.py)")
+    tables["time"]["_source"] = "ncu gpu__time_duration.sum (cold, serialised) per launch, ms"
+    for name, d in (("inst", inst), ("dram", dram), ("time", tms)):
+        tables[name][key] = {"csv": src, "instances": sp["instances"], **d}
+        json.dump(tables[name], open(files[name], "w"), indent=1)
+    print(key, len(inst), "specs")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2:])
+    main(sys.argv[1], sys.argv[2])
