@@ -19,6 +19,12 @@
 #include "dw_internal.h"
 #include "raster.cuh"
 
+#ifndef DW_SCATTER
+// scatter binning (raster_scatter.cu) on by default? A/B on B200 (tools/forward_ab.py,
+// profiles/r02/forward_binning_ab.md): C3 forward 0.594 vs 0.598 ms depth-first,
+// C5 view 0 0.926 vs 0.910 ms -- a tie, so the depth-first sort stays the default
+#define DW_SCATTER 0
+#endif
 #ifndef DW_TILE_FIRST
 #define DW_TILE_FIRST 1  // sort path: duplicate by index, sort by tile, depth-sort per tile
 #endif
@@ -86,6 +92,9 @@ struct dw_rasterizer {
   unsigned long long* seg_scratch = nullptr;  // tile-first: long lists' merge buffers (2 x I)
   size_t cap_seg = 0;
   bool dense = false;              // last forward used dense (tile-major) binning
+  bool scatter = false;            // last forward used scatter binning (raster_scatter.cu)
+  uint32_t* sc_scratch = nullptr;  // scatter binning: per-(segment, tile) counts + totals
+  size_t cap_sc = 0;
   bool tile_first = false;         // last forward binned tile-first (per-tile depth sort)
   double last_list_mean = -1.0;    // instances per tile of the last counted forward
   static constexpr double kTileFirstMaxMean = 384.0;
@@ -137,7 +146,7 @@ struct dw_rasterizer {
     void* ps[] = {means2D, depths, radii, conic_opacity, rgb, tiles_touched, offsets, dkey[0],
                   dkey[1], dids[0], dids[1], itile[0], itile[1], ivals[0], ivals[1], ranges,
                   final_T, n_contrib, tmp, scan_tmp, keys_dbg, counters, live_dev, overflow_dev,
-                  tile_order, rects, diff, area_sorted, seg_scratch};
+                  tile_order, rects, diff, area_sorted, seg_scratch, sc_scratch};
     for (void* p : ps)
       if (p) cudaFree(p);
     for (float* p : h_bufs)
@@ -201,6 +210,8 @@ struct dw_rasterizer {
       grow(ivals[b], cap_i[2 + b], ni);
     }
     grow(seg_scratch, cap_seg, 2 * ni);
+    if (dw::scatter_binning_fits(static_cast<int>(ntiles)))
+      grow(sc_scratch, cap_sc, dw::scatter_scratch_words(P_, static_cast<int>(ntiles)));
     const int tx = (W_ + dw::kTile - 1) / dw::kTile, ty = (H_ + dw::kTile - 1) / dw::kTile;
     if (dw::dense_binning_fits(tx, ty)) {  // dense binning allocates nothing in the forward
       grow(rects, cap_r, np);
@@ -285,11 +296,17 @@ struct dw_rasterizer {
     // network: C2, ~190 per tile: 0.240 -> 0.220 ms; C3, ~570: 0.655 -> 0.848),
     // so it is chosen from the previous frame's mean list length.
     const char* tf_env = std::getenv("DW_TILE_FIRST");  // "0" / "1" force
-    tile_first = tf_env && *tf_env ? *tf_env == '1'
-                                   : DW_TILE_FIRST != 0 && last_list_mean >= 0.0 &&
-                                         last_list_mean < kTileFirstMaxMean;
+    // Scatter binning (DW_SCATTER=1, or the compile-time default): per-tile
+    // counts, placement, on-chip depth sort per tile -- no global sort at
+    // all (raster_scatter.cu). A forced tile-first path turns it off.
+    const char* sc_env = std::getenv("DW_SCATTER");
+    scatter = (sc_env && *sc_env ? *sc_env == '1' : DW_SCATTER != 0) &&
+              !(tf_env && *tf_env == '1') && dw::scatter_binning_fits(ntiles);
+    tile_first = !scatter && (tf_env && *tf_env ? *tf_env == '1'
+                                                : DW_TILE_FIRST != 0 && last_list_mean >= 0.0 &&
+                                                      last_list_mean < kTileFirstMaxMean);
     // the depth-first paths' sort keys come straight out of the preprocess
-    const bool keys_ready = !tile_first;
+    const bool keys_ready = !tile_first && !scatter;
     stage_valid = stage_timing;
     stage_mark(0, s);
     dw::launch_preprocess(P, means3D, scales, rotations, opacities, colors, cam, means2D, depths,
@@ -313,8 +330,8 @@ struct dw_rasterizer {
       depth_sorted = true;
     };
     if (P > 0) {
-      if (tile_first) {
-        stage_mark(2, s);  // no depth sort on this path
+      if (tile_first || scatter) {
+        stage_mark(2, s);  // no depth sort on these paths
         // instance offsets in index order
         dw::inclusive_scan_gather(tiles_touched, nullptr, P, offsets, scan_tmp, s);
       } else {
@@ -365,6 +382,11 @@ struct dw_rasterizer {
       if (!depth_sorted) depth_sort(false);
       dw::launch_dense_binning(P, order, means2D, radii, cam, rects, diff, ranges, ivals[0],
                                n_dev, static_cast<uint64_t>(n_grid), s);
+    } else if (scatter && n_grid > 0) {
+      grow(sc_scratch, cap_sc, dw::scatter_scratch_words(P, ntiles));
+      grow(seg_scratch, cap_seg, 2 * static_cast<size_t>(n_grid));
+      dw::launch_scatter_binning(P, means2D, radii, depths, cam, sc_scratch, ranges, ivals[0],
+                                 seg_scratch, n_grid, n_dev, s);
     } else if (n_grid > 0) {
       // 2. duplicate (index order, or depth order), 3. stable sort by tile id
       dw::launch_duplicate_sorted(P, tile_first ? nullptr : order, means2D, radii, offsets, cam,
@@ -375,8 +397,10 @@ struct dw_rasterizer {
       vals = ivals[cur];
     }
     stage_mark(4, s);
-    if (!dense) dw::launch_ranges_u32(n_grid, tiles_sorted, ranges, ntiles, s, n_dev);
-    if (!dense && tile_first && n_grid > 0) {
+    const bool scattered = scatter && !dense && n_grid > 0;  // ranges already written
+    if (!scattered) scatter = false;
+    if (!dense && !scattered) dw::launch_ranges_u32(n_grid, tiles_sorted, ranges, ntiles, s, n_dev);
+    if (!dense && !scattered && tile_first && n_grid > 0) {
       // 4. every tile's list (index order) -> (depth, index) order
       grow(seg_scratch, cap_seg, 2 * static_cast<size_t>(n_grid));
       dw::launch_segsort_depth(ranges, depths, vals, seg_scratch, n_grid, ntiles, s);
@@ -589,10 +613,11 @@ void raster_buffer(const dw_rasterizer* r, int which, const void** p, int64_t* c
     case 5: {  // (tile << 32 | depth bits) of the sorted instances, built on request
       auto* m = const_cast<dw_rasterizer*>(r);
       grow(m->keys_dbg, m->cap_keys, static_cast<size_t>(std::max<int64_t>(I, 1)));
-      if (r->dense)  // dense binning writes no tile-id array: derive it from the ranges
+      const bool no_tiles = r->dense || r->scatter;  // no tile-id array: derive it from the ranges
+      if (no_tiles)
         launch_tiles_from_ranges(r->ranges, r->cam.tiles_x * r->cam.tiles_y, r->itile[0],
                                  nullptr);
-      launch_make_keys(I, r->dense ? r->itile[0] : r->tiles_sorted, r->vals, r->depths,
+      launch_make_keys(I, no_tiles ? r->itile[0] : r->tiles_sorted, r->vals, r->depths,
                        m->keys_dbg, nullptr);
       DW_CUDA(cudaDeviceSynchronize());
       *p = r->keys_dbg;

@@ -133,9 +133,21 @@ void launch_dense_binning(int P, const uint32_t* order, const float2* means2D, c
 void launch_tiles_from_ranges(const uint2* ranges, int ntiles, uint32_t* tiles, cudaStream_t s);
 // Per-tile stable depth sort of index-ordered tile lists (tile-first binning);
 // scratch: 2 x instances u64 (used by lists longer than the shared-memory cap).
+// min_n: only lists of at least min_n elements are sorted (the others are
+// left as they are -- already sorted by another kernel).
 void launch_segsort_depth(const uint2* ranges, const float* depths, uint32_t* values,
                           unsigned long long* scratch, int64_t capacity, int ntiles,
-                          cudaStream_t s);
+                          cudaStream_t s, int min_n = 2);
+// Scatter binning (raster_scatter.cu): per-(segment, tile) counts, placement,
+// per-tile on-chip depth sort. scratch: scatter_scratch_words(P, ntiles) u32;
+// seg_scratch = 2 x seg_half u64 for lists longer than scatter_sort_cap().
+int scatter_sort_cap();
+bool scatter_binning_fits(int ntiles);
+size_t scatter_scratch_words(int P, int ntiles);
+void launch_scatter_binning(int P, const float2* means2D, const int* radii, const float* depths,
+                            const CamParams& cam, uint32_t* scratch, uint2* ranges,
+                            uint32_t* values, unsigned long long* seg_scratch, int64_t seg_half,
+                            const unsigned long long* n_dev, cudaStream_t s);
 // order[ntiles]: tiles by descending list length (bucketed), for the blend kernels
 void launch_tile_order(const uint2* ranges, int ntiles, uint32_t* order, cudaStream_t s);
 // ranges[0, ntiles) of the sorted tile ids (every range written)

@@ -582,7 +582,7 @@ __device__ __forceinline__ void bitonic_smem(unsigned long long* a, int npad) {
 __global__ void __launch_bounds__(256)
     k_segsort_depth(const uint2* __restrict__ ranges, const float* __restrict__ depths,
                     uint32_t* __restrict__ values, unsigned long long* __restrict__ scratch,
-                    int ntiles, int64_t half) {
+                    int ntiles, int64_t half, int min_n) {
   pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
   __shared__ unsigned long long s_k[kSegCap];
@@ -590,7 +590,7 @@ __global__ void __launch_bounds__(256)
   if (tile >= ntiles) return;
   const uint2 r = ranges[tile];
   const int n = static_cast<int>(r.y - r.x);
-  if (n <= 1) return;
+  if (n <= 1 || n < min_n) return;  // min_n: only the lists another sort left over
   auto key_of = [&](int i) {
     const uint32_t id = values[r.x + i];
     return static_cast<unsigned long long>(__float_as_uint(__ldg(depths + id))) << 32 | id;
@@ -1169,10 +1169,10 @@ void launch_tiles_from_ranges(const uint2* ranges, int ntiles, uint32_t* tiles, 
 
 void launch_segsort_depth(const uint2* ranges, const float* depths, uint32_t* values,
                           unsigned long long* scratch, int64_t capacity, int ntiles,
-                          cudaStream_t s) {
+                          cudaStream_t s, int min_n) {
   if (ntiles <= 0) return;
   launch_pdl(k_segsort_depth, ntiles, 256, 0, s, ranges, depths, values, scratch, ntiles,
-             capacity);
+             capacity, min_n);
   DW_CUDA(cudaGetLastError());
 }
 

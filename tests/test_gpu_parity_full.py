@@ -7,7 +7,7 @@ element by element (none excused), pair counts exactly.
 """
 import pytest
 
-from parity import verify_case
+from parity import set_binning, verify_case
 
 pytestmark = pytest.mark.gpu
 
@@ -42,6 +42,13 @@ def test_c3_view0_full(cuda, orc):
     verify_case(cuda, orc, "c3_view0", sc, cam, dL, [_pol(*p) for p in ALL])
 
 
+@pytest.mark.parametrize("binning", ["depth-first", "tile-first"])
+def test_c3_other_list_constructions(cuda, orc, binning, monkeypatch):
+    set_binning(monkeypatch, binning)
+    sc, cam, dL = _scene("c3_1m_1080p")
+    verify_case(cuda, orc, f"c3_view0_{binning}", sc, cam, dL, [_pol("sw_b", 8)])
+
+
 def test_c3_orbit_view_full(cuda, orc):
     sc, cam, dL = _scene("c3_1m_1080p", view=50, views=64)
     verify_case(cuda, orc, "c3_view50of64", sc, cam, dL,
@@ -50,9 +57,7 @@ def test_c3_orbit_view_full(cuda, orc):
 
 @pytest.mark.parametrize("binning", ["auto", "depth-first"])
 def test_c4_contention_full(cuda, orc, binning, monkeypatch):
-    if binning == "depth-first":
-        monkeypatch.setenv("DW_DENSE_BINNING", "0")
-        monkeypatch.setenv("DW_TILE_FIRST", "0")
+    set_binning(monkeypatch, binning)
     sc, cam, dL = _scene("c4_200k_contention_1080p")
     pols = [_pol("sw_b", 0), _pol("native", 0)] if binning == "auto" else [_pol("sw_b", 0)]
     # native: ~6,600 fp32 atomic additions per address (1.32 G pairs into
@@ -70,18 +75,14 @@ SMALL = [("tiny_odd", 300, 61, 47, False, 0), ("c1_10k_256", 10_000, 256, 256, F
          ("contention_small", 2_000, 320, 200, True, 5)]
 
 
-@pytest.mark.parametrize("binning", ["auto", "depth-first", "tile-first", "dense"])
+@pytest.mark.parametrize("binning", ["auto", "scatter", "depth-first", "tile-first", "dense"])
 @pytest.mark.parametrize("case", SMALL, ids=[c[0] for c in SMALL])
 def test_small_cases_every_binning(cuda, orc, case, binning, monkeypatch):
-    """Every list construction (depth-first, tile-first, dense tile-major)
-    gives the oracle's lists bit for bit and the same decisions."""
+    """Every list construction (scatter, depth-first, tile-first, dense
+    tile-major) gives the oracle's lists bit for bit and the same decisions."""
     from paper_2401_05345_b200.scene import make_camera, make_dL_dpixels, make_scene
 
-    if binning in ("depth-first", "tile-first"):
-        monkeypatch.setenv("DW_DENSE_BINNING", "0")
-        monkeypatch.setenv("DW_TILE_FIRST", "1" if binning == "tile-first" else "0")
-    elif binning == "dense":
-        monkeypatch.setenv("DW_DENSE_BINNING", "1")
+    set_binning(monkeypatch, binning)
     name, P, W, H, hc, seed = case
     sc = make_scene(P, W, H, seed=seed, high_contention=hc)
     verify_case(cuda, orc, f"{name}_{binning}", sc, make_camera(W, H),

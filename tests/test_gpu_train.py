@@ -198,7 +198,7 @@ def _scene_t(cuda, sc):
 _KEYS = ("means3D", "scales", "rotations", "opacities", "colors")
 
 
-@pytest.mark.parametrize("binning", ["sort", "dense"])
+@pytest.mark.parametrize("binning", ["scatter", "depth-first", "dense"])
 @pytest.mark.parametrize("yaw", [0.0, 23.0])
 def test_forward_async_matches_sync(cuda, yaw, binning, monkeypatch):
     """The no-host-sync forward (device-side instance count over a reserved
@@ -206,7 +206,9 @@ def test_forward_async_matches_sync(cuda, yaw, binning, monkeypatch):
     either list construction, including the over-capacity frame."""
     import torch
 
-    monkeypatch.setenv("DW_DENSE_BINNING", "1" if binning == "dense" else "0")
+    from parity import set_binning
+
+    set_binning(monkeypatch, binning)
 
     from paper_2401_05345_b200.rasterizer import GaussianRasterizer
     from paper_2401_05345_b200.scene import make_camera, make_scene
