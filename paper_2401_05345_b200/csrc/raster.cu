@@ -95,6 +95,9 @@ struct dw_rasterizer {
   bool scatter = false;            // last forward used scatter binning (raster_scatter.cu)
   uint32_t* sc_scratch = nullptr;  // scatter binning: per-(segment, tile) counts + totals
   size_t cap_sc = 0;
+  float4* packed = nullptr;        // bulk-copy staging: 48-byte staged record per Gaussian
+  size_t cap_pk = 0;
+  bool bulk = false;               // DW_BULK_STAGING=1: the backward stages by cp.async.bulk
   bool tile_first = false;         // last forward binned tile-first (per-tile depth sort)
   double last_list_mean = -1.0;    // instances per tile of the last counted forward
   static constexpr double kTileFirstMaxMean = 384.0;
@@ -146,7 +149,7 @@ struct dw_rasterizer {
     void* ps[] = {means2D, depths, radii, conic_opacity, rgb, tiles_touched, offsets, dkey[0],
                   dkey[1], dids[0], dids[1], itile[0], itile[1], ivals[0], ivals[1], ranges,
                   final_T, n_contrib, tmp, scan_tmp, keys_dbg, counters, live_dev, overflow_dev,
-                  tile_order, rects, diff, area_sorted, seg_scratch, sc_scratch};
+                  tile_order, rects, diff, area_sorted, seg_scratch, sc_scratch, packed};
     for (void* p : ps)
       if (p) cudaFree(p);
     for (float* p : h_bufs)
@@ -309,9 +312,12 @@ struct dw_rasterizer {
     const bool keys_ready = !tile_first && !scatter;
     stage_valid = stage_timing;
     stage_mark(0, s);
+    const char* bulk_env = std::getenv("DW_BULK_STAGING");
+    bulk = bulk_env && *bulk_env == '1';
+    if (bulk) grow(packed, cap_pk, 3 * np);
     dw::launch_preprocess(P, means3D, scales, rotations, opacities, colors, cam, means2D, depths,
                           radii, conic_opacity, rgb, tiles_touched, keys_ready ? dkey[0] : nullptr,
-                          keys_ready ? dids[0] : nullptr, s);
+                          keys_ready ? dids[0] : nullptr, s, bulk ? packed : nullptr);
     stage_mark(1, s);
     // Instance count: read back (one host sync) to size the buffers, or --
     // nosync -- kept on the device against the reserved capacity
@@ -432,7 +438,8 @@ struct dw_rasterizer {
     }
     ensure_order(s);
     dw::launch_backward_impl(cam, ranges, vals, means2D, conic_opacity, rgb, order_or_null(),
-                             final_T, n_contrib, dL_dpixels, policy, thr, grad, ctr, s);
+                             final_T, n_contrib, dL_dpixels, policy, thr, grad, ctr, s,
+                             bulk ? packed : nullptr);
     if (pairs_out) {
       unsigned long long h[2];
       DW_CUDA(cudaMemcpyAsync(h, counters, sizeof(h), cudaMemcpyDeviceToHost, s));

@@ -74,7 +74,7 @@ void launch_preprocess(int P, const float* means3D, const float* scales, const f
                        const float* opacities, const float* colors, const CamParams& cam,
                        float2* means2D, float* depths, int* radii, float4* conic_opacity,
                        float4* rgb, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* dids,
-                       cudaStream_t s);  // dkey/dids (nullable): depth-sort keys and ids
+                       cudaStream_t s, float4* packed = nullptr);  // dkey/dids (nullable): depth-sort keys and ids
 
 // Device buffers of the backward's WarpRecord tap (SoA like dw_device_trace).
 struct TapBuf {
@@ -169,6 +169,7 @@ void launch_backward_impl(const CamParams& cam, const uint2* ranges, const uint3
                           const uint32_t* tile_order, const float* final_T,
                           const uint32_t* n_contrib,
                           const float* dL, int policy, int thr, float* grad,
-                          unsigned long long* counters, cudaStream_t s);
+                          unsigned long long* counters, cudaStream_t s,
+                          const float4* packed = nullptr);
 
 }  // namespace dw

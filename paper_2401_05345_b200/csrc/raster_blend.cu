@@ -133,6 +133,42 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
+// Bulk-copy staging (the TMA engine's non-tensor cp.async.bulk, completion
+// counted in bytes on an mbarrier): one 48-byte copy of a Gaussian's packed
+// record (preprocess `packed`: xy, conic + opacity, rgb + extents -- the
+// Staged layout) instead of three cp.async. A/B'd against cp.async staging in
+// k_backward_x2 (DW_BULK_STAGING=1 selects it at run time).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_stage(Staged* dst, const float4* src, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 48, [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(smem_u32(bar))
+      : "memory");
+}
+
 #ifndef DW_BWD_MIN_BLOCKS
 #define DW_BWD_MIN_BLOCKS 5  // 5 x 256 threads/SM: <= 51 registers, no spills (ptxas -v)
 #endif
@@ -447,7 +483,7 @@ __global__ void DW_FWD_BOUNDS
 // gradients before the warp runs the DISTWAR policy on the lane sums, so the
 // mask / ballot / staging overhead and the warp reduction are paid once per
 // 64 pixels.
-template <int POL, bool COUNT, bool TAP = false>
+template <int POL, bool COUNT, bool TAP = false, bool BULK = false>
 __global__ void __launch_bounds__(128, (POL == kSwB && !COUNT && !TAP) ? DW_SWB_MIN_BLOCKS
                                                                       : DW_MULTI_MIN_BLOCKS)
     k_backward_x2(const CamParams cam, const uint2* __restrict__ ranges,
@@ -456,7 +492,7 @@ __global__ void __launch_bounds__(128, (POL == kSwB && !COUNT && !TAP) ? DW_SWB_
                   const float* __restrict__ final_Ts, const uint32_t* __restrict__ n_contrib,
                   const float* __restrict__ dL_dpixels, int thr, float* __restrict__ grad,
                   unsigned long long* __restrict__ counters, const TapBuf tap,
-                  const uint32_t* __restrict__ tile_order) {
+                  const uint32_t* __restrict__ tile_order, const float4* __restrict__ packed) {
   pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
   static_assert(POL != kNative, "native runs the thread-per-pixel kernel");
@@ -531,26 +567,53 @@ __global__ void __launch_bounds__(128, (POL == kSwB && !COUNT && !TAP) ? DW_SWB_
   // position top - 1 - (r * 256 + st) (back to front).
   uint32_t cur_id[2], nxt_id[2];
   bool cur_v[2], nxt_v[2];
+  __shared__ uint64_t s_bar[BULK ? 2 : 1];  // bulk staging: one mbarrier per buffer
+  if (BULK) {
+    if (t == 0) {
+      mbar_init(&s_bar[0], 1);
+      mbar_init(&s_bar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (t == 0 && rounds > 0) mbar_expect_tx(&s_bar[0], 48u * min(kBlock, (int)bmax));
+  }
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int st = t + h * 128;
     cur_v[h] = st < (int)bmax;
     cur_id[h] = cur_v[h] ? values[top - 1 - st] : 0u;
-    if (cur_v[h]) stage_async(&sm[0][st], cur_id[h], means2D, conic_opacity, rgb);
+    if (cur_v[h]) {
+      if (BULK) bulk_stage(&sm[0][st], packed + 3 * static_cast<size_t>(cur_id[h]), &s_bar[0]);
+      else stage_async(&sm[0][st], cur_id[h], means2D, conic_opacity, rgb);
+    }
     nxt_v[h] = kBlock + st < (int)bmax;
     nxt_id[h] = nxt_v[h] ? values[top - 1 - (kBlock + st)] : 0u;
   }
-  cp_async_commit();
+  if (!BULK) cp_async_commit();
   for (int i = 0; i < rounds; ++i, todo -= kBlock) {
-    cp_async_wait_all();
+    if (BULK) mbar_wait(&s_bar[i & 1], (i >> 1) & 1);
+    else cp_async_wait_all();
     __syncthreads();  // batch i landed; every warp is done with batch i-1's buffer
     Staged* cur = sm[i & 1];
+    if (BULK) {
+      // the async proxy is about to overwrite a buffer the walk wrote through
+      // the generic proxy (the mask phase's slot rewrites)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const int nn = min(kBlock, (int)bmax - (i + 1) * kBlock);
+      if (t == 0 && nn > 0) mbar_expect_tx(&s_bar[(i + 1) & 1], 48u * nn);
+    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int st = t + h * 128;
-      if (nxt_v[h]) stage_async(&sm[(i + 1) & 1][st], nxt_id[h], means2D, conic_opacity, rgb);
+      if (nxt_v[h]) {
+        if (BULK)
+          bulk_stage(&sm[(i + 1) & 1][st], packed + 3 * static_cast<size_t>(nxt_id[h]),
+                     &s_bar[(i + 1) & 1]);
+        else
+          stage_async(&sm[(i + 1) & 1][st], nxt_id[h], means2D, conic_opacity, rgb);
+      }
     }
-    cp_async_commit();
+    if (!BULK) cp_async_commit();
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int st = t + h * 128;
@@ -679,17 +742,20 @@ void launch_bwd(bool count, const CamParams& cam, const uint2* ranges, const uin
                 const float2* means2D, const float4* co, const float4* rgb,
                 const uint32_t* tile_order, const float* fT,
                 const uint32_t* nc, const float* dL, int thr, float* grad,
-                unsigned long long* ctr, cudaStream_t s) {
+                unsigned long long* ctr, cudaStream_t s, const float4* packed) {
   const int grid = cam.tiles_x * cam.tiles_y;
   // The reduction policies run two pixels per lane; native keeps the paper's
   // thread-per-pixel kernel (profiles/r01/ab_ppt.jsonl).
   if constexpr (POL != kNative) {
     if (count)
       launch_pdl(k_backward_x2<POL, true>, grid, 128, 0, s, cam, ranges, values, means2D, co, rgb,
-                 fT, nc, dL, thr, grad, ctr, TapBuf{}, tile_order);
+                 fT, nc, dL, thr, grad, ctr, TapBuf{}, tile_order, nullptr);
+    else if (packed)
+      launch_pdl(k_backward_x2<POL, false, false, true>, grid, 128, 0, s, cam, ranges, values,
+                 means2D, co, rgb, fT, nc, dL, thr, grad, nullptr, TapBuf{}, tile_order, packed);
     else
       launch_pdl(k_backward_x2<POL, false>, grid, 128, 0, s, cam, ranges, values, means2D, co,
-                 rgb, fT, nc, dL, thr, grad, nullptr, TapBuf{}, tile_order);
+                 rgb, fT, nc, dL, thr, grad, nullptr, TapBuf{}, tile_order, nullptr);
     return;
   }
   if (count)
@@ -709,7 +775,7 @@ void launch_backward_tap(const CamParams& cam, const uint2* ranges, const uint32
                          const TapBuf& tap, cudaStream_t s) {
   const int grid = cam.tiles_x * cam.tiles_y;
   launch_pdl(k_backward_x2<kSwB, false, true>, grid, 128, 0, s, cam, ranges, values, means2D, co,
-             rgb, final_T, n_contrib, dL, thr, grad, nullptr, tap, tile_order);
+             rgb, final_T, n_contrib, dL, thr, grad, nullptr, tap, tile_order, nullptr);
   DW_CUDA(cudaGetLastError());
 }
 
@@ -727,24 +793,25 @@ void launch_backward_impl(const CamParams& cam, const uint2* ranges, const uint3
                           const float2* means2D, const float4* co, const float4* rgb,
                           const uint32_t* tile_order, const float* final_T,
                           const uint32_t* n_contrib, const float* dL, int policy, int thr,
-                          float* grad, unsigned long long* counters, cudaStream_t s) {
+                          float* grad, unsigned long long* counters, cudaStream_t s,
+                          const float4* packed) {
   const bool count = counters != nullptr;
   switch (policy) {
     case kNative:
       launch_bwd<kNative>(count, cam, ranges, values, means2D, co, rgb, tile_order, final_T,
-                          n_contrib, dL, thr, grad, counters, s);
+                          n_contrib, dL, thr, grad, counters, s, packed);
       break;
     case kSwS:
       launch_bwd<kSwS>(count, cam, ranges, values, means2D, co, rgb, tile_order, final_T, n_contrib,
-                       dL, thr, grad, counters, s);
+                       dL, thr, grad, counters, s, packed);
       break;
     case kSwB:
       launch_bwd<kSwB>(count, cam, ranges, values, means2D, co, rgb, tile_order, final_T, n_contrib,
-                       dL, thr, grad, counters, s);
+                       dL, thr, grad, counters, s, packed);
       break;
     default:
       launch_bwd<kCccl>(count, cam, ranges, values, means2D, co, rgb, tile_order, final_T,
-                        n_contrib, dL, thr, grad, counters, s);
+                        n_contrib, dL, thr, grad, counters, s, packed);
   }
   DW_CUDA(cudaGetLastError());
 }

@@ -79,7 +79,8 @@ __global__ void __launch_bounds__(kBlock)
                  float2* __restrict__ means2D, float* __restrict__ depths,
                  int* __restrict__ radii, float4* __restrict__ conic_opacity,
                  float4* __restrict__ rgb, uint32_t* __restrict__ tiles_touched,
-                 uint32_t* __restrict__ dkey, uint32_t* __restrict__ dids) {
+                 uint32_t* __restrict__ dkey, uint32_t* __restrict__ dids,
+                 float4* __restrict__ packed) {
   pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
   __shared__ __align__(16) float s_mean[3 * kBlock];
@@ -195,8 +196,14 @@ __global__ void __launch_bounds__(kBlock)
   // w: the blend kernels' footprint half-extents (raster_blend.cu
   // footprint_mask) as a half2, rounded up with a margin so the mask stays a
   // superset of the alpha >= 1/255 ellipse's pixel bands
-  rgb[i] = make_float4(s_col[3 * t], s_col[3 * t + 1], s_col[3 * t + 2],
-                       __uint_as_float(footprint_extents(co)));
+  const float4 c4 = make_float4(s_col[3 * t], s_col[3 * t + 1], s_col[3 * t + 2],
+                                __uint_as_float(footprint_extents(co)));
+  rgb[i] = c4;
+  if (packed) {  // the blend kernels' 48-byte staged record (bulk-copy staging)
+    packed[3 * i] = make_float4(ix, iy, 0.0f, 0.0f);
+    packed[3 * i + 1] = co;
+    packed[3 * i + 2] = c4;
+  }
   tiles_touched[i] = static_cast<uint32_t>(area);
 }
 
@@ -206,17 +213,19 @@ void launch_preprocess(int P, const float* means3D, const float* scales, const f
                        const float* opacities, const float* colors, const CamParams& cam,
                        float2* means2D, float* depths, int* radii, float4* conic_opacity,
                        float4* rgb, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* dids,
-                       cudaStream_t s) {
+                       cudaStream_t s, float4* packed) {
   if (P <= 0) return;
   auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   const bool vec = aligned(means3D) && aligned(scales) && aligned(colors) && aligned(rotations);
   const int grid = (P + kBlock - 1) / kBlock;
   if (vec)
     launch_pdl(k_preprocess<true>, grid, kBlock, 0, s, P, means3D, scales, rotations, opacities,
-               colors, cam, means2D, depths, radii, conic_opacity, rgb, tiles_touched, dkey, dids);
+               colors, cam, means2D, depths, radii, conic_opacity, rgb, tiles_touched, dkey, dids,
+               packed);
   else
     launch_pdl(k_preprocess<false>, grid, kBlock, 0, s, P, means3D, scales, rotations, opacities,
-               colors, cam, means2D, depths, radii, conic_opacity, rgb, tiles_touched, dkey, dids);
+               colors, cam, means2D, depths, radii, conic_opacity, rgb, tiles_touched, dkey, dids,
+               packed);
   DW_CUDA(cudaGetLastError());
 }
 
