@@ -382,7 +382,9 @@ def main() -> None:
 
     # ---- roofline microbenchmarks: measured L2 RED throughput ------------
     red_peaks = {name: microbench_red(p, 1 << 28) for p, name in
-                 ((0, "distinct"), (1, "same_address_warp"), (2, "v4"), (3, "distwar_9lane"))}
+                 ((0, "distinct"), (1, "same_address_warp"), (2, "v4"), (3, "distwar_9lane"),
+                  (4, "same_address_warp_v4"), (5, "fallback_row_scalar"),
+                  (6, "fallback_row_vector"))}
 
     def time_view(i, policy, reps=3):
         ms = []

@@ -306,7 +306,11 @@ dw_status dw_render_views(dw_rasterizer* r, int32_t P, const float* means3D, con
 /* --------------------------------------------------- roofline microbenchmarks */
 /* Measured f32 RED throughput (REDs/s) for `pattern`: 0 distinct addresses,
  * 1 all 32 lanes of a warp on one address (the naive pattern), 2 distinct
- * addresses with red.global.add.v4.f32 (counted as 4 REDs). */
+ * addresses with red.global.add.v4.f32 (counted as 4 REDs), 3 nine lanes on
+ * one pseudo-random primitive row (SW-B's issue pattern), 4 all lanes on one
+ * 16-byte address with v4, 5 / 6 four lanes on one primitive row with 9
+ * scalar REDs each / the same floats as 3-4 vector REDs (SW-B's per-lane
+ * path without / with DW_VEC_RED). Every float added counts as one RED. */
 dw_status dw_microbench_red(int32_t pattern, int64_t ops, double* reds_per_s, void* stream);
 
 #ifdef __cplusplus

@@ -32,6 +32,12 @@
 #include <cub/warp/warp_reduce.cuh>
 #include <cstdint>
 
+// Per-lane fallback of the rasterizer's SW-B as vector REDs (red_row9); 0 = one
+// scalar RED per param (the A/B baseline).
+#ifndef DW_VEC_RED
+#define DW_VEC_RED 1
+#endif
+
 namespace dw {
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -41,6 +47,50 @@ enum PolicyKind : int { kNative = 0, kSwS = 1, kSwB = 2, kCccl = 3 };
 // One fire-and-forget fp32 reduction at L2 (SASS RED.E.ADD.F32.FTZ.RN).
 __device__ __forceinline__ void red_add(float* addr, float v) {
   asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(addr), "f"(v) : "memory");
+}
+
+// Vector fp32 reductions (sm_90+: RED.E.ADD.F32x2 / x4): one L2 atomic request
+// carries 2 or 4 consecutive floats. `addr` must be 8- / 16-byte aligned.
+__device__ __forceinline__ void red_add_v2(float* addr, float a, float b) {
+  asm volatile("red.relaxed.gpu.global.add.v2.f32 [%0], {%1, %2};" ::"l"(addr), "f"(a), "f"(b)
+               : "memory");
+}
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a),
+               "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+// One primitive's nine consecutive gradient floats (Address order,
+// reducers.hpp:19-23) added with the fewest aligned vector REDs the row's
+// 16-byte phase allows: 3 requests (phase 0 or 3) or 4 (phase 1 or 2) instead
+// of 9. Each float is still one fp32 add at L2, so the per-param semantics
+// (and the reference's request count, which counts params) are unchanged.
+// The phase is warp-uniform where the caller's lanes share a primitive.
+__device__ __forceinline__ void red_row9(float* b, const float (&s)[9]) {
+  switch ((reinterpret_cast<uintptr_t>(b) >> 2) & 3u) {
+    case 0:
+      red_add_v4(b, s[0], s[1], s[2], s[3]);
+      red_add_v4(b + 4, s[4], s[5], s[6], s[7]);
+      red_add(b + 8, s[8]);
+      break;
+    case 1:
+      red_add(b, s[0]);
+      red_add_v2(b + 1, s[1], s[2]);
+      red_add_v4(b + 3, s[3], s[4], s[5], s[6]);
+      red_add_v2(b + 7, s[7], s[8]);
+      break;
+    case 2:
+      red_add_v2(b, s[0], s[1]);
+      red_add_v4(b + 2, s[2], s[3], s[4], s[5]);
+      red_add_v2(b + 6, s[6], s[7]);
+      red_add(b + 8, s[8]);
+      break;
+    default:
+      red_add(b, s[0]);
+      red_add_v4(b + 1, s[1], s[2], s[3], s[4]);
+      red_add_v4(b + 5, s[5], s[6], s[7], s[8]);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -214,8 +264,18 @@ __device__ __forceinline__ void reduce_bfly_scaled(int idx, float* grad, float (
     }
   } else if (active) {
     float* base = grad + static_cast<int64_t>(idx) * N;
+#if DW_VEC_RED
+    if constexpr (N == 9) {
+      float sv[9];
 #pragma unroll
-    for (int p = 0; p < N; ++p) red_add(base + p, v[p] * scale[p]);
+      for (int p = 0; p < 9; ++p) sv[p] = v[p] * scale[p];
+      red_row9(base, sv);
+    } else
+#endif
+    {
+#pragma unroll
+      for (int p = 0; p < N; ++p) red_add(base + p, v[p] * scale[p]);
+    }
     if (COUNT) nred += N;
   }
 }

@@ -7,6 +7,11 @@
 //   2 v4:       red.global.add.v4.f32, 32 lanes -> 128 consecutive floats
 //   3 distwar:  9 lanes -> 9 consecutive floats of a pseudo-random primitive
 //               (the SW-B issue pattern of the rasterizer backward)
+//   4 same v4:  red.global.add.v4.f32, 32 lanes -> ONE 16-byte address
+//   5 fallback, scalar: 4 lanes -> the same pseudo-random primitive row,
+//               9 scalar REDs each (SW-B's per-lane path, DW_VEC_RED=0)
+//   6 fallback, vector: the same traffic as 5 through red_row9 (3-4 vector
+//               REDs per lane, the default per-lane path)
 #include <cuda_runtime.h>
 
 #include "distwar.cuh"
@@ -35,6 +40,23 @@ __global__ void __launch_bounds__(256) k_red(float* __restrict__ buf, int iters)
       asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v),
                    "f"(v), "f"(v), "f"(v)
                    : "memory");
+    } else if (PATTERN == 4) {
+      float* p = buf + ((w * 128) & (kRegionFloats - 1));
+      asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v),
+                   "f"(v), "f"(v), "f"(v)
+                   : "memory");
+    } else if (PATTERN == 5 || PATTERN == 6) {
+      const uint64_t prim = (static_cast<uint64_t>(w) * 2654435761ull) % 1000000ull;
+      float* row = buf + ((prim * 9) & (kRegionFloats - 1));
+      if (lane < 4) {
+        if (PATTERN == 5) {
+#pragma unroll
+          for (int p = 0; p < 9; ++p) red_add(row + p, v);
+        } else {
+          const float s[9] = {v, v, v, v, v, v, v, v, v};
+          red_row9(row, s);
+        }
+      }
     } else {
       // multiplicative hash of the warp-iteration -> primitive id
       const uint64_t prim = (static_cast<uint64_t>(w) * 2654435761ull) % 1000000ull;
@@ -68,7 +90,12 @@ double microbench_red(int pattern, int64_t ops, cudaStream_t s) {
   DW_CUDA(cudaMemsetAsync(buf, 0, (kRegionFloats + 1024) * sizeof(float), s));
   const int grid = sm_count() * 8;
   const int64_t warps = static_cast<int64_t>(grid) * 8;
-  const int reds_per_warp_inst = pattern == 2 ? 128 : (pattern == 3 ? 9 : 32);
+  // floats added per warp-iteration
+  const int reds_per_warp_inst = pattern == 2   ? 128
+                                 : pattern == 3 ? 9
+                                 : pattern == 4 ? 128
+                                 : pattern >= 5 ? 36
+                                                : 32;
   int64_t iters64 = ops / (warps * reds_per_warp_inst);
   if (iters64 < 1) iters64 = 1;
   const int iters = static_cast<int>(iters64 > (1 << 30) ? (1 << 30) : iters64);
@@ -77,6 +104,9 @@ double microbench_red(int pattern, int64_t ops, cudaStream_t s) {
     case 0: ms = run<0>(buf, grid, iters, s); break;
     case 1: ms = run<1>(buf, grid, iters, s); break;
     case 2: ms = run<2>(buf, grid, iters, s); break;
+    case 4: ms = run<4>(buf, grid, iters, s); break;
+    case 5: ms = run<5>(buf, grid, iters, s); break;
+    case 6: ms = run<6>(buf, grid, iters, s); break;
     default: ms = run<3>(buf, grid, iters, s); break;
   }
   DW_CUDA(cudaFree(buf));
