@@ -57,6 +57,10 @@ void grow_zeroed(T*& p, size_t& cap, size_t want, cudaStream_t s) {
 
 }  // namespace
 
+#ifndef DW_BLOCK_BINNING
+#define DW_BLOCK_BINNING 1
+#endif
+
 struct dw_rasterizer {
   int P = 0, W = 0, H = 0;
   int64_t num_rendered = 0;
@@ -101,7 +105,12 @@ struct dw_rasterizer {
   bool tile_first = false;         // last forward binned tile-first (per-tile depth sort)
   double last_list_mean = -1.0;    // instances per tile of the last counted forward
   static constexpr double kTileFirstMaxMean = 384.0;
-  uint2* rects = nullptr;          // dense binning: packed tile rectangle + id, depth order
+  uint2* rects = nullptr;          // dense / block binning: packed tile rectangle + id, depth order
+  bool blocked = false;            // last forward built its lists by block binning
+  uint2* branges = nullptr;        // block binning: coarse block ranges
+  uint32_t* bb_cnt = nullptr;      // block binning: per-(warp, tile) counts + tile totals
+  uint32_t* bb_rect_id = nullptr;  // block binning: packed rectangle by Gaussian id
+  size_t cap_br = 0, cap_bbc = 0, cap_bri = 0;
   int* diff = nullptr;             // dense binning: per-segment difference grids + offsets
   size_t cap_r = 0, cap_diff = 0;
   float* final_T = nullptr;
@@ -149,7 +158,8 @@ struct dw_rasterizer {
     void* ps[] = {means2D, depths, radii, conic_opacity, rgb, tiles_touched, offsets, dkey[0],
                   dkey[1], dids[0], dids[1], itile[0], itile[1], ivals[0], ivals[1], ranges,
                   final_T, n_contrib, tmp, scan_tmp, keys_dbg, counters, live_dev, overflow_dev,
-                  tile_order, rects, diff, area_sorted, seg_scratch, sc_scratch, packed};
+                  tile_order, rects, diff, area_sorted, seg_scratch, sc_scratch, packed,
+                  branges, bb_cnt, live_c_dev, bb_rect_id};
     for (void* p : ps)
       if (p) cudaFree(p);
     for (float* p : h_bufs)
@@ -168,6 +178,7 @@ struct dw_rasterizer {
 
   // no-sync forward state: live instance count + overflow flag on the device
   unsigned long long* live_dev = nullptr;
+  unsigned long long* live_c_dev = nullptr;  // block binning: live level-1 entry count
   unsigned int* overflow_dev = nullptr;
   bool count_pending = false;  // num_rendered not read back yet (no-sync forward)
 
@@ -175,6 +186,7 @@ struct dw_rasterizer {
     if (!counters) DW_CUDA(cudaMalloc(&counters, 2 * sizeof(unsigned long long)));
     if (!h_total) DW_CUDA(cudaMallocHost(&h_total, sizeof(uint64_t)));
     if (!live_dev) DW_CUDA(cudaMalloc(&live_dev, sizeof(unsigned long long)));
+    if (!live_c_dev) DW_CUDA(cudaMalloc(&live_c_dev, sizeof(unsigned long long)));
     if (!overflow_dev) {
       DW_CUDA(cudaMalloc(&overflow_dev, sizeof(unsigned int)));
       DW_CUDA(cudaMemsetAsync(overflow_dev, 0, sizeof(unsigned int), s));
@@ -219,6 +231,12 @@ struct dw_rasterizer {
     if (dw::dense_binning_fits(tx, ty)) {  // dense binning allocates nothing in the forward
       grow(rects, cap_r, np);
       grow(diff, cap_diff, dw::dense_scratch_words(tx, ty));
+    }
+    if (dw::block_binning_fits(tx, ty)) {  // nor does block binning
+      grow(rects, cap_r, np);
+      grow(branges, cap_br, static_cast<size_t>(dw::block_binning_blocks(tx, ty)));
+      grow(bb_cnt, cap_bbc, dw::block_binning_count_words(tx, ty));
+      grow(bb_rect_id, cap_bri, np);
     }
     ensure_tmp(std::max(dw::radix_sort_temp_bytes(P_),
                         dw::radix_sort_temp_bytes(static_cast<int64_t>(std::min(cap_i[0], cap_i[2])))));
@@ -308,6 +326,16 @@ struct dw_rasterizer {
     tile_first = !scatter && (tf_env && *tf_env ? *tf_env == '1'
                                                 : DW_TILE_FIRST != 0 && last_list_mean >= 0.0 &&
                                                       last_list_mean < kTileFirstMaxMean);
+    // Block binning (default on the depth-first path): the lists through
+    // coarse 8x4-tile blocks (raster_blockbin.cu); DW_BLOCK_BINNING=0 selects
+    // the duplicate + tile-sort construction (same output). Block totals must
+    // stay < 2^30 for its packed scan: not used once a frame came near that.
+    const char* bb_env = std::getenv("DW_BLOCK_BINNING");
+    const bool block_mode = !tile_first && !scatter &&
+                            (bb_env && *bb_env ? *bb_env == '1' : DW_BLOCK_BINNING != 0) &&
+                            dw::block_binning_fits(cam.tiles_x, cam.tiles_y) &&
+                            last_list_mean * ntiles < static_cast<double>(1 << 29) &&
+                            static_cast<int64_t>(P) < (int64_t(1) << 29);
     // the depth-first paths' sort keys come straight out of the preprocess
     const bool keys_ready = !tile_first && !scatter;
     stage_valid = stage_timing;
@@ -315,24 +343,30 @@ struct dw_rasterizer {
     const char* bulk_env = std::getenv("DW_BULK_STAGING");
     bulk = bulk_env && *bulk_env == '1';
     if (bulk) grow(packed, cap_pk, 3 * np);
+    if (block_mode) grow(bb_rect_id, cap_bri, np);
     dw::launch_preprocess(P, means3D, scales, rotations, opacities, colors, cam, means2D, depths,
                           radii, conic_opacity, rgb, tiles_touched, keys_ready ? dkey[0] : nullptr,
-                          keys_ready ? dids[0] : nullptr, s, bulk ? packed : nullptr);
+                          keys_ready ? dids[0] : nullptr, s, bulk ? packed : nullptr,
+                          block_mode ? bb_rect_id : nullptr);
     stage_mark(1, s);
     // Instance count: read back (one host sync) to size the buffers, or --
     // nosync -- kept on the device against the reserved capacity
     // (dw_rasterizer_reserve), so the whole forward is graph-capturable.
     int64_t n_grid = 0;                        // element count the grids are sized for
     const unsigned long long* n_dev = nullptr;  // live count on the device (nosync)
+    int64_t n_entries = 0;                      // block binning: level-1 entries (or capacity)
+    const unsigned long long* nc_dev = nullptr;  // block binning: live entries (nosync)
     num_rendered = 0;
     count_pending = false;
     bool depth_sorted = false;
     auto depth_sort = [&](bool with_area) {
       if (!keys_ready) dw::launch_depth_keys(P, depths, radii, dkey[0], dids[0], s);
       ensure_tmp(dw::radix_sort_temp_bytes(P));
-      // (its last pass can also lay tiles_touched out in that order: area_sorted)
+      // (its last pass can also lay tiles_touched -- block binning: the packed
+      // rectangles -- out in that order: area_sorted)
+      const uint32_t* payload = block_mode ? bb_rect_id : tiles_touched;
       order = dids[dw::radix_sort_pairs(dkey, dids, P, 32, tmp, s, nullptr,
-                                        with_area ? tiles_touched : nullptr, area_sorted)];
+                                        with_area ? payload : nullptr, area_sorted)];
       depth_sorted = true;
     };
     if (P > 0) {
@@ -340,6 +374,12 @@ struct dw_rasterizer {
         stage_mark(2, s);  // no depth sort on these paths
         // instance offsets in index order
         dw::inclusive_scan_gather(tiles_touched, nullptr, P, offsets, scan_tmp, s);
+      } else if (block_mode) {
+        // 1. Gaussians in (depth, id) order; one scan over their packed
+        // rectangles in that order gives both the tile and the block offsets
+        depth_sort(true);
+        stage_mark(2, s);
+        dw::inclusive_scan_gather(area_sorted, nullptr, P, offsets, scan_tmp, s, 1);
       } else {
         // 1. Gaussians in (depth, id) order: stable 32-bit LSD sort
         depth_sort(true);
@@ -351,8 +391,15 @@ struct dw_rasterizer {
         if (cap_i[0] == 0 || cap_i[2] == 0)
           throw std::invalid_argument("no-sync forward needs dw_rasterizer_reserve first");
         n_grid = static_cast<int64_t>(std::min(cap_i[0], cap_i[2]));
-        dw::launch_clamp_total(offsets, P, static_cast<uint64_t>(n_grid), live_dev, overflow_dev,
-                               sticky_overflow, s);
+        if (block_mode) {
+          dw::launch_bb_clamp(offsets, P, static_cast<uint64_t>(n_grid), live_dev, live_c_dev,
+                              overflow_dev, sticky_overflow, s);
+          n_entries = n_grid;  // entries <= instances: the same capacity
+          nc_dev = live_c_dev;
+        } else {
+          dw::launch_clamp_total(offsets, P, static_cast<uint64_t>(n_grid), live_dev,
+                                 overflow_dev, sticky_overflow, s);
+        }
         n_dev = live_dev;
         count_pending = true;
       } else {
@@ -360,6 +407,10 @@ struct dw_rasterizer {
                                 cudaMemcpyDeviceToHost, s));
         DW_CUDA(cudaStreamSynchronize(s));
         num_rendered = static_cast<int64_t>(*h_total);
+        if (block_mode) {  // (blocks << 32 | tiles)
+          n_entries = static_cast<int64_t>(*h_total >> 32);
+          num_rendered = static_cast<int64_t>(*h_total & 0xffffffffull);
+        }
         n_grid = num_rendered;
         last_list_mean = static_cast<double>(num_rendered) / ntiles;
       }
@@ -376,6 +427,7 @@ struct dw_rasterizer {
     }
     tiles_sorted = itile[0];
     vals = ivals[0];
+    blocked = false;
     // Dense scenes (large tile rectangles: P x tiles <= 4 x instances) build the
     // per-tile lists directly; the rest duplicate + radix-sort (same output).
     const char* env = std::getenv("DW_DENSE_BINNING");  // "0" / "1" force a path
@@ -393,6 +445,20 @@ struct dw_rasterizer {
       grow(seg_scratch, cap_seg, 2 * static_cast<size_t>(n_grid));
       dw::launch_scatter_binning(P, means2D, radii, depths, cam, sc_scratch, ranges, ivals[0],
                                  seg_scratch, n_grid, n_dev, s);
+    } else if (block_mode && n_grid > 0) {
+      // 2. entries per coarse block, sorted by block; 3. per-tile lists
+      const int nb = dw::block_binning_blocks(cam.tiles_x, cam.tiles_y);
+      grow(branges, cap_br, static_cast<size_t>(nb));
+      grow(bb_cnt, cap_bbc, dw::block_binning_count_words(cam.tiles_x, cam.tiles_y));
+      grow(seg_scratch, cap_seg, 2 * static_cast<size_t>(std::max<int64_t>(n_grid, 1)));
+      ensure_tmp(dw::radix_sort_temp_bytes(std::max<int64_t>(n_entries, 1)));
+      // the sorted entries' rectangles land in seg_scratch (>= n_grid >= entries words)
+      dw::launch_block_binning(P, order, offsets, area_sorted, bb_rect_id, cam, itile, ivals,
+                               n_entries, tmp,
+                               reinterpret_cast<uint32_t*>(seg_scratch), branges, bb_cnt, ranges,
+                               &vals, n_dev, nc_dev, s);
+      tiles_sorted = nullptr;
+      blocked = true;
     } else if (n_grid > 0) {
       // 2. duplicate (index order, or depth order), 3. stable sort by tile id
       dw::launch_duplicate_sorted(P, tile_first ? nullptr : order, means2D, radii, offsets, cam,
@@ -405,7 +471,8 @@ struct dw_rasterizer {
     stage_mark(4, s);
     const bool scattered = scatter && !dense && n_grid > 0;  // ranges already written
     if (!scattered) scatter = false;
-    if (!dense && !scattered) dw::launch_ranges_u32(n_grid, tiles_sorted, ranges, ntiles, s, n_dev);
+    if (!dense && !scattered && !blocked)
+      dw::launch_ranges_u32(n_grid, tiles_sorted, ranges, ntiles, s, n_dev);
     if (!dense && !scattered && tile_first && n_grid > 0) {
       // 4. every tile's list (index order) -> (depth, index) order
       grow(seg_scratch, cap_seg, 2 * static_cast<size_t>(n_grid));
@@ -620,7 +687,7 @@ void raster_buffer(const dw_rasterizer* r, int which, const void** p, int64_t* c
     case 5: {  // (tile << 32 | depth bits) of the sorted instances, built on request
       auto* m = const_cast<dw_rasterizer*>(r);
       grow(m->keys_dbg, m->cap_keys, static_cast<size_t>(std::max<int64_t>(I, 1)));
-      const bool no_tiles = r->dense || r->scatter;  // no tile-id array: derive it from the ranges
+      const bool no_tiles = r->dense || r->scatter || r->blocked;  // no tile-id array: from the ranges
       if (no_tiles)
         launch_tiles_from_ranges(r->ranges, r->cam.tiles_x * r->cam.tiles_y, r->itile[0],
                                  nullptr);

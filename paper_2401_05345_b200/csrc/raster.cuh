@@ -74,7 +74,9 @@ void launch_preprocess(int P, const float* means3D, const float* scales, const f
                        const float* opacities, const float* colors, const CamParams& cam,
                        float2* means2D, float* depths, int* radii, float4* conic_opacity,
                        float4* rgb, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* dids,
-                       cudaStream_t s, float4* packed = nullptr);  // dkey/dids (nullable): depth-sort keys and ids
+                       cudaStream_t s, float4* packed = nullptr,
+                       uint32_t* rect_out = nullptr);  // dkey/dids (nullable): depth-sort keys and ids;
+                                                       // rect_out (nullable): packed tile rectangles
 
 // Device buffers of the backward's WarpRecord tap (SoA like dw_device_trace).
 struct TapBuf {
@@ -113,8 +115,10 @@ size_t scan_temp_bytes(int64_t n);
 int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* temp,
                      cudaStream_t s, const unsigned long long* n_dev = nullptr,
                      const uint32_t* gather_src = nullptr, uint32_t* gather_out = nullptr);
+// mode 1: in[] = packed tile rectangles (launch_preprocess rect_out), out[] =
+// inclusive (coarse blocks << 32 | tiles) -- block binning's two offsets at once
 void inclusive_scan_gather(const uint32_t* in, const uint32_t* order, int64_t n, uint64_t* out,
-                           void* temp, cudaStream_t s);
+                           void* temp, cudaStream_t s, int mode = 0);
 void launch_depth_keys(int P, const float* depths, const int* radii, uint32_t* dkey, uint32_t* ids,
                        cudaStream_t s);
 void launch_duplicate_sorted(int P, const uint32_t* order, const float2* means2D, const int* radii,
@@ -148,6 +152,26 @@ void launch_scatter_binning(int P, const float2* means2D, const int* radii, cons
                             const CamParams& cam, uint32_t* scratch, uint2* ranges,
                             uint32_t* values, unsigned long long* seg_scratch, int64_t seg_half,
                             const unsigned long long* n_dev, cudaStream_t s);
+// Block binning (raster_blockbin.cu): the depth-first lists through coarse
+// 8x4-tile blocks (one sorted entry per (Gaussian, block) instead of the
+// duplicate + two-pass tile sort of every instance).
+bool block_binning_fits(int tiles_x, int tiles_y);
+int block_binning_blocks(int tiles_x, int tiles_y);
+size_t block_binning_count_words(int tiles_x, int tiles_y);
+void launch_bb_clamp(const uint64_t* offsets, int P, uint64_t cap, unsigned long long* n_live,
+                     unsigned long long* n_entries, unsigned int* overflow, bool sticky,
+                     cudaStream_t s);
+// k/v: sort double buffers of >= n_entries (capacity when n_entries_dev is set);
+// brect: >= n_entries words; cnt: block_binning_count_words; writes ranges and
+// the lists (*values_out: one of v)
+// order / rect_sorted: the Gaussians and their packed rectangles in depth order
+void launch_block_binning(int P, const uint32_t* order, const uint64_t* offsets,
+                          const uint32_t* rect_sorted, const uint32_t* rect_by_id,
+                          const CamParams& cam, uint32_t* k[2],
+                          uint32_t* v[2], int64_t n_entries, void* sort_tmp, uint32_t* brect,
+                          uint2* branges, uint32_t* cnt, uint2* ranges, uint32_t** values_out,
+                          const unsigned long long* n_live,
+                          const unsigned long long* n_entries_dev, cudaStream_t s);
 // order[ntiles]: tiles by descending list length (bucketed), for the blend kernels
 void launch_tile_order(const uint2* ranges, int ntiles, uint32_t* order, cudaStream_t s);
 // ranges[0, ntiles) of the sorted tile ids (every range written)

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kBlock)
                  int* __restrict__ radii, float4* __restrict__ conic_opacity,
                  float4* __restrict__ rgb, uint32_t* __restrict__ tiles_touched,
                  uint32_t* __restrict__ dkey, uint32_t* __restrict__ dids,
-                 float4* __restrict__ packed) {
+                 float4* __restrict__ packed, uint32_t* __restrict__ rect_out) {
   pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
   __shared__ __align__(16) float s_mean[3 * kBlock];
@@ -96,6 +96,9 @@ __global__ void __launch_bounds__(kBlock)
   if (i >= P) return;
   radii[i] = 0;
   tiles_touched[i] = 0;
+  // block binning (nullable): the tile rectangle packed x0 | y0 << 8 |
+  // (x1-1) << 16 | (y1-1) << 24 (tile units < 256), empty = 0x0000ff00
+  if (rect_out) rect_out[i] = 0x0000ff00u;
   // depth-sort input (nullable): (depth bits, id), culled Gaussians last
   if (dkey) {
     dkey[i] = 0xffffffffu;
@@ -205,6 +208,9 @@ __global__ void __launch_bounds__(kBlock)
     packed[3 * i + 2] = c4;
   }
   tiles_touched[i] = static_cast<uint32_t>(area);
+  if (rect_out)
+    rect_out[i] = (uint32_t)rminx | (uint32_t)rminy << 8 | (uint32_t)(rmaxx - 1) << 16 |
+                  (uint32_t)(rmaxy - 1) << 24;
 }
 
 }  // namespace
@@ -213,7 +219,7 @@ void launch_preprocess(int P, const float* means3D, const float* scales, const f
                        const float* opacities, const float* colors, const CamParams& cam,
                        float2* means2D, float* depths, int* radii, float4* conic_opacity,
                        float4* rgb, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* dids,
-                       cudaStream_t s, float4* packed) {
+                       cudaStream_t s, float4* packed, uint32_t* rect_out) {
   if (P <= 0) return;
   auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   const bool vec = aligned(means3D) && aligned(scales) && aligned(colors) && aligned(rotations);
@@ -221,11 +227,11 @@ void launch_preprocess(int P, const float* means3D, const float* scales, const f
   if (vec)
     launch_pdl(k_preprocess<true>, grid, kBlock, 0, s, P, means3D, scales, rotations, opacities,
                colors, cam, means2D, depths, radii, conic_opacity, rgb, tiles_touched, dkey, dids,
-               packed);
+               packed, rect_out);
   else
     launch_pdl(k_preprocess<false>, grid, kBlock, 0, s, P, means3D, scales, rotations, opacities,
                colors, cam, means2D, depths, radii, conic_opacity, rgb, tiles_touched, dkey, dids,
-               packed);
+               packed, rect_out);
   DW_CUDA(cudaGetLastError());
 }
 

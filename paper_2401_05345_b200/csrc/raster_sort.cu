@@ -324,46 +324,108 @@ __global__ void __launch_bounds__(kSortThreads)
   }
 }
 
-// Inclusive scan u32 -> u64 of in[order[i]] (order may be null), one pass
-// with decoupled look-back: each CTA takes the next tile id from a counter
-// (so every predecessor is already running: the spin cannot deadlock),
-// publishes its tile aggregate, walks back over its predecessors' flags 32 at
-// a time until one holds an inclusive prefix, and publishes its own inclusive
-// prefix. Flag word = status (2 bits: 1 aggregate, 2 inclusive) | value (62
-// bits) so one relaxed 64-bit store publishes both. The last CTA to finish
-// zeroes the flags and counters again: the state is clean between calls
-// without a memset (and inside a captured graph).
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kSortThreads * kScanItems;  // 2048 elements
-constexpr unsigned long long kScanAgg = 1ull << 62, kScanInc = 2ull << 62;
-constexpr unsigned long long kScanVal = kScanAgg - 1ull;
 
-__device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed_gpu(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// MODE 0: in[] as is; 1: in[] is a packed tile rectangle (x0 | y0 << 8 |
+// (x1-1) << 16 | (y1-1) << 24, empty: y0 > y1-1) and the scan runs on
+// (coarse 8x4-tile blocks it touches << 32 | tiles it touches) -- both offsets
+// of block binning in one pass (raster_blockbin.cu).
+template <int MODE>
+__device__ __forceinline__ unsigned long long scan_widen(uint32_t x) {
+  if (MODE == 1) {
+    const int x0 = (int)(x & 0xffu), y0 = (int)((x >> 8) & 0xffu);
+    const int x1 = (int)((x >> 16) & 0xffu), y1 = (int)(x >> 24);
+    if (y0 > y1) return 0ull;
+    const unsigned long long tiles = static_cast<unsigned long long>((x1 - x0 + 1) * (y1 - y0 + 1));
+    const unsigned long long blocks =
+        static_cast<unsigned long long>((x1 / 8 - x0 / 8 + 1) * (y1 / 4 - y0 / 4 + 1));
+    return (blocks << 32) | tiles;
+  }
+  return x;
 }
 
+// Inclusive scan u32 -> u64 of widen(in[order[i]]) (order may be null) as
+// reduce -> scan of the tile sums -> rescan: three launches and no
+// inter-CTA waiting (a decoupled look-back chains the CTAs of a wave that
+// start together: 30-40 us for 3M elements against ~10 here).
+template <int MODE>
 __global__ void __launch_bounds__(kSortThreads)
-    k_scan_chained(const uint32_t* __restrict__ in, const uint32_t* __restrict__ order, int64_t n,
-                   unsigned long long* __restrict__ state, uint64_t* __restrict__ out) {
+    k_scan_reduce(const uint32_t* __restrict__ in, const uint32_t* __restrict__ order, int64_t n,
+                  unsigned long long* __restrict__ sums) {
+  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+  pdl_trigger();
+  __shared__ unsigned long long s_w[kSortThreads / 32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int64_t tile0 = static_cast<int64_t>(blockIdx.x) * kScanTile;
+  unsigned long long x = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int64_t e = tile0 + k * kSortThreads + t;
+    if (e < n) x += scan_widen<MODE>(__ldg(in + (order ? __ldg(order + e) : e)));
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+  if (lane == 0) s_w[w] = x;
+  __syncthreads();
+  if (t == 0) {
+    unsigned long long a = 0;
+#pragma unroll
+    for (int k = 0; k < kSortThreads / 32; ++k) a += s_w[k];
+    sums[blockIdx.x] = a;
+  }
+}
+
+// One CTA: exclusive scan of the tile sums, in place.
+__global__ void __launch_bounds__(1024) k_scan_top(unsigned long long* __restrict__ sums, int64_t tiles) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ unsigned long long s_w[32];
+  __shared__ unsigned long long s_carry;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  if (t == 0) s_carry = 0;
+  __syncthreads();
+  for (int64_t b = 0; b < tiles; b += 1024) {
+    const int64_t i = b + t;
+    const unsigned long long v = i < tiles ? sums[i] : 0ull;
+    unsigned long long incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_w[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      const unsigned long long sv = s_w[lane];
+      unsigned long long si = sv;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(kFull, si, o);
+        if (lane >= o) si += y;
+      }
+      s_w[lane] = si - sv;
+    }
+    __syncthreads();
+    const unsigned long long carry = s_carry;
+    if (i < tiles) sums[i] = carry + s_w[w] + incl - v;
+    __syncthreads();
+    if (t == 1023) s_carry = carry + s_w[w] + incl;
+    __syncthreads();
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kSortThreads)
+    k_scan_apply(const uint32_t* __restrict__ in, const uint32_t* __restrict__ order, int64_t n,
+                 const unsigned long long* __restrict__ sums, uint64_t* __restrict__ out) {
   pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
   __shared__ uint32_t s_in[kScanTile + kScanTile / 32];          // padded: conflict-free transpose
   __shared__ unsigned long long s_out[kScanTile + kScanTile / 16];
   __shared__ unsigned long long s_wsum[kSortThreads / 32];
-  __shared__ unsigned long long s_excl;
-  __shared__ uint32_t s_tile;
-  unsigned* ctr = reinterpret_cast<unsigned*>(state);  // [0] next tile id, [1] tiles done
-  unsigned long long* flags = state + 1;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  if (t == 0) s_tile = atomicAdd(ctr, 1u);
-  __syncthreads();
-  const int64_t tile = s_tile;
-  const int64_t tile0 = tile * kScanTile;
+  const int64_t tile0 = static_cast<int64_t>(blockIdx.x) * kScanTile;
   // coalesced load (element k*256 + t), transposed so thread t scans [8t, 8t+8)
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
@@ -378,7 +440,7 @@ __global__ void __launch_bounds__(kSortThreads)
   for (int k = 0; k < kScanItems; ++k) {
     const int i = t * kScanItems + k;
     v[k] = s_in[i + (i >> 5)];
-    tot += v[k];
+    tot += scan_widen<MODE>(v[k]);
   }
   unsigned long long incl = tot;
 #pragma unroll
@@ -388,42 +450,13 @@ __global__ void __launch_bounds__(kSortThreads)
   }
   if (lane == 31) s_wsum[w] = incl;
   __syncthreads();
-  unsigned long long wbase = 0, agg = 0;
+  unsigned long long wbase = 0;
 #pragma unroll
-  for (int k = 0; k < kSortThreads / 32; ++k) {
-    const unsigned long long x = s_wsum[k];
-    wbase += k < w ? x : 0ull;
-    agg += x;
-  }
-  if (w == 0) {
-    unsigned long long excl = 0;
-    if (tile == 0) {
-      if (lane == 0) st_relaxed_gpu(flags, kScanInc | agg);
-    } else {
-      if (lane == 0) st_relaxed_gpu(flags + tile, kScanAgg | agg);
-      int64_t end = tile - 1;  // window [end - 31, end]
-      while (true) {
-        const int64_t j = end - lane;
-        const unsigned long long f = j >= 0 ? ld_relaxed_gpu(flags + j) : kScanInc;
-        if (__any_sync(kFull, (f >> 62) == 0ull)) continue;  // a predecessor not published yet
-        const unsigned inc = __ballot_sync(kFull, (f >> 62) == 2ull);
-        const int stop = inc ? __ffs(inc) - 1 : 31;  // nearest inclusive prefix
-        unsigned long long x = lane <= stop ? (f & kScanVal) : 0ull;
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
-        excl += x;
-        if (inc) break;
-        end -= 32;
-      }
-      if (lane == 0) st_relaxed_gpu(flags + tile, kScanInc | (excl + agg));
-    }
-    if (lane == 0) s_excl = excl;
-  }
-  __syncthreads();
-  unsigned long long run = s_excl + wbase + incl - tot;
+  for (int k = 0; k < kSortThreads / 32; ++k) wbase += k < w ? s_wsum[k] : 0ull;
+  unsigned long long run = sums[blockIdx.x] + wbase + incl - tot;
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
-    run += v[k];
+    run += scan_widen<MODE>(v[k]);
     const int i = t * kScanItems + k;
     s_out[i + (i >> 4)] = run;
   }
@@ -433,16 +466,6 @@ __global__ void __launch_bounds__(kSortThreads)
     const int i = k * kSortThreads + t;
     const int64_t e = tile0 + i;
     if (e < n) out[e] = s_out[i + (i >> 4)];
-  }
-  // the last CTA out resets the state for the next call
-  if (t == 0) {
-    const unsigned tiles = gridDim.x;
-    s_tile = atomicAdd(ctr + 1, 1u) == tiles - 1 ? 1u : 0u;
-  }
-  __syncthreads();
-  if (s_tile) {
-    for (unsigned i = t; i < gridDim.x; i += kSortThreads) flags[i] = 0ull;
-    if (t == 0) state[0] = 0ull;
   }
 }
 
@@ -979,7 +1002,7 @@ size_t radix_sort_temp_bytes(int64_t n) {
   return (static_cast<size_t>(tiles) * 256 + 256) * sizeof(uint32_t) + 256;
 }
 
-size_t scan_temp_bytes(int64_t n) {  // look-back state: counters + one flag per tile
+size_t scan_temp_bytes(int64_t n) {  // one u64 sum per tile (+ 1)
   return static_cast<size_t>((n + kScanTile - 1) / kScanTile + 1) * sizeof(unsigned long long);
 }
 
@@ -1063,11 +1086,20 @@ int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* 
 }
 
 void inclusive_scan_gather(const uint32_t* in, const uint32_t* order, int64_t n, uint64_t* out,
-                           void* temp, cudaStream_t s) {
+                           void* temp, cudaStream_t s, int mode) {
   if (n <= 0) return;
   const int64_t tiles = (n + kScanTile - 1) / kScanTile;
-  launch_pdl(k_scan_chained, static_cast<unsigned>(tiles), kSortThreads, 0, s, in, order, n,
-             static_cast<unsigned long long*>(temp), out);
+  auto* sums = static_cast<unsigned long long*>(temp);
+  const unsigned grid = static_cast<unsigned>(tiles);
+  if (mode == 1)
+    launch_pdl(k_scan_reduce<1>, grid, kSortThreads, 0, s, in, order, n, sums);
+  else
+    launch_pdl(k_scan_reduce<0>, grid, kSortThreads, 0, s, in, order, n, sums);
+  launch_pdl(k_scan_top, 1, 1024, 0, s, sums, tiles);
+  if (mode == 1)
+    launch_pdl(k_scan_apply<1>, grid, kSortThreads, 0, s, in, order, n, sums, out);
+  else
+    launch_pdl(k_scan_apply<0>, grid, kSortThreads, 0, s, in, order, n, sums, out);
   DW_CUDA(cudaGetLastError());
 }
 

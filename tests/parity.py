@@ -47,14 +47,19 @@ MEASURE = os.environ.get("DW_PARITY_MEASURE") == "1"
 BINNING_ENV = {  # list constructions of the forward (raster.cu): env overrides
     "auto": {},
     "scatter": {"DW_SCATTER": "1", "DW_DENSE_BINNING": "0", "DW_TILE_FIRST": "0"},
-    "depth-first": {"DW_SCATTER": "0", "DW_DENSE_BINNING": "0", "DW_TILE_FIRST": "0"},
+    # depth sort, then duplicate + stable tile sort (the classic construction)
+    "depth-first": {"DW_SCATTER": "0", "DW_DENSE_BINNING": "0", "DW_TILE_FIRST": "0",
+                    "DW_BLOCK_BINNING": "0"},
+    # depth sort, then coarse-block entries + per-tile appends (the default)
+    "block": {"DW_SCATTER": "0", "DW_DENSE_BINNING": "0", "DW_TILE_FIRST": "0",
+              "DW_BLOCK_BINNING": "1"},
     "tile-first": {"DW_SCATTER": "0", "DW_DENSE_BINNING": "0", "DW_TILE_FIRST": "1"},
     "dense": {"DW_DENSE_BINNING": "1"},
 }
 
 
 def set_binning(monkeypatch, mode: str) -> None:
-    for k in ("DW_SCATTER", "DW_DENSE_BINNING", "DW_TILE_FIRST"):
+    for k in ("DW_SCATTER", "DW_DENSE_BINNING", "DW_TILE_FIRST", "DW_BLOCK_BINNING"):
         monkeypatch.delenv(k, raising=False)
     for k, v in BINNING_ENV[mode].items():
         monkeypatch.setenv(k, v)

@@ -42,7 +42,7 @@ def test_c3_view0_full(cuda, orc):
     verify_case(cuda, orc, "c3_view0", sc, cam, dL, [_pol(*p) for p in ALL])
 
 
-@pytest.mark.parametrize("binning", ["depth-first", "tile-first"])
+@pytest.mark.parametrize("binning", ["depth-first", "tile-first", "block"])
 def test_c3_other_list_constructions(cuda, orc, binning, monkeypatch):
     set_binning(monkeypatch, binning)
     sc, cam, dL = _scene("c3_1m_1080p")
@@ -75,7 +75,8 @@ SMALL = [("tiny_odd", 300, 61, 47, False, 0), ("c1_10k_256", 10_000, 256, 256, F
          ("contention_small", 2_000, 320, 200, True, 5)]
 
 
-@pytest.mark.parametrize("binning", ["auto", "scatter", "depth-first", "tile-first", "dense"])
+@pytest.mark.parametrize("binning", ["auto", "scatter", "depth-first", "tile-first", "dense",
+                                     "block"])
 @pytest.mark.parametrize("case", SMALL, ids=[c[0] for c in SMALL])
 def test_small_cases_every_binning(cuda, orc, case, binning, monkeypatch):
     """Every list construction (scatter, depth-first, tile-first, dense

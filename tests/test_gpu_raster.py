@@ -155,7 +155,7 @@ def test_render_host_e2e(cuda, orc):
     assert np.all(np.abs(grad.astype(np.float64) - want) <= tol)
 
 
-@pytest.mark.parametrize("binning", ["auto", "depth-first", "dense"])
+@pytest.mark.parametrize("binning", ["auto", "depth-first", "dense", "block"])
 def test_render_views_host_matches_per_view(cuda, orc, binning, monkeypatch):
     """Batched host path (one scene upload, views alternating over two
     forward states and compute streams, overlapped per-view copies) == the sum
@@ -204,7 +204,7 @@ def test_binning_paths_agree_on_long_lists(cuda, monkeypatch):
           for k, v in make_scene(P, W, H, seed=7, high_contention=True).items()}
     cam = make_camera(W, H)
     out = {}
-    for path in ("depth-first", "tile-first", "dense", "scatter"):
+    for path in ("depth-first", "tile-first", "dense", "scatter", "block"):
         set_binning(monkeypatch, path)
         r = GaussianRasterizer()
         img, _, nr = r.render_forward(*[sc[k] for k in ("means3D", "scales", "rotations",
@@ -213,7 +213,7 @@ def test_binning_paths_agree_on_long_lists(cuda, monkeypatch):
     ref = out["depth-first"]
     lens = ref[1][:, 1] - ref[1][:, 0]
     assert lens.max() > 4096  # the chunked-merge paths run (tile-first, scatter's long lists)
-    for path in ("tile-first", "dense", "scatter"):
+    for path in ("tile-first", "dense", "scatter", "block"):
         assert out[path][3] == ref[3]
         assert np.array_equal(out[path][0], ref[0]), path
         assert np.array_equal(out[path][1], ref[1]), path
@@ -354,14 +354,14 @@ def test_4k_image_all_binning_paths(cuda, monkeypatch):
     cam = make_camera(W, H)
     keys = ("means3D", "scales", "rotations", "opacities", "colors")
     out = {}
-    for path in ("depth-first", "tile-first", "dense", "scatter"):
+    for path in ("depth-first", "tile-first", "dense", "scatter", "block"):
         set_binning(monkeypatch, path)
         r = GaussianRasterizer()
         img, _, nr = r.render_forward(*[sc[k] for k in keys], cam)
         out[path] = (r.buffer("values"), r.buffer("ranges"), img.cpu().numpy(), nr, r)
     ref = out["depth-first"]
     assert ref[1].shape[0] == 240 * 135 and ref[3] > 1_000_000
-    for path in ("tile-first", "dense", "scatter"):
+    for path in ("tile-first", "dense", "scatter", "block"):
         assert out[path][3] == ref[3], path
         assert np.array_equal(out[path][0], ref[0]), path
         assert np.array_equal(out[path][1], ref[1]), path

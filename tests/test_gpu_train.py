@@ -198,7 +198,7 @@ def _scene_t(cuda, sc):
 _KEYS = ("means3D", "scales", "rotations", "opacities", "colors")
 
 
-@pytest.mark.parametrize("binning", ["scatter", "depth-first", "dense"])
+@pytest.mark.parametrize("binning", ["scatter", "depth-first", "dense", "block"])
 @pytest.mark.parametrize("yaw", [0.0, 23.0])
 def test_forward_async_matches_sync(cuda, yaw, binning, monkeypatch):
     """The no-host-sync forward (device-side instance count over a reserved

@@ -13,7 +13,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 
 ENV = {"scatter": {"DW_SCATTER": "1", "DW_DENSE_BINNING": "0", "DW_TILE_FIRST": "0"},
-       "depth-first": {"DW_SCATTER": "0", "DW_DENSE_BINNING": "0", "DW_TILE_FIRST": "0"},
+       "depth-first": {"DW_SCATTER": "0", "DW_DENSE_BINNING": "0", "DW_TILE_FIRST": "0",
+                       "DW_BLOCK_BINNING": "0"},
+       "block": {"DW_SCATTER": "0", "DW_DENSE_BINNING": "0", "DW_TILE_FIRST": "0",
+                 "DW_BLOCK_BINNING": "1"},
        "tile-first": {"DW_SCATTER": "0", "DW_DENSE_BINNING": "0", "DW_TILE_FIRST": "1"},
        "dense": {"DW_DENSE_BINNING": "1"}, "auto": {}}
 
@@ -39,7 +42,7 @@ def main():
     args = [t[k] for k in ("means3D", "scales", "rotations", "opacities", "colors")]
     out = {"workload": a.workload, "view": f"{a.view}/{a.views}"}
     for mode in a.modes:
-        for k in ("DW_SCATTER", "DW_DENSE_BINNING", "DW_TILE_FIRST"):
+        for k in ("DW_SCATTER", "DW_DENSE_BINNING", "DW_TILE_FIRST", "DW_BLOCK_BINNING"):
             os.environ.pop(k, None)
         os.environ.update(ENV[mode])
         r = GaussianRasterizer()
