@@ -193,6 +193,25 @@ struct dw_rasterizer {
     }
   }
 
+  // Dense-binning choice: DW_DENSE_BINNING=0/1 forces it, else the heuristic.
+  static bool dense_env_ok(bool heuristic) {
+    const char* env = std::getenv("DW_DENSE_BINNING");
+    return env && *env ? *env == '1' : heuristic;
+  }
+
+  // Block binning's entry scan (depth sort done: order, area_sorted = packed
+  // rectangles in depth order): entries into itile[0] / ivals[0], totals to
+  // offsets[P-1]. bb_entry_cap: the entries those buffers held.
+  uint64_t bb_entry_cap = 0;
+  void bb_entries_scan(cudaStream_t s, bool skip_entries) {
+    // (a frame expected to take dense binning writes no entries; should it
+    // not, the synced path rescans)
+    bb_entry_cap = skip_entries ? 0 : static_cast<uint64_t>(std::min(cap_i[0], cap_i[2]));
+    dw::block_entries_scan(area_sorted, order, P, offsets, scan_tmp,
+                           dw::block_binning_nbx(cam.tiles_x), itile[0], ivals[0], bb_entry_cap,
+                           s);
+  }
+
   // Pre-size every buffer (no allocation happens in a later forward/backward
   // that stays within these sizes -- required before CUDA-graph capture).
   void reserve(int32_t P_, int32_t W_, int32_t H_, int64_t max_instances) {
@@ -379,7 +398,7 @@ struct dw_rasterizer {
         // rectangles in that order gives both the tile and the block offsets
         depth_sort(true);
         stage_mark(2, s);
-        dw::inclusive_scan_gather(area_sorted, nullptr, P, offsets, scan_tmp, s, 1);
+        bb_entries_scan(s, dense && !nosync);  // dense: the previous frame's choice
       } else {
         // 1. Gaussians in (depth, id) order: stable 32-bit LSD sort
         depth_sort(true);
@@ -410,6 +429,19 @@ struct dw_rasterizer {
         if (block_mode) {  // (blocks << 32 | tiles)
           n_entries = static_cast<int64_t>(*h_total >> 32);
           num_rendered = static_cast<int64_t>(*h_total & 0xffffffffull);
+          // the scan wrote the entries into buffers that must hold every
+          // instance (the later grows keep them): else grow and rescan
+          const bool will_dense =
+              num_rendered > 0 && dw::dense_binning_fits(cam.tiles_x, cam.tiles_y) &&
+              dense_env_ok(static_cast<double>(P) * ntiles <= 4.0 * static_cast<double>(num_rendered));
+          if (!will_dense && static_cast<uint64_t>(num_rendered) > bb_entry_cap) {
+            const size_t ni = static_cast<size_t>(num_rendered);
+            for (int b = 0; b < 2; ++b) {
+              grow(itile[b], cap_i[b], ni);
+              grow(ivals[b], cap_i[2 + b], ni);
+            }
+            bb_entries_scan(s, false);
+          }
         }
         n_grid = num_rendered;
         last_list_mean = static_cast<double>(num_rendered) / ntiles;
@@ -430,10 +462,8 @@ struct dw_rasterizer {
     blocked = false;
     // Dense scenes (large tile rectangles: P x tiles <= 4 x instances) build the
     // per-tile lists directly; the rest duplicate + radix-sort (same output).
-    const char* env = std::getenv("DW_DENSE_BINNING");  // "0" / "1" force a path
     dense = n_grid > 0 && dw::dense_binning_fits(cam.tiles_x, cam.tiles_y) &&
-            (env && *env ? *env == '1'
-                         : static_cast<double>(P) * ntiles <= 4.0 * static_cast<double>(n_grid));
+            dense_env_ok(static_cast<double>(P) * ntiles <= 4.0 * static_cast<double>(n_grid));
     if (dense) {
       grow(rects, cap_r, static_cast<size_t>(P));
       grow(diff, cap_diff, dw::dense_scratch_words(cam.tiles_x, cam.tiles_y));
@@ -453,8 +483,7 @@ struct dw_rasterizer {
       grow(seg_scratch, cap_seg, 2 * static_cast<size_t>(std::max<int64_t>(n_grid, 1)));
       ensure_tmp(dw::radix_sort_temp_bytes(std::max<int64_t>(n_entries, 1)));
       // the sorted entries' rectangles land in seg_scratch (>= n_grid >= entries words)
-      dw::launch_block_binning(P, order, offsets, area_sorted, bb_rect_id, cam, itile, ivals,
-                               n_entries, tmp,
+      dw::launch_block_binning(bb_rect_id, cam, itile, ivals, n_entries, tmp,
                                reinterpret_cast<uint32_t*>(seg_scratch), branges, bb_cnt, ranges,
                                &vals, n_dev, nc_dev, s);
       tiles_sorted = nullptr;

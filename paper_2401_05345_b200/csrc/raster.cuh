@@ -115,10 +115,16 @@ size_t scan_temp_bytes(int64_t n);
 int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* temp,
                      cudaStream_t s, const unsigned long long* n_dev = nullptr,
                      const uint32_t* gather_src = nullptr, uint32_t* gather_out = nullptr);
-// mode 1: in[] = packed tile rectangles (launch_preprocess rect_out), out[] =
-// inclusive (coarse blocks << 32 | tiles) -- block binning's two offsets at once
 void inclusive_scan_gather(const uint32_t* in, const uint32_t* order, int64_t n, uint64_t* out,
                            void* temp, cudaStream_t s, int mode = 0);
+// Block binning's level-1 entries in one scan: over the depth-ordered packed
+// rectangles (launch_preprocess rect_out, laid out by the depth sort), the
+// inclusive (coarse blocks << 32 | tiles touched) -- its total to out[n-1] --
+// and, at each Gaussian's block offset, (block id, id) for every coarse
+// block it touches (none past cap entries).
+void block_entries_scan(const uint32_t* rect_sorted, const uint32_t* order, int64_t n,
+                        uint64_t* out, void* temp, int nbx, uint32_t* bkey, uint32_t* bval,
+                        uint64_t cap, cudaStream_t s);
 void launch_depth_keys(int P, const float* depths, const int* radii, uint32_t* dkey, uint32_t* ids,
                        cudaStream_t s);
 void launch_duplicate_sorted(int P, const uint32_t* order, const float2* means2D, const int* radii,
@@ -156,6 +162,7 @@ void launch_scatter_binning(int P, const float2* means2D, const int* radii, cons
 // 8x4-tile blocks (one sorted entry per (Gaussian, block) instead of the
 // duplicate + two-pass tile sort of every instance).
 bool block_binning_fits(int tiles_x, int tiles_y);
+int block_binning_nbx(int tiles_x);  // coarse blocks per row
 int block_binning_blocks(int tiles_x, int tiles_y);
 size_t block_binning_count_words(int tiles_x, int tiles_y);
 void launch_bb_clamp(const uint64_t* offsets, int P, uint64_t cap, unsigned long long* n_live,
@@ -164,10 +171,11 @@ void launch_bb_clamp(const uint64_t* offsets, int P, uint64_t cap, unsigned long
 // k/v: sort double buffers of >= n_entries (capacity when n_entries_dev is set);
 // brect: >= n_entries words; cnt: block_binning_count_words; writes ranges and
 // the lists (*values_out: one of v)
-// order / rect_sorted: the Gaussians and their packed rectangles in depth order
-void launch_block_binning(int P, const uint32_t* order, const uint64_t* offsets,
-                          const uint32_t* rect_sorted, const uint32_t* rect_by_id,
-                          const CamParams& cam, uint32_t* k[2],
+// k[0]/v[0]: the entries (block_entries_scan); k/v: sort double buffers of >=
+// n_entries (the capacity when n_entries_dev is set); rect_by_id: packed
+// rectangles by id (the sort payload); brect: >= n_entries words; cnt:
+// block_binning_count_words. Writes ranges and the lists (*values_out: one of v).
+void launch_block_binning(const uint32_t* rect_by_id, const CamParams& cam, uint32_t* k[2],
                           uint32_t* v[2], int64_t n_entries, void* sort_tmp, uint32_t* brect,
                           uint2* branges, uint32_t* cnt, uint2* ranges, uint32_t** values_out,
                           const unsigned long long* n_live,

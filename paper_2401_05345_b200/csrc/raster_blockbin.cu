@@ -67,36 +67,6 @@ __global__ void k_bb_clamp(const uint64_t* __restrict__ offsets, int P, uint64_t
   else if (!sticky) *overflow = 0u;
 }
 
-// Level-1 entries: (block id, Gaussian id) for every block a rectangle
-// touches, in depth order, at the block offsets of the packed scan (high 32
-// bits). Rectangles come packed from the preprocess, laid out in depth order
-// by the depth sort's last pass (rect_sorted).
-__global__ void __launch_bounds__(256)
-    k_bb_entries(int P, const uint32_t* __restrict__ order, const uint32_t* __restrict__ rect_sorted,
-                 const uint64_t* __restrict__ offsets, int nbx, uint32_t* __restrict__ bkey,
-                 uint32_t* __restrict__ bval, const unsigned long long* __restrict__ n_entries,
-                 uint64_t cap) {
-  pdl_wait();
-  pdl_trigger();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= P) return;
-  const uint32_t gid = order[i];
-  const uint32_t pr = rect_sorted[i];
-  const int x0 = (int)(pr & 0xffu), y0 = (int)((pr >> 8) & 0xffu);
-  const int x1 = (int)((pr >> 16) & 0xffu), y1 = (int)(pr >> 24);
-  if (y0 > y1) return;  // empty rectangle
-  const uint64_t lim = n_entries ? static_cast<uint64_t>(*n_entries) : cap;
-  uint64_t o = i == 0 ? 0ull : (offsets[i - 1] >> 32);
-  const int bx0 = x0 / kBBW, bx1 = x1 / kBBW, by0 = y0 / kBBH, by1 = y1 / kBBH;
-  if (o + static_cast<uint64_t>((bx1 - bx0 + 1) * (by1 - by0 + 1)) > lim) return;  // overflow
-  for (int by = by0; by <= by1; ++by)
-    for (int bx = bx0; bx <= bx1; ++bx) {
-      bkey[o] = static_cast<uint32_t>(by * nbx + bx);
-      bval[o] = gid;
-      ++o;
-    }
-}
-
 // 32 x 32 bit-matrix transpose across the warp: lane l holds row l (bit c =
 // column c) on entry, lane c holds column c (bit l = row l) on exit -- five
 // xor-shuffle block swaps. At level j a lane keeps its half of the columns
@@ -163,15 +133,22 @@ __global__ void __launch_bounds__(32 * kBBWarps)
   const uint32_t hi = br.x + static_cast<uint32_t>(static_cast<uint64_t>(len) * (seg + 1) / kBBSegs);
   const Transpose32 tr(lane);
   uint32_t cnt = 0;
+  uint32_t pr[kBBSteps];
+#pragma unroll
+  for (int q = 0; q < kBBSteps; ++q) {
+    const uint32_t kq = lo + 32 * q + lane;
+    pr[q] = kq < hi ? __ldg(brect + kq) : kEmptyRectBB;
+  }
   for (uint32_t k0 = lo; k0 < hi; k0 += 32 * kBBSteps) {
-    uint32_t pr[kBBSteps];
+    uint32_t m[kBBSteps];
 #pragma unroll
     for (int q = 0; q < kBBSteps; ++q) {
-      const uint32_t kq = k0 + 32 * q + lane;
+      m[q] = block_cover(pr[q], bx, by);
+      const uint32_t kq = k0 + 32 * (kBBSteps + q) + lane;  // next round, in flight
       pr[q] = kq < hi ? __ldg(brect + kq) : kEmptyRectBB;
     }
 #pragma unroll
-    for (int q = 0; q < kBBSteps; ++q) cnt += __popc(tr(block_cover(pr[q], bx, by)));
+    for (int q = 0; q < kBBSteps; ++q) cnt += __popc(tr(m[q]));
   }
   s_c[w][lane] = cnt;
   __syncthreads();
@@ -361,6 +338,8 @@ inline unsigned blocks_of(int64_t n, int per) { return static_cast<unsigned>((n 
 
 bool block_binning_fits(int tiles_x, int tiles_y) { return tiles_x <= 255 && tiles_y <= 255; }
 
+int block_binning_nbx(int tiles_x) { return (tiles_x + kBBW - 1) / kBBW; }
+
 int block_binning_blocks(int tiles_x, int tiles_y) {
   return ((tiles_x + kBBW - 1) / kBBW) * ((tiles_y + kBBH - 1) / kBBH);
 }
@@ -377,9 +356,7 @@ void launch_bb_clamp(const uint64_t* offsets, int P, uint64_t cap, unsigned long
   DW_CUDA(cudaGetLastError());
 }
 
-void launch_block_binning(int P, const uint32_t* order, const uint64_t* offsets,
-                          const uint32_t* rect_sorted, const uint32_t* rect_by_id,
-                          const CamParams& cam, uint32_t* k[2],
+void launch_block_binning(const uint32_t* rect_by_id, const CamParams& cam, uint32_t* k[2],
                           uint32_t* v[2], int64_t n_entries, void* sort_tmp, uint32_t* brect,
                           uint2* branges, uint32_t* cnt, uint2* ranges, uint32_t** values_out,
                           const unsigned long long* n_live,
@@ -390,10 +367,8 @@ void launch_block_binning(int P, const uint32_t* order, const uint64_t* offsets,
   uint32_t* tcount = cnt;  // [ntiles][split]
   int bits = 1;
   while ((1 << bits) < nblocks) ++bits;
-  // level 1: entries, stable sort by block id (payload: the packed rectangle), block ranges
-  launch_pdl(k_bb_entries, blocks_of(P, 256), 256, 0, s, P, order, rect_sorted, offsets, nbx,
-             k[0], v[0],
-             n_entries_dev, static_cast<uint64_t>(n_entries));
+  // level 1: the entries (block_entries_scan) stably sorted by block id
+  // (payload: the packed rectangle), block ranges
   const int cur = radix_sort_pairs(k, v, n_entries, bits, sort_tmp, s, n_entries_dev, rect_by_id,
                                    brect);
   launch_ranges_u32(n_entries, k[cur], branges, nblocks, s, n_entries_dev);

@@ -188,22 +188,6 @@ __global__ void __launch_bounds__(1024)
   if (t == 0) digit_total[blockIdx.x] = carry;
 }
 
-__global__ void k_scan_digits(uint32_t* __restrict__ digit_total, int ndigits) {
-  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
-  pdl_trigger();
-  // 256 threads, exclusive scan in place (<= 256 digits)
-  __shared__ uint32_t s[256];
-  const int t = threadIdx.x;
-  s[t] = t < ndigits ? digit_total[t] : 0u;
-  __syncthreads();
-  for (int o = 1; o < 256; o <<= 1) {
-    const uint32_t y = t >= o ? s[t - o] : 0u;
-    __syncthreads();
-    s[t] += y;
-    __syncthreads();
-  }
-  if (t < ndigits) digit_total[t] = s[t] - (t < ndigits ? digit_total[t] : 0u);
-}
 
 // Stable scatter of one tile. Same warp-contiguous chunks as the upsweep:
 // each warp ranks its ITEMS*32 elements against a warp-private running
@@ -217,7 +201,7 @@ template <int ITEMS, int BITS>
 __global__ void __launch_bounds__(kSortThreads)
     k_downsweep(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, int64_t n,
                 int shift, uint32_t mask, int bits, const uint32_t* __restrict__ counts,
-                int64_t tiles, const uint32_t* __restrict__ digit_base,
+                int64_t tiles, const uint32_t* __restrict__ digit_base,  // digit totals
                 uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
                 const unsigned long long* __restrict__ n_dev,
                 const uint32_t* __restrict__ gather_src, uint32_t* __restrict__ gather_out) {
@@ -228,13 +212,24 @@ __global__ void __launch_bounds__(kSortThreads)
   __shared__ uint32_t s_dstart[256];       // tile-local start of each digit's run
   __shared__ uint32_t s_gbase[256];        // global start of this tile's run of each digit
   __shared__ uint32_t s_wsum[kWarps];
+  __shared__ uint32_t s_dsum[kWarps];
   __shared__ uint32_t s_key[TILE], s_val[TILE];
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
   n = live_n(n, n_dev);
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
   for (int k = 0; k < kWarps; ++k) s_cnt[k][t] = 0;
-  s_gbase[t] = digit_base[t] + counts[static_cast<int64_t>(t) * tiles + blockIdx.x];
+  // global start of each digit = exclusive scan of the 256 digit totals
+  // (k_scan_rows), done by every CTA instead of a separate launch
+  const uint32_t dtot = digit_base[t];
+  uint32_t dincl = dtot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, dincl, o);
+    if (lane >= o) dincl += y;
+  }
+  if (lane == 31) s_dsum[w] = dincl;
+  const uint32_t my_count = counts[static_cast<int64_t>(t) * tiles + blockIdx.x];
   const int64_t tile0 = static_cast<int64_t>(blockIdx.x) * TILE;
   const int64_t base = tile0 + static_cast<int64_t>(w) * ITEMS * 32;
   (void)bits;
@@ -255,6 +250,11 @@ __global__ void __launch_bounds__(kSortThreads)
     }
   }
   __syncthreads();
+  {
+    uint32_t before = dincl - dtot;
+    for (int k = 0; k < w; ++k) before += s_dsum[k];
+    s_gbase[t] = before + my_count;
+  }
   // 1. rank inside the warp's contiguous chunk (warp-private counters)
   auto rank_items = [&](auto full_tag) {
     constexpr bool FULL = decltype(full_tag)::value;
@@ -415,10 +415,23 @@ __global__ void __launch_bounds__(1024) k_scan_top(unsigned long long* __restric
   }
 }
 
+// Block binning's level-1 entries (MODE 1): element e (a depth-ordered
+// Gaussian, packed rectangle in[e], id ids[e]) writes (block id, id) for every
+// coarse 8x4-tile block its rectangle touches at its exclusive block offset;
+// only the last element's inclusive (blocks << 32 | tiles) goes to out[n-1].
+struct ScanEntries {
+  const uint32_t* ids = nullptr;
+  uint32_t* bkey = nullptr;
+  uint32_t* bval = nullptr;
+  uint64_t cap = 0;  // entries the buffers hold (no write past it)
+  int nbx = 0;       // coarse blocks per row
+};
+
 template <int MODE>
 __global__ void __launch_bounds__(kSortThreads)
     k_scan_apply(const uint32_t* __restrict__ in, const uint32_t* __restrict__ order, int64_t n,
-                 const unsigned long long* __restrict__ sums, uint64_t* __restrict__ out) {
+                 const unsigned long long* __restrict__ sums, uint64_t* __restrict__ out,
+                 const ScanEntries ent) {
   pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
   __shared__ uint32_t s_in[kScanTile + kScanTile / 32];          // padded: conflict-free transpose
@@ -454,6 +467,69 @@ __global__ void __launch_bounds__(kSortThreads)
 #pragma unroll
   for (int k = 0; k < kSortThreads / 32; ++k) wbase += k < w ? s_wsum[k] : 0ull;
   unsigned long long run = sums[blockIdx.x] + wbase + incl - tot;
+  if (MODE == 1) {
+    // exclusive block offsets to shared memory (thread-blocked), then each
+    // warp expands 32 consecutive Gaussians at a time into their entries with
+    // consecutive lanes on consecutive entries (coalesced stores)
+    uint32_t* s_bo = reinterpret_cast<uint32_t*>(s_out);
+    const int64_t e0 = tile0 + static_cast<int64_t>(t) * kScanItems;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      const int i = t * kScanItems + k;
+      s_bo[i + (i >> 5)] = static_cast<uint32_t>(run >> 32);
+      run += scan_widen<MODE>(v[k]);
+      if (e0 + k == n - 1) out[n - 1] = run;
+    }
+    uint32_t gids[kScanItems];  // all rounds' ids in flight at once
+#pragma unroll
+    for (int r = 0; r < kScanItems; ++r) {
+      const int64_t e = tile0 + w * (32 * kScanItems) + r * 32 + lane;
+      gids[r] = e < n ? __ldg(ent.ids + e) : 0u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kScanItems; ++r) {
+      const int i = w * (32 * kScanItems) + r * 32 + lane;
+      const int64_t e = tile0 + i;
+      const uint32_t x = e < n ? s_in[i + (i >> 5)] : 0x0000ff00u;
+      const int x0 = (int)(x & 0xffu), y0 = (int)((x >> 8) & 0xffu);
+      const int x1 = (int)((x >> 16) & 0xffu), y1 = (int)(x >> 24);
+      const int bx0 = x0 / 8, by0 = y0 / 4;
+      const int bw = x1 / 8 - bx0 + 1;
+      int nb = y0 > y1 ? 0 : bw * (y1 / 4 - by0 + 1);
+      const uint32_t o = s_bo[i + (i >> 5)];
+      if (static_cast<uint64_t>(o) + static_cast<uint64_t>(nb) > ent.cap) nb = 0;  // host regrows
+      const uint32_t gid = gids[r];
+      int incl = nb;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, d);
+        if (lane >= d) incl += y;
+      }
+      const int excl = incl - nb;
+      const int total = __shfl_sync(kFull, incl, 31);
+      for (int q0 = 0; q0 < total; q0 += 32) {  // warp-uniform trips
+        const int q = q0 + lane;
+        int owner = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+          const int probe = owner + step;
+          if (__shfl_sync(kFull, excl, probe) <= q) owner = probe;
+        }
+        const int kk = q - __shfl_sync(kFull, excl, owner);
+        const int w_ = __shfl_sync(kFull, bw, owner);
+        const int ox = __shfl_sync(kFull, bx0, owner), oy = __shfl_sync(kFull, by0, owner);
+        const uint32_t oo = __shfl_sync(kFull, o, owner);
+        const uint32_t og = __shfl_sync(kFull, gid, owner);
+        if (q < total) {
+          const int row = static_cast<int>((static_cast<float>(kk) + 0.5f) / static_cast<float>(w_));
+          ent.bkey[oo + kk] = static_cast<uint32_t>((oy + row) * ent.nbx + ox + (kk - row * w_));
+          ent.bval[oo + kk] = og;
+        }
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
     run += scan_widen<MODE>(v[k]);
@@ -1061,8 +1137,7 @@ int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* 
         launch_pdl(k_upsweep<4>, grid, kSortThreads, 0, s, k[cur], n, shift, mask, b, counts, tiles,
                    n_dev);
     }
-    launch_pdl(k_scan_rows, 256, 1024, 0, s, counts, tiles, digit);
-    launch_pdl(k_scan_digits, 1, 256, 0, s, digit, 256);
+    launch_pdl(k_scan_rows, 256, 1024, 0, s, counts, tiles, digit);  // digit totals: scanned per CTA
     switch (items) {
       case 16:
         launch_downsweep<16>(b, grid, s, k[cur], v[cur], n, shift, mask, counts, tiles, digit,
@@ -1097,9 +1172,27 @@ void inclusive_scan_gather(const uint32_t* in, const uint32_t* order, int64_t n,
     launch_pdl(k_scan_reduce<0>, grid, kSortThreads, 0, s, in, order, n, sums);
   launch_pdl(k_scan_top, 1, 1024, 0, s, sums, tiles);
   if (mode == 1)
-    launch_pdl(k_scan_apply<1>, grid, kSortThreads, 0, s, in, order, n, sums, out);
-  else
-    launch_pdl(k_scan_apply<0>, grid, kSortThreads, 0, s, in, order, n, sums, out);
+    throw std::invalid_argument("scan mode 1 runs through block_entries_scan");
+  launch_pdl(k_scan_apply<0>, grid, kSortThreads, 0, s, in, order, n, sums, out, ScanEntries{});
+  DW_CUDA(cudaGetLastError());
+}
+
+void block_entries_scan(const uint32_t* rect_sorted, const uint32_t* order, int64_t n,
+                        uint64_t* out, void* temp, int nbx, uint32_t* bkey, uint32_t* bval,
+                        uint64_t cap, cudaStream_t s) {
+  if (n <= 0) return;
+  const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+  auto* sums = static_cast<unsigned long long*>(temp);
+  const unsigned grid = static_cast<unsigned>(tiles);
+  launch_pdl(k_scan_reduce<1>, grid, kSortThreads, 0, s, rect_sorted, nullptr, n, sums);
+  launch_pdl(k_scan_top, 1, 1024, 0, s, sums, tiles);
+  ScanEntries ent;
+  ent.ids = order;
+  ent.bkey = bkey;
+  ent.bval = bval;
+  ent.cap = cap;
+  ent.nbx = nbx;
+  launch_pdl(k_scan_apply<1>, grid, kSortThreads, 0, s, rect_sorted, nullptr, n, sums, out, ent);
   DW_CUDA(cudaGetLastError());
 }
 
