@@ -274,6 +274,7 @@ def stage_breakdown(t, cam, P, H, W) -> dict:
     dw_rasterizer_stage_timing) with each stage's algorithmic bytes and HBM
     fraction; the events serialise the programmatic-dependent launches, so
     the stages sum to slightly more than the untimed forward."""
+    import numpy as np
     import torch
 
     from paper_2401_05345_b200.rasterizer import GaussianRasterizer
@@ -292,13 +293,33 @@ def stage_breakdown(t, cam, P, H, W) -> dict:
     hbm, _ = measured_peaks()
     # algorithmic bytes per stage: reads + writes the stage
     # cannot avoid, counted once
-    alg = {"preprocess": 56 * P + 60 * P,           # scene in; means2D..keys out
+    block = os.environ.get("DW_BLOCK_BINNING", "1") != "0" and W <= 255 * 16 and H <= 255 * 16
+    alg = {"preprocess": 56 * P + 64 * P,           # scene in; means2D..keys + packed rect out
            "depth_sort": 4 * 16 * vis,              # 4 LSD passes, 8 B in + 8 B out each
-           "offsets": 12 * P,                       # areas in, u64 offsets out
-           "binning": 20 * vis + 8 * I + 2 * 16 * I,  # duplicate + 2 tile-sort passes
            "ranges": 4 * I + 8 * (W // 16 + 1) * (H // 16 + 1),
            "blend": 4 * I + 44 * vis + 20 * H * W}
-    out = {}
+    if block:
+        # block binning (raster_blockbin.cu): Nc = (Gaussian, coarse 8x4-tile
+        # block) entries, from the rectangles exactly as the kernels form them
+        m2 = r.buffer("means2D").reshape(-1, 2).astype(np.float32)
+        rad = r.buffer("radii").astype(np.float32)
+        live = rad > 0
+        tx, ty = (W + 15) // 16, (H + 15) // 16
+        f16 = np.float32(16.0)
+        x0 = np.clip(np.trunc((m2[:, 0] - rad) / f16), 0, tx).astype(np.int64)
+        y0 = np.clip(np.trunc((m2[:, 1] - rad) / f16), 0, ty).astype(np.int64)
+        x1 = np.clip(np.trunc((m2[:, 0] + rad + np.float32(15)) / f16), 0, tx).astype(np.int64)
+        y1 = np.clip(np.trunc((m2[:, 1] + rad + np.float32(15)) / f16), 0, ty).astype(np.int64)
+        ok = live & (x1 > x0) & (y1 > y0)
+        nc = int((((x1 - 1) // 8 - x0 // 8 + 1) * ((y1 - 1) // 4 - y0 // 4 + 1))[ok].sum())
+        alg["offsets"] = 8 * vis + 8 * nc           # rects + ids in, entries out
+        alg["binning"] = 20 * nc + 4 * nc + 8 * nc + 4 * I  # entry sort pass, count, place
+        alg["_entries"] = nc
+    else:
+        alg["offsets"] = 12 * P                     # areas in, u64 offsets out
+        alg["binning"] = 20 * vis + 8 * I + 2 * 16 * I  # duplicate + 2 tile-sort passes
+    out = {"_list_construction": "block binning" if block else "duplicate + tile sort",
+           "_entries": alg.pop("_entries", None)}
     for k, ms in best.items():
         gbs = alg[k] / (ms * 1e-3) / 1e9 if ms > 0 else None
         out[k] = {"ms": ms, "alg_bytes": alg[k], "GBps": gbs,
