@@ -129,7 +129,10 @@ struct dw_rasterizer {
   cudaStream_t s_in = nullptr, s_out = nullptr;  // copy streams of the batched host path
   cudaStream_t s_aux = nullptr;  // second compute stream: odd views of a batch
   dw_rasterizer* twin = nullptr;  // forward state of the odd views
-  cudaEvent_t ev[10] = {};
+  cudaEvent_t ev[14] = {};
+  // batched host path, DW_FWD_PRIORITY=1: the forwards on two high-priority
+  // streams (a view's binning CTAs dispatched as soon as a backward CTA retires)
+  cudaStream_t s_fwd[2] = {nullptr, nullptr};
 
   // Per-stage forward timing (dw_rasterizer_stage_timing): events recorded
   // between the forward's stages. Diagnostic only: an event between two
@@ -150,7 +153,10 @@ struct dw_rasterizer {
     if (s_in) return;
     DW_CUDA(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
     DW_CUDA(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
-    DW_CUDA(cudaStreamCreateWithFlags(&s_aux, cudaStreamNonBlocking));
+    int lo = 0, hi = 0;
+    DW_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    DW_CUDA(cudaStreamCreateWithPriority(&s_aux, cudaStreamNonBlocking, lo));
+    for (auto& f : s_fwd) DW_CUDA(cudaStreamCreateWithPriority(&f, cudaStreamNonBlocking, hi));
     for (auto& e : ev) DW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
 
@@ -172,6 +178,7 @@ struct dw_rasterizer {
       cudaStreamDestroy(s_in);
       cudaStreamDestroy(s_out);
       cudaStreamDestroy(s_aux);
+      for (auto f : s_fwd) cudaStreamDestroy(f);
       for (auto e : ev) cudaEventDestroy(e);
     }
   }
@@ -797,7 +804,8 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
   float* d_img[2] = {r->host_scratch(6, 3 * npx), r->host_scratch(9, 3 * npx)};
   cudaEvent_t e_scene = r->ev[0], e_in[2] = {r->ev[1], r->ev[2]},
               e_used[2] = {r->ev[3], r->ev[4]}, e_img[2] = {r->ev[5], r->ev[6]},
-              e_start = r->ev[7], e_zero = r->ev[8], e_aux = r->ev[9];
+              e_start = r->ev[7], e_zero = r->ev[8], e_aux = r->ev[9],
+              e_fwd[2] = {r->ev[10], r->ev[11]}, e_fj[2] = {r->ev[12], r->ev[13]};
   // Views alternate between two forward states and two compute streams
   // (R[k & 1], S[k & 1]), so view k+1's projection / sort -- latency-bound
   // launches that leave most SMs idle -- overlaps view k's backward. Both
@@ -805,7 +813,15 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
   // was never fixed, so the sum is the same up to fp32 reassociation.
   if (V > 1 && !r->twin) r->twin = new dw_rasterizer();
   dw_rasterizer* R[2] = {r, V > 1 ? r->twin : r};
-  cudaStream_t S[2] = {s, V > 1 ? r->s_aux : s};
+  cudaStream_t S[2] = {s, V > 1 ? r->s_aux : s};  // backwards
+  // forwards: on the backward's stream (default), or with DW_FWD_PRIORITY=1 on
+  // high-priority streams of their own -- A/B on C5, 64 views: 109.1 ms
+  // default vs 116.0 ms (profiles/r02/ab/fwd_priority.md): the backward keeps
+  // every SM's register file full, so the forward's kernels gain no slots and
+  // only add contention; not the default
+  const char* fp_env = std::getenv("DW_FWD_PRIORITY");
+  const bool fwd_hi = fp_env && *fp_env == '1';
+  cudaStream_t F[2] = {fwd_hi ? r->s_fwd[0] : S[0], fwd_hi ? r->s_fwd[1] : S[1]};
   auto h2d = [&](float* d, const float* h, size_t n, cudaStream_t st) {
     if (n) DW_CUDA(cudaMemcpyAsync(d, h, n * sizeof(float), cudaMemcpyHostToDevice, st));
   };
@@ -814,6 +830,7 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
   DW_CUDA(cudaStreamWaitEvent(r->s_in, e_start, 0));
   DW_CUDA(cudaStreamWaitEvent(r->s_out, e_start, 0));
   DW_CUDA(cudaStreamWaitEvent(S[1], e_start, 0));
+  for (auto f : F) DW_CUDA(cudaStreamWaitEvent(f, e_start, 0));
   h2d(d_m, m, 3 * size_t(P), r->s_in);
   h2d(d_sc, sc, 3 * size_t(P), r->s_in);
   h2d(d_rot, rot, 4 * size_t(P), r->s_in);
@@ -822,6 +839,7 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
   DW_CUDA(cudaEventRecord(e_scene, r->s_in));
   DW_CUDA(cudaStreamWaitEvent(s, e_scene, 0));
   DW_CUDA(cudaStreamWaitEvent(S[1], e_scene, 0));
+  for (auto f : F) DW_CUDA(cudaStreamWaitEvent(f, e_scene, 0));
   // Views 0 and 1 read their instance counts back (host sync on their own
   // stream only) and size a 1.5x reserve for their forward state; later
   // views keep the count on the device (no host sync: the host runs ahead
@@ -837,29 +855,37 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
     for (int k = 0; k < V; ++k) {
       const int b = k & 1;
       dw_rasterizer* Rb = R[b];
-      cudaStream_t Sb = S[b];
+      cudaStream_t Sb = S[b], Fb = F[b];
       if (k + 1 < V) {  // prefetch view k+1 once view k-1 released its buffer
         if (k >= 1) DW_CUDA(cudaStreamWaitEvent(r->s_in, e_used[b ^ 1], 0));
         h2d(d_dl[b ^ 1], dL + static_cast<size_t>(k + 1) * 3 * npx, 3 * npx, r->s_in);
         DW_CUDA(cudaEventRecord(e_in[b ^ 1], r->s_in));
       }
-      DW_CUDA(cudaStreamWaitEvent(Sb, e_in[b], 0));
-      if (k >= 2) DW_CUDA(cudaStreamWaitEvent(Sb, e_img[b], 0));  // image k-2 downloaded
+      if (k >= 2) {
+        DW_CUDA(cudaStreamWaitEvent(Fb, e_used[b], 0));  // view k-2's backward: state free
+        DW_CUDA(cudaStreamWaitEvent(Fb, e_img[b], 0));   // image k-2 downloaded
+      }
       if (nosync_ok && (k == 2 || k == 3)) {  // first reuse of R[b]: size its reserve
         const int64_t want = Rb->num_rendered + Rb->num_rendered / 2 + 4096;
         if (static_cast<int64_t>(std::min(Rb->cap_i[0], Rb->cap_i[2])) < want) {
           DW_CUDA(cudaStreamSynchronize(Sb));  // view k-2 is done with the buffers a reserve moves
+          DW_CUDA(cudaStreamSynchronize(Fb));
           Rb->reserve(P, cams[0].width, cams[0].height, want);
         }
-        DW_CUDA(cudaMemsetAsync(Rb->overflow_dev, 0, sizeof(unsigned int), Sb));
+        DW_CUDA(cudaMemsetAsync(Rb->overflow_dev, 0, sizeof(unsigned int), Fb));
       }
       const bool nosync = nosync_ok && k >= 2;
-      Rb->forward(P, d_m, d_sc, d_rot, d_op, d_col, cams[k], d_img[b], nullptr, Sb, nosync,
+      Rb->forward(P, d_m, d_sc, d_rot, d_op, d_col, cams[k], d_img[b], nullptr, Fb, nosync,
                   /*sticky_overflow=*/true);
+      if (Fb != Sb) {
+        DW_CUDA(cudaEventRecord(e_fwd[b], Fb));
+        DW_CUDA(cudaStreamWaitEvent(Sb, e_fwd[b], 0));
+      }
+      DW_CUDA(cudaStreamWaitEvent(Sb, e_in[b], 0));
       Rb->backward(d_dl[b], policy, thr, d_g, nullptr, Sb);
       DW_CUDA(cudaEventRecord(e_used[b], Sb));
       if (out_images) {
-        DW_CUDA(cudaStreamWaitEvent(r->s_out, e_used[b], 0));
+        DW_CUDA(cudaStreamWaitEvent(r->s_out, Fb != Sb ? e_fwd[b] : e_used[b], 0));
         DW_CUDA(cudaMemcpyAsync(out_images + static_cast<size_t>(k) * 3 * npx, d_img[b],
                                 3 * npx * sizeof(float), cudaMemcpyDeviceToHost, r->s_out));
         DW_CUDA(cudaEventRecord(e_img[b], r->s_out));
@@ -867,6 +893,11 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
         DW_CUDA(cudaEventRecord(e_img[b], Sb));
       }
     }
+    for (int b = 0; b < 2; ++b)
+      if (F[b] != S[b]) {
+        DW_CUDA(cudaEventRecord(e_fj[b], F[b]));
+        DW_CUDA(cudaStreamWaitEvent(s, e_fj[b], 0));
+      }
     DW_CUDA(cudaEventRecord(e_aux, S[1]));
     DW_CUDA(cudaStreamWaitEvent(s, e_aux, 0));
     if (!nosync_ok) break;
