@@ -43,10 +43,19 @@ namespace {
 
 constexpr int kBBW = 8;       // coarse block width in tiles (one warp row)
 constexpr int kBBH = 4;       // coarse block height in tiles (one warp per row)
-constexpr int kBBWarps = 16;  // warps per CTA, each a contiguous segment of the block's list
-constexpr int kBBSplit = 2;   // CTAs per block
+#ifndef DW_BB_WARPS
+#define DW_BB_WARPS 16
+#endif
+#ifndef DW_BB_SPLIT
+#define DW_BB_SPLIT 2
+#endif
+#ifndef DW_BB_STEPS
+#define DW_BB_STEPS 4
+#endif
+constexpr int kBBWarps = DW_BB_WARPS;  // warps per CTA, each a contiguous segment of the list
+constexpr int kBBSplit = DW_BB_SPLIT;  // CTAs per block
 constexpr int kBBSegs = kBBWarps * kBBSplit;  // segments per block list
-constexpr int kBBSteps = 4;   // 32-entry steps per warp per round (loaded together)
+constexpr int kBBSteps = DW_BB_STEPS;  // 32-entry steps per warp per round (loaded together)
 constexpr uint32_t kEmptyRectBB = 0x0000ff00u;  // y0 = 255 > y1 - 1 = 0
 
 // No-sync sizing for block binning: offsets[P-1] holds (tiles, blocks); the
@@ -162,9 +171,10 @@ __global__ void __launch_bounds__(32 * kBBWarps)
 }
 
 __device__ __forceinline__ uint32_t tile_total(const uint32_t* __restrict__ tcount, int tile) {
-  static_assert(kBBSplit == 2, "two CTA partials per tile");
-  const uint2 c = reinterpret_cast<const uint2*>(tcount)[tile];
-  return c.x + c.y;
+  uint32_t c = 0;
+#pragma unroll
+  for (int h = 0; h < kBBSplit; ++h) c += tcount[tile * kBBSplit + h];
+  return c;
 }
 
 // One CTA: per-tile totals -> exclusive scan in tile order -> ranges ((0, 0)
@@ -176,39 +186,45 @@ __global__ void __launch_bounds__(1024)
   pdl_trigger();
   __shared__ uint32_t s_wsum[32];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const int per = (ntiles + 1023) / 1024;
-  uint32_t local = 0;
-  for (int k = 0; k < per; ++k) {
-    const int tile = t * per + k;
-    if (tile < ntiles) local += tile_total(tcount, tile);
-  }
-  uint32_t incl = local;
+  const bool over = n_live && *n_live == 0ull;
+  uint32_t carry = 0;
+  // 1,024 consecutive tiles per round (coalesced), each round's block scan
+  // continuing the previous one's total; all rounds' counts loaded up front
+  const int rounds = (ntiles + 1023) / 1024;  // <= 64 (255 x 255 tiles)
+  uint32_t c[8];
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(kFull, incl, o);
-    if (lane >= o) incl += y;
+  for (int r = 0; r < 8; ++r) {
+    const int tile = r * 1024 + t;
+    c[r] = (r < rounds && tile < ntiles) ? tile_total(tcount, tile) : 0u;
   }
-  if (lane == 31) s_wsum[w] = incl;
-  __syncthreads();
-  if (w == 0) {
-    const uint32_t v = s_wsum[lane];
-    uint32_t vi = v;
+  auto round = [&](int r, uint32_t v) {
+    const int tile = r * 1024 + t;
+    uint32_t incl = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, vi, o);
-      if (lane >= o) vi += y;
+      const uint32_t y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
     }
-    s_wsum[lane] = vi - v;
-  }
-  __syncthreads();
-  const bool over = n_live && *n_live == 0ull;
-  uint32_t run = s_wsum[w] + incl - local;
-  for (int k = 0; k < per; ++k) {
-    const int tile = t * per + k;
-    if (tile >= ntiles) break;
-    const uint32_t c = tile_total(tcount, tile);
-    ranges[tile] = (c == 0 || over) ? make_uint2(0u, 0u) : make_uint2(run, run + c);
-    run += c;
+    if (lane == 31) s_wsum[w] = incl;
+    __syncthreads();
+    uint32_t before = carry + incl - v, total = carry;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const uint32_t x = s_wsum[k];
+      before += k < w ? x : 0u;
+      total += x;
+    }
+    if (tile < ntiles)
+      ranges[tile] = (v == 0 || over) ? make_uint2(0u, 0u) : make_uint2(before, before + v);
+    carry = total;
+    __syncthreads();
+  };
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+    if (r < rounds) round(r, c[r]);
+  for (int r = 8; r < rounds; ++r) {
+    const int tile = r * 1024 + t;
+    round(r, tile < ntiles ? tile_total(tcount, tile) : 0u);
   }
 }
 
