@@ -265,7 +265,26 @@ def reference_arm(args) -> None:
         "cpu_baseline": cpu,
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+# The driver reads ONE JSON line from stdout: native libraries (NCCL prints its
+# version banner on the first collective) are pointed at stderr, the line goes
+# to the original stdout.
+_JSON_OUT = None
+
+
+def quiet_stdout() -> None:
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    print(json.dumps(line), file=out, flush=True)
 
 
 # ----------------------------------------------------------------- our arm
@@ -332,6 +351,7 @@ def stage_breakdown(t, cam, P, H, W) -> dict:
 
 def main() -> None:
     args = parse()
+    quiet_stdout()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -709,7 +729,7 @@ def main() -> None:
             "cpu_port": cpu_port,
             "trace_family": tfam,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
