@@ -46,6 +46,36 @@ def main():
                      big["colors"], cam2)
     r.render_backward(torch.from_numpy(make_dL_dpixels(640, 480)).to(dev),
                       wr.Policy(wr.PolicyKind.sw_b, 8))
+    # every list construction on a scene whose block lists take several
+    # staging rounds (block binning), plus a no-sync forward over its reserve
+    mid = {k: torch.from_numpy(v).to(dev) for k, v in make_scene(60000, 640, 480, seed=4).items()}
+    cam3 = make_camera(640, 480)
+    margs = [mid[k] for k in ("means3D", "scales", "rotations", "opacities", "colors")]
+    dL3 = torch.from_numpy(make_dL_dpixels(640, 480)).to(dev)
+    modes = {"block": {"DW_BLOCK_BINNING": "1"}, "depth-first": {"DW_BLOCK_BINNING": "0"},
+             "tile-first": {"DW_TILE_FIRST": "1"}, "scatter": {"DW_SCATTER": "1"},
+             "dense": {"DW_DENSE_BINNING": "1"}}
+    for mode, env in modes.items():
+        for k in ("DW_BLOCK_BINNING", "DW_TILE_FIRST", "DW_SCATTER", "DW_DENSE_BINNING"):
+            os.environ.pop(k, None)
+        os.environ.update(env)
+        rm = GaussianRasterizer()
+        rm.render_forward(*margs, cam3)
+        rm.render_backward(dL3, wr.Policy(wr.PolicyKind.sw_b, 16))
+        rm.buffer("keys")
+        n = rm.num_rendered
+        ra = GaussianRasterizer()  # buffers only grow: a fresh one for the small reserve
+        ra.reserve(60000, 640, 480, n // 2)  # too small: the async forward must overflow cleanly
+        img3 = torch.empty((3, 480, 640), device=dev)
+        rad3 = torch.empty(60000, dtype=torch.int32, device=dev)
+        ra.render_forward_async(*margs, cam3, img3, rad3)
+        assert ra.instances()[1], mode
+        ra.reserve(60000, 640, 480, n + 4096)
+        ra.render_forward_async(*margs, cam3, img3, rad3)
+        assert not ra.instances()[1], mode
+        ra.render_backward(dL3, wr.Policy(wr.PolicyKind.sw_b, 16))
+    for k in ("DW_BLOCK_BINNING", "DW_TILE_FIRST", "DW_SCATTER", "DW_DENSE_BINNING"):
+        os.environ.pop(k, None)
     # batched host path
     cams = orbit_cameras(W, H, 3)
     pin = {k: v.cpu().pin_memory() for k, v in sc.items()}
