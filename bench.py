@@ -518,12 +518,22 @@ def main() -> None:
     # ---- where the speed-up comes from (view 0): the naive one-pixel kernel,
     # the two-pixel kernel with no warp reduction (SW-B at t = 33: every lane
     # issues its own REDs), and SW-B at the tuned t (PAPER.md:1481-1504 loop)
+    # -- and the per-lane REDs as one scalar RED per param (DW_VEC_RED=0: the
+    # two-pixel layout alone) or as 3-4 aligned vector REDs per row
+    os.environ["DW_VEC_RED"] = "0"
+    x2_scalar = time_view(0, wr.Policy(wr.PolicyKind.sw_b, 33), reps=5)
+    os.environ.pop("DW_VEC_RED", None)
     dec = {"native_1px_ms": time_view(0, wr.Policy(wr.PolicyKind.native, 0), reps=5),
+           "x2_no_reduction_scalar_red_ms": x2_scalar,
            "x2_no_reduction_ms": time_view(0, wr.Policy(wr.PolicyKind.sw_b, 33), reps=5),
            "sw_b_tuned_ms": time_view(0, policy, reps=5)}
-    dec["layout_factor"] = dec["native_1px_ms"] / dec["x2_no_reduction_ms"]
+    dec["layout_factor"] = dec["native_1px_ms"] / dec["x2_no_reduction_scalar_red_ms"]
+    dec["vector_red_factor"] = dec["x2_no_reduction_scalar_red_ms"] / dec["x2_no_reduction_ms"]
     dec["distwar_factor"] = dec["x2_no_reduction_ms"] / dec["sw_b_tuned_ms"]
     dec["total_factor"] = dec["native_1px_ms"] / dec["sw_b_tuned_ms"]
+    dec["_note"] = ("native one-pixel kernel -> two-pixel packed-FP32 kernel with no warp "
+                    "reduction (t = 33) and scalar per-lane REDs -> the same with the per-lane "
+                    "REDs as aligned vector REDs -> SW-B at the tuned t")
 
     # ---- the step's one exchange, timed alone: NCCL all-reduce
     # of grad[P, 9] fp32, device events, max over ranks; bus bandwidth uses

@@ -33,7 +33,8 @@
 #include <cstdint>
 
 // Per-lane fallback of the rasterizer's SW-B as vector REDs (red_row9); 0 = one
-// scalar RED per param (the A/B baseline).
+// scalar RED per param (the A/B baseline; also selectable at run time,
+// DW_VEC_RED=0 in the environment, for bench.py's speed-up decomposition).
 #ifndef DW_VEC_RED
 #define DW_VEC_RED 1
 #endif
@@ -247,7 +248,7 @@ __device__ __forceinline__ void reduce_bfly(int idx, float* grad, float (&v)[N],
 // so the reducing path multiplies once after the butterfly (`lane_scale` =
 // scale[slot], precomputed per lane) and only the per-lane fallback scales all
 // N values. Same request semantics as reduce_bfly<N, COUNT, true>.
-template <int N, bool COUNT>
+template <int N, bool COUNT, bool VEC = DW_VEC_RED != 0>
 __device__ __forceinline__ void reduce_bfly_scaled(int idx, float* grad, float (&v)[N], int thr,
                                                    bool active, int lane, uint32_t& nred,
                                                    unsigned ballot, int slot, bool issuer,
@@ -264,15 +265,12 @@ __device__ __forceinline__ void reduce_bfly_scaled(int idx, float* grad, float (
     }
   } else if (active) {
     float* base = grad + static_cast<int64_t>(idx) * N;
-#if DW_VEC_RED
-    if constexpr (N == 9) {
+    if constexpr (VEC && N == 9) {
       float sv[9];
 #pragma unroll
       for (int p = 0; p < 9; ++p) sv[p] = v[p] * scale[p];
       red_row9(base, sv);
-    } else
-#endif
-    {
+    } else {
 #pragma unroll
       for (int p = 0; p < N; ++p) red_add(base + p, v[p] * scale[p]);
     }

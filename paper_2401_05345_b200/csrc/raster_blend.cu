@@ -28,6 +28,8 @@
 // are all inactive for a Gaussian (ballot == 0) issues nothing, as the
 // reference policies emit no request for an empty active mask
 // (reducers.cpp:154-156).
+#include <cstdlib>
+
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -483,7 +485,7 @@ __global__ void DW_FWD_BOUNDS
 // gradients before the warp runs the DISTWAR policy on the lane sums, so the
 // mask / ballot / staging overhead and the warp reduction are paid once per
 // 64 pixels.
-template <int POL, bool COUNT, bool TAP = false, bool BULK = false>
+template <int POL, bool COUNT, bool TAP = false, bool BULK = false, bool VEC = DW_VEC_RED != 0>
 __global__ void __launch_bounds__(128, (POL == kSwB && !COUNT && !TAP) ? DW_SWB_MIN_BLOCKS
                                                                       : DW_MULTI_MIN_BLOCKS)
     k_backward_x2(const CamParams cam, const uint2* __restrict__ ranges,
@@ -721,8 +723,8 @@ __global__ void __launch_bounds__(128, (POL == kSwB && !COUNT && !TAP) ? DW_SWB_
           reduce_bfly<kNParam, COUNT, true>(id, grad, v, thr, act, lane, nred, ballot, slot,
                                             issuer);
         } else if (POL == kSwB) {
-          reduce_bfly_scaled<kNParam, COUNT>(id, grad, v, thr, act, lane, nred, ballot, slot,
-                                             issuer, lane_scale, scale);
+          reduce_bfly_scaled<kNParam, COUNT, VEC>(id, grad, v, thr, act, lane, nred, ballot,
+                                                  slot, issuer, lane_scale, scale);
         } else if (POL == kSwS) {
           reduce_serial<kNParam, COUNT>(id, grad, v, thr, act, lane, nred, ballot, slot, issuer);
         } else {
@@ -735,6 +737,13 @@ __global__ void __launch_bounds__(128, (POL == kSwB && !COUNT && !TAP) ? DW_SWB_
     flush_count(counters, npairs, lane);
     flush_count(counters + 1, nred, lane);
   }
+}
+
+// DW_VEC_RED=0 in the environment (read per launch): the SW-B per-lane
+// fallback as one scalar RED per param -- bench.py's decomposition arm
+bool scalar_fallback() {
+  const char* e = std::getenv("DW_VEC_RED");
+  return e && *e == '0';
 }
 
 template <int POL>
@@ -753,6 +762,10 @@ void launch_bwd(bool count, const CamParams& cam, const uint2* ranges, const uin
     else if (packed)
       launch_pdl(k_backward_x2<POL, false, false, true>, grid, 128, 0, s, cam, ranges, values,
                  means2D, co, rgb, fT, nc, dL, thr, grad, nullptr, TapBuf{}, tile_order, packed);
+    else if (POL == kSwB && scalar_fallback())  // DW_VEC_RED=0: scalar per-lane REDs
+      launch_pdl(k_backward_x2<POL, false, false, false, false>, grid, 128, 0, s, cam, ranges,
+                 values, means2D, co, rgb, fT, nc, dL, thr, grad, nullptr, TapBuf{}, tile_order,
+                 nullptr);
     else
       launch_pdl(k_backward_x2<POL, false>, grid, 128, 0, s, cam, ranges, values, means2D, co,
                  rgb, fT, nc, dL, thr, grad, nullptr, TapBuf{}, tile_order, nullptr);

@@ -899,7 +899,10 @@ __global__ void __launch_bounds__(1024)
 // row. The segment's rectangles are staged 1,024 at a time; each lane turns
 // one rectangle into the 8-bit mask of the warp's tiles it covers and the warp
 // appends it to each of those tiles' lists by ballot compaction.
-__global__ void __launch_bounds__(256, 4)
+#ifndef DW_DENSE_FILL_MIN_BLOCKS
+#define DW_DENSE_FILL_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(256, DW_DENSE_FILL_MIN_BLOCKS)
     k_dense_fill(int P, const uint2* __restrict__ rects, const int* __restrict__ counts,
                  const uint2* __restrict__ ranges, int tiles_x, int tiles_y, int groups_x,
                  uint32_t* __restrict__ values,
