@@ -464,3 +464,36 @@ def test_tap_on_empty_scene(cuda):
     grad, tr, total = r.render_backward_tap(dL, threshold=0)
     torch.cuda.synchronize()
     assert total == 0 and tr.record_count() == 0 and grad.numel() == 0
+
+
+@pytest.mark.parametrize("thr", [0, 8, 16, 33])
+def test_scalar_and_vector_fallback_agree(cuda, monkeypatch, thr):
+    """The SW-B per-lane path as aligned vector REDs (default) and as one scalar
+    RED per param (DW_VEC_RED=0, bench.py's decomposition arm) add the same
+    floats: equal gradients up to fp32 summation order, on the C2 scene with
+    rows at every 16-byte phase (grad base offset by 0..3 floats)."""
+    import torch
+
+    from paper_2401_05345_b200 import warpred as wr
+    from paper_2401_05345_b200.rasterizer import GaussianRasterizer
+    from paper_2401_05345_b200.scene import make_camera, make_dL_dpixels, make_scene
+
+    P, W, H = 100_000, 800, 800
+    sc = {k: torch.from_numpy(v).to(cuda) for k, v in make_scene(P, W, H, seed=0).items()}
+    dL = torch.from_numpy(make_dL_dpixels(W, H, seed=1)).to(cuda)
+    r = GaussianRasterizer()
+    r.render_forward(*[sc[k] for k in ("means3D", "scales", "rotations", "opacities", "colors")],
+                     make_camera(W, H))
+    pol = wr.Policy(wr.PolicyKind.sw_b, thr)
+    for off in range(4):  # the row phase is (base address / 4 + id) mod 4
+        out = {}
+        for env in ("1", "0"):
+            monkeypatch.setenv("DW_VEC_RED", env)
+            buf = torch.zeros(P * 9 + 4, device=cuda)
+            g = buf[off:off + P * 9].view(P, 9)
+            r.render_backward(dL, pol, grad=g)
+            torch.cuda.synchronize()
+            out[env] = g.double().cpu()
+            assert float(buf[:off].abs().sum()) == 0.0 and float(buf[off + P * 9:].abs().sum()) == 0.0
+        rel = float((out["1"] - out["0"]).norm() / out["0"].norm())
+        assert rel < 1e-6, (thr, off, rel)
