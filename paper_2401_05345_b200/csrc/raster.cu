@@ -163,14 +163,15 @@ struct dw_rasterizer {
   ~dw_rasterizer() {
     void* ps[] = {means2D, depths, radii, conic_opacity, rgb, tiles_touched, offsets, dkey[0],
                   dkey[1], dids[0], dids[1], itile[0], itile[1], ivals[0], ivals[1], ranges,
-                  final_T, n_contrib, tmp, scan_tmp, keys_dbg, counters, live_dev, overflow_dev,
+                  final_T, n_contrib, tmp, scan_tmp, keys_dbg, counters, small_dev,
                   tile_order, rects, diff, area_sorted, seg_scratch, sc_scratch, packed,
-                  branges, bb_cnt, live_c_dev, bb_rect_id};
+                  branges, bb_cnt, bb_rect_id};
     for (void* p : ps)
       if (p) cudaFree(p);
     for (float* p : h_bufs)
       if (p) cudaFree(p);
     if (h_total) cudaFreeHost(h_total);
+    if (h_small) cudaFreeHost(h_small);
     if (st_ev[0])
       for (auto& e : st_ev) cudaEventDestroy(e);
     delete twin;
@@ -184,19 +185,26 @@ struct dw_rasterizer {
   }
 
   // no-sync forward state: live instance count + overflow flag on the device
+  // one device block [live count, live entries, overflow flag] so the host
+  // reads all three with a single copy (and its pinned mirror)
+  unsigned long long* small_dev = nullptr;
+  unsigned long long* h_small = nullptr;
   unsigned long long* live_dev = nullptr;
   unsigned long long* live_c_dev = nullptr;  // block binning: live level-1 entry count
   unsigned int* overflow_dev = nullptr;
+  cudaStream_t last_stream = nullptr;        // stream of the last forward
   bool count_pending = false;  // num_rendered not read back yet (no-sync forward)
 
   void ensure_small(cudaStream_t s) {
     if (!counters) DW_CUDA(cudaMalloc(&counters, 2 * sizeof(unsigned long long)));
     if (!h_total) DW_CUDA(cudaMallocHost(&h_total, sizeof(uint64_t)));
-    if (!live_dev) DW_CUDA(cudaMalloc(&live_dev, sizeof(unsigned long long)));
-    if (!live_c_dev) DW_CUDA(cudaMalloc(&live_c_dev, sizeof(unsigned long long)));
-    if (!overflow_dev) {
-      DW_CUDA(cudaMalloc(&overflow_dev, sizeof(unsigned int)));
-      DW_CUDA(cudaMemsetAsync(overflow_dev, 0, sizeof(unsigned int), s));
+    if (!small_dev) {
+      DW_CUDA(cudaMalloc(&small_dev, 3 * sizeof(unsigned long long)));
+      DW_CUDA(cudaMallocHost(&h_small, 3 * sizeof(unsigned long long)));
+      live_dev = small_dev;
+      live_c_dev = small_dev + 1;
+      overflow_dev = reinterpret_cast<unsigned int*>(small_dev + 2);
+      DW_CUDA(cudaMemsetAsync(small_dev, 0, 3 * sizeof(unsigned long long), s));
     }
   }
 
@@ -277,23 +285,28 @@ struct dw_rasterizer {
   int64_t resolve_count(bool* overflowed) {
     unsigned int ovf = 0;
     if (count_pending) {
-      unsigned long long n = 0;
-      DW_CUDA(cudaMemcpy(&n, live_dev, sizeof(n), cudaMemcpyDeviceToHost));
-      DW_CUDA(cudaMemcpy(&ovf, overflow_dev, sizeof(ovf), cudaMemcpyDeviceToHost));
-      num_rendered = static_cast<int64_t>(n);
+      // one copy on the forward's stream (ordered after its kernels)
+      DW_CUDA(cudaMemcpyAsync(h_small, small_dev, 3 * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, last_stream));
+      DW_CUDA(cudaStreamSynchronize(last_stream));
+      std::memcpy(&ovf, h_small + 2, sizeof(ovf));
+      num_rendered = static_cast<int64_t>(h_small[0]);
       count_pending = false;
       last_overflow = ovf != 0;
+      if (blocked && !last_overflow) last_entries = static_cast<int64_t>(h_small[1]);
     }
     if (overflowed) *overflowed = last_overflow;
     return num_rendered;
   }
   bool last_overflow = false;
+  int64_t last_entries = -1;  // block binning: level-1 entries of the last counted frame
 
   void forward(int32_t P_, const float* means3D, const float* scales, const float* rotations,
                const float* opacities, const float* colors, const dw_camera& c, float* out_color,
                int32_t* radii_out, cudaStream_t s, bool nosync = false,
                bool sticky_overflow = false) {
     last_overflow = false;
+    last_stream = s;
     if (P_ < 0) throw std::invalid_argument("P must be >= 0");
     if (c.width < 1 || c.height < 1) throw std::invalid_argument("camera size must be >= 1");
     if (!(c.tan_fovx > 0.0f) || !(c.tan_fovy > 0.0f))
@@ -418,9 +431,14 @@ struct dw_rasterizer {
           throw std::invalid_argument("no-sync forward needs dw_rasterizer_reserve first");
         n_grid = static_cast<int64_t>(std::min(cap_i[0], cap_i[2]));
         if (block_mode) {
-          dw::launch_bb_clamp(offsets, P, static_cast<uint64_t>(n_grid), live_dev, live_c_dev,
+          // entries <= instances; the level-1 sort's grid is sized from the
+          // last counted frame's entries (+25 %) when known
+          n_entries = last_entries > 0
+                          ? std::min<int64_t>(n_grid, last_entries + last_entries / 4 + 4096)
+                          : n_grid;
+          dw::launch_bb_clamp(offsets, P, static_cast<uint64_t>(n_grid),
+                              static_cast<uint64_t>(n_entries), live_dev, live_c_dev,
                               overflow_dev, sticky_overflow, s);
-          n_entries = n_grid;  // entries <= instances: the same capacity
           nc_dev = live_c_dev;
         } else {
           dw::launch_clamp_total(offsets, P, static_cast<uint64_t>(n_grid), live_dev,
@@ -436,6 +454,7 @@ struct dw_rasterizer {
         if (block_mode) {  // (blocks << 32 | tiles)
           n_entries = static_cast<int64_t>(*h_total >> 32);
           num_rendered = static_cast<int64_t>(*h_total & 0xffffffffull);
+          last_entries = n_entries;
           // the scan wrote the entries into buffers that must hold every
           // instance (the later grows keep them): else grow and rescan
           const bool will_dense =

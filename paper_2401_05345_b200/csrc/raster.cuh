@@ -165,7 +165,8 @@ bool block_binning_fits(int tiles_x, int tiles_y);
 int block_binning_nbx(int tiles_x);  // coarse blocks per row
 int block_binning_blocks(int tiles_x, int tiles_y);
 size_t block_binning_count_words(int tiles_x, int tiles_y);
-void launch_bb_clamp(const uint64_t* offsets, int P, uint64_t cap, unsigned long long* n_live,
+void launch_bb_clamp(const uint64_t* offsets, int P, uint64_t cap, uint64_t entry_cap,
+                     unsigned long long* n_live,
                      unsigned long long* n_entries, unsigned int* overflow, bool sticky,
                      cudaStream_t s);
 // k/v: sort double buffers of >= n_entries (capacity when n_entries_dev is set);

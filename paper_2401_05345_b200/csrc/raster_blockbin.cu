@@ -59,17 +59,18 @@ constexpr int kBBSteps = DW_BB_STEPS;  // 32-entry steps per warp per round (loa
 constexpr uint32_t kEmptyRectBB = 0x0000ff00u;  // y0 = 255 > y1 - 1 = 0
 
 // No-sync sizing for block binning: offsets[P-1] holds (tiles, blocks); the
-// live instance count is the tile total when it fits the reserve (else 0 and
-// the overflow flag), the live entry count the block total (0 on overflow).
+// live instance count is the tile total when it and the block total fit their
+// reserves (else 0 and the overflow flag), the live entry count the block
+// total (0 on overflow). The entry reserve sizes the level-1 sort's grid.
 __global__ void k_bb_clamp(const uint64_t* __restrict__ offsets, int P, uint64_t cap,
-                           unsigned long long* __restrict__ n_live,
+                           uint64_t entry_cap, unsigned long long* __restrict__ n_live,
                            unsigned long long* __restrict__ n_entries,
                            unsigned int* __restrict__ overflow, int sticky) {
   pdl_wait();
   pdl_trigger();
   const uint64_t tot = P > 0 ? offsets[P - 1] : 0;
   const uint64_t tiles = tot & 0xffffffffull, blocks = tot >> 32;
-  const bool fits = tiles <= cap;
+  const bool fits = tiles <= cap && blocks <= entry_cap;
   *n_live = fits ? tiles : 0ull;
   *n_entries = fits ? blocks : 0ull;
   if (!fits) *overflow = 1u;
@@ -364,10 +365,11 @@ size_t block_binning_count_words(int tiles_x, int tiles_y) {
   return static_cast<size_t>(tiles_x) * tiles_y * kBBSplit;
 }
 
-void launch_bb_clamp(const uint64_t* offsets, int P, uint64_t cap, unsigned long long* n_live,
+void launch_bb_clamp(const uint64_t* offsets, int P, uint64_t cap, uint64_t entry_cap,
+                     unsigned long long* n_live,
                      unsigned long long* n_entries, unsigned int* overflow, bool sticky,
                      cudaStream_t s) {
-  launch_pdl(k_bb_clamp, 1, 1, 0, s, offsets, P, cap, n_live, n_entries, overflow,
+  launch_pdl(k_bb_clamp, 1, 1, 0, s, offsets, P, cap, entry_cap, n_live, n_entries, overflow,
              sticky ? 1 : 0);
   DW_CUDA(cudaGetLastError());
 }
