@@ -497,3 +497,40 @@ def test_scalar_and_vector_fallback_agree(cuda, monkeypatch, thr):
             assert float(buf[:off].abs().sum()) == 0.0 and float(buf[off + P * 9:].abs().sum()) == 0.0
         rel = float((out["1"] - out["0"]).norm() / out["0"].norm())
         assert rel < 1e-6, (thr, off, rel)
+
+
+def test_async_forward_entry_reserve_overflow(cuda, monkeypatch):
+    """Block binning's no-sync forward sizes its level-1 sort from the last
+    counted frame's (Gaussian, coarse block) entries + 25 %: a frame whose
+    entries outgrow that (the first frame looks past most of the scene) must
+    raise the overflow flag even with an instance reserve that is large enough,
+    and a counted frame followed by another async one must then render it
+    exactly."""
+    import torch
+
+    from paper_2401_05345_b200.rasterizer import GaussianRasterizer
+    from paper_2401_05345_b200.scene import make_camera, make_scene
+
+    monkeypatch.setenv("DW_BLOCK_BINNING", "1")
+    P, W, H = 200000, 640, 512
+    sc = {k: torch.from_numpy(v).to(cuda) for k, v in make_scene(P, W, H, seed=5).items()}
+    args = [sc[k] for k in ("means3D", "scales", "rotations", "opacities", "colors")]
+    wide, normal = make_camera(W, H, yaw_deg=50.0), make_camera(W, H)  # wide: sees part
+    ref = GaussianRasterizer()
+    img_ref, _, n_ref = ref.render_forward(*args, normal)
+    lists_ref = (ref.buffer("values"), ref.buffer("ranges"))
+    r = GaussianRasterizer()
+    r.render_forward(*args, wide)  # counted: few entries
+    r.reserve(P, W, H, 4 * n_ref)  # instances fit; entries will not
+    img = torch.empty((3, H, W), device=cuda)
+    radii = torch.empty(P, dtype=torch.int32, device=cuda)
+    r.render_forward_async(*args, normal, img, radii)
+    n, ovf = r.instances()
+    assert ovf and n == 0
+    r.render_forward(*args, normal)  # counted again: the entry reserve follows
+    r.render_forward_async(*args, normal, img, radii)
+    n, ovf = r.instances()
+    assert not ovf and n == n_ref
+    assert np.array_equal(r.buffer("values"), lists_ref[0])
+    assert np.array_equal(r.buffer("ranges"), lists_ref[1])
+    assert torch.equal(img, img_ref)
