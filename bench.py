@@ -18,8 +18,9 @@ Gaussians, one 1080p view) is timed beside it (`target_config`).
 
 Printed on rank 0 as ONE JSON line; `value` = all ranks' contributions / the
 max over ranks of the device-timed steps; `e2e` = the same metric through the
-host-buffer C-ABI calls (dw_render_views_host at N = 1; dw_render_views +
-NCCL all-reduce of the device gradient + one D2H at N > 1), the figure to
+host-buffer C-ABI calls (dw_render_views_host at N = 1; at N > 1
+dw_render_views_allreduce: the views, the NCCL all-reduce of the device
+gradient over torch's communicator and one D2H in one call), the figure to
 compare with the reference arm.
 """
 from __future__ import annotations
@@ -366,7 +367,8 @@ def main() -> None:
     from paper_2401_05345_b200 import warpred as wr
     from paper_2401_05345_b200.dist import shard_views, view_parallel_backward
     from paper_2401_05345_b200.rasterizer import (GaussianRasterizer, microbench_red,
-                                                  render_views, render_views_host)
+                                                  nccl_comm_ptr, render_views_allreduce,
+                                                  render_views_host)
     from paper_2401_05345_b200.scene import CONFIGS, make_camera, make_dL_dpixels, make_scene, \
         orbit_cameras
 
@@ -569,13 +571,14 @@ def main() -> None:
     # ---- e2e through the host-buffer C-ABI calls -------------------------
     # per step: pinned H2D of the scene + the rank's dL/dpixel, forward +
     # backward of every view, D2H of the images; N = 1: dw_render_views_host
-    # (gradient D2H inside); N > 1: dw_render_views leaves the gradient in
-    # HBM, NCCL all-reduces it over NVLink, then ONE D2H of the sum
+    # (gradient D2H inside); N > 1: dw_render_views_allreduce -- the views into
+    # a device gradient, the NCCL all-reduce over NVLink (torch's communicator
+    # handed to the C ABI), then ONE D2H of the sum, all inside one C call
     pin = {k: torch.from_numpy(v).pin_memory() for k, v in sc.items()}
     dL_h = torch.stack([d.cpu() for d in dLs]).pin_memory()
     img_h = torch.empty((V, 3, H, W), dtype=torch.float32).pin_memory()
     grad_h = torch.empty((P, 9), dtype=torch.float32).pin_memory()
-    grad_d = torch.empty((P, 9), dtype=torch.float32, device=dev)
+    comm = nccl_comm_ptr() if dist is not None else None
     e2e_r = GaussianRasterizer()
     scene_ptrs = [pin[k].data_ptr() for k in ("means3D", "scales", "rotations", "opacities",
                                                "colors")]
@@ -585,11 +588,8 @@ def main() -> None:
             render_views_host(e2e_r, scene_ptrs, P, cams, dL_h.data_ptr(), policy,
                               img_h.data_ptr(), grad_h.data_ptr(), stream)
         else:
-            render_views(e2e_r, scene_ptrs, P, cams, dL_h.data_ptr(), policy, img_h.data_ptr(),
-                         grad_d, stream)
-            dist.all_reduce(grad_d)
-            grad_h.copy_(grad_d, non_blocking=True)
-            torch.cuda.synchronize()
+            render_views_allreduce(e2e_r, scene_ptrs, P, cams, dL_h.data_ptr(), policy,
+                                   img_h.data_ptr(), grad_h.data_ptr(), comm, stream)
 
     e2e_step()  # warm-up (allocations)
     torch.cuda.synchronize()
@@ -731,7 +731,8 @@ def main() -> None:
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
                     "path": ("dw_render_views_host" if dist is None else
-                             "dw_render_views + NCCL all-reduce of the device gradient + one D2H")
+                             "dw_render_views_allreduce: views into a device gradient + NCCL "
+                             "all-reduce (torch's communicator) + one D2H")
                             + ": pinned H2D scene + V dL/dpixel, forward + backward of V views, "
                               "D2H V images + grad"},
             "allreduce": allreduce,

@@ -295,13 +295,33 @@ dw_status dw_render_views_host(dw_rasterizer* r, int32_t P, const float* means3D
 /* dw_render_views_host with the gradient left in HBM: d_grad is a device
  * buffer of P*9 floats (overwritten, complete when the call returns), so a
  * multi-GPU caller all-reduces it over NVLink before ONE device-to-host copy
- * (SURVEY §8(b) wr_gs_allreduce_grads: the reduction is the caller's NCCL call
- * on this buffer). */
+ * (dw_allreduce_grads, or dw_render_views_allreduce for the whole step). */
 dw_status dw_render_views(dw_rasterizer* r, int32_t P, const float* means3D, const float* scales,
                           const float* rotations, const float* opacities, const float* colors,
                           const dw_camera* cams, int32_t num_views, const float* dL_dpixels,
                           dw_policy_kind policy, int32_t threshold, float* out_images,
                           float* d_grad, void* stream);
+
+/* ----------------------------------------------- multi-GPU exchange (NCCL) */
+/* SURVEY §8(b) wr_gs_allreduce_grads: sum a gradient buffer (count floats,
+ * device, in place) across the ranks of an NCCL communicator on `stream` --
+ * the one exchange of view-parallel training. nccl_comm is a
+ * caller-owned ncclComm_t (e.g. torch's ProcessGroupNCCL._comm_ptr()); the
+ * NCCL library the process already loaded is used (resolved at run time, so
+ * the communicator and the call agree on the library). Returns when the
+ * reduction is enqueued. */
+dw_status dw_allreduce_grads(void* nccl_comm, float* grad, int64_t count, void* stream);
+/* The whole view-parallel step of one rank from host buffers: its views
+ * rendered and back-propagated into d_grad (device, P*9, overwritten), the
+ * buffer summed across nccl_comm, then ONE device-to-host copy into grad
+ * (host, P*9). d_grad may be NULL (an internal buffer is used). */
+dw_status dw_render_views_allreduce(dw_rasterizer* r, int32_t P, const float* means3D,
+                                    const float* scales, const float* rotations,
+                                    const float* opacities, const float* colors,
+                                    const dw_camera* cams, int32_t num_views,
+                                    const float* dL_dpixels, dw_policy_kind policy,
+                                    int32_t threshold, float* out_images, float* d_grad,
+                                    float* grad, void* nccl_comm, void* stream);
 
 /* --------------------------------------------------- roofline microbenchmarks */
 /* Measured f32 RED throughput (REDs/s) for `pattern`: 0 distinct addresses,

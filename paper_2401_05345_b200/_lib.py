@@ -140,6 +140,9 @@ SIGNATURES = {
                                        vp, vp, vp]),
     "dw_render_views": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, vp, i32, vp, C.c_int, i32,
                                   vp, vp, vp]),
+    "dw_allreduce_grads": (C.c_int, [vp, vp, i64, vp]),
+    "dw_render_views_allreduce": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, vp, i32, vp, C.c_int,
+                                            i32, vp, vp, vp, vp, vp]),
     "dw_copy_to_host": (C.c_int, [vp, vp, C.c_size_t]),
     "dw_microbench_red": (C.c_int, [i32, i64, C.POINTER(C.c_double), vp]),
 }

@@ -2,6 +2,8 @@
 // mirrors the reference's capi.cpp:16-44: a thread-local last-error string
 // and an exception -> status mapping in guarded().
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types and enum values only: the symbols are resolved at run time
 
 #include <algorithm>
 #include <cstring>
@@ -33,6 +35,7 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
                        const float* rot, const float* op, const float* col, const dw_camera* cams,
                        int32_t V, const float* dL, int policy, int thr, float* out_images,
                        float* grad, cudaStream_t s, bool grad_on_device);
+float* raster_scratch_grad(dw_rasterizer* r, int32_t P);
 void raster_preprocess_backward(dw_rasterizer* r, const float* means3D, const float* scales,
                                 const float* rotations, const float* grad2d, float* grad3d,
                                 cudaStream_t s);
@@ -620,6 +623,77 @@ dw_status dw_render_views(dw_rasterizer* r, int32_t P, const float* means3D, con
     dw::raster_views_host(r, P, means3D, scales, rotations, opacities, colors, cams, num_views,
                           dL_dpixels, policy, threshold, out_images, d_grad,
                           dw::as_stream(stream), true);
+    return DW_OK;
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+// ncclAllReduce of the NCCL library already loaded in the process (the one
+// that made the caller's communicator: torch bundles its own), else the
+// system's libnccl.so.2.
+using AllReduceFn = ncclResult_t (*)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                                     ncclComm_t, cudaStream_t);
+using ErrStrFn = const char* (*)(ncclResult_t);
+
+struct Nccl {
+  AllReduceFn all_reduce = nullptr;
+  ErrStrFn err = nullptr;
+  Nccl() {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+    if (!h) return;
+    all_reduce = reinterpret_cast<AllReduceFn>(dlsym(h, "ncclAllReduce"));
+    err = reinterpret_cast<ErrStrFn>(dlsym(h, "ncclGetErrorString"));
+  }
+};
+
+void nccl_allreduce(void* comm, float* grad, int64_t count, cudaStream_t s) {
+  static Nccl nccl;
+  if (!nccl.all_reduce) throw std::runtime_error("NCCL (libnccl.so.2) is not available");
+  if (count <= 0) return;
+  const ncclResult_t rc = nccl.all_reduce(grad, grad, static_cast<size_t>(count), ncclFloat32,
+                                          ncclSum, static_cast<ncclComm_t>(comm), s);
+  if (rc != ncclSuccess)
+    throw std::runtime_error(std::string("ncclAllReduce: ") +
+                             (nccl.err ? nccl.err(rc) : std::to_string(static_cast<int>(rc))));
+}
+
+}  // namespace
+
+extern "C" {
+
+dw_status dw_allreduce_grads(void* nccl_comm, float* grad, int64_t count, void* stream) {
+  if (!nccl_comm || (count > 0 && !grad)) return fail_invalid("null argument");
+  return guarded([&] {
+    if (count < 0) throw std::invalid_argument("count must be >= 0");
+    nccl_allreduce(nccl_comm, grad, count, dw::as_stream(stream));
+    return DW_OK;
+  });
+}
+
+dw_status dw_render_views_allreduce(dw_rasterizer* r, int32_t P, const float* means3D,
+                                    const float* scales, const float* rotations,
+                                    const float* opacities, const float* colors,
+                                    const dw_camera* cams, int32_t num_views,
+                                    const float* dL_dpixels, dw_policy_kind policy,
+                                    int32_t threshold, float* out_images, float* d_grad,
+                                    float* grad, void* nccl_comm, void* stream) {
+  if (!r || !cams || !dL_dpixels || !nccl_comm || (P > 0 && !grad) ||
+      (P > 0 && (!means3D || !scales || !rotations || !opacities || !colors)))
+    return fail_invalid("null argument");
+  return guarded([&] {
+    check_policy(policy, threshold);
+    const cudaStream_t s = dw::as_stream(stream);
+    const int64_t n = static_cast<int64_t>(P) * 9;
+    float* dg = d_grad ? d_grad : dw::raster_scratch_grad(r, P);
+    dw::raster_views_host(r, P, means3D, scales, rotations, opacities, colors, cams, num_views,
+                          dL_dpixels, policy, threshold, out_images, dg, s, true);
+    nccl_allreduce(nccl_comm, dg, n, s);
+    if (n > 0) DW_CUDA(cudaMemcpyAsync(grad, dg, n * sizeof(float), cudaMemcpyDeviceToHost, s));
+    DW_CUDA(cudaStreamSynchronize(s));
     return DW_OK;
   });
 }

@@ -802,6 +802,11 @@ void raster_host(dw_rasterizer* r, int32_t P, const float* m, const float* sc, c
 // batch's gradient (overwritten) and stays in HBM -- for a caller that reduces
 // it across GPUs before the one device-to-host copy; otherwise `grad` is host
 // memory and the gradient is copied there.
+// device gradient scratch of the host-buffer paths (host_scratch slot 7)
+float* raster_scratch_grad(dw_rasterizer* r, int32_t P) {
+  return r->host_scratch(7, kNParam * static_cast<size_t>(std::max(P, 1)));
+}
+
 void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float* sc,
                        const float* rot, const float* op, const float* col, const dw_camera* cams,
                        int32_t V, const float* dL, int policy, int thr, float* out_images,

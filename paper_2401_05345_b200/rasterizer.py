@@ -367,6 +367,42 @@ def render_views(rast: "GaussianRasterizer", scene_ptrs, P: int, cams, dL_ptr: i
     return grad
 
 
+def nccl_comm_ptr(group=None) -> int:
+    """The ncclComm_t of a torch.distributed NCCL process group (default: the
+    world), for the C ABI's communicator-aware calls. The communicator is
+    created lazily by torch: one barrier makes sure it exists."""
+    import torch
+    import torch.distributed as dist
+
+    group = group if group is not None else dist.group.WORLD
+    dist.barrier(group=group, device_ids=[torch.cuda.current_device()])
+    backend = group._get_backend(torch.device("cuda"))
+    return int(backend._comm_ptr())
+
+
+def allreduce_grads(grad, comm: int, stream=None):
+    """dw_allreduce_grads: sum a CUDA fp32 gradient tensor in place across the
+    ranks of an NCCL communicator (nccl_comm_ptr) on `stream`."""
+    import torch
+
+    check(lib().dw_allreduce_grads(C.c_void_p(comm), _ptr(grad, "grad", torch.float32),
+                                   grad.numel(), _stream(stream)))
+    return grad
+
+
+def render_views_allreduce(rast: "GaussianRasterizer", scene_ptrs, P: int, cams, dL_ptr: int,
+                           policy: Policy, images_ptr, grad_ptr: int, comm: int, stream=None):
+    """dw_render_views_allreduce: one rank's whole view-parallel step through
+    the C ABI from host buffers -- its views forward + backward into a device
+    gradient, the NCCL all-reduce across `comm`, one D2H into grad_ptr (host,
+    P*9 fp32)."""
+    arr = (_lib.CameraC * len(cams))(*[c.to_c() for c in cams])
+    check(lib().dw_render_views_allreduce(rast.handle, P, *scene_ptrs, arr, len(cams), dL_ptr,
+                                          int(policy.kind), policy.threshold, images_ptr, None,
+                                          grad_ptr, C.c_void_p(comm),
+                                          None if stream is None else _stream(stream)))
+
+
 def microbench_red(pattern: int, ops: int = 1 << 28, stream=None) -> float:
     """Measured REDs/s: 0 distinct, 1 same-address warp, 2 v4, 3 DISTWAR 9-lane."""
     out = C.c_double()
