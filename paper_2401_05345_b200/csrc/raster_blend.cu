@@ -702,7 +702,13 @@ __global__ void __launch_bounds__(128, (POL == kSwB && !COUNT && !TAP) ? DW_SWB_
           const uint32_t cnt = __popc(__ballot_sync(kFull, a0)) + __popc(__ballot_sync(kFull, a1));
           if (lane == 0) npairs += cnt;
         }
-        if (TAP || POL != kSwB) {
+        // SW-S here takes SW-B's path: every lane of the warp walks the same
+        // Gaussian, so SW-S's __match_any_sync grouping (reducers.cpp:95-136)
+        // is provably one group -- all active lanes, reduced iff popc >= t --
+        // which is SW-B's decision and request count (reducers.cpp:138-175);
+        // the counting instantiation keeps reduce_serial and checks exactly that
+        constexpr bool kBflyPath = POL == kSwB || (POL == kSwS && !COUNT);
+        if (TAP || !kBflyPath) {
 #pragma unroll
           for (int p = 0; p < kNParam; ++p) v[p] *= scale[p];
         }
@@ -722,7 +728,7 @@ __global__ void __launch_bounds__(128, (POL == kSwB && !COUNT && !TAP) ? DW_SWB_
           }
           reduce_bfly<kNParam, COUNT, true>(id, grad, v, thr, act, lane, nred, ballot, slot,
                                             issuer);
-        } else if (POL == kSwB) {
+        } else if (kBflyPath) {
           reduce_bfly_scaled<kNParam, COUNT, VEC>(id, grad, v, thr, act, lane, nred, ballot,
                                                   slot, issuer, lane_scale, scale);
         } else if (POL == kSwS) {
