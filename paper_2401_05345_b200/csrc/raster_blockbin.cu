@@ -241,7 +241,10 @@ __global__ void __launch_bounds__(1024)
 constexpr int kBBRound = 32 * kBBWarps * kBBSteps;
 constexpr int kBBBuf = 11264;  // 44 KB: static shared memory stays under 48 KB
 
-__global__ void __launch_bounds__(32 * kBBWarps)
+#ifndef DW_BB_PLACE_MIN_BLOCKS
+#define DW_BB_PLACE_MIN_BLOCKS 4  // <= 32 registers: the 510 CTAs of a 1080p frame in one wave
+#endif
+__global__ void __launch_bounds__(32 * kBBWarps, DW_BB_PLACE_MIN_BLOCKS)
     k_bb_place(const uint2* __restrict__ branges, const uint32_t* __restrict__ brect,
                const uint32_t* __restrict__ bgid, const uint32_t* __restrict__ tcount,
                const uint2* __restrict__ ranges, int tiles_x, int tiles_y, int nbx,
