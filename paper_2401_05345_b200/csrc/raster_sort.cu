@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "distwar.cuh"
@@ -1089,7 +1090,19 @@ constexpr int64_t kBigSortN = int64_t(148) * 4 * 4096;
 #ifndef DW_SORT_BIG_ITEMS
 #define DW_SORT_BIG_ITEMS 8  // A/B on C3: 0.836 vs 0.843 ms forward (16)
 #endif
-inline int sort_items(int64_t n) { return n >= kBigSortN ? DW_SORT_BIG_ITEMS : 4; }
+#ifndef DW_SORT_SMALL_MIN
+#define DW_SORT_SMALL_MIN kBigSortN
+#endif
+inline int sort_items(int64_t n) {
+  // A/B hook: DW_SORT_ITEMS=4/8/16 forces the items per thread
+  static const int forced = [] {
+    const char* e = std::getenv("DW_SORT_ITEMS");
+    const int v = e ? std::atoi(e) : 0;
+    return (v == 4 || v == 8 || v == 16) ? v : 0;
+  }();
+  if (forced) return forced;
+  return n >= DW_SORT_SMALL_MIN ? DW_SORT_BIG_ITEMS : 4;
+}
 
 size_t radix_sort_temp_bytes(int64_t n) {
   const int64_t tiles = (n + 1023) / 1024;  // worst case: 4-item tiles
