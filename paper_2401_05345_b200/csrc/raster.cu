@@ -451,9 +451,9 @@ struct dw_rasterizer {
                                 cudaMemcpyDeviceToHost, s));
         DW_CUDA(cudaStreamSynchronize(s));
         num_rendered = static_cast<int64_t>(*h_total);
-        if (block_mode) {  // (blocks << 32 | tiles)
-          n_entries = static_cast<int64_t>(*h_total >> 32);
-          num_rendered = static_cast<int64_t>(*h_total & 0xffffffffull);
+        if (block_mode) {  // (blocks << 34 | tiles)
+          n_entries = static_cast<int64_t>(*h_total >> dw::kBBTileBits);
+          num_rendered = static_cast<int64_t>(*h_total & dw::kBBTileMask);
           last_entries = n_entries;
           // the scan wrote the entries into buffers that must hold every
           // instance (the later grows keep them): else grow and rescan

@@ -158,6 +158,12 @@ void launch_scatter_binning(int P, const float2* means2D, const int* radii, cons
                             const CamParams& cam, uint32_t* scratch, uint2* ranges,
                             uint32_t* values, unsigned long long* seg_scratch, int64_t seg_half,
                             const unsigned long long* n_dev, cudaStream_t s);
+// Block binning's packed scan value: (coarse-block entries << kBBTileBits) |
+// tile instances -- 34 bits of instances (so a frame past 2^32 instances is
+// detected, not wrapped), 30 of entries.
+constexpr int kBBTileBits = 34;
+constexpr unsigned long long kBBTileMask = (1ull << kBBTileBits) - 1ull;
+
 // Block binning (raster_blockbin.cu): the depth-first lists through coarse
 // 8x4-tile blocks (one sorted entry per (Gaussian, block) instead of the
 // duplicate + two-pass tile sort of every instance).

@@ -69,7 +69,7 @@ __global__ void k_bb_clamp(const uint64_t* __restrict__ offsets, int P, uint64_t
   pdl_wait();
   pdl_trigger();
   const uint64_t tot = P > 0 ? offsets[P - 1] : 0;
-  const uint64_t tiles = tot & 0xffffffffull, blocks = tot >> 32;
+  const uint64_t tiles = tot & kBBTileMask, blocks = tot >> kBBTileBits;
   const bool fits = tiles <= cap && blocks <= entry_cap;
   *n_live = fits ? tiles : 0ull;
   *n_entries = fits ? blocks : 0ull;

@@ -337,7 +337,7 @@ constexpr int kScanTile = kSortThreads * kScanItems;  // 2048 elements
 
 // MODE 0: in[] as is; 1: in[] is a packed tile rectangle (x0 | y0 << 8 |
 // (x1-1) << 16 | (y1-1) << 24, empty: y0 > y1-1) and the scan runs on
-// (coarse 8x4-tile blocks it touches << 32 | tiles it touches) -- both offsets
+// (coarse 8x4-tile blocks it touches << 34 | tiles it touches) -- both offsets
 // of block binning in one pass (raster_blockbin.cu).
 template <int MODE>
 __device__ __forceinline__ unsigned long long scan_widen(uint32_t x) {
@@ -348,7 +348,7 @@ __device__ __forceinline__ unsigned long long scan_widen(uint32_t x) {
     const unsigned long long tiles = static_cast<unsigned long long>((x1 - x0 + 1) * (y1 - y0 + 1));
     const unsigned long long blocks =
         static_cast<unsigned long long>((x1 / 8 - x0 / 8 + 1) * (y1 / 4 - y0 / 4 + 1));
-    return (blocks << 32) | tiles;
+    return (blocks << kBBTileBits) | tiles;
   }
   return x;
 }
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(1024) k_scan_top(unsigned long long* __restric
 // Block binning's level-1 entries (MODE 1): element e (a depth-ordered
 // Gaussian, packed rectangle in[e], id ids[e]) writes (block id, id) for every
 // coarse 8x4-tile block its rectangle touches at its exclusive block offset;
-// only the last element's inclusive (blocks << 32 | tiles) goes to out[n-1].
+// only the last element's inclusive (blocks << 34 | tiles) goes to out[n-1].
 struct ScanEntries {
   const uint32_t* ids = nullptr;
   uint32_t* bkey = nullptr;
@@ -492,7 +492,7 @@ __global__ void DW_SCAN_BOUNDS
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
       const int i = t * kScanItems + k;
-      s_bo[i + (i >> 5)] = static_cast<uint32_t>(run >> 32);
+      s_bo[i + (i >> 5)] = static_cast<uint32_t>(run >> kBBTileBits);
       run += scan_widen<MODE>(v[k]);
       if (e0 + k == n - 1) out[n - 1] = run;
     }
