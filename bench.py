@@ -289,7 +289,7 @@ def emit(line: dict) -> None:
 
 
 # ----------------------------------------------------------------- our arm
-def stage_breakdown(t, cam, P, H, W) -> dict:
+def stage_breakdown(t, cam, P, H, W, prof_key="") -> dict:
     """Per-stage forward times of one view (CUDA events between the stages,
     dw_rasterizer_stage_timing) with each stage's algorithmic bytes and HBM
     fraction; the events serialise the programmatic-dependent launches, so
@@ -345,6 +345,21 @@ def stage_breakdown(t, cam, P, H, W) -> dict:
         out[k] = {"ms": ms, "alg_bytes": alg[k], "GBps": gbs,
                   "hbm_frac": gbs / hbm if gbs else None}
     out["_sum_ms"] = sum(best.values())
+    # the blend's binding roofline: SM instruction issue (warp instructions
+    # per launch from the committed ncu count of this view's blend, over the
+    # event-timed blend stage, vs 148 x 4 issue slots x the max SM clock)
+    fi_path = os.path.join(ROOT, "profiles", "forward_inst.json")
+    fi = json.load(open(fi_path)).get(prof_key) if os.path.exists(fi_path) else None
+    if fi and best.get("blend"):
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+            os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+        clk = peaks.get("sm_max_mhz", 1965.0)
+        ach = fi["k_forward_x2"] / (best["blend"] * 1e-3)
+        out["blend_roofline_issue"] = {
+            "bound": "issue", "achieved": ach, "peak": 148 * 4 * clk * 1e6, "unit": "warp-inst/s",
+            "frac": ach / (148 * 4 * clk * 1e6), "inst_per_launch": fi["k_forward_x2"],
+            "ncu_issue_active_pct": fi.get("issue_active_pct"),
+            "inst_source": f"profiles/forward_inst.json {prof_key}"}
     out["_note"] = ("CUDA events between stages (serialises the PDL chain); blend is "
                     "issue-bound, the others latency/HBM")
     return out
@@ -412,7 +427,9 @@ def main() -> None:
             torch.cuda.synchronize()
             if rep == 1:
                 fwd_ms.append(e0.elapsed_time(e1))
-    stages = stage_breakdown(t, cams[0], P, H, W) if rank == 0 else None
+    stages = (stage_breakdown(t, cams[0], P, H, W,
+                              f"{args.workload}@view{my_views[0]}/{total_views}")
+              if rank == 0 else None)
     grad = torch.zeros((P, 9), dtype=torch.float32, device=dev)
 
     # ---- contributions per step (counting instantiation, untimed) --------
