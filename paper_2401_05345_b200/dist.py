@@ -1,4 +1,4 @@
-"""Data parallelism over camera views (SURVEY.md §8(e)).
+"""Data parallelism over camera views (SURVEY.md §8(e), (f1)).
 
 Every rank owns a contiguous block of the view batch, renders and
 back-propagates its views into ONE local gradient buffer [P, 9] (the backward
@@ -33,3 +33,28 @@ def view_parallel_backward(backward_view: Callable, views: Sequence, grad, group
     if all_reduce and world > 1:
         dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=group)
     return grad
+
+
+def view_parallel_train_step(grads_view: Callable, views: Sequence, grad3d, update: Callable,
+                             group=None, all_reduce: Callable = None):
+    """One data-parallel training step: for this rank's shard
+    of `views`, `grads_view(view, grad3d)` ADDS the view's 3D parameter
+    gradients (render backward + preprocess backward; the preprocess backward
+    is view-dependent, so it runs per view) into grad3d [P, 14]; the ranks sum
+    grad3d with ONE all-reduce; then every rank applies `update(grad3d)` (the
+    optimizer step) to its replica -- identical sums keep the replicas equal.
+    all_reduce (optional): a replacement for torch.distributed.all_reduce,
+    e.g. the C ABI's dw_allreduce_grads over the group's NCCL communicator."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    for i in shard_views(len(views), world, rank):
+        grads_view(views[i], grad3d)
+    if world > 1:
+        if all_reduce is not None:
+            all_reduce(grad3d)
+        else:
+            dist.all_reduce(grad3d, op=dist.ReduceOp.SUM, group=group)
+    update(grad3d)
+    return grad3d

@@ -81,3 +81,65 @@ def test_two_rank_allreduce_equals_single_process(orc):
     mp.start_processes(_worker, args=(2, _free_port(), out), nprocs=2, start_method="spawn")
     for r in (0, 1):
         np.testing.assert_allclose(out[r], want.numpy(), rtol=1e-12, atol=1e-12)
+
+
+def _train_fns(orc, sc, params, state):
+    """CPU oracle stand-ins for the per-rank GPU training step: the view's
+    2D + 3D backward (gs_train_grads) and a float64 Adam on the replica."""
+    from oracle.bindings import Camera as OCam, gs_adam, gs_train_grads
+    from paper_2401_05345_b200.scene import make_dL_dpixels
+
+    def grads_view(cam, grad3d):
+        oc = OCam()
+        cc = cam.to_c()
+        C.memmove(C.byref(oc), C.byref(cc), C.sizeof(oc))
+        seed = int(round((cam.viewmatrix[0, 2] + 1) * 1000))
+        _, g3 = gs_train_grads(orc, sc, oc, make_dL_dpixels(64, 48, seed=seed), threads=2)
+        grad3d += torch.from_numpy(g3)
+
+    def update(grad3d):
+        state["step"] += 1
+        g = grad3d.numpy()
+        gs_adam(orc, params, np.ascontiguousarray(g.reshape(-1)), state["m"], state["v"], 1e-3,
+                0.9, 0.999, 1e-8, state["step"])
+
+    return grads_view, update
+
+
+def _train_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.bindings import Oracle
+    from paper_2401_05345_b200.dist import view_parallel_train_step
+    from paper_2401_05345_b200.scene import make_scene
+
+    sc = make_scene(300, 64, 48, seed=3)
+    params = np.zeros(300 * 14, np.float64)
+    state = {"step": 0, "m": np.zeros_like(params), "v": np.zeros_like(params)}
+    grads_view, update = _train_fns(Oracle(), sc, params, state)
+    grad3d = torch.zeros((300, 14), dtype=torch.float64)
+    view_parallel_train_step(grads_view, _views(), grad3d, update)
+    out[rank] = (grad3d.numpy().copy(), params.copy())
+    dist.destroy_process_group()
+
+
+def test_two_rank_train_step_equals_single_process(orc):
+    """World size 2 over gloo: the summed 3D gradients (per-view preprocess
+    backward before the one all-reduce) and the replicas after the optimizer
+    step equal the single-process step over all views, on both ranks."""
+    from paper_2401_05345_b200.dist import view_parallel_train_step
+    from paper_2401_05345_b200.scene import make_scene
+
+    sc = make_scene(300, 64, 48, seed=3)
+    params = np.zeros(300 * 14, np.float64)
+    state = {"step": 0, "m": np.zeros_like(params), "v": np.zeros_like(params)}
+    grads_view, update = _train_fns(orc, sc, params, state)
+    want_g = torch.zeros((300, 14), dtype=torch.float64)
+    view_parallel_train_step(grads_view, _views(), want_g, update)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_train_worker, args=(2, _free_port(), out), nprocs=2, start_method="spawn")
+    for r in (0, 1):
+        g, p = out[r]
+        np.testing.assert_allclose(g, want_g.numpy(), rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(p, params, rtol=1e-12, atol=1e-15)
