@@ -538,9 +538,11 @@ def test_async_forward_entry_reserve_overflow(cuda, monkeypatch):
 
 def test_block_binning_concentrated_scene(cuda, monkeypatch):
     """A scene packed into the middle tenth of the image (a handful of coarse
-    blocks hold every entry: block lists far above one staging round, rounds
-    whose output overflows the shared staging buffer and takes the direct-store
-    path): block binning gives the duplicate + tile-sort lists bit for bit."""
+    blocks hold every entry: block lists of many staging rounds, the other
+    blocks empty): block binning gives the duplicate + tile-sort lists bit for
+    bit. (Rounds whose output overflows the staging buffer -- the direct-store
+    path -- are exercised by the large-Gaussian scene of
+    test_binning_paths_agree_on_long_lists.)"""
     import torch
 
     from paper_2401_05345_b200.rasterizer import GaussianRasterizer
