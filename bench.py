@@ -382,11 +382,13 @@ def main() -> None:
     from paper_2401_05345_b200 import warpred as wr
     from paper_2401_05345_b200.dist import shard_views, view_parallel_backward
     from paper_2401_05345_b200.rasterizer import (GaussianRasterizer, microbench_red,
-                                                  nccl_comm_ptr, render_views_allreduce,
-                                                  render_views_host)
+                                                  nccl_comm_ptr, render_views,
+                                                  render_views_allreduce, render_views_host)
     from paper_2401_05345_b200.scene import CONFIGS, make_camera, make_dL_dpixels, make_scene, \
         orbit_cameras
 
+    if os.environ.get("DW_BENCH_BACKEND", "nccl") != "nccl":
+        local %= torch.cuda.device_count()  # the test hook's ranks may share a GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
@@ -394,7 +396,14 @@ def main() -> None:
     if world > 1 or os.environ.get("DW_BENCH_FORCE_DIST") == "1":
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        # DW_BENCH_BACKEND=gloo: a test hook that runs the multi-rank logic with
+        # several ranks on ONE GPU (NCCL refuses duplicate GPUs); timings from
+        # such a run are not scaling numbers
+        backend = os.environ.get("DW_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     P, W, H, hc, cfg_views = CONFIGS[args.workload]
     weak = args.views_per_gpu > 0
@@ -597,7 +606,10 @@ def main() -> None:
     dL_h = torch.stack([d.cpu() for d in dLs]).pin_memory()
     img_h = torch.empty((V, 3, H, W), dtype=torch.float32).pin_memory()
     grad_h = torch.empty((P, 9), dtype=torch.float32).pin_memory()
-    comm = nccl_comm_ptr() if dist is not None else None
+    use_nccl_abi = dist is not None and dist.get_backend() == "nccl"
+    comm = nccl_comm_ptr() if use_nccl_abi else None
+    grad_d = torch.empty((P, 9), dtype=torch.float32, device=dev) if (
+        dist is not None and not use_nccl_abi) else None
     e2e_r = GaussianRasterizer()
     scene_ptrs = [pin[k].data_ptr() for k in ("means3D", "scales", "rotations", "opacities",
                                                "colors")]
@@ -606,9 +618,15 @@ def main() -> None:
         if dist is None:
             render_views_host(e2e_r, scene_ptrs, P, cams, dL_h.data_ptr(), policy,
                               img_h.data_ptr(), grad_h.data_ptr(), stream)
-        else:
+        elif use_nccl_abi:
             render_views_allreduce(e2e_r, scene_ptrs, P, cams, dL_h.data_ptr(), policy,
                                    img_h.data_ptr(), grad_h.data_ptr(), comm, stream)
+        else:  # non-NCCL test backend: device gradient, torch all-reduce, one D2H
+            render_views(e2e_r, scene_ptrs, P, cams, dL_h.data_ptr(), policy, img_h.data_ptr(),
+                         grad_d, stream)
+            dist.all_reduce(grad_d)
+            grad_h.copy_(grad_d)
+            torch.cuda.synchronize()
 
     e2e_step()  # warm-up (allocations)
     torch.cuda.synchronize()
@@ -717,7 +735,9 @@ def main() -> None:
             "config": {"workload": args.workload, "gaussians": P, "width": W, "height": H,
                        "views_total": total_views, "views_per_gpu": V,
                        "policy": "sw_b", "threshold": thr,
-                       "parallelism": f"dp{world} (views) + NCCL all-reduce of grad[P,9]"
+                       "parallelism": f"dp{world} (views) + "
+                                      f"{(dist.get_backend() if dist else 'nccl').upper()} "
+                                      f"all-reduce of grad[P,9]"
                        if world > 1 else "dp1",
                        "l2": "flushed between steps (256 MiB write, outside the events)"},
             "gpu_launches": args.steps * V,
