@@ -117,6 +117,9 @@ int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* 
                      const uint32_t* gather_src = nullptr, uint32_t* gather_out = nullptr);
 void inclusive_scan_gather(const uint32_t* in, const uint32_t* order, int64_t n, uint64_t* out,
                            void* temp, cudaStream_t s, int mode = 0);
+// after radix_sort_pairs(..., n, ..., temp): the last pass's 256 digit totals
+// (device; live elements only)
+const uint32_t* radix_sort_digit_totals(const void* temp, int64_t n);
 // Block binning's level-1 entries in one scan: over the depth-ordered packed
 // rectangles (launch_preprocess rect_out, laid out by the depth sort), the
 // inclusive (coarse blocks << 32 | tiles touched) -- its total to out[n-1] --

@@ -129,15 +129,34 @@ __device__ __forceinline__ uint32_t block_cover(uint32_t pr, int bx, int by) {
 // t. Per-(half, tile) totals go to tcount (the tile ranges and pass 2's start
 // positions).
 __global__ void __launch_bounds__(32 * kBBWarps)
-    k_bb_count(const uint2* __restrict__ branges, const uint32_t* __restrict__ brect, int tiles_x,
-               int tiles_y, int nbx, uint32_t* __restrict__ tcount) {
+    k_bb_count(uint2* __restrict__ branges, const uint32_t* __restrict__ digit_totals,
+               const uint32_t* __restrict__ brect, int tiles_x, int tiles_y, int nbx,
+               uint32_t* __restrict__ tcount) {
   pdl_wait();
   pdl_trigger();
   __shared__ uint32_t s_c[kBBWarps][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int b = blockIdx.x / kBBSplit, half = blockIdx.x % kBBSplit, seg = half * kBBWarps + w;
   const int bx = b % nbx, by = b / nbx;
-  const uint2 br = branges[b];
+  uint2 br;
+  if (digit_totals) {
+    // one-pass entry sort (<= 256 blocks): its digit totals are the block
+    // sizes, so the block's range is their prefix -- no search over the entries
+    const uint32_t x = (threadIdx.x < 256) ? digit_totals[threadIdx.x] : 0u;
+    uint32_t below = threadIdx.x < b ? x : 0u;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) below += __shfl_xor_sync(kFull, below, o);
+    if (lane == 0) s_c[w][0] = below;
+    __syncthreads();
+    uint32_t start = 0;
+#pragma unroll
+    for (int q = 0; q < kBBWarps; ++q) start += s_c[q][0];
+    br = make_uint2(start, start + digit_totals[b]);
+    __syncthreads();  // s_c is reused below
+    if (half == 0 && threadIdx.x == 0) branges[b] = br;  // for k_bb_place
+  } else {
+    br = branges[b];
+  }
   const uint32_t len = br.y - br.x;
   const uint32_t lo = br.x + static_cast<uint32_t>(static_cast<uint64_t>(len) * seg / kBBSegs);
   const uint32_t hi = br.x + static_cast<uint32_t>(static_cast<uint64_t>(len) * (seg + 1) / kBBSegs);
@@ -198,6 +217,7 @@ __global__ void __launch_bounds__(1024)
     const int tile = r * 1024 + t;
     c[r] = (r < rounds && tile < ntiles) ? tile_total(tcount, tile) : 0u;
   }
+  __shared__ uint32_t s_total;
   auto round = [&](int r, uint32_t v) {
     const int tile = r * 1024 + t;
     uint32_t incl = v;
@@ -208,16 +228,22 @@ __global__ void __launch_bounds__(1024)
     }
     if (lane == 31) s_wsum[w] = incl;
     __syncthreads();
-    uint32_t before = carry + incl - v, total = carry;
+    if (w == 0) {  // exclusive scan of the 32 warp totals
+      const uint32_t x = s_wsum[lane];
+      uint32_t xi = x;
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      const uint32_t x = s_wsum[k];
-      before += k < w ? x : 0u;
-      total += x;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, xi, o);
+        if (lane >= o) xi += y;
+      }
+      s_wsum[lane] = xi - x;
+      if (lane == 31) s_total = xi;
     }
+    __syncthreads();
+    const uint32_t before = carry + s_wsum[w] + incl - v;
     if (tile < ntiles)
       ranges[tile] = (v == 0 || over) ? make_uint2(0u, 0u) : make_uint2(before, before + v);
-    carry = total;
+    carry += s_total;
     __syncthreads();
   };
 #pragma unroll
@@ -392,9 +418,13 @@ void launch_block_binning(const uint32_t* rect_by_id, const CamParams& cam, uint
   // (payload: the packed rectangle), block ranges
   const int cur = radix_sort_pairs(k, v, n_entries, bits, sort_tmp, s, n_entries_dev, rect_by_id,
                                    brect);
-  launch_ranges_u32(n_entries, k[cur], branges, nblocks, s, n_entries_dev);
+  // block ranges: from the digit totals of a one-pass sort (<= 256 blocks, in
+  // k_bb_count), else by search over the sorted block ids
+  const uint32_t* totals = bits <= 8 ? radix_sort_digit_totals(sort_tmp, n_entries) : nullptr;
+  if (!totals) launch_ranges_u32(n_entries, k[cur], branges, nblocks, s, n_entries_dev);
   // level 2: counts, tile ranges, appends
-  launch_pdl(k_bb_count, static_cast<unsigned>(nblocks * kBBSplit), 32 * kBBWarps, 0, s, branges, brect,
+  launch_pdl(k_bb_count, static_cast<unsigned>(nblocks * kBBSplit), 32 * kBBWarps, 0, s, branges,
+             totals, brect,
              cam.tiles_x, cam.tiles_y, nbx, tcount);
   launch_pdl(k_bb_tile_ranges, 1, 1024, 0, s, tcount, ntiles, ranges, n_live);
   launch_pdl(k_bb_place, static_cast<unsigned>(nblocks * kBBSplit), 32 * kBBWarps, 0, s, branges, brect,

@@ -1191,6 +1191,12 @@ int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* 
   return cur;
 }
 
+const uint32_t* radix_sort_digit_totals(const void* temp, int64_t n) {
+  const int64_t tile_n = static_cast<int64_t>(sort_items(n)) * kSortThreads;
+  const int64_t tiles = (n + tile_n - 1) / tile_n;
+  return static_cast<const uint32_t*>(temp) + static_cast<size_t>(tiles) * 256;
+}
+
 void inclusive_scan_gather(const uint32_t* in, const uint32_t* order, int64_t n, uint64_t* out,
                            void* temp, cudaStream_t s, int mode) {
   if (n <= 0) return;
