@@ -110,7 +110,9 @@ struct dw_rasterizer {
   uint2* branges = nullptr;        // block binning: coarse block ranges
   uint32_t* bb_cnt = nullptr;      // block binning: per-(warp, tile) counts + tile totals
   uint32_t* bb_rect_id = nullptr;  // block binning: packed rectangle by Gaussian id
-  size_t cap_br = 0, cap_bbc = 0, cap_bri = 0;
+  uint32_t* bb_hist = nullptr;     // block binning, fused level 1: per-(block, tile) counts
+  size_t cap_br = 0, cap_bbc = 0, cap_bri = 0, cap_bbh = 0;
+  bool bb_fused = false;           // fused level 1 (DW_BB_FUSED=1, <= 256 blocks)
   int* diff = nullptr;             // dense binning: per-segment difference grids + offsets
   size_t cap_r = 0, cap_diff = 0;
   float* final_T = nullptr;
@@ -165,7 +167,7 @@ struct dw_rasterizer {
                   dkey[1], dids[0], dids[1], itile[0], itile[1], ivals[0], ivals[1], ranges,
                   final_T, n_contrib, tmp, scan_tmp, keys_dbg, counters, small_dev,
                   tile_order, rects, diff, area_sorted, seg_scratch, sc_scratch, packed,
-                  branges, bb_cnt, bb_rect_id};
+                  branges, bb_cnt, bb_rect_id, bb_hist};
     for (void* p : ps)
       if (p) cudaFree(p);
     for (float* p : h_bufs)
@@ -219,6 +221,12 @@ struct dw_rasterizer {
   // offsets[P-1]. bb_entry_cap: the entries those buffers held.
   uint64_t bb_entry_cap = 0;
   void bb_entries_scan(cudaStream_t s, bool skip_entries) {
+    if (bb_fused) {  // counts only: the entries are written after the buffers are sized
+      bb_entry_cap = ~uint64_t(0);
+      DW_CUDA(cudaMemsetAsync(offsets + P - 1, 0, sizeof(uint64_t), s));
+      dw::launch_bb_hist(area_sorted, P, cam, bb_hist, offsets + P - 1, s);
+      return;
+    }
     // (a frame expected to take dense binning writes no entries; should it
     // not, the synced path rescans)
     bb_entry_cap = skip_entries ? 0 : static_cast<uint64_t>(std::min(cap_i[0], cap_i[2]));
@@ -271,6 +279,8 @@ struct dw_rasterizer {
       grow(branges, cap_br, static_cast<size_t>(dw::block_binning_blocks(tx, ty)));
       grow(bb_cnt, cap_bbc, dw::block_binning_count_words(tx, ty));
       grow(bb_rect_id, cap_bri, np);
+      if (dw::block_binning_blocks(tx, ty) <= 256)
+        grow(bb_hist, cap_bbh, dw::block_binning_hist_words(P_));
     }
     ensure_tmp(std::max(dw::radix_sort_temp_bytes(P_),
                         dw::radix_sort_temp_bytes(static_cast<int64_t>(std::min(cap_i[0], cap_i[2])))));
@@ -382,7 +392,14 @@ struct dw_rasterizer {
     const char* bulk_env = std::getenv("DW_BULK_STAGING");
     bulk = bulk_env && *bulk_env == '1';
     if (bulk) grow(packed, cap_pk, 3 * np);
-    if (block_mode) grow(bb_rect_id, cap_bri, np);
+    if (block_mode) {
+      const char* fe = std::getenv("DW_BB_FUSED");
+      // (not kept by default: the per-entry shared-memory atomics of its two
+      // counting sweeps cost what the radix pass saved -- profiles/r02/ab/bb_fused.md)
+      bb_fused = fe && *fe == '1' && dw::block_binning_blocks(cam.tiles_x, cam.tiles_y) <= 256;
+      grow(bb_rect_id, cap_bri, np);
+      if (bb_fused) grow(bb_hist, cap_bbh, dw::block_binning_hist_words(P));
+    }
     dw::launch_preprocess(P, means3D, scales, rotations, opacities, colors, cam, means2D, depths,
                           radii, conic_opacity, rgb, tiles_touched, keys_ready ? dkey[0] : nullptr,
                           keys_ready ? dids[0] : nullptr, s, bulk ? packed : nullptr,
@@ -432,8 +449,9 @@ struct dw_rasterizer {
         n_grid = static_cast<int64_t>(std::min(cap_i[0], cap_i[2]));
         if (block_mode) {
           // entries <= instances; the level-1 sort's grid is sized from the
-          // last counted frame's entries (+25 %) when known
-          n_entries = last_entries > 0
+          // last counted frame's entries (+25 %) when known (fused: no sort,
+          // the entries need only fit the buffers)
+          n_entries = last_entries > 0 && !bb_fused
                           ? std::min<int64_t>(n_grid, last_entries + last_entries / 4 + 4096)
                           : n_grid;
           dw::launch_bb_clamp(offsets, P, static_cast<uint64_t>(n_grid),
@@ -507,11 +525,18 @@ struct dw_rasterizer {
       grow(branges, cap_br, static_cast<size_t>(nb));
       grow(bb_cnt, cap_bbc, dw::block_binning_count_words(cam.tiles_x, cam.tiles_y));
       grow(seg_scratch, cap_seg, 2 * static_cast<size_t>(std::max<int64_t>(n_grid, 1)));
-      ensure_tmp(dw::radix_sort_temp_bytes(std::max<int64_t>(n_entries, 1)));
       // the sorted entries' rectangles land in seg_scratch (>= n_grid >= entries words)
-      dw::launch_block_binning(bb_rect_id, cam, itile, ivals, n_entries, tmp,
-                               reinterpret_cast<uint32_t*>(seg_scratch), branges, bb_cnt, ranges,
-                               &vals, n_dev, nc_dev, s);
+      if (bb_fused) {
+        dw::launch_block_binning_fused(area_sorted, order, P, cam, bb_hist, ivals,
+                                       static_cast<uint64_t>(n_grid),
+                                       reinterpret_cast<uint32_t*>(seg_scratch), branges, bb_cnt,
+                                       ranges, &vals, n_dev, nc_dev, s);
+      } else {
+        ensure_tmp(dw::radix_sort_temp_bytes(std::max<int64_t>(n_entries, 1)));
+        dw::launch_block_binning(bb_rect_id, cam, itile, ivals, n_entries, tmp,
+                                 reinterpret_cast<uint32_t*>(seg_scratch), branges, bb_cnt,
+                                 ranges, &vals, n_dev, nc_dev, s);
+      }
       tiles_sorted = nullptr;
       blocked = true;
     } else if (n_grid > 0) {

@@ -120,6 +120,23 @@ void inclusive_scan_gather(const uint32_t* in, const uint32_t* order, int64_t n,
 // after radix_sort_pairs(..., n, ..., temp): the last pass's 256 digit totals
 // (device; live elements only)
 const uint32_t* radix_sort_digit_totals(const void* temp, int64_t n);
+// per row d of counts[256][tiles]: exclusive scan over the tiles in place and
+// the row total to digit_total[d]
+void launch_scan_rows(uint32_t* counts, int64_t tiles, uint32_t* digit_total, cudaStream_t s);
+// Block binning, fused level 1 (<= 256 coarse blocks): k_bb_hist counts each
+// 2,048-Gaussian tile's entries per block into hist[256][tiles] and adds the
+// frame's packed total (blocks << 34 | tiles) into *total (zeroed by the
+// caller); launch_block_binning_fused then writes the entries straight to
+// their block-sorted positions instead of generating and radix-sorting them.
+size_t block_binning_hist_words(int64_t P);
+void launch_bb_hist(const uint32_t* rect_sorted, int64_t P, const CamParams& cam, uint32_t* hist,
+                    uint64_t* total, cudaStream_t s);
+void launch_block_binning_fused(const uint32_t* rect_sorted, const uint32_t* order, int64_t P,
+                                const CamParams& cam, uint32_t* hist, uint32_t* v[2],
+                                uint64_t entry_cap, uint32_t* brect, uint2* branges,
+                                uint32_t* cnt, uint2* ranges, uint32_t** values_out,
+                                const unsigned long long* n_live,
+                                const unsigned long long* n_entries_dev, cudaStream_t s);
 // Block binning's level-1 entries in one scan: over the depth-ordered packed
 // rectangles (launch_preprocess rect_out, laid out by the depth sort), the
 // inclusive (coarse blocks << 32 | tiles touched) -- its total to out[n-1] --

@@ -33,6 +33,8 @@
 // (y1-1) << 24, tile units < 256), so the path needs tiles_x, tiles_y <= 255.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "distwar.cuh"
 #include "dw_internal.h"
 #include "raster.cuh"
@@ -378,6 +380,211 @@ __global__ void __launch_bounds__(32 * kBBWarps, DW_BB_PLACE_MIN_BLOCKS)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused level 1 (<= 256 coarse blocks). The entries of a tile of 2,048
+// depth-ordered Gaussians go straight to their positions in the block-sorted
+// order -- block start (prefix of the block totals) + the earlier tiles'
+// entries of that block (hist, scanned over tiles) + the rank inside the tile
+// (warp, then entry order: the stable order of the radix pass this replaces).
+constexpr int kFuseItems = 8;
+constexpr int kFuseTile = 256 * kFuseItems;
+constexpr int kFuseCap = 4096;  // staged entries per tile (else direct stores)
+
+__device__ __forceinline__ void rect_blocks(uint32_t x, int* bx0, int* by0, int* bw, int* nb) {
+  const int x0 = (int)(x & 0xffu), y0 = (int)((x >> 8) & 0xffu);
+  const int x1 = (int)((x >> 16) & 0xffu), y1 = (int)(x >> 24);
+  *bx0 = x0 / kBBW;
+  *by0 = y0 / kBBH;
+  *bw = x1 / kBBW - *bx0 + 1;
+  *nb = y0 > y1 ? 0 : *bw * (y1 / kBBH - *by0 + 1);
+}
+
+__global__ void __launch_bounds__(256)
+    k_bb_hist(const uint32_t* __restrict__ rect_sorted, int64_t n, int nbx, int64_t tiles,
+              uint32_t* __restrict__ hist, unsigned long long* __restrict__ total) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ uint32_t s_h[256];
+  __shared__ unsigned long long s_w[8];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  s_h[t] = 0u;
+  __syncthreads();
+  const int64_t tile0 = static_cast<int64_t>(blockIdx.x) * kFuseTile;
+  unsigned long long mine = 0;
+#pragma unroll
+  for (int k = 0; k < kFuseItems; ++k) {
+    const int64_t e = tile0 + k * 256 + t;
+    if (e >= n) break;
+    const uint32_t x = __ldg(rect_sorted + e);
+    int bx0, by0, bw, nb;
+    rect_blocks(x, &bx0, &by0, &bw, &nb);
+    if (nb == 0) continue;
+    const int area = ((int)((x >> 16) & 0xffu) - (int)(x & 0xffu) + 1) *
+                     ((int)(x >> 24) - (int)((x >> 8) & 0xffu) + 1);
+    mine += (static_cast<unsigned long long>(nb) << kBBTileBits) | static_cast<unsigned>(area);
+    for (int q = 0; q < nb; ++q)
+      atomicAdd(&s_h[(by0 + q / bw) * nbx + bx0 + q % bw], 1u);
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) mine += __shfl_xor_sync(kFull, mine, o);
+  if (lane == 0) s_w[w] = mine;
+  __syncthreads();
+  if (t == 0) {
+    unsigned long long a = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a += s_w[q];
+    if (a) atomicAdd(total, a);
+  }
+  hist[static_cast<int64_t>(t) * tiles + blockIdx.x] = s_h[t];
+}
+
+__global__ void __launch_bounds__(256)
+    k_bb_emit(const uint32_t* __restrict__ rect_sorted, const uint32_t* __restrict__ order,
+              int64_t n, int nbx, int64_t tiles, const uint32_t* __restrict__ hist,
+              const uint32_t* __restrict__ block_totals, uint32_t* __restrict__ bval,
+              uint32_t* __restrict__ brect, const unsigned long long* __restrict__ n_entries,
+              uint64_t cap) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ uint32_t s_cnt[8][256];  // per (warp, block): count -> next staging position
+  __shared__ uint32_t s_bstart[256];  // start of each block's run in the staging buffer
+  __shared__ uint32_t s_gbase[256];   // global position of that run
+  __shared__ uint32_t s_wsum[8], s_dsum[8], s_tot;
+  __shared__ uint32_t s_val[kFuseCap], s_rect[kFuseCap];
+  __shared__ uint8_t s_blk[kFuseCap];
+  if (n_entries && *n_entries == 0ull) return;  // no-sync frame over capacity (or empty)
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  const int64_t g0 = static_cast<int64_t>(blockIdx.x) * kFuseTile + w * 256;  // warp's chunk
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s_cnt[q][t] = 0u;
+  __syncthreads();
+  // sweep 1: this warp's entries per block
+#pragma unroll
+  for (int r = 0; r < kFuseItems; ++r) {
+    const int64_t e = g0 + r * 32 + lane;
+    const uint32_t x = e < n ? __ldg(rect_sorted + e) : kEmptyRectBB;
+    int bx0, by0, bw, nb;
+    rect_blocks(x, &bx0, &by0, &bw, &nb);
+    for (int q = 0; q < nb; ++q) atomicAdd(&s_cnt[w][(by0 + q / bw) * nbx + bx0 + q % bw], 1u);
+  }
+  __syncthreads();
+  // thread t = block t: run of the block in this tile (warp order), the
+  // tile's staging layout (block order) and the global positions
+  uint32_t c[8], tot = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    c[q] = s_cnt[q][t];
+    tot += c[q];
+  }
+  uint32_t incl = tot, dincl = block_totals[t];
+  const uint32_t dtot = dincl;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, incl, o), dy = __shfl_up_sync(kFull, dincl, o);
+    if (lane >= o) {
+      incl += y;
+      dincl += dy;
+    }
+  }
+  if (lane == 31) {
+    s_wsum[w] = incl;
+    s_dsum[w] = dincl;
+  }
+  __syncthreads();
+  uint32_t bstart = incl - tot, dstart = dincl - dtot;
+  for (int q = 0; q < w; ++q) {
+    bstart += s_wsum[q];
+    dstart += s_dsum[q];
+  }
+  s_bstart[t] = bstart;
+  s_gbase[t] = dstart + hist[static_cast<int64_t>(t) * tiles + blockIdx.x];
+  uint32_t run = bstart;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    s_cnt[q][t] = run;
+    run += c[q];
+  }
+  if (t == 255) s_tot = run;
+  __syncthreads();
+  const uint32_t ntot = s_tot;
+  const bool staged = ntot <= static_cast<uint32_t>(kFuseCap);
+  // sweep 2: each round's entries, warp-cooperatively in (Gaussian, block)
+  // order, ranked per block (ballot multi-split) against the warp's cursor
+#pragma unroll 1
+  for (int r = 0; r < kFuseItems; ++r) {
+    const int64_t e = g0 + r * 32 + lane;
+    const uint32_t x = e < n ? __ldg(rect_sorted + e) : kEmptyRectBB;
+    int bx0, by0, bw, nb;
+    rect_blocks(x, &bx0, &by0, &bw, &nb);
+    const uint32_t gid = e < n ? __ldg(order + e) : 0u;
+    int inc = nb;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(kFull, inc, d);
+      if (lane >= d) inc += y;
+    }
+    const int excl = inc - nb, total = __shfl_sync(kFull, inc, 31);
+    for (int q0 = 0; q0 < total; q0 += 32) {
+      const int q = q0 + lane;
+      int owner = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int probe = owner + step;
+        if (__shfl_sync(kFull, excl, probe) <= q) owner = probe;
+      }
+      const int kk = q - __shfl_sync(kFull, excl, owner);
+      const int ow = __shfl_sync(kFull, bw, owner);
+      const int ox = __shfl_sync(kFull, bx0, owner), oy = __shfl_sync(kFull, by0, owner);
+      const uint32_t og = __shfl_sync(kFull, gid, owner), orc = __shfl_sync(kFull, x, owner);
+      const bool valid = q < total;
+      const int row = valid ? kk / ow : 0;
+      const uint32_t blk = valid ? static_cast<uint32_t>((oy + row) * nbx + ox + (kk - row * ow))
+                                 : 0u;
+      unsigned peers = __ballot_sync(kFull, valid);
+      if (!valid) peers = ~peers;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const bool bit = (blk >> b) & 1u;
+        const unsigned m = __ballot_sync(kFull, bit);
+        peers &= bit ? m : ~m;
+      }
+      const int leader = __ffs(peers) - 1;
+      uint32_t base = 0;
+      if (valid && lane == leader) {
+        base = s_cnt[w][blk];
+        s_cnt[w][blk] = base + __popc(peers);
+      }
+      base = __shfl_sync(kFull, base, leader);
+      if (valid) {
+        const uint32_t pos = base + __popc(peers & lt);
+        if (staged) {
+          s_val[pos] = og;
+          s_rect[pos] = orc;
+          s_blk[pos] = static_cast<uint8_t>(blk);
+        } else {
+          const uint64_t g = s_gbase[blk] + (pos - s_bstart[blk]);
+          if (g < cap) {
+            bval[g] = og;
+            brect[g] = orc;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  if (!staged) return;
+  __syncthreads();
+  for (uint32_t i = t; i < ntot; i += 256) {  // each block's run, coalesced
+    const uint32_t b = s_blk[i];
+    const uint64_t g = s_gbase[b] + (i - s_bstart[b]);
+    if (g < cap) {
+      bval[g] = s_val[i];
+      brect[g] = s_rect[i];
+    }
+  }
+}
+
 inline unsigned blocks_of(int64_t n, int per) { return static_cast<unsigned>((n + per - 1) / per); }
 
 }  // namespace
@@ -430,6 +637,43 @@ void launch_block_binning(const uint32_t* rect_by_id, const CamParams& cam, uint
   launch_pdl(k_bb_place, static_cast<unsigned>(nblocks * kBBSplit), 32 * kBBWarps, 0, s, branges, brect,
              v[cur], tcount, ranges, cam.tiles_x, cam.tiles_y, nbx, v[cur ^ 1], n_live);
   *values_out = v[cur ^ 1];
+  DW_CUDA(cudaGetLastError());
+}
+
+size_t block_binning_hist_words(int64_t P) {
+  return static_cast<size_t>((std::max<int64_t>(P, 1) + kFuseTile - 1) / kFuseTile) * 256 + 256;
+}
+
+void launch_bb_hist(const uint32_t* rect_sorted, int64_t P, const CamParams& cam, uint32_t* hist,
+                    uint64_t* total, cudaStream_t s) {
+  if (P <= 0) return;
+  const int64_t tiles = (P + kFuseTile - 1) / kFuseTile;
+  launch_pdl(k_bb_hist, static_cast<unsigned>(tiles), 256, 0, s, rect_sorted, P,
+             block_binning_nbx(cam.tiles_x), tiles, hist,
+             reinterpret_cast<unsigned long long*>(total));
+  DW_CUDA(cudaGetLastError());
+}
+
+void launch_block_binning_fused(const uint32_t* rect_sorted, const uint32_t* order, int64_t P,
+                                const CamParams& cam, uint32_t* hist, uint32_t* v[2],
+                                uint64_t entry_cap, uint32_t* brect, uint2* branges,
+                                uint32_t* cnt, uint2* ranges, uint32_t** values_out,
+                                const unsigned long long* n_live,
+                                const unsigned long long* n_entries_dev, cudaStream_t s) {
+  const int nbx = block_binning_nbx(cam.tiles_x);
+  const int nblocks = block_binning_blocks(cam.tiles_x, cam.tiles_y);
+  const int ntiles = cam.tiles_x * cam.tiles_y;
+  const int64_t tiles = (P + kFuseTile - 1) / kFuseTile;
+  uint32_t* totals = hist + static_cast<size_t>(tiles) * 256;
+  launch_scan_rows(hist, tiles, totals, s);
+  launch_pdl(k_bb_emit, static_cast<unsigned>(tiles), 256, 0, s, rect_sorted, order, P, nbx, tiles,
+             hist, totals, v[1], brect, n_entries_dev, entry_cap);
+  launch_pdl(k_bb_count, static_cast<unsigned>(nblocks * kBBSplit), 32 * kBBWarps, 0, s, branges,
+             static_cast<const uint32_t*>(totals), brect, cam.tiles_x, cam.tiles_y, nbx, cnt);
+  launch_pdl(k_bb_tile_ranges, 1, 1024, 0, s, cnt, ntiles, ranges, n_live);
+  launch_pdl(k_bb_place, static_cast<unsigned>(nblocks * kBBSplit), 32 * kBBWarps, 0, s, branges,
+             brect, v[1], cnt, ranges, cam.tiles_x, cam.tiles_y, nbx, v[0], n_live);
+  *values_out = v[0];
   DW_CUDA(cudaGetLastError());
 }
 

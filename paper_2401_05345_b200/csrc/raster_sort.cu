@@ -1191,6 +1191,11 @@ int radix_sort_pairs(uint32_t* k[2], uint32_t* v[2], int64_t n, int bits, void* 
   return cur;
 }
 
+void launch_scan_rows(uint32_t* counts, int64_t tiles, uint32_t* digit_total, cudaStream_t s) {
+  launch_pdl(k_scan_rows, 256, 1024, 0, s, counts, tiles, digit_total);
+  DW_CUDA(cudaGetLastError());
+}
+
 const uint32_t* radix_sort_digit_totals(const void* temp, int64_t n) {
   const int64_t tile_n = static_cast<int64_t>(sort_items(n)) * kSortThreads;
   const int64_t tiles = (n + tile_n - 1) / tile_n;
