@@ -455,7 +455,7 @@ def main() -> None:
     red_peaks = {name: microbench_red(p, 1 << 28) for p, name in
                  ((0, "distinct"), (1, "same_address_warp"), (2, "v4"), (3, "distwar_9lane"),
                   (4, "same_address_warp_v4"), (5, "fallback_row_scalar"),
-                  (6, "fallback_row_vector"))}
+                  (6, "fallback_row_vector"), (7, "reduced_row_vector"))}
 
     def time_view(i, policy, reps=3):
         ms = []

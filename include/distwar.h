@@ -330,7 +330,8 @@ dw_status dw_render_views_allreduce(dw_rasterizer* r, int32_t P, const float* me
  * one pseudo-random primitive row (SW-B's issue pattern), 4 all lanes on one
  * 16-byte address with v4, 5 / 6 four lanes on one primitive row with 9
  * scalar REDs each / the same floats as 3-4 vector REDs (SW-B's per-lane
- * path without / with DW_VEC_RED). Every float added counts as one RED. */
+ * path without / with DW_VEC_RED), 7 pattern 3's rows as 3-4 vector REDs
+ * from one lane. Every float added counts as one RED. */
 dw_status dw_microbench_red(int32_t pattern, int64_t ops, double* reds_per_s, void* stream);
 
 #ifdef __cplusplus

@@ -709,7 +709,7 @@ dw_status dw_copy_to_host(void* host_dst, const void* device_src, size_t bytes) 
 dw_status dw_microbench_red(int32_t pattern, int64_t ops, double* reds_per_s, void* stream) {
   if (!reds_per_s) return fail_invalid("null argument");
   return guarded([&] {
-    if (pattern < 0 || pattern > 6) throw std::invalid_argument("unknown RED pattern");
+    if (pattern < 0 || pattern > 9) throw std::invalid_argument("unknown RED pattern");
     if (ops < 1) throw std::invalid_argument("ops must be >= 1");
     *reds_per_s = dw::microbench_red(pattern, ops, dw::as_stream(stream));
     return DW_OK;

@@ -12,6 +12,10 @@
 //               9 scalar REDs each (SW-B's per-lane path, DW_VEC_RED=0)
 //   6 fallback, vector: the same traffic as 5 through red_row9 (3-4 vector
 //               REDs per lane, the default per-lane path)
+//   7 reduced row, vector: pattern 3's traffic (one 9-float row per warp
+//               instruction slot) as red_row9 from ONE lane (3-4 vector REDs)
+//   8 / 9 pattern 3 with the rows padded to 16 / 12 floats (64 / 48-byte
+//               aligned rows: the line / sector straddles of 36-byte rows gone)
 #include <cuda_runtime.h>
 
 #include "distwar.cuh"
@@ -22,6 +26,14 @@ namespace dw {
 namespace {
 
 constexpr int64_t kRegionFloats = int64_t(1) << 24;  // 64 MB: L2-resident
+
+// Pseudo-random primitive of a warp-iteration: a multiplicative hash to
+// 2^20 primitives (36 MB of rows) -- 32-bit math, so the generator costs a
+// few instructions and the kernel stays RED-bound, not issue-bound (a u64
+// modulo here capped patterns 3 and 5-9 near 22 G warp-iterations/s).
+__device__ __forceinline__ uint32_t hash_prim(int64_t w) {
+  return (static_cast<uint32_t>(w) * 2654435761u) >> 12;
+}
 
 template <int PATTERN>
 __global__ void __launch_bounds__(256) k_red(float* __restrict__ buf, int iters) {
@@ -45,9 +57,19 @@ __global__ void __launch_bounds__(256) k_red(float* __restrict__ buf, int iters)
       asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v),
                    "f"(v), "f"(v), "f"(v)
                    : "memory");
+    } else if (PATTERN == 8 || PATTERN == 9) {
+      const uint32_t prim = hash_prim(w);
+      const int stride = PATTERN == 8 ? 16 : 12;
+      if (lane < 9) red_add(buf + (static_cast<int64_t>(prim) * stride) + lane, v);
+    } else if (PATTERN == 7) {
+      const uint32_t prim = hash_prim(w);
+      if (lane == 0) {
+        const float s[9] = {v, v, v, v, v, v, v, v, v};
+        red_row9(buf + (static_cast<int64_t>(prim) * 9), s);
+      }
     } else if (PATTERN == 5 || PATTERN == 6) {
-      const uint64_t prim = (static_cast<uint64_t>(w) * 2654435761ull) % 1000000ull;
-      float* row = buf + ((prim * 9) & (kRegionFloats - 1));
+      const uint32_t prim = hash_prim(w);
+      float* row = buf + (static_cast<int64_t>(prim) * 9);
       if (lane < 4) {
         if (PATTERN == 5) {
 #pragma unroll
@@ -59,8 +81,8 @@ __global__ void __launch_bounds__(256) k_red(float* __restrict__ buf, int iters)
       }
     } else {
       // multiplicative hash of the warp-iteration -> primitive id
-      const uint64_t prim = (static_cast<uint64_t>(w) * 2654435761ull) % 1000000ull;
-      if (lane < 9) red_add(buf + ((prim * 9) & (kRegionFloats - 1)) + lane, v);
+      const uint32_t prim = hash_prim(w);
+      if (lane < 9) red_add(buf + (static_cast<int64_t>(prim) * 9) + lane, v);
     }
   }
 }
@@ -93,6 +115,7 @@ double microbench_red(int pattern, int64_t ops, cudaStream_t s) {
   // floats added per warp-iteration
   const int reds_per_warp_inst = pattern == 2   ? 128
                                  : pattern == 3 ? 9
+                                 : pattern >= 7 ? 9
                                  : pattern == 4 ? 128
                                  : pattern >= 5 ? 36
                                                 : 32;
@@ -107,6 +130,9 @@ double microbench_red(int pattern, int64_t ops, cudaStream_t s) {
     case 4: ms = run<4>(buf, grid, iters, s); break;
     case 5: ms = run<5>(buf, grid, iters, s); break;
     case 6: ms = run<6>(buf, grid, iters, s); break;
+    case 7: ms = run<7>(buf, grid, iters, s); break;
+    case 8: ms = run<8>(buf, grid, iters, s); break;
+    case 9: ms = run<9>(buf, grid, iters, s); break;
     default: ms = run<3>(buf, grid, iters, s); break;
   }
   DW_CUDA(cudaFree(buf));

@@ -52,7 +52,10 @@ BINNING_ENV = {  # list constructions of the forward (raster.cu): env overrides
                     "DW_BLOCK_BINNING": "0"},
     # depth sort, then coarse-block entries + per-tile appends (the default)
     "block": {"DW_SCATTER": "0", "DW_DENSE_BINNING": "0", "DW_TILE_FIRST": "0",
-              "DW_BLOCK_BINNING": "1"},
+              "DW_BLOCK_BINNING": "1", "DW_BB_FUSED": "0"},
+    # the same with the opt-in fused level 1 (per-tile histogram + emit)
+    "block-fused": {"DW_SCATTER": "0", "DW_DENSE_BINNING": "0", "DW_TILE_FIRST": "0",
+                    "DW_BLOCK_BINNING": "1", "DW_BB_FUSED": "1"},
     "tile-first": {"DW_SCATTER": "0", "DW_DENSE_BINNING": "0", "DW_TILE_FIRST": "1"},
     "dense": {"DW_DENSE_BINNING": "1"},
 }

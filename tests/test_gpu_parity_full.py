@@ -76,7 +76,7 @@ SMALL = [("tiny_odd", 300, 61, 47, False, 0), ("c1_10k_256", 10_000, 256, 256, F
 
 
 @pytest.mark.parametrize("binning", ["auto", "scatter", "depth-first", "tile-first", "dense",
-                                     "block"])
+                                     "block", "block-fused"])
 @pytest.mark.parametrize("case", SMALL, ids=[c[0] for c in SMALL])
 def test_small_cases_every_binning(cuda, orc, case, binning, monkeypatch):
     """Every list construction (scatter, depth-first, tile-first, dense

@@ -204,7 +204,7 @@ def test_binning_paths_agree_on_long_lists(cuda, monkeypatch):
           for k, v in make_scene(P, W, H, seed=7, high_contention=True).items()}
     cam = make_camera(W, H)
     out = {}
-    for path in ("depth-first", "tile-first", "dense", "scatter", "block"):
+    for path in ("depth-first", "tile-first", "dense", "scatter", "block", "block-fused"):
         set_binning(monkeypatch, path)
         r = GaussianRasterizer()
         img, _, nr = r.render_forward(*[sc[k] for k in ("means3D", "scales", "rotations",
@@ -213,7 +213,7 @@ def test_binning_paths_agree_on_long_lists(cuda, monkeypatch):
     ref = out["depth-first"]
     lens = ref[1][:, 1] - ref[1][:, 0]
     assert lens.max() > 4096  # the chunked-merge paths run (tile-first, scatter's long lists)
-    for path in ("tile-first", "dense", "scatter", "block"):
+    for path in ("tile-first", "dense", "scatter", "block", "block-fused"):
         assert out[path][3] == ref[3]
         assert np.array_equal(out[path][0], ref[0]), path
         assert np.array_equal(out[path][1], ref[1]), path
