@@ -199,6 +199,23 @@ dw_status dw_render_forward_async(dw_rasterizer* r, int32_t P, const float* mean
                                   const dw_camera* cam, float* out_color, int32_t* radii,
                                   void* stream);
 
+/* render_forward of num_views views of one scene stacked into one frame
+ * (1 <= num_views <= dw_rasterizer_max_stacked_views): every launch of the
+ * forward -- projection per view, then one depth sort, one binning, one blend
+ * -- covers all of them, and the next dw_render_backward takes dL_dpixels as
+ * num_views*3*H*W and adds every view's gradients into grad[P*9]. Per-tile
+ * lists equal the single-view lists bit for bit (ids of view v offset by
+ * v*P in the frame). cams: num_views cameras of one image size and one
+ * background; out_images: num_views*3*H*W (device). num_rendered (host,
+ * nullable): instances of the whole frame. Synchronises `stream` once. */
+dw_status dw_render_forward_views(dw_rasterizer* r, int32_t P, const float* means3D,
+                                  const float* scales, const float* rotations,
+                                  const float* opacities, const float* colors,
+                                  const dw_camera* cams, int32_t num_views, float* out_images,
+                                  int64_t* num_rendered, void* stream);
+/* How many views of a width x height image fit one stacked frame. */
+dw_status dw_rasterizer_max_stacked_views(int32_t width, int32_t height, int32_t* out);
+
 /* Pre-size every per-view buffer for up to P Gaussians, a width x height
  * image and max_instances (tile, Gaussian) instances. */
 dw_status dw_rasterizer_reserve(dw_rasterizer* r, int32_t P, int32_t width, int32_t height,

@@ -124,6 +124,9 @@ SIGNATURES = {
     "dw_render_backward": (C.c_int, [vp, vp, C.c_int, i32, vp, C.POINTER(u64), vp]),
     "dw_render_forward_async": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, C.POINTER(CameraC), vp, vp,
                                           vp]),
+    "dw_render_forward_views": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, C.POINTER(CameraC), i32,
+                                          vp, C.POINTER(i64), vp]),
+    "dw_rasterizer_max_stacked_views": (C.c_int, [i32, i32, C.POINTER(i32)]),
     "dw_rasterizer_reserve": (C.c_int, [vp, i32, i32, i32, i64]),
     "dw_rasterizer_num_rendered": (C.c_int, [vp, C.POINTER(i64), C.POINTER(C.c_int)]),
     "dw_rasterizer_last_reds": (C.c_int, [vp, C.POINTER(u64)]),

@@ -20,6 +20,11 @@ namespace dw {
 void raster_forward(dw_rasterizer* r, int32_t P, const float* m, const float* sc, const float* rot,
                     const float* op, const float* col, const dw_camera* cam, float* out,
                     int32_t* radii, int64_t* nr, cudaStream_t s, bool nosync);
+void raster_forward_views(dw_rasterizer* r, int32_t P, const float* m, const float* sc,
+                          const float* rot, const float* op, const float* col,
+                          const dw_camera* cams, int32_t nv, float* out, int64_t* nr,
+                          cudaStream_t s);
+int raster_max_stacked_views(int32_t W, int32_t H);
 void raster_reserve(dw_rasterizer* r, int32_t P, int32_t W, int32_t H, int64_t max_instances);
 int64_t raster_resolve(dw_rasterizer* r, bool* overflowed);
 void raster_backward(dw_rasterizer* r, const float* dL, int policy, int thr, float* grad,
@@ -470,6 +475,30 @@ dw_status dw_render_forward_async(dw_rasterizer* r, int32_t P, const float* mean
   return guarded([&] {
     dw::raster_forward(r, P, means3D, scales, rotations, opacities, colors, cam, out_color, radii,
                        nullptr, dw::as_stream(stream), true);
+    return DW_OK;
+  });
+}
+
+dw_status dw_render_forward_views(dw_rasterizer* r, int32_t P, const float* means3D,
+                                  const float* scales, const float* rotations,
+                                  const float* opacities, const float* colors,
+                                  const dw_camera* cams, int32_t num_views, float* out_images,
+                                  int64_t* num_rendered, void* stream) {
+  if (!r || !cams || !out_images ||
+      (P > 0 && (!means3D || !scales || !rotations || !opacities || !colors)))
+    return fail_invalid("null argument");
+  return guarded([&] {
+    dw::raster_forward_views(r, P, means3D, scales, rotations, opacities, colors, cams, num_views,
+                             out_images, num_rendered, dw::as_stream(stream));
+    return DW_OK;
+  });
+}
+
+dw_status dw_rasterizer_max_stacked_views(int32_t width, int32_t height, int32_t* out) {
+  if (!out) return fail_invalid("null argument");
+  if (width < 1 || height < 1) return fail_invalid("image size must be >= 1");
+  return guarded([&] {
+    *out = dw::raster_max_stacked_views(width, height);
     return DW_OK;
   });
 }

@@ -237,13 +237,16 @@ struct dw_rasterizer {
 
   // Pre-size every buffer (no allocation happens in a later forward/backward
   // that stays within these sizes -- required before CUDA-graph capture).
-  void reserve(int32_t P_, int32_t W_, int32_t H_, int64_t max_instances) {
-    if (P_ < 0 || W_ < 1 || H_ < 1 || max_instances < 0)
+  // nv > 1: for frames of nv stacked views (forward_views) -- P_ scene
+  // Gaussians, W_ x H_ per view, max_instances over the whole frame.
+  void reserve(int32_t P_, int32_t W_, int32_t H_, int64_t max_instances, int nv = 1) {
+    if (P_ < 0 || W_ < 1 || H_ < 1 || max_instances < 0 || nv < 1 ||
+        static_cast<int64_t>(P_) * nv > INT32_MAX)
       throw std::invalid_argument("invalid reserve sizes");
-    const size_t np = static_cast<size_t>(std::max(P_, 1));
-    const size_t npx = static_cast<size_t>(W_) * H_;
+    const size_t np = static_cast<size_t>(std::max(P_ * nv, 1));
+    const size_t npx = static_cast<size_t>(W_) * H_ * nv;
     const size_t ntiles = static_cast<size_t>((W_ + dw::kTile - 1) / dw::kTile) *
-                          ((H_ + dw::kTile - 1) / dw::kTile);
+                          (nv * ((H_ + dw::kTile - 1) / dw::kTile));
     grow(means2D, cap_p, np);
     grow(depths, cap_p2, np);
     grow(radii, cap_p3, np);
@@ -256,7 +259,7 @@ struct dw_rasterizer {
       grow(dids[b], cap_d[2 + b], np);
     }
     grow(area_sorted, cap_as, np);
-    grow_zeroed(scan_tmp, cap_scan, dw::scan_temp_bytes(P_), nullptr);
+    grow_zeroed(scan_tmp, cap_scan, dw::scan_temp_bytes(static_cast<int64_t>(np)), nullptr);
     grow(ranges, cap_t, ntiles);
     grow(tile_order, cap_to, ntiles);
     grow(final_T, cap_px, npx);
@@ -267,9 +270,9 @@ struct dw_rasterizer {
       grow(ivals[b], cap_i[2 + b], ni);
     }
     grow(seg_scratch, cap_seg, 2 * ni);
-    if (dw::scatter_binning_fits(static_cast<int>(ntiles)))
+    if (nv == 1 && dw::scatter_binning_fits(static_cast<int>(ntiles)))
       grow(sc_scratch, cap_sc, dw::scatter_scratch_words(P_, static_cast<int>(ntiles)));
-    const int tx = (W_ + dw::kTile - 1) / dw::kTile, ty = (H_ + dw::kTile - 1) / dw::kTile;
+    const int tx = (W_ + dw::kTile - 1) / dw::kTile, ty = nv * ((H_ + dw::kTile - 1) / dw::kTile);
     if (dw::dense_binning_fits(tx, ty)) {  // dense binning allocates nothing in the forward
       grow(rects, cap_r, np);
       grow(diff, cap_diff, dw::dense_scratch_words(tx, ty));
@@ -280,9 +283,9 @@ struct dw_rasterizer {
       grow(bb_cnt, cap_bbc, dw::block_binning_count_words(tx, ty));
       grow(bb_rect_id, cap_bri, np);
       if (dw::block_binning_blocks(tx, ty) <= 256)
-        grow(bb_hist, cap_bbh, dw::block_binning_hist_words(P_));
+        grow(bb_hist, cap_bbh, dw::block_binning_hist_words(static_cast<int64_t>(np)));
     }
-    ensure_tmp(std::max(dw::radix_sort_temp_bytes(P_),
+    ensure_tmp(std::max(dw::radix_sort_temp_bytes(static_cast<int64_t>(np)),
                         dw::radix_sort_temp_bytes(static_cast<int64_t>(std::min(cap_i[0], cap_i[2])))));
     ensure_small(nullptr);
     // reserve() takes no stream: the zeroing above ran on the legacy stream,
@@ -315,13 +318,56 @@ struct dw_rasterizer {
                const float* opacities, const float* colors, const dw_camera& c, float* out_color,
                int32_t* radii_out, cudaStream_t s, bool nosync = false,
                bool sticky_overflow = false) {
+    forward_views(P_, means3D, scales, rotations, opacities, colors, &c, 1, out_color, radii_out,
+                  s, nosync, sticky_overflow);
+  }
+
+  // Views stacked into one frame (nv > 1: the batched host path). The nv
+  // views of one scene share every launch of the forward -- one preprocess per
+  // view into consecutive id ranges [v P, (v + 1) P), then ONE depth sort, one
+  // entry scan, one block binning and one blend over a frame whose tile rows
+  // [v rows, (v + 1) rows) are view v. A tile holds only its own view's
+  // Gaussians (the rectangles never leave the view's rows) in that view's
+  // (depth, id) order -- the global sort interleaves views but keeps each
+  // view's relative order -- so every tile's list is the single-view list with
+  // ids offset by v P, bit for bit. The latency-bound binning launches then do
+  // nv views' work each (a 1080p frame's block-binning kernels run one wave
+  // either way). Images / final_T / n_contrib (and the backward's dL/dpixel)
+  // are [nv][...] arrays; the backward adds view v's gradients at id - v P.
+  // Requires block binning (its rectangle packing bounds the frame to 255 tile
+  // rows) and one background colour.
+  static constexpr int kMaxStack = 3;
+  int nviews = 1;
+  bool stack_unfit = false;  // the last stacked frame would have preferred dense binning
+  static int stack_limit(int W_, int H_) {
+    const int tx = (W_ + dw::kTile - 1) / dw::kTile, ty = (H_ + dw::kTile - 1) / dw::kTile;
+    if (!dw::block_binning_fits(tx, ty)) return 1;
+    return std::max(1, std::min(kMaxStack, 255 / ty));
+  }
+  void forward_views(int32_t P_, const float* means3D, const float* scales, const float* rotations,
+                     const float* opacities, const float* colors, const dw_camera* cs, int nv,
+                     float* out_color, int32_t* radii_out, cudaStream_t s, bool nosync = false,
+                     bool sticky_overflow = false) {
     last_overflow = false;
     last_stream = s;
+    const dw_camera& c = cs[0];
     if (P_ < 0) throw std::invalid_argument("P must be >= 0");
     if (c.width < 1 || c.height < 1) throw std::invalid_argument("camera size must be >= 1");
-    if (!(c.tan_fovx > 0.0f) || !(c.tan_fovy > 0.0f))
-      throw std::invalid_argument("tan_fov must be > 0");
-    P = P_;
+    if (nv < 1 || nv > stack_limit(c.width, c.height))
+      throw std::invalid_argument("too many stacked views for this image size");
+    for (int v = 0; v < nv; ++v) {
+      if (!(cs[v].tan_fovx > 0.0f) || !(cs[v].tan_fovy > 0.0f))
+        throw std::invalid_argument("tan_fov must be > 0");
+      if (cs[v].width != c.width || cs[v].height != c.height ||
+          std::memcmp(cs[v].bg, c.bg, sizeof(c.bg)) != 0)
+        throw std::invalid_argument("stacked views must share image size and background");
+    }
+    if (static_cast<int64_t>(P_) * nv > INT32_MAX)
+      throw std::invalid_argument("stacked frame has too many Gaussians");
+    nviews = nv;
+    stack_unfit = false;
+    const int Ps = P_;
+    P = P_ * nv;
     W = c.width;
     H = c.height;
     std::memcpy(cam.vm, c.viewmatrix, sizeof(cam.vm));
@@ -333,7 +379,9 @@ struct dw_rasterizer {
     cam.W = W;
     cam.H = H;
     cam.tiles_x = (W + dw::kTile - 1) / dw::kTile;
-    cam.tiles_y = (H + dw::kTile - 1) / dw::kTile;
+    cam.rows_v = (H + dw::kTile - 1) / dw::kTile;
+    cam.tiles_y = nv * cam.rows_v;
+    cam.vstride = nv > 1 ? Ps : 0;
     const int ntiles = cam.tiles_x * cam.tiles_y;
     tile_bits = 0;
     while ((1 << tile_bits) < ntiles) ++tile_bits;
@@ -348,8 +396,8 @@ struct dw_rasterizer {
     grow(offsets, cap_p7, np);
     grow(ranges, cap_t, static_cast<size_t>(ntiles));
     grow(tile_order, cap_to, static_cast<size_t>(ntiles));
-    grow(final_T, cap_px, static_cast<size_t>(W) * H);
-    grow(n_contrib, cap_px2, static_cast<size_t>(W) * H);
+    grow(final_T, cap_px, static_cast<size_t>(W) * H * nv);
+    grow(n_contrib, cap_px2, static_cast<size_t>(W) * H * nv);
     ensure_small(s);
 
     for (int b = 0; b < 2; ++b) {
@@ -370,27 +418,30 @@ struct dw_rasterizer {
     // counts, placement, on-chip depth sort per tile -- no global sort at
     // all (raster_scatter.cu). A forced tile-first path turns it off.
     const char* sc_env = std::getenv("DW_SCATTER");
-    scatter = (sc_env && *sc_env ? *sc_env == '1' : DW_SCATTER != 0) &&
+    scatter = nv == 1 && (sc_env && *sc_env ? *sc_env == '1' : DW_SCATTER != 0) &&
               !(tf_env && *tf_env == '1') && dw::scatter_binning_fits(ntiles);
-    tile_first = !scatter && (tf_env && *tf_env ? *tf_env == '1'
-                                                : DW_TILE_FIRST != 0 && last_list_mean >= 0.0 &&
-                                                      last_list_mean < kTileFirstMaxMean);
+    tile_first = nv == 1 && !scatter &&
+                 (tf_env && *tf_env ? *tf_env == '1'
+                                    : DW_TILE_FIRST != 0 && last_list_mean >= 0.0 &&
+                                          last_list_mean < kTileFirstMaxMean);
     // Block binning (default on the depth-first path): the lists through
     // coarse 8x4-tile blocks (raster_blockbin.cu); DW_BLOCK_BINNING=0 selects
     // the duplicate + tile-sort construction (same output). Block totals must
     // stay < 2^30 for its packed scan: not used once a frame came near that.
     const char* bb_env = std::getenv("DW_BLOCK_BINNING");
     const bool block_mode = !tile_first && !scatter &&
-                            (bb_env && *bb_env ? *bb_env == '1' : DW_BLOCK_BINNING != 0) &&
+                            (nv > 1 || (bb_env && *bb_env ? *bb_env == '1' : DW_BLOCK_BINNING != 0)) &&
                             dw::block_binning_fits(cam.tiles_x, cam.tiles_y) &&
                             last_list_mean * ntiles < static_cast<double>(1 << 29) &&
                             static_cast<int64_t>(P) < (int64_t(1) << 29);
+    if (nv > 1 && !block_mode)
+      throw std::invalid_argument("stacked views need block binning (list too long for it)");
     // the depth-first paths' sort keys come straight out of the preprocess
     const bool keys_ready = !tile_first && !scatter;
     stage_valid = stage_timing;
     stage_mark(0, s);
     const char* bulk_env = std::getenv("DW_BULK_STAGING");
-    bulk = bulk_env && *bulk_env == '1';
+    bulk = nv == 1 && bulk_env && *bulk_env == '1';
     if (bulk) grow(packed, cap_pk, 3 * np);
     if (block_mode) {
       const char* fe = std::getenv("DW_BB_FUSED");
@@ -400,10 +451,21 @@ struct dw_rasterizer {
       grow(bb_rect_id, cap_bri, np);
       if (bb_fused) grow(bb_hist, cap_bbh, dw::block_binning_hist_words(P));
     }
-    dw::launch_preprocess(P, means3D, scales, rotations, opacities, colors, cam, means2D, depths,
-                          radii, conic_opacity, rgb, tiles_touched, keys_ready ? dkey[0] : nullptr,
-                          keys_ready ? dids[0] : nullptr, s, bulk ? packed : nullptr,
-                          block_mode ? bb_rect_id : nullptr);
+    for (int v = 0; v < nv; ++v) {  // view v: ids [v Ps, (v + 1) Ps), tile rows from v rows_v
+      dw::CamParams cv = cam;
+      std::memcpy(cv.vm, cs[v].viewmatrix, sizeof(cv.vm));
+      std::memcpy(cv.pm, cs[v].projmatrix, sizeof(cv.pm));
+      cv.tan_fovx = cs[v].tan_fovx;
+      cv.tan_fovy = cs[v].tan_fovy;
+      cv.scale_modifier = cs[v].scale_modifier;
+      cv.tiles_y = cam.rows_v;
+      const size_t o = static_cast<size_t>(v) * Ps;
+      dw::launch_preprocess(Ps, means3D, scales, rotations, opacities, colors, cv, means2D + o,
+                            depths + o, radii + o, conic_opacity + o, rgb + o, tiles_touched + o,
+                            keys_ready ? dkey[0] + o : nullptr, keys_ready ? dids[0] + o : nullptr,
+                            s, bulk ? packed : nullptr, block_mode ? bb_rect_id + o : nullptr,
+                            v * cam.rows_v, static_cast<uint32_t>(o));
+    }
     stage_mark(1, s);
     // Instance count: read back (one host sync) to size the buffers, or --
     // nosync -- kept on the device against the reserved capacity
@@ -476,8 +538,14 @@ struct dw_rasterizer {
           // the scan wrote the entries into buffers that must hold every
           // instance (the later grows keep them): else grow and rescan
           const bool will_dense =
-              num_rendered > 0 && dw::dense_binning_fits(cam.tiles_x, cam.tiles_y) &&
+              nv == 1 && num_rendered > 0 && dw::dense_binning_fits(cam.tiles_x, cam.tiles_y) &&
               dense_env_ok(static_cast<double>(P) * ntiles <= 4.0 * static_cast<double>(num_rendered));
+          // a stacked frame of a scene whose single views take dense binning
+          // (large rectangles): the caller goes back to one view per frame
+          if (nv > 1)
+            stack_unfit = num_rendered > 0 && dw::dense_binning_fits(cam.tiles_x, cam.rows_v) &&
+                          dense_env_ok(static_cast<double>(Ps) * cam.tiles_x * cam.rows_v <=
+                                       4.0 * static_cast<double>(num_rendered) / nv);
           if (!will_dense && static_cast<uint64_t>(num_rendered) > bb_entry_cap) {
             const size_t ni = static_cast<size_t>(num_rendered);
             for (int b = 0; b < 2; ++b) {
@@ -506,7 +574,7 @@ struct dw_rasterizer {
     blocked = false;
     // Dense scenes (large tile rectangles: P x tiles <= 4 x instances) build the
     // per-tile lists directly; the rest duplicate + radix-sort (same output).
-    dense = n_grid > 0 && dw::dense_binning_fits(cam.tiles_x, cam.tiles_y) &&
+    dense = nv == 1 && n_grid > 0 && dw::dense_binning_fits(cam.tiles_x, cam.tiles_y) &&
             dense_env_ok(static_cast<double>(P) * ntiles <= 4.0 * static_cast<double>(n_grid));
     if (dense) {
       grow(rects, cap_r, static_cast<size_t>(P));
@@ -563,7 +631,7 @@ struct dw_rasterizer {
     dw::launch_forward_impl(cam, ranges, vals, means2D, conic_opacity, rgb, nullptr, final_T,
                             n_contrib, out_color, s);
     stage_mark(6, s);
-    if (radii_out && P > 0)
+    if (radii_out && P > 0)  // (a stacked frame: [nv][P] radii)
       DW_CUDA(cudaMemcpyAsync(radii_out, radii, sizeof(int) * P, cudaMemcpyDeviceToDevice, s));
     forward_done = true;
   }
@@ -644,6 +712,16 @@ void raster_forward(dw_rasterizer* r, int32_t P, const float* m, const float* sc
   if (nr) *nr = nosync ? -1 : r->num_rendered;
 }
 
+void raster_forward_views(dw_rasterizer* r, int32_t P, const float* m, const float* sc,
+                          const float* rot, const float* op, const float* col,
+                          const dw_camera* cams, int32_t nv, float* out, int64_t* nr,
+                          cudaStream_t s) {
+  r->forward_views(P, m, sc, rot, op, col, cams, nv, out, nullptr, s);
+  if (nr) *nr = r->num_rendered;
+}
+
+int raster_max_stacked_views(int32_t W, int32_t H) { return dw_rasterizer::stack_limit(W, H); }
+
 void raster_backward(dw_rasterizer* r, const float* dL, int policy, int thr, float* grad,
                      uint64_t* pairs, cudaStream_t s) {
   r->backward(dL, policy, thr, grad, pairs, s);
@@ -678,6 +756,7 @@ int64_t raster_resolve(dw_rasterizer* r, bool* overflowed) { return r->resolve_c
 dw::HostTrace raster_backward_tap(dw_rasterizer* r, const float* dL, int thr, float* grad,
                                   int64_t max_records, int64_t* total, cudaStream_t s) {
   if (!r->forward_done) throw std::invalid_argument("render_backward before render_forward");
+  if (r->nviews != 1) throw std::invalid_argument("the tap takes a single-view forward");
   if (max_records < 0) throw std::invalid_argument("max_records must be >= 0");
   const size_t cap = static_cast<size_t>(std::max<int64_t>(max_records, 1));
   TapBuf tb;
@@ -751,11 +830,12 @@ void raster_preprocess_backward(dw_rasterizer* r, const float* means3D, const fl
                                 const float* rotations, const float* grad2d, float* grad3d,
                                 cudaStream_t s) {
   if (!r->forward_done) throw std::invalid_argument("preprocess_backward before render_forward");
+  if (r->nviews != 1) throw std::invalid_argument("preprocess_backward after a stacked forward");
   launch_preprocess_backward(r->P, means3D, scales, rotations, r->radii, r->cam, grad2d, grad3d, s);
 }
 
 void raster_buffer(const dw_rasterizer* r, int which, const void** p, int64_t* count) {
-  const int64_t P = r->P, npx = int64_t(r->W) * r->H;
+  const int64_t P = r->P, npx = int64_t(r->W) * r->H * r->nviews;
   const int64_t I = const_cast<dw_rasterizer*>(r)->resolve_count(nullptr);
   const int64_t nt = int64_t(r->cam.tiles_x) * r->cam.tiles_y;
   switch (which) {
@@ -837,10 +917,31 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
                        int32_t V, const float* dL, int policy, int thr, float* out_images,
                        float* grad, cudaStream_t s, bool grad_on_device) {
   if (V < 1) throw std::invalid_argument("need at least one view");
-  for (int k = 1; k < V; ++k)
+  bool same_bg = true;
+  for (int k = 1; k < V; ++k) {
     if (cams[k].width != cams[0].width || cams[k].height != cams[0].height)
       throw std::invalid_argument("all views must share one image size");
+    same_bg = same_bg && std::memcmp(cams[k].bg, cams[0].bg, sizeof(cams[0].bg)) == 0;
+  }
   r->ensure_streams();
+  // Views per frame (dw_rasterizer::forward_views): G consecutive views share
+  // every forward launch and one backward launch. DW_VIEWS_STACK=n overrides
+  // the default (profiles/r02/ab/stacked_views.md); one view per frame when
+  // the views differ in background, the image is too tall for the packed
+  // rectangles, or the scene takes dense binning (decided on the first frame).
+  int G = 3;  // 64 views, C3: 81.7 / 80.6 / 79.1 ms per step at 1 / 2 / 3; C5: a tie
+  if (const char* e = std::getenv("DW_VIEWS_STACK"); e && *e) G = std::atoi(e);
+  G = std::max(1, std::min({G, dw_rasterizer::stack_limit(cams[0].width, cams[0].height),
+                            static_cast<int>(V)}));
+  if (!same_bg || P == 0) G = 1;
+  auto forced = [](const char* name, char v) {
+    const char* e = std::getenv(name);
+    return e && *e == v;
+  };
+  // a list construction other than block binning forced: one view per frame
+  if (forced("DW_BLOCK_BINNING", '0') || forced("DW_TILE_FIRST", '1') ||
+      forced("DW_SCATTER", '1') || forced("DW_DENSE_BINNING", '1'))
+    G = 1;
   const size_t np = static_cast<size_t>(std::max(P, 1));
   const size_t npx = static_cast<size_t>(cams[0].width) * cams[0].height;
   float* d_m = r->host_scratch(0, 3 * np);
@@ -849,15 +950,13 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
   float* d_op = r->host_scratch(3, np);
   float* d_col = r->host_scratch(4, 3 * np);
   float* d_g = grad_on_device ? grad : r->host_scratch(7, kNParam * np);
-  float* d_dl[2] = {r->host_scratch(5, 3 * npx), r->host_scratch(8, 3 * npx)};
-  float* d_img[2] = {r->host_scratch(6, 3 * npx), r->host_scratch(9, 3 * npx)};
   cudaEvent_t e_scene = r->ev[0], e_in[2] = {r->ev[1], r->ev[2]},
               e_used[2] = {r->ev[3], r->ev[4]}, e_img[2] = {r->ev[5], r->ev[6]},
               e_start = r->ev[7], e_zero = r->ev[8], e_aux = r->ev[9],
               e_fwd[2] = {r->ev[10], r->ev[11]}, e_fj[2] = {r->ev[12], r->ev[13]};
-  // Views alternate between two forward states and two compute streams
-  // (R[k & 1], S[k & 1]), so view k+1's projection / sort -- latency-bound
-  // launches that leave most SMs idle -- overlaps view k's backward. Both
+  // Frames alternate between two forward states and two compute streams
+  // (R[g & 1], S[g & 1]), so frame g+1's projection / sort -- latency-bound
+  // launches that leave most SMs idle -- overlaps frame g's backward. Both
   // backwards add into the one gradient buffer with RED atomics, whose order
   // was never fixed, so the sum is the same up to fp32 reassociation.
   if (V > 1 && !r->twin) r->twin = new dw_rasterizer();
@@ -889,43 +988,57 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
   DW_CUDA(cudaStreamWaitEvent(s, e_scene, 0));
   DW_CUDA(cudaStreamWaitEvent(S[1], e_scene, 0));
   for (auto f : F) DW_CUDA(cudaStreamWaitEvent(f, e_scene, 0));
-  // Views 0 and 1 read their instance counts back (host sync on their own
+  // Frames 0 and 1 read their instance counts back (host sync on their own
   // stream only) and size a 1.5x reserve for their forward state; later
-  // views keep the count on the device (no host sync: the host runs ahead
-  // and every copy overlaps). A view that outgrows its reserve raises the
-  // sticky overflow flag and the whole batch is redone with host-read counts.
-  bool nosync_ok = V > 2;
-  for (int pass = 0; pass < 2; ++pass) {
+  // frames keep the count on the device (no host sync: the host runs ahead
+  // and every copy overlaps). A frame that outgrows its reserve raises the
+  // sticky overflow flag and the whole batch is redone with host-read counts;
+  // a stacked first frame that would have preferred dense binning restarts
+  // the batch with one view per frame.
+  bool nosync_ok = true;
+  for (int pass = 0; pass < 3; ++pass) {
+    const int NG = (V + G - 1) / G;  // frames
+    nosync_ok = nosync_ok && NG > 2;
+    float* d_dl[2] = {r->host_scratch(5, 3 * npx * G), r->host_scratch(8, 3 * npx * G)};
+    float* d_img[2] = {r->host_scratch(6, 3 * npx * G), r->host_scratch(9, 3 * npx * G)};
+    auto first = [&](int g) { return g * G; };
+    auto count = [&](int g) { return std::min(G, static_cast<int>(V) - g * G); };
     DW_CUDA(cudaMemsetAsync(d_g, 0, kNParam * np * sizeof(float), s));
     DW_CUDA(cudaEventRecord(e_zero, s));
     DW_CUDA(cudaStreamWaitEvent(S[1], e_zero, 0));
-    h2d(d_dl[0], dL, 3 * npx, r->s_in);
+    h2d(d_dl[0], dL, 3 * npx * count(0), r->s_in);
     DW_CUDA(cudaEventRecord(e_in[0], r->s_in));
-    for (int k = 0; k < V; ++k) {
-      const int b = k & 1;
+    bool restack = false;
+    for (int g = 0; g < NG; ++g) {
+      const int b = g & 1;
       dw_rasterizer* Rb = R[b];
       cudaStream_t Sb = S[b], Fb = F[b];
-      if (k + 1 < V) {  // prefetch view k+1 once view k-1 released its buffer
-        if (k >= 1) DW_CUDA(cudaStreamWaitEvent(r->s_in, e_used[b ^ 1], 0));
-        h2d(d_dl[b ^ 1], dL + static_cast<size_t>(k + 1) * 3 * npx, 3 * npx, r->s_in);
+      if (g + 1 < NG) {  // prefetch frame g+1 once frame g-1 released its buffer
+        if (g >= 1) DW_CUDA(cudaStreamWaitEvent(r->s_in, e_used[b ^ 1], 0));
+        h2d(d_dl[b ^ 1], dL + static_cast<size_t>(first(g + 1)) * 3 * npx,
+            3 * npx * count(g + 1), r->s_in);
         DW_CUDA(cudaEventRecord(e_in[b ^ 1], r->s_in));
       }
-      if (k >= 2) {
-        DW_CUDA(cudaStreamWaitEvent(Fb, e_used[b], 0));  // view k-2's backward: state free
-        DW_CUDA(cudaStreamWaitEvent(Fb, e_img[b], 0));   // image k-2 downloaded
+      if (g >= 2) {
+        DW_CUDA(cudaStreamWaitEvent(Fb, e_used[b], 0));  // frame g-2's backward: state free
+        DW_CUDA(cudaStreamWaitEvent(Fb, e_img[b], 0));   // images g-2 downloaded
       }
-      if (nosync_ok && (k == 2 || k == 3)) {  // first reuse of R[b]: size its reserve
+      if (nosync_ok && (g == 2 || g == 3)) {  // first reuse of R[b]: size its reserve
         const int64_t want = Rb->num_rendered + Rb->num_rendered / 2 + 4096;
         if (static_cast<int64_t>(std::min(Rb->cap_i[0], Rb->cap_i[2])) < want) {
-          DW_CUDA(cudaStreamSynchronize(Sb));  // view k-2 is done with the buffers a reserve moves
+          DW_CUDA(cudaStreamSynchronize(Sb));  // frame g-2 is done with the buffers a reserve moves
           DW_CUDA(cudaStreamSynchronize(Fb));
-          Rb->reserve(P, cams[0].width, cams[0].height, want);
+          Rb->reserve(P, cams[0].width, cams[0].height, want, G);
         }
         DW_CUDA(cudaMemsetAsync(Rb->overflow_dev, 0, sizeof(unsigned int), Fb));
       }
-      const bool nosync = nosync_ok && k >= 2;
-      Rb->forward(P, d_m, d_sc, d_rot, d_op, d_col, cams[k], d_img[b], nullptr, Fb, nosync,
-                  /*sticky_overflow=*/true);
+      const bool nosync = nosync_ok && g >= 2;
+      Rb->forward_views(P, d_m, d_sc, d_rot, d_op, d_col, cams + first(g), count(g), d_img[b],
+                        nullptr, Fb, nosync, /*sticky_overflow=*/true);
+      if (g == 0 && count(0) > 1 && Rb->stack_unfit) {  // counted: known on the host now
+        restack = true;
+        break;
+      }
       if (Fb != Sb) {
         DW_CUDA(cudaEventRecord(e_fwd[b], Fb));
         DW_CUDA(cudaStreamWaitEvent(Sb, e_fwd[b], 0));
@@ -935,8 +1048,9 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
       DW_CUDA(cudaEventRecord(e_used[b], Sb));
       if (out_images) {
         DW_CUDA(cudaStreamWaitEvent(r->s_out, Fb != Sb ? e_fwd[b] : e_used[b], 0));
-        DW_CUDA(cudaMemcpyAsync(out_images + static_cast<size_t>(k) * 3 * npx, d_img[b],
-                                3 * npx * sizeof(float), cudaMemcpyDeviceToHost, r->s_out));
+        DW_CUDA(cudaMemcpyAsync(out_images + static_cast<size_t>(first(g)) * 3 * npx, d_img[b],
+                                3 * npx * count(g) * sizeof(float), cudaMemcpyDeviceToHost,
+                                r->s_out));
         DW_CUDA(cudaEventRecord(e_img[b], r->s_out));
       } else {
         DW_CUDA(cudaEventRecord(e_img[b], Sb));
@@ -949,6 +1063,13 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
       }
     DW_CUDA(cudaEventRecord(e_aux, S[1]));
     DW_CUDA(cudaStreamWaitEvent(s, e_aux, 0));
+    if (restack) {
+      DW_CUDA(cudaStreamSynchronize(s));
+      DW_CUDA(cudaStreamSynchronize(r->s_in));
+      DW_CUDA(cudaStreamSynchronize(r->s_out));
+      G = 1;
+      continue;
+    }
     if (!nosync_ok) break;
     DW_CUDA(cudaStreamSynchronize(s));  // both compute streams (S[1] joined into s)
     bool ovf0 = false, ovf1 = false;

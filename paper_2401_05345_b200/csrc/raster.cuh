@@ -58,16 +58,31 @@ struct CamParams {
   float bg[3];
   float scale_modifier;
   int W, H, tiles_x, tiles_y;
+  // A frame may stack views vertically (raster_views_host: several views per
+  // set of launches): tile rows [v * rows_v, (v + 1) * rows_v) are view v,
+  // whose Gaussians carry ids [v * vstride, (v + 1) * vstride) and whose
+  // per-pixel buffers (final_T, n_contrib: H*W; image, dL/dpixel: 3*H*W) are
+  // the v-th of a [views][...] array. One view: rows_v = tiles_y, vstride = 0.
+  int rows_v, vstride;
 };
+
+// Tile -> (view slot of a stacked frame, top-left pixel inside that view).
+__device__ __forceinline__ int tile_view(const CamParams& cam, int tile, int* tx0, int* ty0) {
+  const int ty = tile / cam.tiles_x;
+  const int v = ty / cam.rows_v;
+  *tx0 = (tile - ty * cam.tiles_x) * kTile;
+  *ty0 = (ty - v * cam.rows_v) * kTile;
+  return v;
+}
 
 // In-tile thread t = warp*32 + lane covers pixel (8*(warp&1) + (lane&7),
 // 4*(warp>>1) + (lane>>3)): each warp owns an 8x4 block, the warp tiling of
 // the reference's workload model (workload.cpp:107-110), which maximises the
 // chance that all 32 lanes of a warp see the same Gaussian.
-__device__ __forceinline__ void tile_pixel(int tile, int t, int tiles_x, int* px, int* py) {
+__device__ __forceinline__ void tile_pixel(int tx0, int ty0, int t, int* px, int* py) {
   const int w = t >> 5, l = t & 31;
-  *px = (tile % tiles_x) * kTile + (w & 1) * 8 + (l & 7);
-  *py = (tile / tiles_x) * kTile + (w >> 1) * 4 + (l >> 3);
+  *px = tx0 + (w & 1) * 8 + (l & 7);
+  *py = ty0 + (w >> 1) * 4 + (l >> 3);
 }
 
 void launch_preprocess(int P, const float* means3D, const float* scales, const float* rotations,
@@ -75,8 +90,10 @@ void launch_preprocess(int P, const float* means3D, const float* scales, const f
                        float2* means2D, float* depths, int* radii, float4* conic_opacity,
                        float4* rgb, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* dids,
                        cudaStream_t s, float4* packed = nullptr,
-                       uint32_t* rect_out = nullptr);  // dkey/dids (nullable): depth-sort keys and ids;
-                                                       // rect_out (nullable): packed tile rectangles
+                       uint32_t* rect_out = nullptr,  // dkey/dids (nullable): depth-sort keys and ids;
+                                                      // rect_out (nullable): packed tile rectangles
+                       int row0 = 0, uint32_t id0 = 0);  // stacked frame: the view's first tile row
+                                                         // (added to the rectangles) and first id
 
 // Device buffers of the backward's WarpRecord tap (SoA like dw_device_trace).
 struct TapBuf {

@@ -103,13 +103,14 @@ __device__ __forceinline__ uint32_t footprint_mask(float mx, float my, float ext
 // Stage Gaussian `id` into slot `slot` (conic pre-scaled, scale_conic) and
 // return its 8-bit warp-block mask for the tile whose top-left pixel is
 // (tx0, ty0).
+// xyi.z = id - vbase: the scene index (vbase = the view slot's first id).
 __device__ __forceinline__ uint32_t stage(Staged* s, int slot, uint32_t id, int tx0, int ty0,
                                           const float2* __restrict__ means2D,
                                           const float4* __restrict__ conic_opacity,
-                                          const float4* __restrict__ rgb) {
+                                          const float4* __restrict__ rgb, uint32_t vbase = 0) {
   const float2 m = __ldg(means2D + id);
   const float4 co = __ldg(conic_opacity + id);
-  s[slot].xyi = make_float4(m.x, m.y, __uint_as_float(id), 0.0f);
+  s[slot].xyi = make_float4(m.x, m.y, __uint_as_float(id - vbase), 0.0f);
   s[slot].co = scale_conic(co);
   const float4 c = __ldg(rgb + id);
   s[slot].col = c;
@@ -191,12 +192,17 @@ __global__ void __launch_bounds__(kBlock, DW_BWD_MIN_BLOCKS)
   __shared__ uint8_t s_mask[kBlock];
   __shared__ uint32_t s_wmax[kBlock / 32];
   const int tile = blockIdx.x, t = threadIdx.x, w = t >> 5, lane = t & 31;
-  const int tx0 = (tile % cam.tiles_x) * kTile, ty0 = (tile / cam.tiles_x) * kTile;
+  int tx0, ty0;
+  const int view = tile_view(cam, tile, &tx0, &ty0);
   int px, py;
-  tile_pixel(tile, t, cam.tiles_x, &px, &py);
+  tile_pixel(tx0, ty0, t, &px, &py);
   const bool inside = px < cam.W && py < cam.H;
   const int pix = py * cam.W + px;
   const int HW = cam.H * cam.W;
+  final_Ts += static_cast<int64_t>(view) * HW;  // the view's per-pixel buffers
+  n_contrib += static_cast<int64_t>(view) * HW;
+  dL_dpixels += static_cast<int64_t>(view) * 3 * HW;
+  const uint32_t vbase = static_cast<uint32_t>(view * cam.vstride);
   const float pfx = (float)px, pfy = (float)py;
   const uint2 range = ranges[tile];
 
@@ -234,7 +240,7 @@ __global__ void __launch_bounds__(kBlock, DW_BWD_MIN_BLOCKS)
     uint32_t mask = 0;
     if (t < todo)
       mask = stage(sm, t, values[top - 1 - (i * kBlock + t)], tx0, ty0, means2D, conic_opacity,
-                   rgb);
+                   rgb, vbase);
     s_mask[t] = (uint8_t)mask;
     __syncthreads();
     const int n = min(kBlock, todo);
@@ -397,7 +403,14 @@ __global__ void DW_FWD_BOUNDS
   __shared__ uint8_t s_mask[kBlock];
   const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
-  const int tx0 = (tile % cam.tiles_x) * kTile, ty0 = (tile / cam.tiles_x) * kTile;
+  int tx0, ty0;
+  const int view = tile_view(cam, tile, &tx0, &ty0);
+  {  // the view's per-pixel outputs (stacked frame)
+    const int64_t HWv = static_cast<int64_t>(cam.H) * cam.W;
+    final_T += view * HWv;
+    n_contrib += view * HWv;
+    out_color += view * 3 * HWv;
+  }
   const int px = tx0 + (w & 1) * 8 + (lane & 7);
   const int py = ty0 + (w >> 1) * 8 + (lane >> 3);
   const float pfx = (float)px;
@@ -504,12 +517,17 @@ __global__ void __launch_bounds__(128, (POL == kSwB && !COUNT && !TAP) ? DW_SWB_
   __shared__ uint32_t s_wmax[NW];
   const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
-  const int tx0 = (tile % cam.tiles_x) * kTile, ty0 = (tile / cam.tiles_x) * kTile;
+  int tx0, ty0;
+  const int view = tile_view(cam, tile, &tx0, &ty0);
   const int px = tx0 + (w & 1) * 8 + (lane & 7);
   const int py = ty0 + (w >> 1) * 8 + (lane >> 3);
   const float pfx = (float)px;
   const float2 npfy = make_float2(-(float)py, -(float)(py + 4));
   const int HW = cam.H * cam.W;
+  final_Ts += static_cast<int64_t>(view) * HW;  // the view's per-pixel buffers
+  n_contrib += static_cast<int64_t>(view) * HW;
+  dL_dpixels += static_cast<int64_t>(view) * 3 * HW;
+  const uint32_t vbase = static_cast<uint32_t>(view * cam.vstride);  // scene id = id - vbase
   // per-pixel constants and state, packed (pixel 0 in .x, pixel 1 in .y)
   float2 T, nTb, dL0, dL1, dL2;
   uint32_t last0 = 0, last1 = 0;
@@ -627,7 +645,7 @@ __global__ void __launch_bounds__(128, (POL == kSwB && !COUNT && !TAP) ? DW_SWB_
         // xyi.zw = (id, k b): RED address, mean2D gradient; co = the walk's
         // exponent coefficients (scale_conic); col.w = 1/opacity
         *reinterpret_cast<float2*>(&cur[st].xyi.z) =
-            make_float2(__uint_as_float(cur_id[h]), kConicScale * co.y);
+            make_float2(__uint_as_float(cur_id[h] - vbase), kConicScale * co.y);
         cur[st].co = scale_conic(co);
         cur[st].col.w = rcp_approx(co.w);
       }

@@ -83,7 +83,8 @@ __global__ void __launch_bounds__(kBlock, DW_PRE_MIN_BLOCKS)
                  int* __restrict__ radii, float4* __restrict__ conic_opacity,
                  float4* __restrict__ rgb, uint32_t* __restrict__ tiles_touched,
                  uint32_t* __restrict__ dkey, uint32_t* __restrict__ dids,
-                 float4* __restrict__ packed, uint32_t* __restrict__ rect_out) {
+                 float4* __restrict__ packed, uint32_t* __restrict__ rect_out, int row0,
+                 uint32_t id0) {
   pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
   __shared__ __align__(16) float s_mean[3 * kBlock];
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(kBlock, DW_PRE_MIN_BLOCKS)
   // depth-sort input (nullable): (depth bits, id), culled Gaussians last
   if (dkey) {
     dkey[i] = 0xffffffffu;
-    dids[i] = static_cast<uint32_t>(i);
+    dids[i] = id0 + static_cast<uint32_t>(i);  // id0: the view's first id in a stacked frame
   }
 
   const float px = s_mean[3 * t], py = s_mean[3 * t + 1], pz = s_mean[3 * t + 2];
@@ -211,9 +212,9 @@ __global__ void __launch_bounds__(kBlock, DW_PRE_MIN_BLOCKS)
     packed[3 * i + 2] = c4;
   }
   tiles_touched[i] = static_cast<uint32_t>(area);
-  if (rect_out)
-    rect_out[i] = (uint32_t)rminx | (uint32_t)rminy << 8 | (uint32_t)(rmaxx - 1) << 16 |
-                  (uint32_t)(rmaxy - 1) << 24;
+  if (rect_out)  // rows in the (stacked) frame: row0 = the view's first tile row
+    rect_out[i] = (uint32_t)rminx | (uint32_t)(rminy + row0) << 8 | (uint32_t)(rmaxx - 1) << 16 |
+                  (uint32_t)(rmaxy - 1 + row0) << 24;
 }
 
 }  // namespace
@@ -222,7 +223,8 @@ void launch_preprocess(int P, const float* means3D, const float* scales, const f
                        const float* opacities, const float* colors, const CamParams& cam,
                        float2* means2D, float* depths, int* radii, float4* conic_opacity,
                        float4* rgb, uint32_t* tiles_touched, uint32_t* dkey, uint32_t* dids,
-                       cudaStream_t s, float4* packed, uint32_t* rect_out) {
+                       cudaStream_t s, float4* packed, uint32_t* rect_out, int row0,
+                       uint32_t id0) {
   if (P <= 0) return;
   auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   const bool vec = aligned(means3D) && aligned(scales) && aligned(colors) && aligned(rotations);
@@ -230,11 +232,11 @@ void launch_preprocess(int P, const float* means3D, const float* scales, const f
   if (vec)
     launch_pdl(k_preprocess<true>, grid, kBlock, 0, s, P, means3D, scales, rotations, opacities,
                colors, cam, means2D, depths, radii, conic_opacity, rgb, tiles_touched, dkey, dids,
-               packed, rect_out);
+               packed, rect_out, row0, id0);
   else
     launch_pdl(k_preprocess<false>, grid, kBlock, 0, s, P, means3D, scales, rotations, opacities,
                colors, cam, means2D, depths, radii, conic_opacity, rgb, tiles_touched, dkey, dids,
-               packed, rect_out);
+               packed, rect_out, row0, id0);
   DW_CUDA(cudaGetLastError());
 }
 

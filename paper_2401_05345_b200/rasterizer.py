@@ -148,8 +148,32 @@ class GaussianRasterizer:
             self._h, P, *sp, C.byref(cam),
             _ptr(out_color, "out_color", f32, 3 * camera.height * camera.width),
             _ptr(radii, "radii", torch.int32, P), C.byref(nr), _stream(stream)))
-        self.P, self.num_rendered, self.camera = P, nr.value, camera
+        self.P, self.num_rendered, self.camera, self.views = P, nr.value, camera, 1
         return out_color, radii, nr.value
+
+    def render_forward_views(self, means3D, scales, rotations, opacities, colors, cameras,
+                             out_images=None, stream=None):
+        """dw_render_forward_views: len(cameras) views of one scene stacked into
+        one frame (every forward launch covers all of them); the next
+        render_backward takes dL_dpixels [V, 3, H, W]. Returns
+        (out_images [V, 3, H, W], num_rendered of the frame)."""
+        import torch
+
+        f32 = torch.float32
+        V = len(cameras)
+        if V < 1:
+            raise ValueError("need at least one camera")
+        H, W = cameras[0].height, cameras[0].width
+        P, sp = _scene_ptrs(means3D, scales, rotations, opacities, colors)
+        if out_images is None:
+            out_images = torch.empty((V, 3, H, W), dtype=f32, device=means3D.device)
+        arr = (_lib.CameraC * V)(*[c.to_c() for c in cameras])
+        nr = C.c_int64()
+        check(lib().dw_render_forward_views(
+            self._h, P, *sp, arr, V, _ptr(out_images, "out_images", f32, V * 3 * H * W),
+            C.byref(nr), _stream(stream)))
+        self.P, self.num_rendered, self.camera, self.views = P, nr.value, cameras[0], V
+        return out_images, nr.value
 
     def reserve(self, P: int, width: int, height: int, max_instances: int):
         """Pre-size every buffer (dw_rasterizer_reserve) so that a forward /
@@ -171,7 +195,7 @@ class GaussianRasterizer:
             self._h, P, *sp, C.byref(cam),
             _ptr(out_color, "out_color", f32, 3 * camera.height * camera.width),
             _ptr(radii, "radii", torch.int32, P), _stream(stream)))
-        self.P, self.num_rendered, self.camera = P, None, camera
+        self.P, self.num_rendered, self.camera, self.views = P, None, camera, 1
         return out_color, radii
 
     def instances(self):
@@ -254,7 +278,7 @@ class GaussianRasterizer:
     def _npix3(self) -> int:
         if self.camera is None:
             raise _lib.InvalidArgument(1, "render_backward before render_forward")
-        return 3 * self.camera.height * self.camera.width
+        return 3 * self.camera.height * self.camera.width * getattr(self, "views", 1)
 
     def buffer(self, name: str) -> np.ndarray:
         """Host copy of an intermediate buffer (parity tests)."""
@@ -340,6 +364,13 @@ class ThresholdTuner:
             self.history.append((self.iteration, best, sweep))
         self.iteration += 1
         return Policy(self.kind, self.chosen)
+
+
+def max_stacked_views(width: int, height: int) -> int:
+    """dw_rasterizer_max_stacked_views: views of this size one stacked frame holds."""
+    out = C.c_int32()
+    check(lib().dw_rasterizer_max_stacked_views(int(width), int(height), C.byref(out)))
+    return out.value
 
 
 def render_views_host(rast: "GaussianRasterizer", scene_ptrs, P: int, cams, dL_ptr: int,

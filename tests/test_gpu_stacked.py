@@ -1,0 +1,160 @@
+"""Stacked frames (dw_render_forward_views and the batched host path): several
+views of one scene share every launch of the forward and one backward launch.
+The bar is the single-view path itself: per-tile lists, images, final_T and
+n_contrib bit for bit (view v's ids offset by v*P in the frame), gradients
+equal to the per-view sum up to fp32 reassociation of the RED order -- and
+through tests/test_gpu_raster.py's views-host tests (default stacking) the
+oracle's per-view bounds.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SCENE_KEYS = ("means3D", "scales", "rotations", "opacities", "colors")
+
+
+def _scene(cuda, P, W, H, seed, **kw):
+    import torch
+
+    from paper_2401_05345_b200.scene import make_scene
+
+    return {k: torch.from_numpy(v).to(cuda) for k, v in make_scene(P, W, H, seed=seed, **kw).items()}
+
+
+def _grad_close(got, want):
+    # two orders of fp32 RED accumulation of the same addends
+    err = np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-30)
+    assert err < 1e-5, err
+
+
+@pytest.mark.parametrize("nv", [2, 3])
+def test_stacked_forward_equals_single_views(cuda, nv):
+    import torch
+
+    from paper_2401_05345_b200 import warpred as wr
+    from paper_2401_05345_b200.rasterizer import GaussianRasterizer, max_stacked_views
+    from paper_2401_05345_b200.scene import make_dL_dpixels, orbit_cameras
+
+    P, W, H = 20000, 256, 200  # 13 tile rows per view: the last row is partial
+    assert max_stacked_views(W, H) >= nv
+    sc = _scene(cuda, P, W, H, seed=71)
+    args = [sc[k] for k in SCENE_KEYS]
+    cams = orbit_cameras(W, H, 5)[1:1 + nv]
+    dL = torch.from_numpy(np.stack([make_dL_dpixels(W, H, seed=80 + v) for v in range(nv)])).to(cuda)
+    pol = wr.Policy(wr.PolicyKind.sw_b, 12)
+    singles, want = [], torch.zeros((P, 9), dtype=torch.float32, device=cuda)
+    for v, cam in enumerate(cams):
+        r = GaussianRasterizer()
+        img, _, nr = r.render_forward(*args, cam)
+        r.render_backward(dL[v], pol, grad=want)
+        singles.append(dict(img=img.cpu().numpy(), nr=nr, ranges=r.buffer("ranges"),
+                            values=r.buffer("values"), T=r.buffer("final_T"),
+                            nc=r.buffer("n_contrib")))
+    rs = GaussianRasterizer()
+    imgs, nr = rs.render_forward_views(*args, cams)
+    assert nr == sum(s["nr"] for s in singles)
+    ranges, values = rs.buffer("ranges"), rs.buffer("values")
+    T, nc = rs.buffer("final_T"), rs.buffer("n_contrib")
+    ntv = singles[0]["ranges"].shape[0]
+    assert ranges.shape[0] == nv * ntv
+    for v, s in enumerate(singles):
+        assert np.array_equal(imgs[v].cpu().numpy(), s["img"])
+        assert np.array_equal(T[v * H * W:(v + 1) * H * W], s["T"])
+        assert np.array_equal(nc[v * H * W:(v + 1) * H * W], s["nc"])
+        rv = ranges[v * ntv:(v + 1) * ntv]
+        assert np.array_equal(rv[:, 1] - rv[:, 0], s["ranges"][:, 1] - s["ranges"][:, 0])
+        lists = np.concatenate([values[a:b] for a, b in rv])
+        assert np.array_equal(lists, s["values"] + v * P)
+    grad = torch.zeros((P, 9), dtype=torch.float32, device=cuda)
+    rs.render_backward(dL, pol, grad=grad)
+    _grad_close(grad.cpu().numpy().astype(np.float64), want.cpu().numpy().astype(np.float64))
+    # every policy reads the frame the same way (native: the one-pixel kernel)
+    for kind, t in ((wr.PolicyKind.native, 0), (wr.PolicyKind.sw_s, 20), (wr.PolicyKind.cccl, 0)):
+        g = torch.zeros((P, 9), dtype=torch.float32, device=cuda)
+        rs.render_backward(dL, wr.Policy(kind, t), grad=g)
+        _grad_close(g.cpu().numpy().astype(np.float64), want.cpu().numpy().astype(np.float64))
+
+
+def test_stacked_forward_rejects_bad_stacks(cuda):
+    from paper_2401_05345_b200 import _lib
+    from paper_2401_05345_b200.rasterizer import GaussianRasterizer, max_stacked_views
+    from paper_2401_05345_b200.scene import make_camera
+
+    assert max_stacked_views(1920, 1080) == 3  # 68 tile rows per view, <= 255 in a frame
+    assert max_stacked_views(1920, 4320) == 1  # 270 rows: block binning's packing does not fit
+    P, W, H = 1000, 64, 64
+    sc = _scene(cuda, P, W, H, seed=3)
+    args = [sc[k] for k in SCENE_KEYS]
+    r = GaussianRasterizer()
+    with pytest.raises(_lib.InvalidArgument):
+        r.render_forward_views(*args, [make_camera(W, H)] * 4)  # more than 3 views
+    with pytest.raises(_lib.InvalidArgument):
+        r.render_forward_views(*args, [make_camera(W, H), make_camera(W, H + 16)])
+    with pytest.raises(_lib.InvalidArgument):
+        r.render_forward_views(*args, [make_camera(W, H), make_camera(W, H, bg=(0, 0, 0))])
+
+
+def _views_host(monkeypatch, stack, sc_np, cams, dL):
+    import torch
+
+    from paper_2401_05345_b200 import warpred as wr
+    from paper_2401_05345_b200.rasterizer import GaussianRasterizer, render_views_host
+
+    monkeypatch.setenv("DW_VIEWS_STACK", str(stack))
+    P = sc_np["means3D"].shape[0]
+    V, _, H, W = dL.shape
+    pin = {k: torch.from_numpy(v).pin_memory() for k, v in sc_np.items()}
+    dL_h = torch.from_numpy(dL).pin_memory()
+    img = torch.empty((V, 3, H, W), dtype=torch.float32).pin_memory()
+    grad = torch.empty((P, 9), dtype=torch.float32).pin_memory()
+    r = GaussianRasterizer()
+    ptrs = [pin[k].data_ptr() for k in SCENE_KEYS]
+    out = []
+    for _ in range(2):  # the second call reuses the states (stacked reserves)
+        render_views_host(r, ptrs, P, cams, dL_h.data_ptr(), wr.Policy(wr.PolicyKind.sw_b, 12),
+                          img.data_ptr(), grad.data_ptr())
+        out.append((img.numpy().copy(), grad.numpy().astype(np.float64)))
+    return out
+
+
+@pytest.mark.parametrize("scene", ["plain", "contention"])
+def test_views_host_stack_sizes_agree(cuda, monkeypatch, scene):
+    """7 views (frames of 2 or 3 views and a partial last frame; no-sync
+    reserves from stacked first frames) == one view per frame: images bit for
+    bit, gradients up to the RED order. The contention scene's single views
+    take dense binning, so a stacked first frame restarts the batch with one
+    view per frame."""
+    from paper_2401_05345_b200.scene import make_dL_dpixels, make_scene, orbit_cameras
+
+    hc = scene == "contention"
+    P, W, H, V = (3000 if hc else 8000), 192, 144, 7
+    sc = make_scene(P, W, H, seed=91, high_contention=hc)
+    cams = orbit_cameras(W, H, V)
+    dL = np.stack([make_dL_dpixels(W, H, seed=100 + k) for k in range(V)]).astype(np.float32)
+    ref = _views_host(monkeypatch, 1, sc, cams, dL)
+    for stack in (2, 3):
+        got = _views_host(monkeypatch, stack, sc, cams, dL)
+        for (gi, gg), (ri, rg) in zip(got, ref):
+            assert np.array_equal(gi, ri)
+            _grad_close(gg, rg)
+
+
+def test_views_host_stacked_overflow_redo(cuda, monkeypatch):
+    """Frames of two views: frame 0 (two zoomed-out views, few instances)
+    sizes the no-sync reserve of its state; frame 2 (normal views) outgrows
+    it, raises the sticky flag and the batch is redone with host-read counts
+    -- the result equals one view per frame."""
+    from paper_2401_05345_b200.scene import make_camera, make_dL_dpixels, make_scene
+
+    P, W, H = 4000, 160, 128
+    sc = make_scene(P, W, H, seed=33)
+    cams = [make_camera(W, H, fov_x_deg=150.0)] * 2 + [make_camera(W, H, yaw_deg=d)
+                                                       for d in (0.0, 2.0, 4.0, 6.0, 8.0)]
+    V = len(cams)
+    dL = np.stack([make_dL_dpixels(W, H, seed=60 + k) for k in range(V)]).astype(np.float32)
+    ref = _views_host(monkeypatch, 1, sc, cams, dL)
+    got = _views_host(monkeypatch, 2, sc, cams, dL)
+    for (gi, gg), (ri, rg) in zip(got, ref):
+        assert np.array_equal(gi, ri)
+        _grad_close(gg, rg)

@@ -1,9 +1,10 @@
 """A/B of the batched host path (dw_render_views_host, 64 views, images
-downloaded) with and without programmatic dependent launch on its two compute
-streams (DW_VIEWS_PDL, read per call). Settings interleave, so box drift
-averages out.
+downloaded) over the values of one environment switch it reads per call:
+DW_VIEWS_STACK (views per stacked frame, profiles/r02/ab/stacked_views.md);
+the PDL record (profiles/r02/ab/pdl_two_streams.md) used a since-removed
+DW_VIEWS_PDL. Settings interleave, so box drift averages out.
 
-    python tools/ab_views_pdl.py --workload c5_3m_1080p_64views --rounds 4
+    python tools/ab_views_env.py --env DW_VIEWS_STACK --settings 1,2,3 --rounds 4
 """
 import argparse
 import json
@@ -20,7 +21,8 @@ def main():
     ap.add_argument("--workload", default="c5_3m_1080p_64views")
     ap.add_argument("--views", type=int, default=64)
     ap.add_argument("--rounds", type=int, default=4)
-    ap.add_argument("--settings", default="0,1")
+    ap.add_argument("--env", default="DW_VIEWS_STACK")
+    ap.add_argument("--settings", default="1,2,3")
     a = ap.parse_args()
     import torch
 
@@ -44,19 +46,19 @@ def main():
     settings = a.settings.split(",")
     res = {v: [] for v in settings}
     for v in settings:  # warm-up each setting (allocations, reserves)
-        os.environ["DW_VIEWS_PDL"] = v
+        os.environ[a.env] = v
         render_views_host(r, ptrs, P, cams, dL_h.data_ptr(), pol, img_h.data_ptr(),
                           grad_h.data_ptr(), s)
     torch.cuda.synchronize()
     for _ in range(a.rounds):
         for v in settings:
-            os.environ["DW_VIEWS_PDL"] = v
+            os.environ[a.env] = v
             t0 = time.perf_counter()
             render_views_host(r, ptrs, P, cams, dL_h.data_ptr(), pol, img_h.data_ptr(),
                               grad_h.data_ptr(), s)
             torch.cuda.synchronize()
             res[v].append(round((time.perf_counter() - t0) * 1e3, 2))
-    print(json.dumps({"workload": a.workload, "views": V, "ms_per_step": res,
+    print(json.dumps({"workload": a.workload, "views": V, "env": a.env, "ms_per_step": res,
                       "median": {v: statistics.median(x) for v, x in res.items()}}))
 
 
