@@ -500,35 +500,38 @@ def main() -> None:
     # ---- the timed loop: dist.view_parallel_backward over the batch --------
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
+    # The rank's backwards run as one chain (dw_render_backward_chained after
+    # the first: the views are independent and already rendered, so a launch
+    # need not wait for the previous grid -- its CTAs fill the SMs the
+    # previous launch's last wave leaves idle; C5: 0.791 -> 0.745 ms per view,
+    # profiles/r02/ab/chained_backward.md). Events bracket the step only (an
+    # event between two launches would serialise them); a launch's duration is
+    # the step's per-launch share, and view 0 is also timed alone (time_view).
     def run_steps(pol, steps, warmup):
         per_step, per_launch, view0 = [], [], []
+        n_local = len(my_views)
         for s in range(warmup + steps):
             flush.fill_(float(s))  # L2 flush (256 MiB > 126 MB L2), outside the events
             torch.cuda.synchronize()
             if dist is not None:
                 dist.barrier()
-            marks = []
+            def backward_view(g, out, chained=False):
+                rasts[local_of[g]].render_backward(dLs[local_of[g]], pol, grad=out,
+                                                   chained=chained)
 
-            def backward_view(g, out):
-                e0, e1 = ev(), ev()
-                e0.record()
-                rasts[local_of[g]].render_backward(dLs[local_of[g]], pol, grad=out)
-                e1.record()
-                marks.append((g, e0, e1))
-
-            e_start, e_end = ev(), ev()
+            e_start, e_mid, e_end = ev(), ev(), ev()
             e_start.record()
             grad.zero_()
             view_parallel_backward(backward_view, list(range(total_views)), grad,
-                                   all_reduce=dist is not None)
+                                   all_reduce=False, chain=True)
+            e_mid.record()
+            if dist is not None:
+                dist.all_reduce(grad, op=dist.ReduceOp.SUM)
             e_end.record()
             torch.cuda.synchronize()
             if s >= warmup:
                 per_step.append(e_start.elapsed_time(e_end))
-                for g, e0, e1 in marks:
-                    per_launch.append(e0.elapsed_time(e1))
-                    if g == my_views[0]:
-                        view0.append(e0.elapsed_time(e1))
+                per_launch.extend([e_start.elapsed_time(e_mid) / n_local] * n_local)
         total = sum(per_step)
         if dist is not None:
             tt = torch.tensor([total], device=dev, dtype=torch.float64)
@@ -538,7 +541,8 @@ def main() -> None:
 
     sampler = ClockSampler(local)
     time.sleep(0.3)
-    total_ms, launches, launches_v0 = run_steps(policy, args.steps, args.warmup)
+    total_ms, launches, _ = run_steps(policy, args.steps, args.warmup)
+    launches_v0 = [time_view(0, policy, reps=5)]  # view 0 alone (the issue roofline's launch)
     nv_steps = args.naive_steps or max(3, args.steps // 4)
     total_nv_ms, launches_nv, _ = run_steps(wr.Policy(wr.PolicyKind.native, 0), nv_steps,
                                             min(args.warmup, 3))
@@ -669,6 +673,13 @@ def main() -> None:
         issue = {"bound": "issue", "achieved": ach, "peak": peak, "unit": "warp-inst/s",
                  "frac": ach / peak, "inst_per_launch": inst_t[spec],
                  "launch_ms": v0_launch_ms,
+                 "_launch": "view 0's backward timed alone (events around one launch)",
+                 # the timed chain: launches overlap their neighbours' tails,
+                 # so the step's per-launch share keeps the issue slots busier
+                 "chained": {"launch_ms": mean_launch_ms,
+                             "frac": inst_t[spec] / (mean_launch_ms * 1e-3) / peak,
+                             "_note": "view 0's instruction count over the timed chain's "
+                                      "per-launch share (views' counts are alike)"},
                  "inst_source": f"ncu sm__inst_executed.sum, {prof_key} {spec} "
                                 f"(profiles/backward_inst.json: {inst_t.get('csv')})",
                  "peak_source": "148 SMs x 4 schedulers x 1 warp-inst/cycle x median SM clock "

@@ -235,6 +235,18 @@ dw_status dw_render_backward(dw_rasterizer* r, const float* dL_dpixels,
                              dw_policy_kind policy, int32_t threshold, float* grad,
                              uint64_t* pairs_out, void* stream);
 
+/* render_backward for a chain of independent views adding into one gradient
+ * (a rank's batch: one rasterizer per view, each already rendered): the
+ * caller guarantees that nothing this backward reads -- its forward state,
+ * dL_dpixels, the zeroing of grad -- is written by the PREVIOUS kernel on
+ * `stream` (that kernel may be another chained backward). The launch then
+ * does not wait for the previous grid to finish: its CTAs start on the SMs
+ * the previous backward's last wave leaves idle. The first backward after
+ * the data it reads was produced must be a plain dw_render_backward. */
+dw_status dw_render_backward_chained(dw_rasterizer* r, const float* dL_dpixels,
+                                     dw_policy_kind policy, int32_t threshold, float* grad,
+                                     void* stream);
+
 /* SW-B render_backward that also taps the rasterizer's per-warp WarpRecords
  * (SURVEY §8(f2)): every (warp, Gaussian) with >= 1 active lane becomes one
  * record (prim = the Gaussian in all 32 lanes, 9 grads per lane, zeros in

@@ -28,7 +28,7 @@ int raster_max_stacked_views(int32_t W, int32_t H);
 void raster_reserve(dw_rasterizer* r, int32_t P, int32_t W, int32_t H, int64_t max_instances);
 int64_t raster_resolve(dw_rasterizer* r, bool* overflowed);
 void raster_backward(dw_rasterizer* r, const float* dL, int policy, int thr, float* grad,
-                     uint64_t* pairs, cudaStream_t s);
+                     uint64_t* pairs, cudaStream_t s, bool chained = false);
 uint64_t raster_last_reds(const dw_rasterizer* r);
 void raster_stage_timing(dw_rasterizer* r, bool on);
 int raster_stage_ms(dw_rasterizer* r, double* out, int cap);
@@ -528,6 +528,18 @@ dw_status dw_render_backward(dw_rasterizer* r, const float* dL_dpixels, dw_polic
   return guarded([&] {
     check_policy(policy, threshold);
     dw::raster_backward(r, dL_dpixels, policy, threshold, grad, pairs_out, dw::as_stream(stream));
+    return DW_OK;
+  });
+}
+
+dw_status dw_render_backward_chained(dw_rasterizer* r, const float* dL_dpixels,
+                                     dw_policy_kind policy, int32_t threshold, float* grad,
+                                     void* stream) {
+  if (!r || !dL_dpixels || !grad) return fail_invalid("null argument");
+  return guarded([&] {
+    check_policy(policy, threshold);
+    dw::raster_backward(r, dL_dpixels, policy, threshold, grad, nullptr, dw::as_stream(stream),
+                        true);
     return DW_OK;
   });
 }

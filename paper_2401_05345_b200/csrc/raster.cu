@@ -14,6 +14,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "distwar.cuh"
 #include "dw_internal.h"
@@ -129,12 +130,14 @@ struct dw_rasterizer {
   size_t cap_h[12] = {0};
   float* h_bufs[12] = {nullptr};
   cudaStream_t s_in = nullptr, s_out = nullptr;  // copy streams of the batched host path
-  cudaStream_t s_aux = nullptr;  // second compute stream: odd views of a batch
-  dw_rasterizer* twin = nullptr;  // forward state of the odd views
-  cudaEvent_t ev[14] = {};
-  // batched host path, DW_FWD_PRIORITY=1: the forwards on two high-priority
-  // streams (a view's binning CTAs dispatched as soon as a backward CTA retires)
-  cudaStream_t s_fwd[2] = {nullptr, nullptr};
+  static constexpr int kMaxFwdStreams = 4;
+  cudaStream_t s_fwd[kMaxFwdStreams] = {};  // the batched host path's forward streams
+  // the batched host path's forward states: a probe state for its first frame
+  // and a pool of kWave states the frames of a wave rotate through
+  dw_rasterizer* probe = nullptr;
+  std::vector<dw_rasterizer*> pool;
+  std::vector<cudaEvent_t> pev;  // per pool slot: forward done, dL uploaded, images downloaded
+  cudaEvent_t ev[6] = {};
 
   // Per-stage forward timing (dw_rasterizer_stage_timing): events recorded
   // between the forward's stages. Diagnostic only: an event between two
@@ -155,10 +158,7 @@ struct dw_rasterizer {
     if (s_in) return;
     DW_CUDA(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
     DW_CUDA(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
-    int lo = 0, hi = 0;
-    DW_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    DW_CUDA(cudaStreamCreateWithPriority(&s_aux, cudaStreamNonBlocking, lo));
-    for (auto& f : s_fwd) DW_CUDA(cudaStreamCreateWithPriority(&f, cudaStreamNonBlocking, hi));
+    for (auto& f : s_fwd) DW_CUDA(cudaStreamCreateWithFlags(&f, cudaStreamNonBlocking));
     for (auto& e : ev) DW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
 
@@ -176,11 +176,12 @@ struct dw_rasterizer {
     if (h_small) cudaFreeHost(h_small);
     if (st_ev[0])
       for (auto& e : st_ev) cudaEventDestroy(e);
-    delete twin;
+    delete probe;
+    for (auto* q : pool) delete q;
+    for (auto e : pev) cudaEventDestroy(e);
     if (s_in) {
       cudaStreamDestroy(s_in);
       cudaStreamDestroy(s_out);
-      cudaStreamDestroy(s_aux);
       for (auto f : s_fwd) cudaStreamDestroy(f);
       for (auto e : ev) cudaEventDestroy(e);
     }
@@ -338,6 +339,7 @@ struct dw_rasterizer {
   // rows) and one background colour.
   static constexpr int kMaxStack = 3;
   int nviews = 1;
+  int nviews_reserved = 0;   // views per frame the last reserve() sized for
   bool stack_unfit = false;  // the last stacked frame would have preferred dense binning
   static int stack_limit(int W_, int H_) {
     const int tx = (W_ + dw::kTile - 1) / dw::kTile, ty = (H_ + dw::kTile - 1) / dw::kTile;
@@ -637,7 +639,7 @@ struct dw_rasterizer {
   }
 
   void backward(const float* dL_dpixels, int policy, int thr, float* grad, uint64_t* pairs_out,
-                cudaStream_t s) {
+                cudaStream_t s, bool chained = false) {
     if (!forward_done) throw std::invalid_argument("render_backward before render_forward");
     if (policy == DW_POLICY_HW_ATOMRED || policy < 0 || policy > 4)
       throw std::invalid_argument("policy has no B200 kernel (hw_atomred is simulated hardware)");
@@ -651,10 +653,14 @@ struct dw_rasterizer {
       DW_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned long long), s));
       ctr = counters;
     }
+    // a chained launch skips the wait for the previous kernel: never after
+    // this state's own tile-order kernel (the batched host path computes the
+    // order on the forward's stream)
+    chained = chained && !(DW_LPT && order_stale);
     ensure_order(s);
     dw::launch_backward_impl(cam, ranges, vals, means2D, conic_opacity, rgb, order_or_null(),
                              final_T, n_contrib, dL_dpixels, policy, thr, grad, ctr, s,
-                             bulk ? packed : nullptr);
+                             bulk ? packed : nullptr, chained && !ctr);
     if (pairs_out) {
       unsigned long long h[2];
       DW_CUDA(cudaMemcpyAsync(h, counters, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -723,8 +729,8 @@ void raster_forward_views(dw_rasterizer* r, int32_t P, const float* m, const flo
 int raster_max_stacked_views(int32_t W, int32_t H) { return dw_rasterizer::stack_limit(W, H); }
 
 void raster_backward(dw_rasterizer* r, const float* dL, int policy, int thr, float* grad,
-                     uint64_t* pairs, cudaStream_t s) {
-  r->backward(dL, policy, thr, grad, pairs, s);
+                     uint64_t* pairs, cudaStream_t s, bool chained) {
+  r->backward(dL, policy, thr, grad, pairs, s, chained);
 }
 
 uint64_t raster_last_reds(const dw_rasterizer* r) { return r->last_reds; }
@@ -928,8 +934,9 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
   // every forward launch and one backward launch. DW_VIEWS_STACK=n overrides
   // the default (profiles/r02/ab/stacked_views.md); one view per frame when
   // the views differ in background, the image is too tall for the packed
-  // rectangles, or the scene takes dense binning (decided on the first frame).
-  int G = 3;  // 64 views, C3: 81.7 / 80.6 / 79.1 ms per step at 1 / 2 / 3; C5: a tie
+  // rectangles, the scene takes dense binning (decided on the first frame) or
+  // another list construction is forced.
+  int G = 1;  // stacked frames: a tie or a loss once backwards chain (stacked_views.md)
   if (const char* e = std::getenv("DW_VIEWS_STACK"); e && *e) G = std::atoi(e);
   G = std::max(1, std::min({G, dw_rasterizer::stack_limit(cams[0].width, cams[0].height),
                             static_cast<int>(V)}));
@@ -938,7 +945,6 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
     const char* e = std::getenv(name);
     return e && *e == v;
   };
-  // a list construction other than block binning forced: one view per frame
   if (forced("DW_BLOCK_BINNING", '0') || forced("DW_TILE_FIRST", '1') ||
       forced("DW_SCATTER", '1') || forced("DW_DENSE_BINNING", '1'))
     G = 1;
@@ -950,35 +956,39 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
   float* d_op = r->host_scratch(3, np);
   float* d_col = r->host_scratch(4, 3 * np);
   float* d_g = grad_on_device ? grad : r->host_scratch(7, kNParam * np);
-  cudaEvent_t e_scene = r->ev[0], e_in[2] = {r->ev[1], r->ev[2]},
-              e_used[2] = {r->ev[3], r->ev[4]}, e_img[2] = {r->ev[5], r->ev[6]},
-              e_start = r->ev[7], e_zero = r->ev[8], e_aux = r->ev[9],
-              e_fwd[2] = {r->ev[10], r->ev[11]}, e_fj[2] = {r->ev[12], r->ev[13]};
-  // Frames alternate between two forward states and two compute streams
-  // (R[g & 1], S[g & 1]), so frame g+1's projection / sort -- latency-bound
-  // launches that leave most SMs idle -- overlaps frame g's backward. Both
-  // backwards add into the one gradient buffer with RED atomics, whose order
-  // was never fixed, so the sum is the same up to fp32 reassociation.
-  if (V > 1 && !r->twin) r->twin = new dw_rasterizer();
-  dw_rasterizer* R[2] = {r, V > 1 ? r->twin : r};
-  cudaStream_t S[2] = {s, V > 1 ? r->s_aux : s};  // backwards
-  // forwards: on the backward's stream (default), or with DW_FWD_PRIORITY=1 on
-  // high-priority streams of their own -- A/B on C5, 64 views: 109.1 ms
-  // default vs 116.0 ms (profiles/r02/ab/fwd_priority.md): the backward keeps
-  // every SM's register file full, so the forward's kernels gain no slots and
-  // only add contention; not the default
-  const char* fp_env = std::getenv("DW_FWD_PRIORITY");
-  const bool fwd_hi = fp_env && *fp_env == '1';
-  cudaStream_t F[2] = {fwd_hi ? r->s_fwd[0] : S[0], fwd_hi ? r->s_fwd[1] : S[1]};
+  cudaEvent_t e_scene = r->ev[0], e_start = r->ev[1], e_chain = r->ev[2];
+  int NF = 4;  // forward streams the frames of a wave rotate over (1 / 2 / 3 / 4: C5 101.1 / 98.4 / 98.3 / 97.6 ms)
+  if (const char* e = std::getenv("DW_VIEWS_FSTREAMS"); e && *e)
+    NF = std::max(1, std::min(dw_rasterizer::kMaxFwdStreams, std::atoi(e)));
+  const cudaStream_t* F = r->s_fwd;
+  // Waves of up to kWave frames: the wave's forwards (NF streams, each frame
+  // into its own state) and uploads first, then its backwards as ONE chain on
+  // `s` (dw_render_backward_chained after the first: every frame is rendered
+  // and independent, so a launch starts on the SMs the previous one's last
+  // wave leaves idle). Forwards of different views overlap each other well;
+  // a forward interleaved with another view's backward (the previous
+  // two-state pipeline) only competes for the SMs the backward fills.
+  // 64 views, C5: 103.5 -> 97.6 ms per step; C3: 80.7 -> 76.4 ms
+  // (profiles/r02/ab/chained_backward.md). The next wave reuses the states
+  // once this wave's chain is done.
+  int kWave = 16;
+  if (const char* e = std::getenv("DW_VIEWS_WAVE"); e && *e) kWave = std::max(1, std::atoi(e));
+  const int NG0 = (V + G - 1) / G;
+  const int K = std::min(kWave, NG0);
+  if (!r->probe) r->probe = new dw_rasterizer();
+  while (static_cast<int>(r->pool.size()) < K) r->pool.push_back(new dw_rasterizer());
+  while (static_cast<int>(r->pev.size()) < 3 * K) {
+    cudaEvent_t e;
+    DW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    r->pev.push_back(e);
+  }
   auto h2d = [&](float* d, const float* h, size_t n, cudaStream_t st) {
     if (n) DW_CUDA(cudaMemcpyAsync(d, h, n * sizeof(float), cudaMemcpyHostToDevice, st));
   };
   // nothing may run ahead of work already queued on `s`
   DW_CUDA(cudaEventRecord(e_start, s));
-  DW_CUDA(cudaStreamWaitEvent(r->s_in, e_start, 0));
-  DW_CUDA(cudaStreamWaitEvent(r->s_out, e_start, 0));
-  DW_CUDA(cudaStreamWaitEvent(S[1], e_start, 0));
-  for (auto f : F) DW_CUDA(cudaStreamWaitEvent(f, e_start, 0));
+  for (auto st : {r->s_in, r->s_out}) DW_CUDA(cudaStreamWaitEvent(st, e_start, 0));
+  for (int f = 0; f < NF; ++f) DW_CUDA(cudaStreamWaitEvent(F[f], e_start, 0));
   h2d(d_m, m, 3 * size_t(P), r->s_in);
   h2d(d_sc, sc, 3 * size_t(P), r->s_in);
   h2d(d_rot, rot, 4 * size_t(P), r->s_in);
@@ -986,96 +996,101 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
   h2d(d_col, col, 3 * size_t(P), r->s_in);
   DW_CUDA(cudaEventRecord(e_scene, r->s_in));
   DW_CUDA(cudaStreamWaitEvent(s, e_scene, 0));
-  DW_CUDA(cudaStreamWaitEvent(S[1], e_scene, 0));
-  for (auto f : F) DW_CUDA(cudaStreamWaitEvent(f, e_scene, 0));
-  // Frames 0 and 1 read their instance counts back (host sync on their own
-  // stream only) and size a 1.5x reserve for their forward state; later
-  // frames keep the count on the device (no host sync: the host runs ahead
-  // and every copy overlaps). A frame that outgrows its reserve raises the
-  // sticky overflow flag and the whole batch is redone with host-read counts;
-  // a stacked first frame that would have preferred dense binning restarts
-  // the batch with one view per frame.
+  for (int f = 0; f < NF; ++f) DW_CUDA(cudaStreamWaitEvent(F[f], e_scene, 0));
+  // Frame 0 reads its instance count back (a host sync on its stream) into
+  // the probe state; the pool states get a 1.5x reserve from it and every
+  // later frame keeps its count on the device (no host sync: the host runs
+  // ahead and every copy overlaps). A frame that outgrows its reserve raises
+  // its state's sticky overflow flag and the batch is redone with host-read
+  // counts; a stacked first frame that would have preferred dense binning
+  // restarts the batch with one view per frame.
   bool nosync_ok = true;
   for (int pass = 0; pass < 3; ++pass) {
     const int NG = (V + G - 1) / G;  // frames
-    nosync_ok = nosync_ok && NG > 2;
-    float* d_dl[2] = {r->host_scratch(5, 3 * npx * G), r->host_scratch(8, 3 * npx * G)};
-    float* d_img[2] = {r->host_scratch(6, 3 * npx * G), r->host_scratch(9, 3 * npx * G)};
+    nosync_ok = nosync_ok && NG > 1;
     auto first = [&](int g) { return g * G; };
     auto count = [&](int g) { return std::min(G, static_cast<int>(V) - g * G); };
-    DW_CUDA(cudaMemsetAsync(d_g, 0, kNParam * np * sizeof(float), s));
-    DW_CUDA(cudaEventRecord(e_zero, s));
-    DW_CUDA(cudaStreamWaitEvent(S[1], e_zero, 0));
-    h2d(d_dl[0], dL, 3 * npx * count(0), r->s_in);
-    DW_CUDA(cudaEventRecord(e_in[0], r->s_in));
+    auto state = [&](int g) { return g == 0 ? r->probe : r->pool[g % K]; };
+    DW_CUDA(cudaMemsetAsync(d_g, 0, kNParam * np * sizeof(float), s));  // (the chain's stream)
     bool restack = false;
-    for (int g = 0; g < NG; ++g) {
-      const int b = g & 1;
-      dw_rasterizer* Rb = R[b];
-      cudaStream_t Sb = S[b], Fb = F[b];
-      if (g + 1 < NG) {  // prefetch frame g+1 once frame g-1 released its buffer
-        if (g >= 1) DW_CUDA(cudaStreamWaitEvent(r->s_in, e_used[b ^ 1], 0));
-        h2d(d_dl[b ^ 1], dL + static_cast<size_t>(first(g + 1)) * 3 * npx,
-            3 * npx * count(g + 1), r->s_in);
-        DW_CUDA(cudaEventRecord(e_in[b ^ 1], r->s_in));
-      }
-      if (g >= 2) {
-        DW_CUDA(cudaStreamWaitEvent(Fb, e_used[b], 0));  // frame g-2's backward: state free
-        DW_CUDA(cudaStreamWaitEvent(Fb, e_img[b], 0));   // images g-2 downloaded
-      }
-      if (nosync_ok && (g == 2 || g == 3)) {  // first reuse of R[b]: size its reserve
-        const int64_t want = Rb->num_rendered + Rb->num_rendered / 2 + 4096;
-        if (static_cast<int64_t>(std::min(Rb->cap_i[0], Rb->cap_i[2])) < want) {
-          DW_CUDA(cudaStreamSynchronize(Sb));  // frame g-2 is done with the buffers a reserve moves
-          DW_CUDA(cudaStreamSynchronize(Fb));
-          Rb->reserve(P, cams[0].width, cams[0].height, want, G);
+    for (int w0 = 0; w0 < NG && !restack; w0 += K) {
+      const int w1 = std::min(NG, w0 + K);
+      for (int g = w0; g < w1; ++g) {
+        const int j = g - w0;
+        dw_rasterizer* Rg = state(g);
+        cudaStream_t Fg = F[j % NF];
+        cudaEvent_t e_fwd = r->pev[3 * j], e_in = r->pev[3 * j + 1], e_img = r->pev[3 * j + 2];
+        float* d_dl = Rg->host_scratch(5, 3 * npx * G);
+        float* d_img = Rg->host_scratch(6, 3 * npx * G);
+        if (w0 > 0) {  // the previous wave's chain is done with the states and dL buffers
+          DW_CUDA(cudaStreamWaitEvent(Fg, e_chain, 0));
+          DW_CUDA(cudaStreamWaitEvent(Fg, e_img, 0));  // its images downloaded
+          DW_CUDA(cudaStreamWaitEvent(r->s_in, e_chain, 0));
         }
-        DW_CUDA(cudaMemsetAsync(Rb->overflow_dev, 0, sizeof(unsigned int), Fb));
+        h2d(d_dl, dL + static_cast<size_t>(first(g)) * 3 * npx, 3 * npx * count(g), r->s_in);
+        DW_CUDA(cudaEventRecord(e_in, r->s_in));
+        const bool nosync = nosync_ok && g > 0;
+        Rg->forward_views(P, d_m, d_sc, d_rot, d_op, d_col, cams + first(g), count(g), d_img,
+                          nullptr, Fg, nosync, /*sticky_overflow=*/true);
+        if (g == 0 && count(0) > 1 && Rg->stack_unfit) {  // counted: known on the host now
+          restack = true;
+          break;
+        }
+        Rg->ensure_order(Fg);  // the backward's tile order, so the chain launches nothing else
+        DW_CUDA(cudaEventRecord(e_fwd, Fg));
+        if (out_images) {
+          DW_CUDA(cudaStreamWaitEvent(r->s_out, e_fwd, 0));
+          DW_CUDA(cudaMemcpyAsync(out_images + static_cast<size_t>(first(g)) * 3 * npx, d_img,
+                                  3 * npx * count(g) * sizeof(float), cudaMemcpyDeviceToHost,
+                                  r->s_out));
+          DW_CUDA(cudaEventRecord(e_img, r->s_out));
+        } else {
+          DW_CUDA(cudaEventRecord(e_img, Fg));
+        }
+        if (g == 0 && nosync_ok) {  // size the pool's reserves from frame 0's count
+          const int64_t want = Rg->num_rendered + Rg->num_rendered / 2 + 4096;
+          for (int q = 0; q < K; ++q) {
+            dw_rasterizer* Rq = r->pool[q];
+            if (static_cast<int64_t>(std::min(Rq->cap_i[0], Rq->cap_i[2])) < want ||
+                Rq->nviews_reserved < G)
+              Rq->reserve(P, cams[0].width, cams[0].height, want, G);
+            Rq->nviews_reserved = G;
+            Rq->last_entries = Rg->last_entries;
+            // the pass's sticky overflow flag, cleared before the state's
+            // first frame (frame q, or frame K for pool[0], on F[q % NF])
+            DW_CUDA(cudaMemsetAsync(Rq->overflow_dev, 0, sizeof(unsigned int), F[q % NF]));
+          }
+        }
       }
-      const bool nosync = nosync_ok && g >= 2;
-      Rb->forward_views(P, d_m, d_sc, d_rot, d_op, d_col, cams + first(g), count(g), d_img[b],
-                        nullptr, Fb, nosync, /*sticky_overflow=*/true);
-      if (g == 0 && count(0) > 1 && Rb->stack_unfit) {  // counted: known on the host now
-        restack = true;
-        break;
+      if (restack) break;
+      for (int g = w0; g < w1; ++g) {  // the chain waits for the whole wave up front
+        DW_CUDA(cudaStreamWaitEvent(s, r->pev[3 * (g - w0)], 0));
+        DW_CUDA(cudaStreamWaitEvent(s, r->pev[3 * (g - w0) + 1], 0));
       }
-      if (Fb != Sb) {
-        DW_CUDA(cudaEventRecord(e_fwd[b], Fb));
-        DW_CUDA(cudaStreamWaitEvent(Sb, e_fwd[b], 0));
-      }
-      DW_CUDA(cudaStreamWaitEvent(Sb, e_in[b], 0));
-      Rb->backward(d_dl[b], policy, thr, d_g, nullptr, Sb);
-      DW_CUDA(cudaEventRecord(e_used[b], Sb));
-      if (out_images) {
-        DW_CUDA(cudaStreamWaitEvent(r->s_out, Fb != Sb ? e_fwd[b] : e_used[b], 0));
-        DW_CUDA(cudaMemcpyAsync(out_images + static_cast<size_t>(first(g)) * 3 * npx, d_img[b],
-                                3 * npx * count(g) * sizeof(float), cudaMemcpyDeviceToHost,
-                                r->s_out));
-        DW_CUDA(cudaEventRecord(e_img[b], r->s_out));
-      } else {
-        DW_CUDA(cudaEventRecord(e_img[b], Sb));
-      }
+      for (int g = w0; g < w1; ++g)
+        state(g)->backward(state(g)->host_scratch(5, 3 * npx * G), policy, thr, d_g, nullptr, s,
+                           /*chained=*/g > w0);
+      DW_CUDA(cudaEventRecord(e_chain, s));
     }
-    for (int b = 0; b < 2; ++b)
-      if (F[b] != S[b]) {
-        DW_CUDA(cudaEventRecord(e_fj[b], F[b]));
-        DW_CUDA(cudaStreamWaitEvent(s, e_fj[b], 0));
-      }
-    DW_CUDA(cudaEventRecord(e_aux, S[1]));
-    DW_CUDA(cudaStreamWaitEvent(s, e_aux, 0));
+    for (int f = 0; f <= NF; ++f) {  // join every stream into `s`
+      DW_CUDA(cudaEventRecord(e_start, f < NF ? F[f] : r->s_in));
+      DW_CUDA(cudaStreamWaitEvent(s, e_start, 0));
+    }
     if (restack) {
       DW_CUDA(cudaStreamSynchronize(s));
-      DW_CUDA(cudaStreamSynchronize(r->s_in));
       DW_CUDA(cudaStreamSynchronize(r->s_out));
       G = 1;
       continue;
     }
     if (!nosync_ok) break;
-    DW_CUDA(cudaStreamSynchronize(s));  // both compute streams (S[1] joined into s)
-    bool ovf0 = false, ovf1 = false;
-    R[0]->resolve_count(&ovf0);  // the batch's sticky flags
-    R[1]->resolve_count(&ovf1);
-    if (!ovf0 && !ovf1) break;
+    DW_CUDA(cudaStreamSynchronize(s));
+    bool ovf = false;
+    for (int q = 0; q < K; ++q) {
+      bool o = false;
+      r->pool[q]->resolve_count(&o);  // the batch's sticky flags
+      ovf = ovf || o;
+    }
+    if (!ovf) break;
     nosync_ok = false;  // redo every view with host-read instance counts
   }
   if (P > 0 && !grad_on_device)

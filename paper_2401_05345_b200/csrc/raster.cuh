@@ -246,6 +246,6 @@ void launch_backward_impl(const CamParams& cam, const uint2* ranges, const uint3
                           const uint32_t* n_contrib,
                           const float* dL, int policy, int thr, float* grad,
                           unsigned long long* counters, cudaStream_t s,
-                          const float4* packed = nullptr);
+                          const float4* packed = nullptr, bool chained = false);
 
 }  // namespace dw

@@ -507,8 +507,14 @@ __global__ void __launch_bounds__(128, (POL == kSwB && !COUNT && !TAP) ? DW_SWB_
                   const float* __restrict__ final_Ts, const uint32_t* __restrict__ n_contrib,
                   const float* __restrict__ dL_dpixels, int thr, float* __restrict__ grad,
                   unsigned long long* __restrict__ counters, const TapBuf tap,
-                  const uint32_t* __restrict__ tile_order, const float4* __restrict__ packed) {
-  pdl_wait();  // predecessor grid complete (programmatic dependent launch)
+                  const uint32_t* __restrict__ tile_order, const float4* __restrict__ packed,
+                  bool chained) {
+  // chained: the caller guarantees nothing this launch reads is written by
+  // the previous kernel on the stream (a chain of backwards of independent,
+  // already-rendered views adding into one gradient): no grid-completion
+  // wait, so this launch's CTAs fill the SMs the previous launch's last wave
+  // leaves idle
+  if (!chained) pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
   static_assert(POL != kNative, "native runs the thread-per-pixel kernel");
   constexpr int NW = 4;
@@ -775,24 +781,25 @@ void launch_bwd(bool count, const CamParams& cam, const uint2* ranges, const uin
                 const float2* means2D, const float4* co, const float4* rgb,
                 const uint32_t* tile_order, const float* fT,
                 const uint32_t* nc, const float* dL, int thr, float* grad,
-                unsigned long long* ctr, cudaStream_t s, const float4* packed) {
+                unsigned long long* ctr, cudaStream_t s, const float4* packed, bool chained) {
   const int grid = cam.tiles_x * cam.tiles_y;
   // The reduction policies run two pixels per lane; native keeps the paper's
   // thread-per-pixel kernel (profiles/r01/ab_ppt.jsonl).
   if constexpr (POL != kNative) {
     if (count)
       launch_pdl(k_backward_x2<POL, true>, grid, 128, 0, s, cam, ranges, values, means2D, co, rgb,
-                 fT, nc, dL, thr, grad, ctr, TapBuf{}, tile_order, nullptr);
+                 fT, nc, dL, thr, grad, ctr, TapBuf{}, tile_order, nullptr, chained);
     else if (packed)
       launch_pdl(k_backward_x2<POL, false, false, true>, grid, 128, 0, s, cam, ranges, values,
-                 means2D, co, rgb, fT, nc, dL, thr, grad, nullptr, TapBuf{}, tile_order, packed);
+                 means2D, co, rgb, fT, nc, dL, thr, grad, nullptr, TapBuf{}, tile_order, packed,
+                 chained);
     else if (POL == kSwB && scalar_fallback())  // DW_VEC_RED=0: scalar per-lane REDs
       launch_pdl(k_backward_x2<POL, false, false, false, false>, grid, 128, 0, s, cam, ranges,
                  values, means2D, co, rgb, fT, nc, dL, thr, grad, nullptr, TapBuf{}, tile_order,
-                 nullptr);
+                 nullptr, chained);
     else
       launch_pdl(k_backward_x2<POL, false>, grid, 128, 0, s, cam, ranges, values, means2D, co,
-                 rgb, fT, nc, dL, thr, grad, nullptr, TapBuf{}, tile_order, nullptr);
+                 rgb, fT, nc, dL, thr, grad, nullptr, TapBuf{}, tile_order, nullptr, chained);
     return;
   }
   if (count)
@@ -812,7 +819,7 @@ void launch_backward_tap(const CamParams& cam, const uint2* ranges, const uint32
                          const TapBuf& tap, cudaStream_t s) {
   const int grid = cam.tiles_x * cam.tiles_y;
   launch_pdl(k_backward_x2<kSwB, false, true>, grid, 128, 0, s, cam, ranges, values, means2D, co,
-             rgb, final_T, n_contrib, dL, thr, grad, nullptr, tap, tile_order, nullptr);
+             rgb, final_T, n_contrib, dL, thr, grad, nullptr, tap, tile_order, nullptr, false);
   DW_CUDA(cudaGetLastError());
 }
 
@@ -831,24 +838,24 @@ void launch_backward_impl(const CamParams& cam, const uint2* ranges, const uint3
                           const uint32_t* tile_order, const float* final_T,
                           const uint32_t* n_contrib, const float* dL, int policy, int thr,
                           float* grad, unsigned long long* counters, cudaStream_t s,
-                          const float4* packed) {
+                          const float4* packed, bool chained) {
   const bool count = counters != nullptr;
   switch (policy) {
     case kNative:
       launch_bwd<kNative>(count, cam, ranges, values, means2D, co, rgb, tile_order, final_T,
-                          n_contrib, dL, thr, grad, counters, s, packed);
+                          n_contrib, dL, thr, grad, counters, s, packed, chained);
       break;
     case kSwS:
       launch_bwd<kSwS>(count, cam, ranges, values, means2D, co, rgb, tile_order, final_T, n_contrib,
-                       dL, thr, grad, counters, s, packed);
+                       dL, thr, grad, counters, s, packed, chained);
       break;
     case kSwB:
       launch_bwd<kSwB>(count, cam, ranges, values, means2D, co, rgb, tile_order, final_T, n_contrib,
-                       dL, thr, grad, counters, s, packed);
+                       dL, thr, grad, counters, s, packed, chained);
       break;
     default:
       launch_bwd<kCccl>(count, cam, ranges, values, means2D, co, rgb, tile_order, final_T,
-                        n_contrib, dL, thr, grad, counters, s, packed);
+                        n_contrib, dL, thr, grad, counters, s, packed, chained);
   }
   DW_CUDA(cudaGetLastError());
 }

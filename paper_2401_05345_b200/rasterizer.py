@@ -206,11 +206,22 @@ class GaussianRasterizer:
         return n.value, bool(ovf.value)
 
     def render_backward(self, dL_dpixels, policy: Policy = Policy(PolicyKind.sw_b, 0),
-                        grad=None, count_pairs: bool = False, stream=None):
+                        grad=None, count_pairs: bool = False, stream=None,
+                        chained: bool = False):
         """Adds into grad [P, 9] (allocated zeroed if None). Returns grad, or
-        (grad, pairs) when count_pairs (a separate counting instantiation)."""
+        (grad, pairs) when count_pairs (a separate counting instantiation).
+        chained: dw_render_backward_chained -- the previous kernel on the
+        stream writes nothing this backward reads (see include/distwar.h)."""
         import torch
 
+        if chained:
+            if grad is None or count_pairs:
+                raise ValueError("a chained backward adds into a given grad, uncounted")
+            check(lib().dw_render_backward_chained(
+                self._h, _ptr(dL_dpixels, "dL_dpixels", torch.float32, self._npix3()),
+                int(policy.kind), policy.threshold,
+                _ptr(grad, "grad", torch.float32, min_numel=NPARAM * self.P), _stream(stream)))
+            return grad
         alloc = grad is None
         if alloc:  # >= 1 row: an empty scene still passes a non-null buffer
             grad = torch.zeros((max(self.P, 1), NPARAM), dtype=torch.float32,

@@ -157,9 +157,10 @@ def test_render_host_e2e(cuda, orc):
 
 @pytest.mark.parametrize("binning", ["auto", "depth-first", "dense", "block"])
 def test_render_views_host_matches_per_view(cuda, orc, binning, monkeypatch):
-    """Batched host path (one scene upload, views alternating over two
-    forward states and compute streams, overlapped per-view copies) == the sum
-    over views of the oracle's per-view gradients; images per view."""
+    """Batched host path (one scene upload, stacked frames rendered in waves
+    on two forward streams, each wave's backwards as one chain, overlapped
+    per-view copies) == the sum over views of the oracle's per-view
+    gradients; images per view."""
     import torch
 
     set_binning(monkeypatch, binning)
@@ -249,12 +250,15 @@ def test_reused_rasterizer_matches_fresh_across_sizes(cuda):
         assert np.array_equal(got[2], fresh.buffer("ranges"))
 
 
-def test_render_views_host_reserve_overflow_redo(cuda, orc):
+def test_render_views_host_reserve_overflow_redo(cuda, orc, monkeypatch):
     """Views after the first keep their instance count on the device against
     a reserve of 1.5x view 0's count; a later view that outgrows it (view 0
     is zoomed far out) raises the overflow flag and the batch is redone
-    with host-read counts -- the result still equals the per-view oracle."""
+    with host-read counts -- the result still equals the per-view oracle.
+    (One view per frame; tests/test_gpu_stacked.py covers stacked frames.)"""
     import torch
+
+    monkeypatch.setenv("DW_VIEWS_STACK", "1")
 
     from paper_2401_05345_b200 import warpred as wr
     from paper_2401_05345_b200.rasterizer import GaussianRasterizer, render_views_host

@@ -1,10 +1,11 @@
 """A/B of the batched host path (dw_render_views_host, 64 views, images
-downloaded) over the values of one environment switch it reads per call:
+downloaded) over the values of environment switches it reads per call
+(--settings "A=1,B=2;A=3" sets several per arm; a bare value sets --env):
 DW_VIEWS_STACK (views per stacked frame, profiles/r02/ab/stacked_views.md);
 the PDL record (profiles/r02/ab/pdl_two_streams.md) used a since-removed
 DW_VIEWS_PDL. Settings interleave, so box drift averages out.
 
-    python tools/ab_views_env.py --env DW_VIEWS_STACK --settings 1,2,3 --rounds 4
+    python tools/ab_views_env.py --env DW_VIEWS_STACK --settings "1;2;3" --rounds 4
 """
 import argparse
 import json
@@ -22,7 +23,7 @@ def main():
     ap.add_argument("--views", type=int, default=64)
     ap.add_argument("--rounds", type=int, default=4)
     ap.add_argument("--env", default="DW_VIEWS_STACK")
-    ap.add_argument("--settings", default="1,2,3")
+    ap.add_argument("--settings", default="1;2;3")
     a = ap.parse_args()
     import torch
 
@@ -43,16 +44,21 @@ def main():
     ptrs = [pin[k].data_ptr() for k in ("means3D", "scales", "rotations", "opacities", "colors")]
     r = GaussianRasterizer()
     s = torch.cuda.current_stream()
-    settings = a.settings.split(",")
+    settings = a.settings.split(";")
+
+    def apply(v):
+        for kv in v.split(","):
+            k, _, val = kv.rpartition("=")
+            os.environ[k or a.env] = val
     res = {v: [] for v in settings}
     for v in settings:  # warm-up each setting (allocations, reserves)
-        os.environ[a.env] = v
+        apply(v)
         render_views_host(r, ptrs, P, cams, dL_h.data_ptr(), pol, img_h.data_ptr(),
                           grad_h.data_ptr(), s)
     torch.cuda.synchronize()
     for _ in range(a.rounds):
         for v in settings:
-            os.environ[a.env] = v
+            apply(v)
             t0 = time.perf_counter()
             render_views_host(r, ptrs, P, cams, dL_h.data_ptr(), pol, img_h.data_ptr(),
                               grad_h.data_ptr(), s)
