@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--views", type=int, default=16)
     ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--threshold", type=int, default=15)
+    ap.add_argument("--modes", default="events,plain,chained")
     a = ap.parse_args()
     import torch
 
@@ -45,6 +46,13 @@ def main():
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
     def step(mode):
+        # "chained+DW_BWD_WARPS=2": a mode with environment switches set for it
+        mode, *envs = mode.split("+")
+        for k in ("DW_BWD_WARPS",):
+            os.environ.pop(k, None)
+        for kv in envs:
+            k, _, v = kv.partition("=")
+            os.environ[k] = v
         flush.fill_(1.0)
         torch.cuda.synchronize()
         e0, e1 = ev(), ev()
@@ -62,19 +70,21 @@ def main():
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / len(rasts)
 
-    modes = ("events", "plain", "chained")
+    modes = tuple(a.modes.split(","))
     for m in modes:
         step(m)
     res = {m: [] for m in modes}
     for _ in range(a.rounds):
         for m in modes:
             res[m].append(round(step(m), 4))
-    g_chain = grad.clone()
-    step("plain")
-    rel = float((grad - g_chain).norm() / grad.norm())
+    step(modes[-1])
+    g_last = grad.clone()
+    step(modes[0])
+    rel = float((grad - g_last).norm() / grad.norm())
     print(json.dumps({"workload": a.workload, "views": a.views, "ms_per_view": res,
                       "median": {m: statistics.median(v) for m, v in res.items()},
-                      "grad_rel_diff_chained_vs_plain": rel}))
+                      "lib": os.environ.get("DISTWAR_LIB", "libdistwar.so"),
+                      f"grad_rel_diff_{modes[-1]}_vs_{modes[0]}": rel}))
 
 
 if __name__ == "__main__":
