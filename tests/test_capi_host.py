@@ -63,6 +63,24 @@ def test_null_arguments_are_invalid_argument():
     assert lib.dw_trace_record_count(None) == -1
     assert lib.dw_render_backward(None, None, 2, 0, None, None, None) == 1
     assert lib.dw_rasterizer_buffer(None, 0, None, None) == 1
+    assert lib.dw_render_backward_chained(None, None, 2, 0, None, None) == 1
+    assert lib.dw_render_forward_views(None, 0, None, None, None, None, None, None, 1, None,
+                                       None, None) == 1
+
+
+def test_max_stacked_views_without_gpu():
+    """Stacked frames (dw_render_forward_views): block binning packs tile rows
+    into 8 bits, so a frame holds at most 255 tile rows, and at most 3 views."""
+    from paper_2401_05345_b200 import _lib
+    from paper_2401_05345_b200.rasterizer import max_stacked_views
+
+    assert max_stacked_views(1920, 1080) == 3   # 68 tile rows per view
+    assert max_stacked_views(256, 256) == 3
+    assert max_stacked_views(1920, 1440) == 2   # 90 rows
+    assert max_stacked_views(1920, 4320) == 1   # 270 rows: no block binning at all
+    assert max_stacked_views(5000, 64) == 1     # 313 tile columns
+    out = C.c_int32()
+    assert _lib.lib().dw_rasterizer_max_stacked_views(0, 10, C.byref(out)) == 1
 
 
 def test_policy_validation_without_gpu():

@@ -1,10 +1,12 @@
-"""Stacked frames (dw_render_forward_views and the batched host path): several
-views of one scene share every launch of the forward and one backward launch.
+"""Batched views: stacked frames (dw_render_forward_views: several views of
+one scene share every launch of the forward and one backward launch), chained
+backwards (dw_render_backward_chained) and the batched host path built on
+them.
 The bar is the single-view path itself: per-tile lists, images, final_T and
 n_contrib bit for bit (view v's ids offset by v*P in the frame), gradients
 equal to the per-view sum up to fp32 reassociation of the RED order -- and
-through tests/test_gpu_raster.py's views-host tests (default stacking) the
-oracle's per-view bounds.
+through tests/test_gpu_raster.py's views-host tests (the default host path:
+waves of forwards, chained backwards) the oracle's per-view bounds.
 """
 import numpy as np
 import pytest
@@ -142,9 +144,9 @@ def test_views_host_stack_sizes_agree(cuda, monkeypatch, scene):
 
 def test_views_host_stacked_overflow_redo(cuda, monkeypatch):
     """Frames of two views: frame 0 (two zoomed-out views, few instances)
-    sizes the no-sync reserve of its state; frame 2 (normal views) outgrows
-    it, raises the sticky flag and the batch is redone with host-read counts
-    -- the result equals one view per frame."""
+    sizes the no-sync reserves of the pool states; frame 1 (normal views)
+    outgrows its reserve, raises the sticky flag and the batch is redone with
+    host-read counts -- the result equals one view per frame."""
     from paper_2401_05345_b200.scene import make_camera, make_dL_dpixels, make_scene
 
     P, W, H = 4000, 160, 128
@@ -158,3 +160,44 @@ def test_views_host_stacked_overflow_redo(cuda, monkeypatch):
     for (gi, gg), (ri, rg) in zip(got, ref):
         assert np.array_equal(gi, ri)
         _grad_close(gg, rg)
+
+
+def test_chained_backwards_equal_plain(cuda):
+    """A chain of independent views' backwards (the first plain, the rest
+    dw_render_backward_chained -- no wait for the previous grid) adds the same
+    gradients as plain launches; a chained call right after its own forward
+    (tile order not yet computed) falls back to a plain launch."""
+    import torch
+
+    from paper_2401_05345_b200 import warpred as wr
+    from paper_2401_05345_b200.rasterizer import GaussianRasterizer
+    from paper_2401_05345_b200.scene import make_dL_dpixels, orbit_cameras
+
+    P, W, H = 30000, 320, 240
+    sc = _scene(cuda, P, W, H, seed=12)
+    args = [sc[k] for k in SCENE_KEYS]
+    cams = orbit_cameras(W, H, 4)
+    dLs = [torch.from_numpy(make_dL_dpixels(W, H, seed=20 + k)).to(cuda) for k in range(4)]
+    pol = wr.Policy(wr.PolicyKind.sw_b, 14)
+    rs = []
+    for c in cams:
+        r = GaussianRasterizer()
+        r.render_forward(*args, c)
+        rs.append(r)
+    # first backward of each state right after its forward, chained: the tile
+    # order is computed first and the launch waits for it
+    g0 = torch.zeros((P, 9), dtype=torch.float32, device=cuda)
+    for k, (r, dL) in enumerate(zip(rs, dLs)):
+        r.render_backward(dL, pol, grad=g0, chained=k > 0)
+    plain = torch.zeros((P, 9), dtype=torch.float32, device=cuda)
+    for r, dL in zip(rs, dLs):
+        r.render_backward(dL, pol, grad=plain)
+    chain = torch.zeros((P, 9), dtype=torch.float32, device=cuda)
+    for rep in range(3):  # back-to-back chains: launches overlap their neighbours
+        for k, (r, dL) in enumerate(zip(rs, dLs)):
+            r.render_backward(dL, pol, grad=chain, chained=k > 0 or rep > 0)
+    want = plain.cpu().numpy().astype(np.float64)
+    _grad_close(g0.cpu().numpy().astype(np.float64), want)
+    _grad_close(chain.cpu().numpy().astype(np.float64) / 3.0, want)
+    with pytest.raises(ValueError):
+        rs[0].render_backward(dLs[0], pol, chained=True)  # needs a given gradient
