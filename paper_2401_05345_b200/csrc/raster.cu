@@ -653,12 +653,16 @@ struct dw_rasterizer {
       DW_CUDA(cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned long long), s));
       ctr = counters;
     }
-    // a chained launch skips the wait for the previous kernel: never after
-    // this state's own tile-order kernel (the batched host path computes the
-    // order on the forward's stream)
-    chained = chained && !(DW_LPT && order_stale);
-    ensure_order(s);
-    dw::launch_backward_impl(cam, ranges, vals, means2D, conic_opacity, rgb, order_or_null(),
+    // A chained launch skips the wait for the previous kernel, so it launches
+    // nothing before itself, and takes the tiles in their natural (row-major)
+    // order: longest-list-first only shortens a lone launch's last wave, which
+    // a chain overlaps anyway (C5: 0.7496 vs 0.7493 ms per view), while
+    // neighbouring tiles running together re-read far less -- DRAM reads of
+    // the C5 view 0 backward 439 MB in LPT order vs 339 MB (= the algorithmic
+    // bytes) in row order (profiles/r02/ab/chained_backward.md).
+    if (!chained) ensure_order(s);
+    dw::launch_backward_impl(cam, ranges, vals, means2D, conic_opacity, rgb,
+                             chained ? nullptr : order_or_null(),
                              final_T, n_contrib, dL_dpixels, policy, thr, grad, ctr, s,
                              bulk ? packed : nullptr, chained && !ctr);
     if (pairs_out) {

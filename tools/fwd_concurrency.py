@@ -88,7 +88,49 @@ def main():
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / len(cams)
 
+    def run_waves(nstreams):
+        """All views' forwards rotating over `nstreams` streams (one state per
+        view), then their backwards as one chain -- the batched host path's
+        device work without its copies."""
+        rs_all = [GaussianRasterizer() for _ in cams]
+        sts = [torch.cuda.Stream() for _ in range(nstreams)]
+        for r in rs_all:
+            r.render_forward(*args, cams[0])
+        imgs_all = [torch.empty((3, H, W), device=dev) for _ in cams]
+        rad_all = [torch.empty(P, dtype=torch.int32, device=dev) for _ in cams]
+        for r in rs_all:
+            r.reserve(P, W, H, int(r.num_rendered * 1.5) + 4096)
+
+        def once():
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for s in sts:
+                s.wait_event(e0)
+            for k, cam in enumerate(cams):
+                rs_all[k].render_forward_async(*args, cam, imgs_all[k], rad_all[k],
+                                               stream=sts[k % nstreams])
+            cur = torch.cuda.current_stream()
+            e_f = torch.cuda.Event(enable_timing=True)
+            for s in sts:
+                cur.wait_stream(s)
+            e_f.record()
+            for k in range(len(cams)):
+                rs_all[k].render_backward(dL, pol, grad=grad, chained=k > 0)
+            e1.record()
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e_f) / len(cams), e0.elapsed_time(e1) / len(cams)
+
+        once()
+        runs = [once() for _ in range(3)]
+        return (round(statistics.median(r[0] for r in runs), 4),
+                round(statistics.median(r[1] for r in runs), 4))
+
     out = {}
+    for ns in (1, 2, 4):
+        f, t = run_waves(ns)
+        out[f"waves_{ns}streams_fwd"] = f
+        out[f"waves_{ns}streams_total"] = t
     run_grouped()
     out["fwd_pair_then_bwd"] = round(statistics.median(run_grouped() for _ in range(3)), 4)
     for name, pairs, bwd in (("fwd_serial", False, False), ("fwd_two_streams", True, False),
