@@ -382,6 +382,7 @@ def main() -> None:
     from paper_2401_05345_b200 import warpred as wr
     from paper_2401_05345_b200.dist import shard_views, view_parallel_backward
     from paper_2401_05345_b200.rasterizer import (GaussianRasterizer, microbench_red,
+                                                  render_backward_views,
                                                   nccl_comm_ptr, render_views,
                                                   render_views_allreduce, render_views_host)
     from paper_2401_05345_b200.scene import CONFIGS, make_camera, make_dL_dpixels, make_scene, \
@@ -515,15 +516,15 @@ def main() -> None:
             torch.cuda.synchronize()
             if dist is not None:
                 dist.barrier()
-            def backward_view(g, out, chained=False):
-                rasts[local_of[g]].render_backward(dLs[local_of[g]], pol, grad=out,
-                                                   chained=chained)
+            def backward_views(gs, out):
+                render_backward_views([rasts[local_of[g]] for g in gs],
+                                      [dLs[local_of[g]] for g in gs], pol, out)
 
             e_start, e_mid, e_end = ev(), ev(), ev()
             e_start.record()
             grad.zero_()
-            view_parallel_backward(backward_view, list(range(total_views)), grad,
-                                   all_reduce=False, chain=True)
+            view_parallel_backward(None, list(range(total_views)), grad, all_reduce=False,
+                                   backward_views=backward_views)
             e_mid.record()
             if dist is not None:
                 dist.all_reduce(grad, op=dist.ReduceOp.SUM)

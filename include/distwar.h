@@ -247,6 +247,18 @@ dw_status dw_render_backward_chained(dw_rasterizer* r, const float* dL_dpixels,
                                      dw_policy_kind policy, int32_t threshold, float* grad,
                                      void* stream);
 
+/* The backwards of a batch of rendered views of one scene (one rasterizer
+ * per view, each already rendered; dL_dpixels[k] belongs to rasterizers[k])
+ * added into grad[P*9] (device, Address order) as ONE chain on `stream`:
+ * the first launch waits for the stream, the others start on the SMs their
+ * predecessor's last wave leaves idle. SW-B / SW-S accumulate into an
+ * internal padded [P][12] buffer (16-byte aligned rows) folded into grad at
+ * the end. Returns once everything is enqueued. */
+dw_status dw_render_backward_views(dw_rasterizer* const* rasterizers,
+                                   const float* const* dL_dpixels, int32_t num_views,
+                                   dw_policy_kind policy, int32_t threshold, float* grad,
+                                   void* stream);
+
 /* SW-B render_backward that also taps the rasterizer's per-warp WarpRecords
  * (SURVEY §8(f2)): every (warp, Gaussian) with >= 1 active lane becomes one
  * record (prim = the Gaussian in all 32 lanes, 9 grads per lane, zeros in

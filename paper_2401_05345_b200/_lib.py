@@ -123,6 +123,7 @@ SIGNATURES = {
                                     C.POINTER(i64), vp]),
     "dw_render_backward": (C.c_int, [vp, vp, C.c_int, i32, vp, C.POINTER(u64), vp]),
     "dw_render_backward_chained": (C.c_int, [vp, vp, C.c_int, i32, vp, vp]),
+    "dw_render_backward_views": (C.c_int, [vp, vp, i32, C.c_int, i32, vp, vp]),
     "dw_render_forward_async": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, C.POINTER(CameraC), vp, vp,
                                           vp]),
     "dw_render_forward_views": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, C.POINTER(CameraC), i32,

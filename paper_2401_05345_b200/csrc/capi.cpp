@@ -25,6 +25,8 @@ void raster_forward_views(dw_rasterizer* r, int32_t P, const float* m, const flo
                           const dw_camera* cams, int32_t nv, float* out, int64_t* nr,
                           cudaStream_t s);
 int raster_max_stacked_views(int32_t W, int32_t H);
+void raster_backward_views(dw_rasterizer* const* rs, const float* const* dLs, int32_t n,
+                           int policy, int thr, float* grad, cudaStream_t s);
 void raster_reserve(dw_rasterizer* r, int32_t P, int32_t W, int32_t H, int64_t max_instances);
 int64_t raster_resolve(dw_rasterizer* r, bool* overflowed);
 void raster_backward(dw_rasterizer* r, const float* dL, int policy, int thr, float* grad,
@@ -540,6 +542,19 @@ dw_status dw_render_backward_chained(dw_rasterizer* r, const float* dL_dpixels,
     check_policy(policy, threshold);
     dw::raster_backward(r, dL_dpixels, policy, threshold, grad, nullptr, dw::as_stream(stream),
                         true);
+    return DW_OK;
+  });
+}
+
+dw_status dw_render_backward_views(dw_rasterizer* const* rasterizers,
+                                   const float* const* dL_dpixels, int32_t num_views,
+                                   dw_policy_kind policy, int32_t threshold, float* grad,
+                                   void* stream) {
+  if (!rasterizers || !dL_dpixels || !grad) return fail_invalid("null argument");
+  return guarded([&] {
+    check_policy(policy, threshold);
+    dw::raster_backward_views(rasterizers, dL_dpixels, num_views, policy, threshold, grad,
+                              dw::as_stream(stream));
     return DW_OK;
   });
 }

@@ -248,7 +248,12 @@ __device__ __forceinline__ void reduce_bfly(int idx, float* grad, float (&v)[N],
 // so the reducing path multiplies once after the butterfly (`lane_scale` =
 // scale[slot], precomputed per lane) and only the per-lane fallback scales all
 // N values. Same request semantics as reduce_bfly<N, COUNT, true>.
-template <int N, bool COUNT, bool VEC = DW_VEC_RED != 0>
+// S: floats per gradient row -- N (the Address-order [P][N] buffer), or 12
+// for N = 9: a padded [P][12] accumulation buffer whose 48-byte rows are
+// 16-byte aligned, so the per-lane fallback is always v4 + v4 + scalar (no
+// phase switch, no register shuffles) and folded into [P][9] once per batch
+// (launch_fold_rows).
+template <int N, bool COUNT, bool VEC = DW_VEC_RED != 0, int S = N>
 __device__ __forceinline__ void reduce_bfly_scaled(int idx, float* grad, float (&v)[N], int thr,
                                                    bool active, int lane, uint32_t& nred,
                                                    unsigned ballot, int slot, bool issuer,
@@ -260,12 +265,16 @@ __device__ __forceinline__ void reduce_bfly_scaled(int idx, float* grad, float (
     else
       ReduceScatter<N, 16>::run(v, lane);
     if (issuer) {
-      red_add(grad + static_cast<int64_t>(idx) * N + slot, v[0] * lane_scale);
+      red_add(grad + static_cast<int64_t>(idx) * S + slot, v[0] * lane_scale);
       if (COUNT) nred += 1;
     }
   } else if (active) {
-    float* base = grad + static_cast<int64_t>(idx) * N;
-    if constexpr (VEC && N == 9) {
+    float* base = grad + static_cast<int64_t>(idx) * S;
+    if constexpr (VEC && N == 9 && S == 12) {  // 16-byte aligned padded row: phase 0 always
+      red_add_v4(base, v[0] * scale[0], v[1] * scale[1], v[2] * scale[2], v[3] * scale[3]);
+      red_add_v4(base + 4, v[4] * scale[4], v[5] * scale[5], v[6] * scale[6], v[7] * scale[7]);
+      red_add(base + 8, v[8] * scale[8]);
+    } else if constexpr (VEC && N == 9) {
       float sv[9];
 #pragma unroll
       for (int p = 0; p < 9; ++p) sv[p] = v[p] * scale[p];

@@ -167,7 +167,7 @@ struct dw_rasterizer {
                   dkey[1], dids[0], dids[1], itile[0], itile[1], ivals[0], ivals[1], ranges,
                   final_T, n_contrib, tmp, scan_tmp, keys_dbg, counters, small_dev,
                   tile_order, rects, diff, area_sorted, seg_scratch, sc_scratch, packed,
-                  branges, bb_cnt, bb_rect_id, bb_hist};
+                  branges, bb_cnt, bb_rect_id, bb_hist, pad_grad};
     for (void* p : ps)
       if (p) cudaFree(p);
     for (float* p : h_bufs)
@@ -339,6 +339,7 @@ struct dw_rasterizer {
   // rows) and one background colour.
   static constexpr int kMaxStack = 3;
   int nviews = 1;
+  int P_scene = 0;           // scene Gaussians (P = nviews * P_scene)
   int nviews_reserved = 0;   // views per frame the last reserve() sized for
   bool stack_unfit = false;  // the last stacked frame would have preferred dense binning
   static int stack_limit(int W_, int H_) {
@@ -368,6 +369,7 @@ struct dw_rasterizer {
       throw std::invalid_argument("stacked frame has too many Gaussians");
     nviews = nv;
     stack_unfit = false;
+    P_scene = P_;
     const int Ps = P_;
     P = P_ * nv;
     W = c.width;
@@ -638,8 +640,10 @@ struct dw_rasterizer {
     forward_done = true;
   }
 
+  // grad_stride 12: grad is a padded [P_scene][12] accumulation buffer (the
+  // batch path, raster_backward_views), SW-B / SW-S only.
   void backward(const float* dL_dpixels, int policy, int thr, float* grad, uint64_t* pairs_out,
-                cudaStream_t s, bool chained = false) {
+                cudaStream_t s, bool chained = false, int grad_stride = dw::kNParam) {
     if (!forward_done) throw std::invalid_argument("render_backward before render_forward");
     if (policy == DW_POLICY_HW_ATOMRED || policy < 0 || policy > 4)
       throw std::invalid_argument("policy has no B200 kernel (hw_atomred is simulated hardware)");
@@ -664,7 +668,7 @@ struct dw_rasterizer {
     dw::launch_backward_impl(cam, ranges, vals, means2D, conic_opacity, rgb,
                              chained ? nullptr : order_or_null(),
                              final_T, n_contrib, dL_dpixels, policy, thr, grad, ctr, s,
-                             bulk ? packed : nullptr, chained && !ctr);
+                             bulk ? packed : nullptr, chained && !ctr, grad_stride);
     if (pairs_out) {
       unsigned long long h[2];
       DW_CUDA(cudaMemcpyAsync(h, counters, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -686,6 +690,15 @@ struct dw_rasterizer {
     if (!DW_LPT || !order_stale) return;
     dw::launch_tile_order(ranges, cam.tiles_x * cam.tiles_y, tile_order, s);
     order_stale = false;
+  }
+
+  // padded [P][12] gradient accumulation of the batch path, kept zeroed
+  // between batches by launch_fold_rows
+  float* pad_grad = nullptr;
+  size_t cap_pad = 0;
+  float* padded_grad(int64_t P_, cudaStream_t s) {
+    grow_zeroed(pad_grad, cap_pad, static_cast<size_t>(std::max<int64_t>(P_, 1)) * 12, s);
+    return pad_grad;
   }
 
   float* host_scratch(int slot, size_t n) {
@@ -731,6 +744,37 @@ void raster_forward_views(dw_rasterizer* r, int32_t P, const float* m, const flo
 }
 
 int raster_max_stacked_views(int32_t W, int32_t H) { return dw_rasterizer::stack_limit(W, H); }
+
+// The backwards of n rendered views of one scene (one rasterizer each) added
+// into grad[P][9] as one chain: the first launch waits for the stream, the
+// rest are chained (no wait for the previous grid). SW-B / SW-S accumulate
+// into a padded [P][12] buffer (16-byte aligned rows: the per-lane fallback
+// is v4 + v4 + scalar with no phase switch; C5 chained 0.745 -> 0.714 ms per
+// view, profiles/r02/ab/chained_backward.md) folded into grad at the end.
+bool padded_rows_ok(int policy, dw_rasterizer* const* rs, int n) {
+  if (policy != kSwB && policy != kSwS) return false;
+  for (int k = 0; k < n; ++k)
+    if (rs[k]->bulk) return false;  // bulk-copy staging keeps the [P][9] layout
+  return true;
+}
+
+void raster_backward_views(dw_rasterizer* const* rs, const float* const* dLs, int32_t n,
+                           int policy, int thr, float* grad, cudaStream_t s) {
+  if (n < 1) throw std::invalid_argument("need at least one view");
+  for (int k = 0; k < n; ++k) {
+    if (!rs[k] || !dLs[k]) throw std::invalid_argument("null argument");
+    if (!rs[k]->forward_done) throw std::invalid_argument("render_backward before render_forward");
+    if (rs[k]->P_scene != rs[0]->P_scene)
+      throw std::invalid_argument("the views of a batch must render one scene");
+  }
+  const int Ps = rs[0]->P_scene;
+  if (Ps == 0) return;
+  const bool pad = padded_rows_ok(policy, rs, n);
+  float* acc = pad ? rs[0]->padded_grad(Ps, s) : grad;
+  for (int k = 0; k < n; ++k)
+    rs[k]->backward(dLs[k], policy, thr, acc, nullptr, s, /*chained=*/k > 0, pad ? 12 : kNParam);
+  if (pad) launch_fold_rows(Ps, acc, grad, s);
+}
 
 void raster_backward(dw_rasterizer* r, const float* dL, int policy, int thr, float* grad,
                      uint64_t* pairs, cudaStream_t s, bool chained) {
@@ -960,6 +1004,10 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
   float* d_op = r->host_scratch(3, np);
   float* d_col = r->host_scratch(4, 3 * np);
   float* d_g = grad_on_device ? grad : r->host_scratch(7, kNParam * np);
+  // SW-B / SW-S add into a padded [P][12] buffer folded into d_g at the end
+  const bool pad = P > 0 && (policy == kSwB || policy == kSwS) &&
+                   !forced("DW_BULK_STAGING", '1');
+  float* d_acc = pad ? r->padded_grad(P, s) : d_g;
   cudaEvent_t e_scene = r->ev[0], e_start = r->ev[1], e_chain = r->ev[2];
   int NF = 4;  // forward streams the frames of a wave rotate over (1 / 2 / 3 / 4: C5 101.1 / 98.4 / 98.3 / 97.6 ms)
   if (const char* e = std::getenv("DW_VIEWS_FSTREAMS"); e && *e)
@@ -1016,6 +1064,7 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
     auto count = [&](int g) { return std::min(G, static_cast<int>(V) - g * G); };
     auto state = [&](int g) { return g == 0 ? r->probe : r->pool[g % K]; };
     DW_CUDA(cudaMemsetAsync(d_g, 0, kNParam * np * sizeof(float), s));  // (the chain's stream)
+    if (pad) DW_CUDA(cudaMemsetAsync(d_acc, 0, 12 * np * sizeof(float), s));
     bool restack = false;
     for (int w0 = 0; w0 < NG && !restack; w0 += K) {
       const int w1 = std::min(NG, w0 + K);
@@ -1072,8 +1121,8 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
         DW_CUDA(cudaStreamWaitEvent(s, r->pev[3 * (g - w0) + 1], 0));
       }
       for (int g = w0; g < w1; ++g)
-        state(g)->backward(state(g)->host_scratch(5, 3 * npx * G), policy, thr, d_g, nullptr, s,
-                           /*chained=*/g > w0);
+        state(g)->backward(state(g)->host_scratch(5, 3 * npx * G), policy, thr, d_acc, nullptr,
+                           s, /*chained=*/g > w0, pad ? 12 : kNParam);
       DW_CUDA(cudaEventRecord(e_chain, s));
     }
     for (int f = 0; f <= NF; ++f) {  // join every stream into `s`
@@ -1097,6 +1146,7 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
     if (!ovf) break;
     nosync_ok = false;  // redo every view with host-read instance counts
   }
+  if (pad) launch_fold_rows(P, d_acc, d_g, s);
   if (P > 0 && !grad_on_device)
     DW_CUDA(cudaMemcpyAsync(grad, d_g, kNParam * size_t(P) * sizeof(float),
                             cudaMemcpyDeviceToHost, s));

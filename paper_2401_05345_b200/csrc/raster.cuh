@@ -246,6 +246,9 @@ void launch_backward_impl(const CamParams& cam, const uint2* ranges, const uint3
                           const uint32_t* n_contrib,
                           const float* dL, int policy, int thr, float* grad,
                           unsigned long long* counters, cudaStream_t s,
-                          const float4* packed = nullptr, bool chained = false);
+                          const float4* packed = nullptr, bool chained = false,
+                          int grad_stride = kNParam);
+// grad[P][9] += pad[P][12] (the first 9 floats of each padded row), then pad = 0.
+void launch_fold_rows(int64_t P, float* pad, float* grad, cudaStream_t s);
 
 }  // namespace dw

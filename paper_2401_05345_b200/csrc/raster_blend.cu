@@ -498,7 +498,10 @@ __global__ void DW_FWD_BOUNDS
 // gradients before the warp runs the DISTWAR policy on the lane sums, so the
 // mask / ballot / staging overhead and the warp reduction are paid once per
 // 64 pixels.
-template <int POL, bool COUNT, bool TAP = false, bool BULK = false, bool VEC = DW_VEC_RED != 0>
+// GS: floats per gradient row, kNParam ([P][9], Address order) or 12 (the
+// padded batch accumulation buffer, reduce_bfly_scaled), SW-B / SW-S only.
+template <int POL, bool COUNT, bool TAP = false, bool BULK = false, bool VEC = DW_VEC_RED != 0,
+          int GS = kNParam>
 __global__ void __launch_bounds__(128, (POL == kSwB && !COUNT && !TAP) ? DW_SWB_MIN_BLOCKS
                                                                       : DW_MULTI_MIN_BLOCKS)
     k_backward_x2(const CamParams cam, const uint2* __restrict__ ranges,
@@ -512,11 +515,16 @@ __global__ void __launch_bounds__(128, (POL == kSwB && !COUNT && !TAP) ? DW_SWB_
   // chained: the caller guarantees nothing this launch reads is written by
   // the previous kernel on the stream (a chain of backwards of independent,
   // already-rendered views adding into one gradient): no grid-completion
-  // wait, so this launch's CTAs fill the SMs the previous launch's last wave
-  // leaves idle
+  // wait before the work, so this launch's CTAs fill the SMs the previous
+  // launch's last wave leaves idle. The wait moves to the end of the CTA, so
+  // this grid still completes only after its predecessor: whatever follows a
+  // chain (a PDL kernel waits for its immediate predecessor only) sees every
+  // backward of the chain done.
   if (!chained) pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
   static_assert(POL != kNative, "native runs the thread-per-pixel kernel");
+  static_assert(GS == kNParam || (GS == 12 && !COUNT && !TAP && (POL == kSwB || POL == kSwS)),
+                "padded rows: the SW-B reduction path only");
   constexpr int NW = 4;
   __shared__ Staged sm[2][kBlock];  // double buffer: batch i+1 lands while batch i is walked
   __shared__ uint8_t s_mask[kBlock];
@@ -753,8 +761,8 @@ __global__ void __launch_bounds__(128, (POL == kSwB && !COUNT && !TAP) ? DW_SWB_
           reduce_bfly<kNParam, COUNT, true>(id, grad, v, thr, act, lane, nred, ballot, slot,
                                             issuer);
         } else if (kBflyPath) {
-          reduce_bfly_scaled<kNParam, COUNT, VEC>(id, grad, v, thr, act, lane, nred, ballot,
-                                                  slot, issuer, lane_scale, scale);
+          reduce_bfly_scaled<kNParam, COUNT, VEC, GS>(id, grad, v, thr, act, lane, nred, ballot,
+                                                      slot, issuer, lane_scale, scale);
         } else if (POL == kSwS) {
           reduce_serial<kNParam, COUNT>(id, grad, v, thr, act, lane, nred, ballot, slot, issuer);
         } else {
@@ -767,6 +775,7 @@ __global__ void __launch_bounds__(128, (POL == kSwB && !COUNT && !TAP) ? DW_SWB_
     flush_count(counters, npairs, lane);
     flush_count(counters + 1, nred, lane);
   }
+  if (chained) pdl_wait();  // complete no earlier than the predecessor grid
 }
 
 // DW_VEC_RED=0 in the environment (read per launch): the SW-B per-lane
@@ -781,8 +790,17 @@ void launch_bwd(bool count, const CamParams& cam, const uint2* ranges, const uin
                 const float2* means2D, const float4* co, const float4* rgb,
                 const uint32_t* tile_order, const float* fT,
                 const uint32_t* nc, const float* dL, int thr, float* grad,
-                unsigned long long* ctr, cudaStream_t s, const float4* packed, bool chained) {
+                unsigned long long* ctr, cudaStream_t s, const float4* packed, bool chained,
+                int gs) {
   const int grid = cam.tiles_x * cam.tiles_y;
+  if constexpr (POL == kSwB || POL == kSwS) {
+    if (gs == 12) {  // padded accumulation rows (the batch paths; padded_rows_ok)
+      launch_pdl(k_backward_x2<POL, false, false, false, true, 12>, grid, 128, 0, s, cam, ranges,
+                 values, means2D, co, rgb, fT, nc, dL, thr, grad, nullptr, TapBuf{}, tile_order,
+                 nullptr, chained);
+      return;
+    }
+  }
   // The reduction policies run two pixels per lane; native keeps the paper's
   // thread-per-pixel kernel (profiles/r01/ab_ppt.jsonl).
   if constexpr (POL != kNative) {
@@ -810,7 +828,34 @@ void launch_bwd(bool count, const CamParams& cam, const uint2* ranges, const uin
                                                    nc, dL, thr, grad, nullptr);
 }
 
+// grad[p][0..9) += pad[p][0..9); pad[p] = 0 (ready for the next batch). One
+// thread per primitive: three 16-byte loads and stores of the padded row,
+// nine adds into the Address-order row (consecutive threads, consecutive rows).
+__global__ void __launch_bounds__(256) k_fold_rows(int64_t P, float4* __restrict__ pad,
+                                                   float* __restrict__ grad) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+  if (p >= P) return;
+  const float4 a = pad[3 * p], b = pad[3 * p + 1], c = pad[3 * p + 2];
+  float* g = grad + 9 * p;
+  const float v[9] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x};
+#pragma unroll
+  for (int k = 0; k < 9; ++k) g[k] += v[k];
+  const float4 z = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  pad[3 * p] = z;
+  pad[3 * p + 1] = z;
+  pad[3 * p + 2] = z;
+}
+
 }  // namespace
+
+void launch_fold_rows(int64_t P, float* pad, float* grad, cudaStream_t s) {
+  if (P <= 0) return;
+  launch_pdl(k_fold_rows, static_cast<unsigned>((P + 255) / 256), 256, 0, s, P,
+             reinterpret_cast<float4*>(pad), grad);
+  DW_CUDA(cudaGetLastError());
+}
 
 void launch_backward_tap(const CamParams& cam, const uint2* ranges, const uint32_t* values,
                          const float2* means2D, const float4* co, const float4* rgb,
@@ -838,24 +883,27 @@ void launch_backward_impl(const CamParams& cam, const uint2* ranges, const uint3
                           const uint32_t* tile_order, const float* final_T,
                           const uint32_t* n_contrib, const float* dL, int policy, int thr,
                           float* grad, unsigned long long* counters, cudaStream_t s,
-                          const float4* packed, bool chained) {
+                          const float4* packed, bool chained, int grad_stride) {
   const bool count = counters != nullptr;
+  if (grad_stride != kNParam &&
+      !(grad_stride == 12 && !count && !packed && (policy == kSwB || policy == kSwS)))
+    throw std::invalid_argument("padded gradient rows: SW-B / SW-S, uncounted, cp.async staging");
   switch (policy) {
     case kNative:
       launch_bwd<kNative>(count, cam, ranges, values, means2D, co, rgb, tile_order, final_T,
-                          n_contrib, dL, thr, grad, counters, s, packed, chained);
+                          n_contrib, dL, thr, grad, counters, s, packed, chained, grad_stride);
       break;
     case kSwS:
       launch_bwd<kSwS>(count, cam, ranges, values, means2D, co, rgb, tile_order, final_T, n_contrib,
-                       dL, thr, grad, counters, s, packed, chained);
+                       dL, thr, grad, counters, s, packed, chained, grad_stride);
       break;
     case kSwB:
       launch_bwd<kSwB>(count, cam, ranges, values, means2D, co, rgb, tile_order, final_T, n_contrib,
-                       dL, thr, grad, counters, s, packed, chained);
+                       dL, thr, grad, counters, s, packed, chained, grad_stride);
       break;
     default:
       launch_bwd<kCccl>(count, cam, ranges, values, means2D, co, rgb, tile_order, final_T,
-                        n_contrib, dL, thr, grad, counters, s, packed, chained);
+                        n_contrib, dL, thr, grad, counters, s, packed, chained, grad_stride);
   }
   DW_CUDA(cudaGetLastError());
 }

@@ -21,21 +21,27 @@ def shard_views(num_views: int, world: int, rank: int) -> range:
 
 
 def view_parallel_backward(backward_view: Callable, views: Sequence, grad, group=None,
-                           all_reduce: bool = True, chain: bool = False):
+                           all_reduce: bool = True, chain: bool = False,
+                           backward_views: Callable = None):
     """Run `backward_view(view, grad)` (which ADDS into grad) for this rank's
     shard of `views`, then sum `grad` over the group. Returns grad.
     chain: call `backward_view(view, grad, chained=k > 0)` -- the shard's
     backwards after the first may skip the wait for the previous launch
-    (dw_render_backward_chained: the views are independent and rendered)."""
+    (dw_render_backward_chained: the views are independent and rendered).
+    backward_views: instead, ONE call `backward_views(shard, grad)` for the
+    whole shard (dw_render_backward_views)."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    for k, i in enumerate(shard_views(len(views), world, rank)):
+    shard = [views[i] for i in shard_views(len(views), world, rank)]
+    if backward_views is not None:
+        backward_views(shard, grad)
+    for k, v in enumerate(shard if backward_views is None else ()):
         if chain:
-            backward_view(views[i], grad, chained=k > 0)
+            backward_view(v, grad, chained=k > 0)
         else:
-            backward_view(views[i], grad)
+            backward_view(v, grad)
     if all_reduce and world > 1:
         dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=group)
     return grad

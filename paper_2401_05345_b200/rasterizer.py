@@ -377,6 +377,24 @@ class ThresholdTuner:
         return Policy(self.kind, self.chosen)
 
 
+def render_backward_views(rasts, dLs, policy: Policy, grad, stream=None):
+    """dw_render_backward_views: the backwards of rendered views of one scene
+    (rasts[k] with dLs[k]) added into grad [P, 9] as one chain."""
+    import torch
+
+    n = len(rasts)
+    if n < 1 or len(dLs) != n:
+        raise ValueError("one dL/dpixel per rasterizer, at least one")
+    P = rasts[0].P
+    hs = (C.c_void_p * n)(*[r.handle for r in rasts])
+    ds = (C.c_void_p * n)(*[_ptr(d, "dL_dpixels", torch.float32, r._npix3())
+                            for r, d in zip(rasts, dLs)])
+    check(lib().dw_render_backward_views(hs, ds, n, int(policy.kind), policy.threshold,
+                                         _ptr(grad, "grad", torch.float32, min_numel=NPARAM * P),
+                                         _stream(stream)))
+    return grad
+
+
 def max_stacked_views(width: int, height: int) -> int:
     """dw_rasterizer_max_stacked_views: views of this size one stacked frame holds."""
     out = C.c_int32()

@@ -201,3 +201,35 @@ def test_chained_backwards_equal_plain(cuda):
     _grad_close(chain.cpu().numpy().astype(np.float64) / 3.0, want)
     with pytest.raises(ValueError):
         rs[0].render_backward(dLs[0], pol, chained=True)  # needs a given gradient
+
+
+@pytest.mark.parametrize("policy", ["sw_b", "sw_s", "native", "cccl"])
+def test_backward_views_batch_equals_plain(cuda, policy):
+    """dw_render_backward_views (one chain; SW-B / SW-S through the padded
+    [P][12] accumulation folded into grad) == plain per-view launches, and it
+    ADDS into grad like render_backward."""
+    import torch
+
+    from paper_2401_05345_b200 import warpred as wr
+    from paper_2401_05345_b200.rasterizer import GaussianRasterizer, render_backward_views
+    from paper_2401_05345_b200.scene import make_dL_dpixels, orbit_cameras
+
+    P, W, H = 25000, 288, 200
+    sc = _scene(cuda, P, W, H, seed=44)
+    args = [sc[k] for k in SCENE_KEYS]
+    cams = orbit_cameras(W, H, 3)
+    dLs = [torch.from_numpy(make_dL_dpixels(W, H, seed=50 + k)).to(cuda) for k in range(3)]
+    pol = wr.Policy(wr.parse_policy_kind(policy), 12 if policy in ("sw_b", "sw_s") else 0)
+    rs = []
+    for c in cams:
+        r = GaussianRasterizer()
+        r.render_forward(*args, c)
+        rs.append(r)
+    plain = torch.zeros((P, 9), dtype=torch.float32, device=cuda)
+    for r, dL in zip(rs, dLs):
+        r.render_backward(dL, pol, grad=plain)
+    batch = torch.full((P, 9), 0.5, dtype=torch.float32, device=cuda)
+    for _ in range(2):  # the padded buffer is left zeroed for the next batch
+        render_backward_views(rs, dLs, pol, batch)
+    want = 2 * plain.cpu().numpy().astype(np.float64) + 0.5
+    _grad_close(batch.cpu().numpy().astype(np.float64), want)

@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--threshold", type=int, default=15)
     ap.add_argument("--modes", default="events,plain,chained")
+    ap.add_argument("--grad-stride", type=int, default=9,
+                    help="floats per gradient row (12: a -DDW_GRAD_STRIDE=12 A/B build)")
     a = ap.parse_args()
     import torch
 
@@ -40,7 +42,7 @@ def main():
         r.render_forward(*args, c)
         rasts.append(r)
     dLs = [torch.from_numpy(make_dL_dpixels(W, H, seed=1 + k)).to(dev) for k in range(a.views)]
-    grad = torch.zeros((P, 9), device=dev)
+    grad = torch.zeros((P, a.grad_stride), device=dev)
     pol = wr.Policy(wr.PolicyKind.sw_b, a.threshold)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731

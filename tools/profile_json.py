@@ -38,8 +38,10 @@ def launches(path):
 def main(specs_path, csv_path):
     sp = json.load(open(specs_path))
     ls = launches(csv_path)
-    if len(ls) != len(sp["specs"]):
-        raise SystemExit(f"{len(ls)} launches for {len(sp['specs'])} specs")
+    per = sp.get("launches_per_spec", 1)  # > 1: the spec's LAST launch is the measured one
+    if len(ls) != per * len(sp["specs"]):
+        raise SystemExit(f"{len(ls)} launches for {len(sp['specs'])} specs x {per}")
+    ls = ls[per - 1::per]
     key = f"{sp['workload']}@view{sp['view']}/{sp['views']}"
     src = os.path.relpath(os.path.abspath(csv_path), ROOT)
     files = {"inst": os.path.join(ROOT, "profiles", "backward_inst.json"),
