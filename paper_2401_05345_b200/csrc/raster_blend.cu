@@ -516,10 +516,11 @@ __global__ void __launch_bounds__(128, (POL == kSwB && !COUNT && !TAP) ? DW_SWB_
   // the previous kernel on the stream (a chain of backwards of independent,
   // already-rendered views adding into one gradient): no grid-completion
   // wait before the work, so this launch's CTAs fill the SMs the previous
-  // launch's last wave leaves idle. The wait moves to the end of the CTA, so
-  // this grid still completes only after its predecessor: whatever follows a
-  // chain (a PDL kernel waits for its immediate predecessor only) sees every
-  // backward of the chain done.
+  // launch's last wave leaves idle. The wait moves to the end of the last
+  // CTA (the last dispatched, so it rarely waits), so this grid still
+  // completes only after its predecessor: whatever follows a chain (a PDL
+  // kernel waits for its immediate predecessor only) sees every backward of
+  // the chain done.
   if (!chained) pdl_wait();  // predecessor grid complete (programmatic dependent launch)
   pdl_trigger();
   static_assert(POL != kNative, "native runs the thread-per-pixel kernel");
@@ -775,7 +776,11 @@ __global__ void __launch_bounds__(128, (POL == kSwB && !COUNT && !TAP) ? DW_SWB_
     flush_count(counters, npairs, lane);
     flush_count(counters + 1, nred, lane);
   }
-  if (chained) pdl_wait();  // complete no earlier than the predecessor grid
+#ifndef DW_CHAIN_ENDWAIT  // A/B hook: 0 none (unsafe), 1 the last CTA, 2 every CTA
+#define DW_CHAIN_ENDWAIT 1
+#endif
+  if (chained && (DW_CHAIN_ENDWAIT == 2 || (DW_CHAIN_ENDWAIT == 1 && blockIdx.x == gridDim.x - 1)))
+    pdl_wait();  // complete after the predecessor
 }
 
 // DW_VEC_RED=0 in the environment (read per launch): the SW-B per-lane

@@ -28,7 +28,7 @@ def main():
     import torch
 
     from paper_2401_05345_b200 import warpred as wr
-    from paper_2401_05345_b200.rasterizer import GaussianRasterizer
+    from paper_2401_05345_b200.rasterizer import GaussianRasterizer, render_backward_views
     from paper_2401_05345_b200.scene import CONFIGS, make_dL_dpixels, make_scene, orbit_cameras
 
     P, W, H, hc, nviews = CONFIGS[a.workload]
@@ -60,14 +60,16 @@ def main():
         e0, e1 = ev(), ev()
         e0.record()
         grad.zero_()
-        for i, (r, dL) in enumerate(zip(rasts, dLs)):
+        for i, (r, dL) in enumerate(zip(rasts, dLs) if mode != "batch" else ()):
             if mode == "events":
                 a0, a1 = ev(), ev()
                 a0.record()
                 r.render_backward(dL, pol, grad=grad)
                 a1.record()
-            else:
+            elif mode != "batch":
                 r.render_backward(dL, pol, grad=grad, chained=(mode == "chained" and i > 0))
+        if mode == "batch":  # dw_render_backward_views: chain + padded rows + fold
+            render_backward_views(rasts, dLs, pol, grad)
         e1.record()
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / len(rasts)
