@@ -692,13 +692,21 @@ struct dw_rasterizer {
     order_stale = false;
   }
 
-  // padded [P][12] gradient accumulation of the batch path, kept zeroed
-  // between batches by launch_fold_rows
+  // padded [P][12] gradient accumulation of the batch paths, kept zeroed
+  // between batches by launch_fold_rows; pad_dirty: a batch started adding
+  // into it and did not fold (an error between the two) -- zero it again
   float* pad_grad = nullptr;
   size_t cap_pad = 0;
+  bool pad_dirty = false;
   float* padded_grad(int64_t P_, cudaStream_t s) {
     grow_zeroed(pad_grad, cap_pad, static_cast<size_t>(std::max<int64_t>(P_, 1)) * 12, s);
+    if (pad_dirty) DW_CUDA(cudaMemsetAsync(pad_grad, 0, cap_pad * sizeof(float), s));
+    pad_dirty = true;
     return pad_grad;
+  }
+  void fold_padded(int64_t P_, float* grad, cudaStream_t s) {
+    dw::launch_fold_rows(P_, pad_grad, grad, s);
+    pad_dirty = false;
   }
 
   float* host_scratch(int slot, size_t n) {
@@ -773,7 +781,7 @@ void raster_backward_views(dw_rasterizer* const* rs, const float* const* dLs, in
   float* acc = pad ? rs[0]->padded_grad(Ps, s) : grad;
   for (int k = 0; k < n; ++k)
     rs[k]->backward(dLs[k], policy, thr, acc, nullptr, s, /*chained=*/k > 0, pad ? 12 : kNParam);
-  if (pad) launch_fold_rows(Ps, acc, grad, s);
+  if (pad) rs[0]->fold_padded(Ps, grad, s);
 }
 
 void raster_backward(dw_rasterizer* r, const float* dL, int policy, int thr, float* grad,
@@ -1146,7 +1154,7 @@ void raster_views_host(dw_rasterizer* r, int32_t P, const float* m, const float*
     if (!ovf) break;
     nosync_ok = false;  // redo every view with host-read instance counts
   }
-  if (pad) launch_fold_rows(P, d_acc, d_g, s);
+  if (pad) r->fold_padded(P, d_g, s);
   if (P > 0 && !grad_on_device)
     DW_CUDA(cudaMemcpyAsync(grad, d_g, kNParam * size_t(P) * sizeof(float),
                             cudaMemcpyDeviceToHost, s));
