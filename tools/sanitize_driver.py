@@ -13,7 +13,8 @@ def main():
     import torch
 
     from paper_2401_05345_b200 import warpred as wr
-    from paper_2401_05345_b200.rasterizer import Adam, GaussianRasterizer, render_views_host
+    from paper_2401_05345_b200.rasterizer import (Adam, GaussianRasterizer, render_backward_views,
+                                                  render_views_host)
     from paper_2401_05345_b200.scene import make_camera, make_dL_dpixels, make_scene, orbit_cameras
 
     dev = torch.device("cuda:0")
@@ -86,6 +87,31 @@ def main():
                                                       "opacities", "colors")],
                       P, cams, dLh.data_ptr(), wr.Policy(wr.PolicyKind.sw_b, 8), img.data_ptr(),
                       grad.data_ptr())
+    # the same with stacked frames and more views (waves, no-sync pool states)
+    os.environ["DW_VIEWS_STACK"] = "3"
+    cams7 = orbit_cameras(W, H, 7)
+    dLh7 = torch.stack([dL.cpu()] * 7).pin_memory()
+    img7 = torch.empty((7, 3, H, W)).pin_memory()
+    render_views_host(r, [pin[k].data_ptr() for k in ("means3D", "scales", "rotations",
+                                                      "opacities", "colors")],
+                      P, cams7, dLh7.data_ptr(), wr.Policy(wr.PolicyKind.sw_b, 8), img7.data_ptr(),
+                      grad.data_ptr())
+    os.environ.pop("DW_VIEWS_STACK")
+    # stacked forward + its backward; a batch chain (padded rows + fold), chained calls
+    rs3 = GaussianRasterizer()
+    args = [sc[k] for k in ("means3D", "scales", "rotations", "opacities", "colors")]
+    rs3.render_forward_views(*args, orbit_cameras(W, H, 3))
+    rs3.render_backward(torch.stack([dL] * 3), wr.Policy(wr.PolicyKind.sw_b, 8))
+    views = []
+    for c in orbit_cameras(W, H, 3):
+        rv = GaussianRasterizer()
+        rv.render_forward(*args, c)
+        views.append(rv)
+    g = torch.zeros((P, 9), device=dev)
+    render_backward_views(views, [dL] * 3, wr.Policy(wr.PolicyKind.sw_b, 8), g)
+    render_backward_views(views, [dL] * 3, wr.Policy(wr.PolicyKind.native, 0), g)
+    for k, rv in enumerate(views):
+        rv.render_backward(dL, wr.Policy(wr.PolicyKind.sw_b, 8), grad=g, chained=k > 0)
     torch.cuda.synchronize()
     print("sanitize driver OK")
 
