@@ -233,3 +233,32 @@ def test_backward_views_batch_equals_plain(cuda, policy):
         render_backward_views(rs, dLs, pol, batch)
     want = 2 * plain.cpu().numpy().astype(np.float64) + 0.5
     _grad_close(batch.cpu().numpy().astype(np.float64), want)
+
+
+def test_backward_views_batch_full_size_c5(cuda):
+    """BASELINE configs[4] at full size (3M Gaussians, 1080p): bench.py's timed
+    call -- the batch of views as one dw_render_backward_views chain into the
+    padded rows -- equals plain per-view launches (here three orbit views)."""
+    import torch
+
+    from paper_2401_05345_b200 import warpred as wr
+    from paper_2401_05345_b200.rasterizer import GaussianRasterizer, render_backward_views
+    from paper_2401_05345_b200.scene import CONFIGS, make_dL_dpixels, orbit_cameras
+
+    P, W, H, _, V = CONFIGS["c5_3m_1080p_64views"]
+    sc = _scene(cuda, P, W, H, seed=0)
+    args = [sc[k] for k in SCENE_KEYS]
+    cams = [orbit_cameras(W, H, V)[k] for k in (0, 21, 63)]
+    dLs = [torch.from_numpy(make_dL_dpixels(W, H, seed=1 + k)).to(cuda) for k in range(3)]
+    pol = wr.Policy(wr.PolicyKind.sw_b, 16)
+    rs = []
+    for c in cams:
+        r = GaussianRasterizer()
+        r.render_forward(*args, c)
+        rs.append(r)
+    plain = torch.zeros((P, 9), dtype=torch.float32, device=cuda)
+    for r, dL in zip(rs, dLs):
+        r.render_backward(dL, pol, grad=plain)
+    batch = torch.zeros((P, 9), dtype=torch.float32, device=cuda)
+    render_backward_views(rs, dLs, pol, batch)
+    _grad_close(batch.cpu().numpy().astype(np.float64), plain.cpu().numpy().astype(np.float64))
