@@ -439,6 +439,37 @@ def main() -> None:
             if rep >= 1:
                 reps.append(e0.elapsed_time(e1))
         fwd_ms.append(statistics.median(reps))
+    # the rank's forwards without host synchronisation (render_forward_async
+    # over a 1.5x reserve: the graph-capturable path), back to back on one
+    # stream and rotating over four streams (the batched host path's forward
+    # phase); the same cameras, so every state ends as the counted forward left it
+    for r in rasts:
+        r.reserve(P, W, H, r.num_rendered + r.num_rendered // 2 + 4096)
+    img_s = [torch.empty((3, H, W), device=dev) for _ in range(4)]
+    rad_s = [torch.empty(P, dtype=torch.int32, device=dev) for _ in range(4)]
+    fstreams = [torch.cuda.Stream() for _ in range(4)]
+
+    def forwards_async(nstreams):
+        torch.cuda.synchronize()
+        e0, e1 = ev(), ev()
+        e0.record()
+        for fs in fstreams[:nstreams]:
+            fs.wait_event(e0)
+        for i, r in enumerate(rasts):
+            j = i % nstreams
+            r.render_forward_async(t["means3D"], t["scales"], t["rotations"], t["opacities"],
+                                   t["colors"], cams[i], img_s[j], rad_s[j], stream=fstreams[j])
+        for fs in fstreams[:nstreams]:
+            torch.cuda.current_stream().wait_stream(fs)
+        e1.record()
+        torch.cuda.synchronize()
+        assert not any(r.instances()[1] for r in rasts), "forward reserve overflow"
+        return e0.elapsed_time(e1) / len(rasts)
+
+    fwd_async = {}
+    for ns in (1, 4):
+        forwards_async(ns)
+        fwd_async[ns] = statistics.median(forwards_async(ns) for _ in range(3))
     stages = (stage_breakdown(t, cams[0], P, H, W,
                               f"{args.workload}@view{my_views[0]}/{total_views}")
               if rank == 0 else None)
@@ -761,6 +792,13 @@ def main() -> None:
             "target_config": target,
             "forward": {"ms_per_view": statistics.mean(fwd_ms),
                         "fps": 1e3 / statistics.mean(fwd_ms),
+                        "async_one_stream": {"ms_per_view": fwd_async[1],
+                                             "fps": 1e3 / fwd_async[1]},
+                        "async_four_streams": {"ms_per_view": fwd_async[4],
+                                               "fps": 1e3 / fwd_async[4]},
+                        "_async": "the rank's views back to back without host synchronisation "
+                                  "(render_forward_async over a 1.5x reserve), on one stream / "
+                                  "rotating over four (the batched host path's forward phase)",
                         "_timing": "render_forward (counted: one host read of the instance "
                                    "count mid-forward), per view the median of 3 warm calls, "
                                    "mean over the rank's views",
