@@ -783,7 +783,8 @@ def main() -> None:
                                       f"all-reduce of grad[P,9]"
                        if world > 1 else "dp1",
                        "l2": "flushed between steps (256 MiB write, outside the events)"},
-            "gpu_launches": args.steps * V,
+            # per step: the rank's V backward launches + the padded-row fold
+            "gpu_launches": args.steps * (V + 1),
             "clocks": clocks,
             "naive": {"value": naive_value, "ms_per_step": total_nv_ms / nv_steps,
                       "steps": nv_steps,
