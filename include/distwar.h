@@ -251,7 +251,7 @@ dw_status dw_render_backward_chained(dw_rasterizer* r, const float* dL_dpixels,
  * per view, each already rendered; dL_dpixels[k] belongs to rasterizers[k])
  * added into grad[P*9] (device, Address order) as ONE chain on `stream`:
  * the first launch waits for the stream, the others start on the SMs their
- * predecessor's last wave leaves idle. SW-B / SW-S accumulate into an
+ * predecessor's last wave leaves idle. SW-B / SW-S accumulate into a
  * padded [P][12] buffer (16-byte aligned rows) held by rasterizers[0] and
  * folded into grad at the end -- one batch per rasterizers[0] in flight at a
  * time (like every call on one handle). Returns once everything is enqueued. */
