@@ -97,13 +97,18 @@ def test_stacked_forward_rejects_bad_stacks(cuda):
         r.render_forward_views(*args, [make_camera(W, H), make_camera(W, H, bg=(0, 0, 0))])
 
 
-def _views_host(monkeypatch, stack, sc_np, cams, dL):
+def _views_host(monkeypatch, stack, sc_np, cams, dL, wave=None, fstreams=None):
     import torch
 
     from paper_2401_05345_b200 import warpred as wr
     from paper_2401_05345_b200.rasterizer import GaussianRasterizer, render_views_host
 
     monkeypatch.setenv("DW_VIEWS_STACK", str(stack))
+    for name, val in (("DW_VIEWS_WAVE", wave), ("DW_VIEWS_FSTREAMS", fstreams)):
+        if val is None:
+            monkeypatch.delenv(name, raising=False)
+        else:
+            monkeypatch.setenv(name, str(val))
     P = sc_np["means3D"].shape[0]
     V, _, H, W = dL.shape
     pin = {k: torch.from_numpy(v).pin_memory() for k, v in sc_np.items()}
@@ -262,3 +267,22 @@ def test_backward_views_batch_full_size_c5(cuda):
     batch = torch.zeros((P, 9), dtype=torch.float32, device=cuda)
     render_backward_views(rs, dLs, pol, batch)
     _grad_close(batch.cpu().numpy().astype(np.float64), plain.cpu().numpy().astype(np.float64))
+
+
+@pytest.mark.parametrize("wave,fstreams,stack", [(2, 4, 1), (3, 1, 1), (1, 2, 2), (2, 3, 3)])
+def test_views_host_multi_wave(cuda, monkeypatch, wave, fstreams, stack):
+    """Batches longer than one wave: the pool states are reused wave after
+    wave (a wave's forwards wait for the previous wave's chain and image
+    downloads), over 1-4 forward streams, with and without stacked frames --
+    images bit for bit and gradients equal to the default (one wave)."""
+    from paper_2401_05345_b200.scene import make_dL_dpixels, make_scene, orbit_cameras
+
+    P, W, H, V = 9000, 176, 128, 9
+    sc = make_scene(P, W, H, seed=17)
+    cams = orbit_cameras(W, H, V)
+    dL = np.stack([make_dL_dpixels(W, H, seed=300 + k) for k in range(V)]).astype(np.float32)
+    ref = _views_host(monkeypatch, 1, sc, cams, dL)
+    got = _views_host(monkeypatch, stack, sc, cams, dL, wave=wave, fstreams=fstreams)
+    for (gi, gg), (ri, rg) in zip(got, ref):
+        assert np.array_equal(gi, ri)
+        _grad_close(gg, rg)
