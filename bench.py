@@ -705,7 +705,10 @@ def main() -> None:
         issue = {"bound": "issue", "achieved": ach, "peak": peak, "unit": "warp-inst/s",
                  "frac": ach / peak, "inst_per_launch": inst_t[spec],
                  "launch_ms": v0_launch_ms,
-                 "_launch": "view 0's backward timed alone (events around one launch)",
+                 "_launch": "view 0's backward timed alone (events around one launch, "
+                            "[P][9] rows); the instruction count is the timed path's "
+                            "(a chained launch into the padded rows, a few % fewer "
+                            "instructions), so this alone-fraction reads slightly low",
                  # the timed chain: launches overlap their neighbours' tails,
                  # so the step's per-launch share keeps the issue slots busier
                  "chained": {"launch_ms": mean_launch_ms,
