@@ -516,13 +516,22 @@ __global__ void DW_SCAN_BOUNDS
       const uint32_t o = s_bo[i + (i >> 5)];
       if (static_cast<uint64_t>(o) + static_cast<uint64_t>(nb) > ent.cap) nb = 0;  // host regrows
       const uint32_t gid = gids[r];
-      int incl = nb;
+      // every Gaussian's first block (its top-left one) is written by its own
+      // lane; only the entries beyond the first (~1/3 of them at 1080p) go
+      // through the warp-cooperative expansion -- one trip per round instead
+      // of two, and none when every rectangle sits inside one block
+      if (nb > 0) {
+        ent.bkey[o] = static_cast<uint32_t>(by0 * ent.nbx + bx0);
+        ent.bval[o] = gid;
+      }
+      const int extra = nb > 1 ? nb - 1 : 0;
+      int incl = extra;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const int y = __shfl_up_sync(kFull, incl, d);
         if (lane >= d) incl += y;
       }
-      const int excl = incl - nb;
+      const int excl = incl - extra;
       const int total = __shfl_sync(kFull, incl, 31);
       for (int q0 = 0; q0 < total; q0 += 32) {  // warp-uniform trips
         const int q = q0 + lane;
@@ -532,7 +541,7 @@ __global__ void DW_SCAN_BOUNDS
           const int probe = owner + step;
           if (__shfl_sync(kFull, excl, probe) <= q) owner = probe;
         }
-        const int kk = q - __shfl_sync(kFull, excl, owner);
+        const int kk = q - __shfl_sync(kFull, excl, owner) + 1;  // entry 1.. of the owner
         const int w_ = __shfl_sync(kFull, bw, owner);
         const int ox = __shfl_sync(kFull, bx0, owner), oy = __shfl_sync(kFull, by0, owner);
         const uint32_t oo = __shfl_sync(kFull, o, owner);
